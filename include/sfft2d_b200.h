@@ -1,0 +1,181 @@
+/*
+ * sfft2d_b200 — C ABI of the B200-native 2D sparse FFT (SFFT, Algorithm 1) and
+ * adaptive-sparsity ATSFFT (Algorithm 2) of arXiv 1908.02461.
+ *
+ * The reference (`/root/reference/pkg/src/sfft2d`) is a pure-Python package
+ * with no FFI; its drop-in boundary is its Python API.  Each entry point below
+ * replaces one reference function (cited) and is what a binding of that API
+ * calls (see INTEGRATION.md for the ctypes stub the Python mirror uses).
+ *
+ * Conventions
+ *  - Images are square N x N, N a power of two, row-major complex64
+ *    (SFFT2D_C64) or complex128 (SFFT2D_C128), i.e. numpy's memory layout.
+ *    `x_on_host` = 1: `x` is a host pointer (pinned or pageable) and the
+ *    library performs the host->device copy on `stream`.
+ *  - Arithmetic precision is selected per call: SFFT2D_FP64 reproduces the
+ *    reference's float64 arithmetic (verification mode, 1e-10 parity);
+ *    SFFT2D_FP32 is the fast path (1e-4 parity on values).
+ *  - Permutations are drawn by the caller (numpy Generator, reference draw
+ *    order, hashing.py:72-80) and passed in; the library never draws random
+ *    numbers, so results are bit-reproducible for a given permutation list.
+ *  - Window and twiddle tables are built by the caller on the host with the
+ *    reference's formulas (hashing.py:138-246) and registered once per
+ *    (N, delta_pass, delta_stop) with sfft2d_ctx_set_tables.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Every call is
+ *    stream-ordered; the transform entry points synchronise `stream` at the
+ *    data-dependent decision points of the algorithm (tuner counts).
+ *  - Return value: SFFT2D_OK or a negative status; nothing throws across the
+ *    ABI.  sfft2d_ctx_last_error returns the message of the last failure.
+ *  - A context owns a grow-only device workspace and the registered tables;
+ *    it is bound to one device and must not be used concurrently from two
+ *    host threads.
+ */
+#ifndef SFFT2D_B200_H
+#define SFFT2D_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SFFT2D_ABI_VERSION 1
+#define SFFT2D_MAX_HISTORY 256
+
+enum sfft2d_status {
+  SFFT2D_OK = 0,
+  SFFT2D_ERR_VALUE = -1,       /* maps to ValueError (corefft.py:45-50, hashing.py:306-311) */
+  SFFT2D_ERR_CONFIG = -2,      /* maps to ConfigurationError (engine.py:45-109) */
+  SFFT2D_ERR_CUDA = -3,
+  SFFT2D_ERR_NOMEM = -4,
+  SFFT2D_ERR_UNSUPPORTED = -5,
+  SFFT2D_ERR_STATE = -6        /* missing tables / nothing to fetch */
+};
+
+enum sfft2d_dtype { SFFT2D_C64 = 0, SFFT2D_C128 = 1 };
+enum sfft2d_precision { SFFT2D_FP32 = 0, SFFT2D_FP64 = 1 };
+
+typedef struct sfft2d_ctx sfft2d_ctx;
+
+/* PermutationParams (hashing.py:45-69) */
+typedef struct {
+  int64_t sigma1, sigma2, tau1, tau2, sigma1_inv, sigma2_inv;
+} sfft2d_perm;
+
+/* SfftConfig after __post_init__ defaults (engine.py:69-113) */
+typedef struct {
+  int32_t n, k, loops, d_factor, vote_threshold, b_bins;
+  double window_delta_pass, window_delta_stop, gain_floor, prune_rel;
+} sfft2d_sfft_config;
+
+/* TunerConfig (tuner.py:47-78); max_tuning_iters < 0 means 2*log2(n) */
+typedef struct {
+  int32_t b0, max_tuning_iters;
+  double eps1, eps2, delta1, delta2, mag_floor;
+  double window_delta_pass, window_delta_stop, gain_floor, prune_rel;
+} sfft2d_tuner_config;
+
+/* TunerState (tuner.py:81-94) plus bookkeeping */
+typedef struct {
+  int32_t passes;
+  int32_t hist_bins[SFFT2D_MAX_HISTORY];
+  int64_t hist_count[SFFT2D_MAX_HISTORY];
+  double hist_ratio[SFFT2D_MAX_HISTORY];
+  int32_t hist_has_ratio[SFFT2D_MAX_HISTORY];
+  int32_t converged;
+  int64_t detected_k;
+  int32_t b_detect, b_estimate, vote_passes;
+  int32_t perms_used;       /* permutations consumed from the caller's list   */
+  int64_t n_votes;          /* distinct voted coordinates (detect_sparsity)   */
+  int64_t n_candidates;     /* coordinates at or above the vote threshold     */
+} sfft2d_tuner_state;
+
+typedef struct {
+  int64_t count;                 /* recovered coefficients available to fetch  */
+  int32_t ordered_by_magnitude;  /* 1: reference dict order is lexsort(-|v|, i, j)
+                                    (top-k cut happened, engine.py:245-248);
+                                    0: row-major (i, j) order                  */
+  int32_t precision;             /* element type of fetched values            */
+  int64_t n_candidates;          /* voted coordinates that were estimated      */
+  int32_t perms_used;
+  int32_t gpu_launches;          /* kernels launched by this call             */
+} sfft2d_result;
+
+int sfft2d_abi_version(void);
+int sfft2d_ctx_create(int device, sfft2d_ctx** out);
+void sfft2d_ctx_destroy(sfft2d_ctx* ctx);
+const char* sfft2d_ctx_last_error(const sfft2d_ctx* ctx);
+
+/* Register host-built tables for side n and window tolerances
+ * (WindowCache.get, hashing.py:249-261):
+ *   space/freq: float64[(log2(n)+1) * n], row log2(B) = FlatWindow.space_1d /
+ *               freq_1d for B bins (rows for B < 4 ignored; row log2(n) is the
+ *               all-pass window, hashing.py:228-246);
+ *   twiddle:    float64[2n] interleaved exp(-2*pi*i*k/n), k < n.             */
+int sfft2d_ctx_set_tables(sfft2d_ctx* ctx, int n, double delta_pass, double delta_stop,
+                          const double* space, const double* freq, const double* twiddle);
+
+/* Algorithm 1 — replaces sfft2d(x, cfg, rng) (engine.py:256-284).
+ * perms: 2*loops permutations; [0, loops) location loops, [loops, 2 loops)
+ * estimation loops (the per-loop child streams of engine.py:268).          */
+int sfft2d_sfft(sfft2d_ctx* ctx, const void* x, int x_dtype, int x_on_host,
+                const sfft2d_sfft_config* cfg, const sfft2d_perm* perms, int precision,
+                void* stream, sfft2d_result* res);
+
+/* Algorithm 2 — replaces atsfft2d(x, cfg, est_loops, rng) (tuner.py:244-282).
+ * perms: the shared Generator's draws in order; at least
+ * iters(n) + 2 + max(est_loops, 1) of them (tuner passes, confirmation passes,
+ * estimation loops).  state->perms_used reports how many were consumed.   */
+int sfft2d_atsfft(sfft2d_ctx* ctx, const void* x, int x_dtype, int x_on_host, int n,
+                  const sfft2d_tuner_config* cfg, int est_loops, const sfft2d_perm* perms,
+                  int n_perms, int precision, void* stream, sfft2d_result* res,
+                  sfft2d_tuner_state* state);
+
+/* detect_sparsity (tuner.py:142-241): tuning loop + votes only; fetch the
+ * (coordinate, tally) pairs with sfft2d_fetch_votes.                      */
+int sfft2d_detect_sparsity(sfft2d_ctx* ctx, const void* x, int x_dtype, int x_on_host, int n,
+                           const sfft2d_tuner_config* cfg, const sfft2d_perm* perms,
+                           int n_perms, int precision, void* stream,
+                           sfft2d_tuner_state* state);
+
+/* Copy the last transform's recovered spectrum: ij int64[count][2], values
+ * complex (float2 for FP32, double2 for FP64)[count], row-major (i, j) order. */
+int sfft2d_fetch_result(sfft2d_ctx* ctx, int64_t* ij, void* values, int dst_on_host,
+                        void* stream);
+
+/* Copy the last detection's votes: keys int32[n_votes] (i*n + j, ascending)
+ * and tallies int32[n_votes].                                             */
+int sfft2d_fetch_votes(sfft2d_ctx* ctx, int32_t* keys, int32_t* tallies, int dst_on_host,
+                       void* stream);
+
+/* ---- building blocks (device pointers, stream-ordered, no host sync) ---- */
+
+/* binned_spectrum (hashing.py:308-337) for `nloops` permutations sharing one
+ * read of x: out = complex[nloops][b][b] of `precision`.                  */
+int sfft2d_binned_spectrum(sfft2d_ctx* ctx, const void* x, int x_dtype, int n, int b,
+                           const sfft2d_perm* perms, int nloops, double delta_pass,
+                           double delta_stop, int precision, void* out, void* stream);
+
+/* fft2d (corefft.py:101-109): unscaled forward 2D DFT of `count` b x b grids
+ * in place; uses the twiddle table registered for side n_table >= b.      */
+int sfft2d_fft2d(sfft2d_ctx* ctx, void* grids, int b, int count, int n_table, int precision,
+                 void* stream);
+
+/* count_local_maxima (tuner.py:97-118) of one b x b grid; *count is written
+ * to host memory (this call synchronises `stream`); the first min(count,
+ * capacity) flat indices (row-major) are written to out_flat (device).    */
+int sfft2d_local_maxima(sfft2d_ctx* ctx, const void* grid, int b, double mag_floor,
+                        int precision, int64_t* count, int32_t* out_flat, int64_t capacity,
+                        void* stream);
+
+/* _top_bins (engine.py:122-127) for `nseg` b x b grids: the `num` largest
+ * |Z| per grid, ties to the lowest flat index, written in ascending flat
+ * index order to out_flat[nseg][num] (device).                            */
+int sfft2d_top_bins(sfft2d_ctx* ctx, const void* grids, int b, int nseg, int64_t num,
+                    int precision, int32_t* out_flat, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SFFT2D_B200_H */

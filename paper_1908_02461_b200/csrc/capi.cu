@@ -1,0 +1,1064 @@
+// C ABI + native controllers for the B200 sparse FFT (see include/sfft2d_b200.h).
+//
+// Controllers (host C++, stream-ordered, one host sync per data-dependent
+// decision):
+//   run_sfft  — Algorithm 1, engine.py:256-284
+//   run_ats   — Algorithm 2, tuner.py:142-282 (tuning loop, confirmation
+//               passes, vote budget, fallback, estimation)
+// Kernels live in the .cuh files next to this one.
+#include "../../include/sfft2d_b200.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "common.cuh"
+#include "estimate.cuh"
+#include "fft.cuh"
+#include "fold.cuh"
+#include "select.cuh"
+#include "vote.cuh"
+
+using namespace sfft;
+
+namespace {
+
+struct SfftError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw SfftError{code, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(SFFT2D_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+bool is_pow2(long long v) { return v >= 1 && (v & (v - 1)) == 0; }
+int ilog2(long long v) {
+  int l = 0;
+  while ((1LL << l) < v) ++l;
+  return l;
+}
+
+template <typename T> constexpr int prec_of();
+template <> constexpr int prec_of<float>() { return SFFT2D_FP32; }
+template <> constexpr int prec_of<double>() { return SFFT2D_FP64; }
+
+struct DevTables {
+  int n = 0, lgn = 0;
+  double dpass = 0, dstop = 0;
+  void* space[2] = {nullptr, nullptr};
+  void* freq[2] = {nullptr, nullptr};
+  void* tw[2] = {nullptr, nullptr};
+};
+
+}  // namespace
+
+struct sfft2d_ctx {
+  int device = 0;
+  std::string err;
+  std::vector<DevTables> tables;
+  std::map<std::string, std::pair<void*, size_t>> bufs;
+  unsigned* pinned = nullptr;  // small host scratch for counts
+  // last results
+  long long res_count = 0;
+  int res_prec = SFFT2D_FP64;
+  bool has_res = false;
+  long long votes_count = 0;
+  bool has_votes = false;
+  int launches = 0;
+};
+
+namespace {
+
+void* ws(sfft2d_ctx* c, const char* name, size_t bytes) {
+  auto& e = c->bufs[name];
+  if (bytes == 0) bytes = 16;
+  if (e.second < bytes) {
+    if (e.first) ck(cudaFree(e.first), "cudaFree");
+    e.first = nullptr;
+    e.second = 0;
+    size_t cap = (bytes + bytes / 8 + 4095) & ~(size_t)4095;
+    if (cudaMalloc(&e.first, cap) != cudaSuccess) {
+      cudaGetLastError();
+      e.first = nullptr;
+      fail(SFFT2D_ERR_NOMEM, std::string("cannot allocate workspace '") + name + "' of " +
+                                 std::to_string(cap) + " bytes");
+    }
+    e.second = cap;
+  }
+  return e.first;
+}
+
+void post(sfft2d_ctx* c, const char* what) {
+  ++c->launches;
+  ck(cudaGetLastError(), what);
+}
+
+template <typename K>
+void allow_smem(K kernel) {
+  static std::mutex mu;
+  static std::map<const void*, bool> done;
+  std::lock_guard<std::mutex> g(mu);
+  const void* key = (const void*)kernel;
+  if (done.count(key)) return;
+  ck(cudaFuncSetAttribute(key, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)kMaxDynSmem),
+     "cudaFuncSetAttribute");
+  done[key] = true;
+}
+
+template <typename T>
+void allow_all_T() {
+  using C = cplx<T>;
+  allow_smem(k_fft2d_small<T>);
+  allow_smem(k_fft_rows<T, C>);
+  allow_smem(k_fft_rows<T, float2>);
+  allow_smem(k_fft_rows<T, double2>);
+  allow_smem(k_fft_cols<T>);
+  allow_smem(k_fold<float2, T, 1, 2>);
+  allow_smem(k_fold<float2, T, 8, 1>);
+  allow_smem(k_fold<double2, T, 1, 2>);
+  allow_smem(k_fold<double2, T, 8, 1>);
+  allow_smem(k_fold_reduce_fft_small<T>);
+  allow_smem(k_permute_grid<T>);
+}
+
+const DevTables& find_tables(sfft2d_ctx* c, int n, double dpass, double dstop) {
+  for (auto& t : c->tables)
+    if (t.n == n && t.dpass == dpass && t.dstop == dstop) return t;
+  fail(SFFT2D_ERR_STATE, "no tables registered for n=" + std::to_string(n) +
+                             " (call sfft2d_ctx_set_tables)");
+}
+
+const DevTables& find_twiddles(sfft2d_ctx* c, int n) {
+  for (auto& t : c->tables)
+    if (t.n == n) return t;
+  fail(SFFT2D_ERR_STATE, "no twiddle table registered for n=" + std::to_string(n));
+}
+
+Perm to_perm(const sfft2d_perm& p, int n) {
+  const long long m = n;
+  auto md = [m](long long v) { return (uint32_t)(((v % m) + m) % m); };
+  Perm q;
+  q.s1 = md(p.sigma1);
+  q.s2 = md(p.sigma2);
+  q.t1 = md(p.tau1);
+  q.t2 = md(p.tau2);
+  q.s1i = md(p.sigma1_inv);
+  q.s2i = md(p.sigma2_inv);
+  return q;
+}
+
+unsigned read_u32(sfft2d_ctx* c, const unsigned* dev, cudaStream_t st) {
+  ck(cudaMemcpyAsync(c->pinned, dev, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H");
+  ck(cudaStreamSynchronize(st), "sync");
+  return c->pinned[0];
+}
+
+unsigned grid_for(long long work, int per_block = 256, int cap = kNumSMs * 16) {
+  long long b = (work + per_block - 1) / per_block;
+  if (b < 1) b = 1;
+  if (b > cap) b = cap;
+  return (unsigned)b;
+}
+
+// ------------------------------------------------------------------ pieces
+template <typename Tin>
+__global__ void k_check_finite(const Tin* __restrict__ x, long n, unsigned* flag) {
+  bool bad = false;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
+       i += (long)gridDim.x * blockDim.x) {
+    const Tin v = x[i];
+    bad |= !isfinite(v.x) || !isfinite(v.y);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
+__global__ void k_sel_init(SelState* st, int nseg, long long num, long long seglen) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < nseg) {
+    st[s].prefix = 0;
+    st[s].mask = 0;
+    st[s].need = num;
+    st[s].take_all = num >= seglen ? 1 : 0;
+  }
+}
+
+__global__ void k_iota_segments(int32_t* out, long seglen, int nseg) {
+  const long total = seglen * nseg;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
+       e += (long)gridDim.x * blockDim.x)
+    out[e] = (int32_t)(e % seglen);
+}
+
+// Fold (+window, +permutation) and bucket FFT for `nloops` permutations.
+template <typename T, typename Tin>
+void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTables& tb,
+                   const Perm* hp, int nloops, cplx<T>* spec, cudaStream_t st) {
+  using C = cplx<T>;
+  const int B = 1 << lgB;
+  const int P = prec_of<T>();
+  const T* space = (const T*)tb.space[P] + ((size_t)lgB << lgN);
+  const C* tw = (const C*)tb.tw[P];
+  const size_t BB = (size_t)B * B;
+  for (int g0 = 0; g0 < nloops; g0 += kMaxFoldLoops) {
+    const int g = std::min(kMaxFoldLoops, nloops - g0);
+    PermPack pp;
+    std::memset(&pp, 0, sizeof(pp));
+    for (int i = 0; i < g; ++i) pp.p[i] = hp[g0 + i];
+    const int cpt = (g == 1) ? 2 : 1;
+    const FoldGeom gm = fold_geometry(lgN, lgB, cpt);
+    const int threads = gm.TW / cpt;
+    const dim3 grid(gm.ktiles, B, gm.Z);
+    const int nlt = (g == 1) ? 1 : kMaxFoldLoops;
+    const size_t dyn = (B < gm.TW) ? (size_t)nlt * gm.TW * sizeof(C) : 0;
+    C* out = spec + (size_t)g0 * BB;
+    C* dst = (gm.Z == 1) ? out : (C*)ws(c, "fold_part", (size_t)gm.Z * g * BB * sizeof(C));
+    if (g == 1)
+      k_fold<Tin, T, 1, 2><<<grid, threads, dyn, st>>>(x, space, pp, g, gm, dst);
+    else
+      k_fold<Tin, T, kMaxFoldLoops, 1><<<grid, threads, dyn, st>>>(x, space, pp, g, gm, dst);
+    post(c, "k_fold");
+    if (gm.Z == 1) {
+      ck(launch_fft2d<T>(out, lgB, g, tw, lgN, st), "fft2d");
+      c->launches += (BB * sizeof(C) <= (size_t)kSmall2DBytes) ? 1 : 2;
+    } else if (BB * sizeof(C) <= (size_t)kSmall2DBytes) {
+      k_fold_reduce_fft_small<T><<<g, 256, BB * sizeof(C), st>>>(dst, gm.Z, g, lgB, pp, tw, lgN,
+                                                                  out);
+      post(c, "k_fold_reduce_fft_small");
+    } else {
+      k_fold_reduce<T><<<grid_for((long long)BB * g), 256, 0, st>>>(dst, gm.Z, g, lgB, pp, out);
+      post(c, "k_fold_reduce");
+      ck(launch_fft2d<T>(out, lgB, g, tw, lgN, st), "fft2d");
+      c->launches += 2;
+    }
+  }
+}
+
+// Compact the set bits of `nseg` segments (bits/counts from a *_bits kernel).
+void compact(sfft2d_ctx* c, const uint32_t* bits, const unsigned* cnts, long seglen, int nseg,
+             int32_t* out, long out_stride, unsigned* total_dev, cudaStream_t st) {
+  const int nblk = blocks_for(seglen);
+  unsigned* offs = (unsigned*)ws(c, "cmp_off", (size_t)nblk * nseg * sizeof(unsigned));
+  k_scan_blocks<<<nseg, 1024, 0, st>>>(cnts, nblk, offs, total_dev);
+  post(c, "k_scan_blocks");
+  k_compact_bits<<<dim3(nblk, nseg), kCmpThreads, 0, st>>>(bits, seglen, offs, out, out_stride);
+  post(c, "k_compact_bits");
+}
+
+// Local maxima of one B x B magnitude grid -> row-major flat list; returns count.
+template <typename T>
+unsigned local_maxima_dev(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long long* peak,
+                          double floor_rel, int32_t* out, cudaStream_t st) {
+  const long BB = 1L << (2 * lgB);
+  const int nblk = blocks_for(BB);
+  uint32_t* bits = (uint32_t*)ws(c, "lm_bits", words_for(BB) * 4);
+  unsigned* cnts = (unsigned*)ws(c, "lm_cnt", (size_t)nblk * 4);
+  unsigned* tot = (unsigned*)ws(c, "lm_tot", 16);
+  k_lmax_bits<T><<<dim3(nblk, 1), kCmpThreads, 0, st>>>(mags, lgB, 0, peak, floor_rel, bits, cnts);
+  post(c, "k_lmax_bits");
+  compact(c, bits, cnts, BB, 1, out, 0, tot, st);
+  return read_u32(c, tot, st);
+}
+
+// Exact top-`num` selection bitmask per segment (ties -> lowest index).
+template <typename T>
+void topk_bits(sfft2d_ctx* c, const T* vals, long seglen, int nseg, long long num, uint32_t* bits,
+               unsigned* cnts, cudaStream_t st) {
+  SelState* sst = (SelState*)ws(c, "sel_state", (size_t)nseg * sizeof(SelState));
+  unsigned* hist = (unsigned*)ws(c, "sel_hist", (size_t)nseg * 256 * sizeof(unsigned));
+  ck(cudaMemsetAsync(hist, 0, (size_t)nseg * 256 * sizeof(unsigned), st), "memset");
+  k_sel_init<<<(nseg + 127) / 128, 128, 0, st>>>(sst, nseg, num, seglen);
+  post(c, "k_sel_init");
+  const int nblk = blocks_for(seglen);
+  if (num < seglen) {
+    unsigned hb = (unsigned)std::max<long long>(1, std::min<long long>(256, (seglen + 4095) / 4096));
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      k_radix_hist<T><<<dim3(hb, nseg), 256, 0, st>>>(vals, seglen, sst, shift, hist);
+      post(c, "k_radix_hist");
+      k_radix_pick<<<(nseg + 31) / 32, 32, 0, st>>>(sst, hist, shift, nseg);
+      post(c, "k_radix_pick");
+    }
+  }
+  unsigned* tie_blk = (unsigned*)ws(c, "sel_tie", (size_t)nblk * nseg * sizeof(unsigned));
+  unsigned* tie_off = (unsigned*)ws(c, "sel_tieoff", (size_t)nblk * nseg * sizeof(unsigned));
+  k_tie_counts<T><<<dim3(nblk, nseg), kCmpThreads, 0, st>>>(vals, seglen, sst, tie_blk);
+  post(c, "k_tie_counts");
+  k_scan_blocks<<<nseg, 1024, 0, st>>>(tie_blk, nblk, tie_off, nullptr);
+  post(c, "k_scan_blocks");
+  k_select_bits<T><<<dim3(nblk, nseg), kCmpThreads, 0, st>>>(vals, seglen, sst, tie_off, bits, cnts);
+  post(c, "k_select_bits");
+}
+
+// keys (ascending) of histogram entries >= thr; returns the count (synchronises).
+unsigned hist_compact(sfft2d_ctx* c, const uint32_t* hist, long nkeys, int mode, unsigned thr,
+                      int32_t* keys, unsigned* total_dev, cudaStream_t st) {
+  const int nblk = blocks_for(nkeys);
+  uint32_t* bits = (uint32_t*)ws(c, "hc_bits", words_for(nkeys) * 4);
+  unsigned* cnts = (unsigned*)ws(c, "hc_cnt", (size_t)nblk * 4);
+  k_hist_bits<<<nblk, kCmpThreads, 0, st>>>(hist, nkeys, mode, thr, bits, cnts);
+  post(c, "k_hist_bits");
+  compact(c, bits, cnts, nkeys, 1, keys, 0, total_dev, st);
+  return read_u32(c, total_dev, st);
+}
+
+size_t hist_bytes(long nkeys, int mode) {
+  if (mode == kVoteAdd32) return (size_t)nkeys * 4;
+  return (size_t)((nkeys + 31) / 32) * 32;  // bytes, padded to whole 32-key groups
+}
+
+template <typename T, typename Tin>
+void dense_xhat(sfft2d_ctx* c, const Tin* x, int lgN, const DevTables& tb, cplx<T>* xhat,
+                cudaStream_t st) {
+  ck(launch_dense_fft2d<T, Tin>(x, xhat, lgN, (const cplx<T>*)tb.tw[prec_of<T>()], st),
+     "dense fft2d");
+  c->launches += 2;
+}
+
+// K6 + K7 + output compaction, shared by both algorithms.
+template <typename T, typename Tin>
+void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTables& tb,
+                         const Perm* hp, const Perm* dp, int L, const int32_t* keys, unsigned m,
+                         const unsigned* m_dev, long long k, double gain_floor, double prune_rel,
+                         bool dense, const cplx<T>* xhat, cudaStream_t st, sfft2d_result* res) {
+  using C = cplx<T>;
+  const int P = prec_of<T>();
+  C* med = (C*)ws(c, "med", (size_t)m * sizeof(C));
+  T* mags = (T*)ws(c, "emag", (size_t)m * sizeof(T));
+  uint8_t* alive = (uint8_t*)ws(c, "alive", (size_t)m);
+  unsigned long long* peak = (unsigned long long*)ws(c, "epeak", 16);
+  unsigned* alive_cnt = (unsigned*)ws(c, "ealive", 16);
+  ck(cudaMemsetAsync(peak, 0, 16, st), "memset");
+  ck(cudaMemsetAsync(alive_cnt, 0, 16, st), "memset");
+  long long n_alive;
+  if (dense) {
+    // gain = freq[0]^2 = 1 for the all-pass window (hashing.py:228-246)
+    const bool usable_all = 1.0 >= gain_floor;
+    k_estimate_dense<T><<<grid_for(m), 256, 0, st>>>(xhat, keys, m_dev, usable_all, med, mags,
+                                                      alive, peak);
+    post(c, "k_estimate_dense");
+    n_alive = usable_all ? (long long)m : 0;
+  } else {
+    if (L > kMaxLoops) fail(SFFT2D_ERR_UNSUPPORTED, "more than 64 estimation loops");
+    const int B = 1 << lgB;
+    const size_t BB = (size_t)B * B;
+    C* grids = (C*)ws(c, "est_grids", (size_t)L * BB * sizeof(C));
+    fold_spectrum<T, Tin>(c, x, lgN, lgB, tb, hp, L, grids, st);
+    C* vals = (C*)ws(c, "vals", (size_t)L * m * sizeof(C));
+    uint8_t* usable = (uint8_t*)ws(c, "usable", (size_t)L * m);
+    const T* freq = (const T*)tb.freq[P] + ((size_t)lgB << lgN);
+    k_estimate<T><<<grid_for((long long)m * L), 256, 0, st>>>(
+        grids, L, keys, m_dev, dp, lgN, lgB, freq, (const C*)tb.tw[P], gain_floor, vals, usable,
+        (long)m);
+    post(c, "k_estimate");
+    k_median<T><<<grid_for(m, 128), 128, 0, st>>>(vals, usable, L, (long)m, m_dev, med, mags,
+                                                   alive, alive_cnt, peak);
+    post(c, "k_median");
+    n_alive = read_u32(c, alive_cnt, st);
+  }
+  res->n_candidates = m;
+  if (n_alive == 0) {
+    res->count = 0;
+    res->ordered_by_magnitude = 0;
+    c->res_count = 0;
+    return;
+  }
+  const bool cut = n_alive > k;
+  const int nblk = blocks_for(m);
+  uint32_t* sel = nullptr;
+  if (cut) {
+    sel = (uint32_t*)ws(c, "fsel_bits", words_for(m) * 4);
+    unsigned* scnt = (unsigned*)ws(c, "fsel_cnt", (size_t)nblk * 4);
+    topk_bits<T>(c, mags, (long)m, 1, k, sel, scnt, st);
+  }
+  uint32_t* fb = (uint32_t*)ws(c, "fin_bits", words_for(m) * 4);
+  unsigned* fc = (unsigned*)ws(c, "fin_cnt", (size_t)nblk * 4);
+  k_final_bits<T><<<nblk, kCmpThreads, 0, st>>>(mags, alive, sel, (long)m, peak, prune_rel, fb, fc);
+  post(c, "k_final_bits");
+  int32_t* pos = (int32_t*)ws(c, "fin_pos", (size_t)m * 4);
+  unsigned* tot = (unsigned*)ws(c, "fin_tot", 16);
+  compact(c, fb, fc, (long)m, 1, pos, 0, tot, st);
+  const unsigned count = read_u32(c, tot, st);
+  int64_t* oij = (int64_t*)ws(c, "out_ij", (size_t)count * 16);
+  C* ov = (C*)ws(c, "out_v", (size_t)count * sizeof(C));
+  if (count) {
+    k_gather_out<T><<<grid_for(count), 256, 0, st>>>(pos, tot, keys, med, lgN, oij, ov);
+    post(c, "k_gather_out");
+  }
+  res->count = count;
+  res->ordered_by_magnitude = cut ? 1 : 0;
+  c->res_count = count;
+}
+
+// ------------------------------------------------------------------ ATSFFT
+int nearest_pow2(double v) {
+  long long lo = 1;
+  if (v >= 1) {
+    int e = (int)std::floor(std::log2(v));
+    if (e < 0) e = 0;
+    lo = 1LL << e;
+  }
+  const long long hi = lo * 2;
+  return (int)((v - lo) <= (hi - v) ? lo : hi);
+}
+
+int default_bins(int n, long long k) {
+  if (k < 1) k = 1;
+  const int b = nearest_pow2(std::sqrt((double)(std::min(n, 256)) * (double)k));
+  return std::max(4, std::min(b, n));
+}
+
+int update_bins(int b, double r, const sfft2d_tuner_config& cf, int n) {
+  double v;
+  if (r < cf.delta1) v = b * cf.eps1;
+  else if (r < cf.delta2) v = (double)b;
+  else v = b * (1.0 + cf.eps2);
+  return std::max(4, std::min(nearest_pow2(v), n));
+}
+
+template <typename T, typename Tin>
+void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, int est_loops,
+             const sfft2d_perm* perms, int n_perms, cudaStream_t st, bool do_estimate,
+             sfft2d_result* res, sfft2d_tuner_state* S) {
+  using C = cplx<T>;
+  const int lgN = ilog2(n);
+  const DevTables& tb = find_tables(c, n, cf.window_delta_pass, cf.window_delta_stop);
+  const int max_iters = cf.max_tuning_iters >= 0 ? cf.max_tuning_iters : 2 * std::max(lgN, 1);
+  if (max_iters + 2 > SFFT2D_MAX_HISTORY)
+    fail(SFFT2D_ERR_UNSUPPORTED, "max_tuning_iters too large for the history buffer");
+  if (!is_pow2(cf.b0)) fail(SFFT2D_ERR_CONFIG, "b0 is not a power of 2");
+  const int L = std::max(est_loops, 1);
+  std::vector<Perm> hp(n_perms);
+  for (int i = 0; i < n_perms; ++i) hp[i] = to_perm(perms[i], n);
+  Perm* dp = (Perm*)ws(c, "perms", (size_t)std::max(n_perms, 1) * sizeof(Perm));
+  if (n_perms)
+    ck(cudaMemcpyAsync(dp, hp.data(), (size_t)n_perms * sizeof(Perm), cudaMemcpyHostToDevice, st),
+       "H2D perms");
+  const long nkeys = (long)n * n;
+  const int mode = (4 * (max_iters + 2) <= 255) ? kVoteAdd8 : kVoteAdd32;
+  uint32_t* hist = (uint32_t*)ws(c, "hist", hist_bytes(nkeys, mode));
+  ck(cudaMemsetAsync(hist, 0, hist_bytes(nkeys, mode), st), "memset hist");
+  unsigned* finite = (unsigned*)ws(c, "finite", 16);
+  ck(cudaMemsetAsync(finite, 0, 16, st), "memset");
+  k_check_finite<Tin><<<grid_for(nkeys, 256, kNumSMs * 8), 256, 0, st>>>(x, nkeys, finite);
+  post(c, "k_check_finite");
+  bool finite_checked = false;
+
+  std::memset(S, 0, sizeof(*S));
+  int b = std::max(4, std::min(cf.b0, n));
+  const long long budget = std::max((long long)n * n / 8, 1LL << 16);
+  bool xhat_ready = false;
+  C* xhat = nullptr;
+  T* M = nullptr;
+  unsigned long long* peakM = nullptr;
+  int32_t* maxlist = (int32_t*)ws(c, "maxlist", (size_t)(nkeys / 4 + 64) * 4);
+  int pidx = 0;
+  bool have_votes = false;
+  int vote_passes = 0;
+  bool last_valid = false;
+  int last_b = 0, last_pi = 0;
+  long long last_count = 0;
+
+  auto ensure_xhat = [&](bool need_mags) {
+    if (!xhat_ready) {
+      xhat = (C*)ws(c, "xhat", (size_t)nkeys * sizeof(C));
+      dense_xhat<T, Tin>(c, x, lgN, tb, xhat, st);
+      xhat_ready = true;
+    }
+    if (need_mags && !M) {
+      M = (T*)ws(c, "xmag", (size_t)nkeys * sizeof(T));
+      peakM = (unsigned long long*)ws(c, "xpeak", 16);
+      ck(cudaMemsetAsync(peakM, 0, 16, st), "memset");
+      k_mags<T><<<dim3(grid_for(nkeys, 256, kNumSMs * 8), 1), 256, 0, st>>>(xhat, nkeys, M, peakM);
+      post(c, "k_mags");
+    }
+  };
+
+  auto vote_list = [&](int pi, int lgb, long long count) {
+    const int w = n >> lgb;
+    const long long len = (w == 1) ? 3 : std::min<long long>(w + 2, n);
+    k_vote<<<dim3(grid_for(count * len * len, 256, kNumSMs * 8), 1), 256, 0, st>>>(
+        maxlist, 0, nullptr, (long)count, dp + pi, lgN, lgb, 1, mode, 0, hist);
+    post(c, "k_vote");
+  };
+
+  auto run_pass = [&](int bb) -> long long {
+    if (pidx >= n_perms) fail(SFFT2D_ERR_VALUE, "permutation list exhausted");
+    const int pi = pidx++;
+    const Perm& p = hp[pi];
+    const int lgb = ilog2(bb);
+    const T* lmag;
+    const unsigned long long* peak;
+    if (bb == n) {
+      ensure_xhat(true);
+      T* G = (T*)ws(c, "grid_mag", (size_t)nkeys * sizeof(T));
+      k_permute_grid<T><<<n, 256, (size_t)n * sizeof(T), st>>>(M, lgN, p.s1i, p.s2i, G);
+      post(c, "k_permute_grid");
+      lmag = G;
+      peak = peakM;
+    } else {
+      const size_t BB = (size_t)bb * bb;
+      C* spec = (C*)ws(c, "spec", BB * sizeof(C));
+      fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, &p, 1, spec, st);
+      T* mg = (T*)ws(c, "grid_mag", BB * sizeof(T));
+      unsigned long long* pk = (unsigned long long*)ws(c, "gpeak", 16);
+      ck(cudaMemsetAsync(pk, 0, 16, st), "memset");
+      k_mags<T><<<dim3(grid_for((long long)BB, 256, kNumSMs * 8), 1), 256, 0, st>>>(spec, (long)BB,
+                                                                                   mg, pk);
+      post(c, "k_mags");
+      lmag = mg;
+      peak = pk;
+    }
+    const long long count = local_maxima_dev<T>(c, lmag, lgb, peak, cf.mag_floor, maxlist, st);
+    if (!finite_checked) {
+      finite_checked = true;
+      if (read_u32(c, finite, st)) fail(SFFT2D_ERR_VALUE, "matrix contains NaN or Inf");
+    }
+    last_valid = true;
+    last_b = bb;
+    last_pi = pi;
+    last_count = count;
+    const long long w = n / bb;
+    if (count > 0 && count * (w + 2) * (w + 2) <= budget) {
+      ++vote_passes;
+      have_votes = true;
+      vote_list(pi, lgb, count);
+    }
+    return count;
+  };
+
+  auto push = [&](int bb, long long cnt, double r, bool has) {
+    const int i = S->passes++;
+    S->hist_bins[i] = bb;
+    S->hist_count[i] = cnt;
+    S->hist_ratio[i] = has ? r : NAN;
+    S->hist_has_ratio[i] = has ? 1 : 0;
+  };
+
+  std::map<std::pair<int, long long>, int> seen;
+  bool moved = false;
+  bool converged = false;
+  long long prev = -1;
+  for (int it = 0; it < max_iters; ++it) {
+    const long long cnt = run_pass(b);
+    bool has = false;
+    double r = 0.0;
+    if (prev < 0) {
+      has = false;
+    } else if (prev == 0 && cnt == 0) {
+      push(b, cnt, 0.0, true);
+      converged = true;
+      break;
+    } else {
+      has = true;
+      r = (prev == 0) ? INFINITY : std::fabs(1.0 - (double)cnt / (double)prev);
+    }
+    push(b, cnt, r, has);
+    if (has && cf.delta1 <= r && r < cf.delta2) {
+      converged = true;
+      break;
+    }
+    int& sc = seen[std::make_pair(b, cnt)];
+    ++sc;
+    if (sc >= 3 && moved) {
+      converged = true;
+      break;
+    }
+    prev = cnt;
+    if (has) {
+      const int nb = update_bins(b, r, cf, n);
+      moved = moved || nb != b;
+      b = nb;
+    }
+  }
+  long long maxc = 0;
+  int btop = 0;
+  for (int i = 0; i < S->passes; ++i) {
+    maxc = std::max(maxc, (long long)S->hist_count[i]);
+    btop = std::max(btop, S->hist_bins[i]);
+  }
+  if (S->passes > 0 && maxc > 0) {
+    for (int mult = 2; mult <= 4; mult *= 2) {
+      const long long bc = (long long)mult * btop;
+      if (bc <= n) {
+        const long long cnt = run_pass((int)bc);
+        push((int)bc, cnt, NAN, false);
+        maxc = std::max(maxc, cnt);
+      }
+    }
+  }
+  int bdet = b;
+  if (S->passes > 0) {
+    bdet = 0;
+    for (int i = 0; i < S->passes; ++i) bdet = std::max(bdet, S->hist_bins[i]);
+  }
+  S->converged = converged ? 1 : 0;
+  S->detected_k = maxc;
+  S->b_detect = bdet;
+  S->b_estimate = default_bins(n, maxc);
+  if (!have_votes && last_valid && maxc > 0) {
+    // every pass exceeded the vote budget: fall back to the final pass (tuner.py:228-234)
+    if (last_count > 0) {
+      vote_list(last_pi, ilog2(last_b), last_count);
+      have_votes = true;
+    }
+    vote_passes = 1;
+  }
+  S->vote_passes = vote_passes;
+  int32_t* keys = (int32_t*)ws(c, "keys", (size_t)nkeys * 4);
+  unsigned* kt = (unsigned*)ws(c, "keys_tot", 16);
+
+  if (!do_estimate) {
+    unsigned nv = 0;
+    if (have_votes) {
+      nv = hist_compact(c, hist, nkeys, mode, 1u, keys, kt, st);
+      int32_t* tal = (int32_t*)ws(c, "tallies", (size_t)std::max(nv, 1u) * 4);
+      k_gather_tallies<<<grid_for(nv), 256, 0, st>>>(hist, mode, keys, kt, tal);
+      post(c, "k_gather_tallies");
+    }
+    S->n_votes = nv;
+    S->perms_used = pidx;
+    c->votes_count = nv;
+    c->has_votes = true;
+    return;
+  }
+
+  res->count = 0;
+  res->ordered_by_magnitude = 0;
+  res->n_candidates = 0;
+  c->res_count = 0;
+  if (maxc == 0 || !have_votes) {
+    S->perms_used = pidx;
+    res->perms_used = pidx;
+    return;
+  }
+  const unsigned thr = (unsigned)((std::max(vote_passes, 1) + 1) / 2);
+  const unsigned m = hist_compact(c, hist, nkeys, mode, thr, keys, kt, st);
+  S->n_candidates = m;
+  if (m == 0) {
+    S->perms_used = pidx;
+    res->perms_used = pidx;
+    return;
+  }
+  const long long k = maxc;
+  const int best = S->b_estimate;
+  if (std::max(1LL, 2 * k) > (long long)best * best) {
+    S->perms_used = pidx;
+    fail(SFFT2D_ERR_CONFIG, "d_factor*k = " + std::to_string(std::max(1LL, 2 * k)) +
+                                " exceeds the " + std::to_string(best) + "x" +
+                                std::to_string(best) + " bin budget");
+  }
+  if (pidx + L > n_perms) fail(SFFT2D_ERR_VALUE, "permutation list exhausted");
+  const bool dense = (best == n);
+  if (dense) ensure_xhat(false);
+  estimate_and_select<T, Tin>(c, x, lgN, ilog2(best), tb, hp.data() + pidx, dp + pidx, L, keys, m,
+                              kt, k, cf.gain_floor, cf.prune_rel, dense, xhat, st, res);
+  pidx += L;
+  S->perms_used = pidx;
+  res->perms_used = pidx;
+}
+
+// ------------------------------------------------------------------ SFFT
+template <typename T, typename Tin>
+void run_sfft(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, const sfft2d_perm* perms,
+              cudaStream_t st, sfft2d_result* res) {
+  using C = cplx<T>;
+  const int n = cf.n;
+  const int lgN = ilog2(n);
+  const int b = cf.b_bins;
+  const int L = cf.loops;
+  if (!is_pow2(b) || b > n || n % b) fail(SFFT2D_ERR_CONFIG, "bin count must be a power of 2 dividing n");
+  if (L < 1) fail(SFFT2D_ERR_CONFIG, "loops must be >= 1");
+  if (cf.vote_threshold < 1 || cf.vote_threshold > L) fail(SFFT2D_ERR_CONFIG, "vote_threshold out of range");
+  if (L > kMaxLoops) fail(SFFT2D_ERR_UNSUPPORTED, "more than 64 loops");
+  const long long num = std::max(1LL, (long long)cf.d_factor * cf.k);
+  const int lgb = ilog2(b);
+  const long BB = (long)b * b;
+  if (num > BB) fail(SFFT2D_ERR_CONFIG, "d_factor*k exceeds the bin budget");
+  const DevTables& tb = find_tables(c, n, cf.window_delta_pass, cf.window_delta_stop);
+  std::vector<Perm> hp(2 * L);
+  for (int i = 0; i < 2 * L; ++i) hp[i] = to_perm(perms[i], n);
+  Perm* dp = (Perm*)ws(c, "perms", (size_t)2 * L * sizeof(Perm));
+  ck(cudaMemcpyAsync(dp, hp.data(), (size_t)2 * L * sizeof(Perm), cudaMemcpyHostToDevice, st),
+     "H2D perms");
+  const long nkeys = (long)n * n;
+  unsigned* finite = (unsigned*)ws(c, "finite", 16);
+  ck(cudaMemsetAsync(finite, 0, 16, st), "memset");
+  k_check_finite<Tin><<<grid_for(nkeys, 256, kNumSMs * 8), 256, 0, st>>>(x, nkeys, finite);
+  post(c, "k_check_finite");
+
+  // location loops: L grids from one read of x, top-num bins per grid
+  C* grids = (C*)ws(c, "loc_grids", (size_t)L * BB * sizeof(C));
+  fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, hp.data(), L, grids, st);
+  T* mags = (T*)ws(c, "loc_mags", (size_t)L * BB * sizeof(T));
+  k_mags<T><<<dim3(grid_for(BB, 256, 1024), L), 256, 0, st>>>(grids, BB, mags, nullptr);
+  post(c, "k_mags");
+  int32_t* bins = (int32_t*)ws(c, "loc_bins", (size_t)L * num * 4);
+  if (num >= BB) {
+    k_iota_segments<<<grid_for(BB * L), 256, 0, st>>>(bins, BB, L);
+    post(c, "k_iota_segments");
+  } else {
+    const int nblk = blocks_for(BB);
+    uint32_t* sb = (uint32_t*)ws(c, "loc_selbits", (size_t)L * words_for(BB) * 4);
+    unsigned* sc = (unsigned*)ws(c, "loc_selcnt", (size_t)L * nblk * 4);
+    topk_bits<T>(c, mags, BB, L, num, sb, sc, st);
+    unsigned* tots = (unsigned*)ws(c, "loc_tot", (size_t)L * 4 + 16);
+    compact(c, sb, sc, BB, L, bins, (long)num, tots, st);
+  }
+  if (read_u32(c, finite, st)) fail(SFFT2D_ERR_VALUE, "matrix contains NaN or Inf");
+
+  // votes with per-loop dedup (bit per loop), threshold
+  uint32_t* hist = (uint32_t*)ws(c, "hist", hist_bytes(nkeys, kVoteAdd8));
+  ck(cudaMemsetAsync(hist, 0, hist_bytes(nkeys, kVoteAdd8), st), "memset hist");
+  const int w = n / b;
+  const long long len = (w == 1) ? 3 : std::min<long long>(w + 2, n);
+  const long long per = num * len * len;
+  int cmode = kVoteOrBit;
+  const uint32_t* chist = hist;
+  if (L <= 8) {
+    k_vote<<<dim3(grid_for(per, 256, kNumSMs * 8), L), 256, 0, st>>>(bins, (long)num, nullptr, (long)num, dp,
+                                                                   lgN, lgb, 1, kVoteOrBit, 0, hist);
+    post(c, "k_vote");
+  } else {
+    uint32_t* counts = (uint32_t*)ws(c, "hist_cnt", hist_bytes(nkeys, kVoteAdd8));
+    ck(cudaMemsetAsync(counts, 0, hist_bytes(nkeys, kVoteAdd8), st), "memset");
+    const long nw = (long)(hist_bytes(nkeys, kVoteAdd8) / 4);
+    for (int g0 = 0; g0 < L; g0 += 8) {
+      const int g = std::min(8, L - g0);
+      k_vote<<<dim3(grid_for(per, 256, kNumSMs * 8), g), 256, 0, st>>>(
+          bins + (size_t)g0 * num, (long)num, nullptr, (long)num, dp + g0, lgN, lgb, 1, kVoteOrBit,
+          0, hist);
+      post(c, "k_vote");
+      k_mask_to_counts<<<grid_for(nw, 256, kNumSMs * 8), 256, 0, st>>>(hist, counts, nw);
+      post(c, "k_mask_to_counts");
+    }
+    cmode = kVoteAdd8;
+    chist = counts;
+  }
+  int32_t* keys = (int32_t*)ws(c, "keys", (size_t)nkeys * 4);
+  unsigned* kt = (unsigned*)ws(c, "keys_tot", 16);
+  const unsigned m = hist_compact(c, chist, nkeys, cmode, (unsigned)cf.vote_threshold, keys, kt, st);
+  res->count = 0;
+  res->ordered_by_magnitude = 0;
+  res->n_candidates = m;
+  res->perms_used = 2 * L;
+  c->res_count = 0;
+  if (m == 0) return;
+  estimate_and_select<T, Tin>(c, x, lgN, lgb, tb, hp.data() + L, dp + L, L, keys, m, kt, cf.k,
+                              cf.gain_floor, cf.prune_rel, false, (const C*)nullptr, st, res);
+}
+
+template <typename F>
+void dispatch(int x_dtype, int prec, F&& f) {
+  if (x_dtype != SFFT2D_C64 && x_dtype != SFFT2D_C128) fail(SFFT2D_ERR_VALUE, "unknown x_dtype");
+  if (prec != SFFT2D_FP32 && prec != SFFT2D_FP64) fail(SFFT2D_ERR_VALUE, "unknown precision");
+  if (prec == SFFT2D_FP64) {
+    if (x_dtype == SFFT2D_C64) f(double(), float2());
+    else f(double(), double2());
+  } else {
+    if (x_dtype == SFFT2D_C64) f(float(), float2());
+    else f(float(), double2());
+  }
+}
+
+template <typename F>
+void dispatch_prec(int prec, F&& f) {
+  if (prec == SFFT2D_FP64) f(double());
+  else if (prec == SFFT2D_FP32) f(float());
+  else fail(SFFT2D_ERR_VALUE, "unknown precision");
+}
+
+const void* stage_input(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host, int n,
+                        cudaStream_t st) {
+  if (!x_on_host) return x;
+  const size_t bytes = (size_t)n * n * (x_dtype == SFFT2D_C64 ? 8 : 16);
+  void* d = ws(c, "x_in", bytes);
+  ck(cudaMemcpyAsync(d, x, bytes, cudaMemcpyHostToDevice, st), "H2D x");
+  return d;
+}
+
+template <typename Fn>
+int guarded(sfft2d_ctx* c, Fn&& fn) {
+  if (!c) return SFFT2D_ERR_STATE;
+  try {
+    c->err.clear();
+    ck(cudaSetDevice(c->device), "cudaSetDevice");
+    fn();
+    return SFFT2D_OK;
+  } catch (const SfftError& e) {
+    c->err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    c->err = e.what();
+    return SFFT2D_ERR_CUDA;
+  }
+}
+
+void check_side(int n) {
+  if (!is_pow2(n)) fail(SFFT2D_ERR_VALUE, "side " + std::to_string(n) + " is not a power of 2");
+  if (n < 4) fail(SFFT2D_ERR_UNSUPPORTED, "side must be >= 4");
+  if ((long long)n * n > (1LL << 30)) fail(SFFT2D_ERR_UNSUPPORTED, "side too large");
+}
+
+}  // namespace
+
+// ====================================================================== ABI
+extern "C" {
+
+int sfft2d_abi_version(void) { return SFFT2D_ABI_VERSION; }
+
+int sfft2d_ctx_create(int device, sfft2d_ctx** out) {
+  if (!out) return SFFT2D_ERR_VALUE;
+  *out = nullptr;
+  sfft2d_ctx* c = new sfft2d_ctx();
+  c->device = device;
+  int rc = guarded(c, [&] {
+    ck(cudaMallocHost(&c->pinned, 4096), "cudaMallocHost");
+    allow_all_T<float>();
+    allow_all_T<double>();
+  });
+  if (rc != SFFT2D_OK) {
+    fprintf(stderr, "sfft2d_ctx_create: %s\n", c->err.c_str());
+    delete c;
+    return rc;
+  }
+  *out = c;
+  return SFFT2D_OK;
+}
+
+void sfft2d_ctx_destroy(sfft2d_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (auto& kv : c->bufs)
+    if (kv.second.first) cudaFree(kv.second.first);
+  for (auto& t : c->tables)
+    for (int p = 0; p < 2; ++p) {
+      cudaFree(t.space[p]);
+      cudaFree(t.freq[p]);
+      cudaFree(t.tw[p]);
+    }
+  if (c->pinned) cudaFreeHost(c->pinned);
+  delete c;
+}
+
+const char* sfft2d_ctx_last_error(const sfft2d_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int sfft2d_ctx_set_tables(sfft2d_ctx* c, int n, double dpass, double dstop, const double* space,
+                          const double* freq, const double* twiddle) {
+  return guarded(c, [&] {
+    check_side(n);
+    if (!space || !freq || !twiddle) fail(SFFT2D_ERR_VALUE, "null table");
+    for (auto& t : c->tables)
+      if (t.n == n && t.dpass == dpass && t.dstop == dstop) return;  // already registered
+    DevTables t;
+    t.n = n;
+    t.lgn = ilog2(n);
+    t.dpass = dpass;
+    t.dstop = dstop;
+    const size_t rows = (size_t)(t.lgn + 1) * n;
+    std::vector<float> f32(std::max(rows, (size_t)2 * n));
+    auto up = [&](const double* src, size_t cnt, void** d64, void** d32) {
+      ck(cudaMalloc(d64, cnt * 8), "cudaMalloc");
+      ck(cudaMemcpy(*d64, src, cnt * 8, cudaMemcpyHostToDevice), "H2D table");
+      for (size_t i = 0; i < cnt; ++i) f32[i] = (float)src[i];
+      ck(cudaMalloc(d32, cnt * 4), "cudaMalloc");
+      ck(cudaMemcpy(*d32, f32.data(), cnt * 4, cudaMemcpyHostToDevice), "H2D table");
+    };
+    up(space, rows, &t.space[SFFT2D_FP64], &t.space[SFFT2D_FP32]);
+    up(freq, rows, &t.freq[SFFT2D_FP64], &t.freq[SFFT2D_FP32]);
+    up(twiddle, (size_t)2 * n, &t.tw[SFFT2D_FP64], &t.tw[SFFT2D_FP32]);
+    c->tables.push_back(t);
+  });
+}
+
+int sfft2d_sfft(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host,
+                const sfft2d_sfft_config* cfg, const sfft2d_perm* perms, int precision,
+                void* stream, sfft2d_result* res) {
+  return guarded(c, [&] {
+    if (!cfg || !perms || !res || !x) fail(SFFT2D_ERR_VALUE, "null argument");
+    check_side(cfg->n);
+    cudaStream_t st = (cudaStream_t)stream;
+    std::memset(res, 0, sizeof(*res));
+    c->launches = 0;
+    c->has_res = false;
+    const void* xd = stage_input(c, x, x_dtype, x_on_host, cfg->n, st);
+    dispatch(x_dtype, precision, [&](auto t, auto tin) {
+      using T = decltype(t);
+      using Tin = decltype(tin);
+      run_sfft<T, Tin>(c, (const Tin*)xd, *cfg, perms, st, res);
+    });
+    res->precision = precision;
+    res->gpu_launches = c->launches;
+    c->res_prec = precision;
+    c->has_res = true;
+  });
+}
+
+int sfft2d_atsfft(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host, int n,
+                  const sfft2d_tuner_config* cfg, int est_loops, const sfft2d_perm* perms,
+                  int n_perms, int precision, void* stream, sfft2d_result* res,
+                  sfft2d_tuner_state* state) {
+  return guarded(c, [&] {
+    if (!cfg || !res || !state || !x || (n_perms > 0 && !perms)) fail(SFFT2D_ERR_VALUE, "null argument");
+    check_side(n);
+    cudaStream_t st = (cudaStream_t)stream;
+    std::memset(res, 0, sizeof(*res));
+    c->launches = 0;
+    c->has_res = false;
+    const void* xd = stage_input(c, x, x_dtype, x_on_host, n, st);
+    dispatch(x_dtype, precision, [&](auto t, auto tin) {
+      using T = decltype(t);
+      using Tin = decltype(tin);
+      run_ats<T, Tin>(c, (const Tin*)xd, n, *cfg, est_loops, perms, n_perms, st, true, res, state);
+    });
+    res->precision = precision;
+    res->gpu_launches = c->launches;
+    c->res_prec = precision;
+    c->has_res = true;
+  });
+}
+
+int sfft2d_detect_sparsity(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host, int n,
+                           const sfft2d_tuner_config* cfg, const sfft2d_perm* perms, int n_perms,
+                           int precision, void* stream, sfft2d_tuner_state* state) {
+  return guarded(c, [&] {
+    if (!cfg || !state || !x || (n_perms > 0 && !perms)) fail(SFFT2D_ERR_VALUE, "null argument");
+    check_side(n);
+    cudaStream_t st = (cudaStream_t)stream;
+    c->launches = 0;
+    c->has_votes = false;
+    const void* xd = stage_input(c, x, x_dtype, x_on_host, n, st);
+    sfft2d_result dummy;
+    std::memset(&dummy, 0, sizeof(dummy));
+    dispatch(x_dtype, precision, [&](auto t, auto tin) {
+      using T = decltype(t);
+      using Tin = decltype(tin);
+      run_ats<T, Tin>(c, (const Tin*)xd, n, *cfg, 0, perms, n_perms, st, false, &dummy, state);
+    });
+  });
+}
+
+int sfft2d_fetch_result(sfft2d_ctx* c, int64_t* ij, void* values, int dst_on_host, void* stream) {
+  return guarded(c, [&] {
+    if (!c->has_res) fail(SFFT2D_ERR_STATE, "no transform result to fetch");
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = (size_t)c->res_count;
+    if (n == 0) return;
+    const size_t vb = n * (c->res_prec == SFFT2D_FP64 ? 16 : 8);
+    if (ij) ck(cudaMemcpyAsync(ij, c->bufs["out_ij"].first, n * 16, cudaMemcpyDefault, st), "copy ij");
+    if (values) ck(cudaMemcpyAsync(values, c->bufs["out_v"].first, vb, cudaMemcpyDefault, st), "copy v");
+    if (dst_on_host) ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+int sfft2d_fetch_votes(sfft2d_ctx* c, int32_t* keys, int32_t* tallies, int dst_on_host,
+                       void* stream) {
+  return guarded(c, [&] {
+    if (!c->has_votes) fail(SFFT2D_ERR_STATE, "no detection votes to fetch");
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t n = (size_t)c->votes_count;
+    if (n == 0) return;
+    if (keys) ck(cudaMemcpyAsync(keys, c->bufs["keys"].first, n * 4, cudaMemcpyDefault, st), "copy keys");
+    if (tallies)
+      ck(cudaMemcpyAsync(tallies, c->bufs["tallies"].first, n * 4, cudaMemcpyDefault, st), "copy tallies");
+    if (dst_on_host) ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+int sfft2d_binned_spectrum(sfft2d_ctx* c, const void* x, int x_dtype, int n, int b,
+                           const sfft2d_perm* perms, int nloops, double dpass, double dstop,
+                           int precision, void* out, void* stream) {
+  return guarded(c, [&] {
+    check_side(n);
+    if (!is_pow2(b) || b > n || b < 4) fail(SFFT2D_ERR_VALUE, "bin count must be a power of 2 in [4, n]");
+    if (nloops < 1 || !perms || !x || !out) fail(SFFT2D_ERR_VALUE, "bad arguments");
+    const DevTables& tb = find_tables(c, n, dpass, dstop);
+    std::vector<Perm> hp(nloops);
+    for (int i = 0; i < nloops; ++i) hp[i] = to_perm(perms[i], n);
+    cudaStream_t st = (cudaStream_t)stream;
+    c->launches = 0;
+    dispatch(x_dtype, precision, [&](auto t, auto tin) {
+      using T = decltype(t);
+      using Tin = decltype(tin);
+      fold_spectrum<T, Tin>(c, (const Tin*)x, ilog2(n), ilog2(b), tb, hp.data(), nloops,
+                            (cplx<T>*)out, st);
+    });
+  });
+}
+
+int sfft2d_fft2d(sfft2d_ctx* c, void* grids, int b, int count, int n_table, int precision,
+                 void* stream) {
+  return guarded(c, [&] {
+    if (!is_pow2(b) || b < 2 || b > n_table) fail(SFFT2D_ERR_VALUE, "bad grid side");
+    const DevTables& tb = find_twiddles(c, n_table);
+    cudaStream_t st = (cudaStream_t)stream;
+    dispatch_prec(precision, [&](auto t) {
+      using T = decltype(t);
+      ck(launch_fft2d<T>((cplx<T>*)grids, ilog2(b), count, (const cplx<T>*)tb.tw[prec_of<T>()],
+                         tb.lgn, st),
+         "fft2d");
+    });
+  });
+}
+
+int sfft2d_local_maxima(sfft2d_ctx* c, const void* grid, int b, double mag_floor, int precision,
+                        int64_t* count, int32_t* out_flat, int64_t capacity, void* stream) {
+  return guarded(c, [&] {
+    if (!is_pow2(b) || b < 4) fail(SFFT2D_ERR_VALUE, "bin grid must be at least 4x4 and a power of 2");
+    cudaStream_t st = (cudaStream_t)stream;
+    dispatch_prec(precision, [&](auto t) {
+      using T = decltype(t);
+      const long BB = (long)b * b;
+      T* mg = (T*)ws(c, "api_mag", BB * sizeof(T));
+      unsigned long long* pk = (unsigned long long*)ws(c, "api_peak", 16);
+      ck(cudaMemsetAsync(pk, 0, 16, st), "memset");
+      k_mags<T><<<dim3(grid_for(BB, 256, 1024), 1), 256, 0, st>>>((const cplx<T>*)grid, BB, mg, pk);
+      post(c, "k_mags");
+      int32_t* tmp = (int32_t*)ws(c, "api_lm", (size_t)(BB / 4 + 64) * 4);
+      const long long cnt = local_maxima_dev<T>(c, mg, ilog2(b), pk, mag_floor, tmp, st);
+      if (count) *count = cnt;
+      const long long cp = std::min<long long>(cnt, capacity);
+      if (out_flat && cp > 0)
+        ck(cudaMemcpyAsync(out_flat, tmp, (size_t)cp * 4, cudaMemcpyDefault, st), "copy");
+    });
+  });
+}
+
+int sfft2d_top_bins(sfft2d_ctx* c, const void* grids, int b, int nseg, int64_t num, int precision,
+                    int32_t* out_flat, void* stream) {
+  return guarded(c, [&] {
+    if (!is_pow2(b) || b < 1 || nseg < 1 || num < 1 || !out_flat) fail(SFFT2D_ERR_VALUE, "bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    dispatch_prec(precision, [&](auto t) {
+      using T = decltype(t);
+      const long BB = (long)b * b;
+      if (num > BB) fail(SFFT2D_ERR_VALUE, "num exceeds the number of bins");
+      T* mg = (T*)ws(c, "api_mag", (size_t)nseg * BB * sizeof(T));
+      k_mags<T><<<dim3(grid_for(BB, 256, 1024), nseg), 256, 0, st>>>((const cplx<T>*)grids, BB, mg,
+                                                                     nullptr);
+      post(c, "k_mags");
+      if (num >= BB) {
+        k_iota_segments<<<grid_for(BB * nseg), 256, 0, st>>>(out_flat, BB, nseg);
+        post(c, "k_iota_segments");
+        return;
+      }
+      const int nblk = blocks_for(BB);
+      uint32_t* sb = (uint32_t*)ws(c, "api_selbits", (size_t)nseg * words_for(BB) * 4);
+      unsigned* sc = (unsigned*)ws(c, "api_selcnt", (size_t)nseg * nblk * 4);
+      topk_bits<T>(c, mg, BB, nseg, num, sb, sc, st);
+      unsigned* tots = (unsigned*)ws(c, "api_tot", (size_t)nseg * 4 + 16);
+      compact(c, sb, sc, BB, nseg, out_flat, (long)num, tots, st);
+    });
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,85 @@
+// Shared device helpers for the sm_100a sparse-FFT kernels.
+//
+// Complex numbers are stored as float2 / double2 (interleaved re, im) — the
+// same byte layout as numpy complex64 / complex128, so images cross the C-ABI
+// without repacking.  "T" is the arithmetic type of a kernel (float or double);
+// "Tin" is the element type of the input image (float2 or double2).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sfft {
+
+constexpr int kNumSMs = 148;  // B200
+
+template <typename T> struct CT;
+template <> struct CT<float>  { using type = float2; };
+template <> struct CT<double> { using type = double2; };
+template <typename T> using cplx = typename CT<T>::type;
+
+template <typename T> __host__ __device__ __forceinline__ cplx<T> mk(T re, T im) {
+  cplx<T> z; z.x = re; z.y = im; return z;
+}
+template <typename C> __host__ __device__ __forceinline__ C cadd(C a, C b) {
+  C z; z.x = a.x + b.x; z.y = a.y + b.y; return z;
+}
+template <typename C> __host__ __device__ __forceinline__ C csub(C a, C b) {
+  C z; z.x = a.x - b.x; z.y = a.y - b.y; return z;
+}
+template <typename C> __host__ __device__ __forceinline__ C cmul(C a, C b) {
+  C z; z.x = a.x * b.x - a.y * b.y; z.y = a.x * b.y + a.y * b.x; return z;
+}
+template <typename C, typename T> __host__ __device__ __forceinline__ C cscale(C a, T s) {
+  C z; z.x = a.x * s; z.y = a.y * s; return z;
+}
+
+// widen / narrow an input element to the arithmetic type
+template <typename T, typename Tin> __device__ __forceinline__ cplx<T> load_c(const Tin* p) {
+  Tin v = *p;
+  return mk<T>((T)v.x, (T)v.y);
+}
+
+// |z| the way numpy's np.abs(complex) computes it (hypot, no overflow)
+__device__ __forceinline__ double cabs_(double2 z) { return hypot(z.x, z.y); }
+__device__ __forceinline__ float  cabs_(float2 z)  { return hypotf(z.x, z.y); }
+
+// order-preserving unsigned key of a non-negative (or any) floating value:
+// a < b  <=>  key(a) < key(b)   (NaN-free inputs)
+__device__ __forceinline__ uint64_t fkey(double v) {
+  uint64_t u = (uint64_t)__double_as_longlong(v);
+  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+__device__ __forceinline__ uint64_t fkey(float v) { return fkey((double)v); }
+__device__ __forceinline__ double fkey_inv(uint64_t k) {
+  uint64_t u = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)u);
+}
+
+__device__ __forceinline__ unsigned bitrev(unsigned v, int bits) {
+  return bits ? (__brev(v) >> (32 - bits)) : 0u;
+}
+
+// one permutation as the kernels consume it (see hashing.py:45-80)
+struct Perm {
+  uint32_t s1, s2, t1, t2, s1i, s2i;
+};
+
+// up to kMaxFoldLoops permutations passed by value to a fold launch
+constexpr int kMaxFoldLoops = 8;
+struct PermPack {
+  Perm p[kMaxFoldLoops];
+};
+
+// block-wide inclusive scan helper over 32-bit counts (blockDim <= 1024)
+__device__ __forceinline__ unsigned warp_incl_scan(unsigned v) {
+  const unsigned lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    unsigned t = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= (unsigned)o) v += t;
+  }
+  return v;
+}
+
+}  // namespace sfft

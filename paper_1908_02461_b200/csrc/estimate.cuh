@@ -1,0 +1,194 @@
+// K6 / K7 — estimation and median-of-loops.
+//   K6 replaces _estimate_arrays (engine.py:163-177): per coordinate (i, j) and
+//      loop l:  q = sigma*i mod N,  u = floor((q + floor(w/2)) / w),
+//      gain = F[(q_i - w u_i) mod N] * F[(q_j - w u_j) mod N],
+//      val  = Z_l[u_i mod B, u_j mod B] * exp(-2 pi i ((tau1 i + tau2 j) mod N)/N) / gain
+//      usable iff |gain| >= gain_floor (else 0 and excluded from the median).
+//      The phase factor is tw[(tau1 i + tau2 j) mod N] from the same host table
+//      (identical numpy expression, so identical values).
+//   K7 replaces _median_select (engine.py:228-253): componentwise nan-median
+//      over the usable loops (even count -> mean of the two middle values),
+//      coordinates with no usable loop dropped, then top-k by |median| with
+//      lexicographic (i, j) tie-break (select.cuh), then prune >= rel * max.
+#pragma once
+#include "common.cuh"
+#include "select.cuh"
+
+namespace sfft {
+
+constexpr int kMaxLoops = 64;
+
+template <typename T>
+__global__ void k_estimate(const cplx<T>* __restrict__ spec, int nloops, const int32_t* __restrict__ keys,
+                           const unsigned* __restrict__ m_dev, const Perm* __restrict__ perms,
+                           int lgN, int lgB, const T* __restrict__ freq,
+                           const cplx<T>* __restrict__ tw, double gain_floor,
+                           cplx<T>* __restrict__ vals, uint8_t* __restrict__ usable, long stride) {
+  using C = cplx<T>;
+  const long m = *m_dev;
+  const int N = 1 << lgN, B = 1 << lgB;
+  const unsigned maskN = (unsigned)N - 1u, maskB = (unsigned)B - 1u;
+  const int lgw = lgN - lgB;
+  const unsigned hw = (unsigned)((1 << lgw) / 2);
+  const long total = m * nloops;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
+       e += (long)gridDim.x * blockDim.x) {
+    const int l = (int)(e / m);
+    const long idx = e - (long)l * m;
+    const Perm p = perms[l];
+    const unsigned key = (unsigned)keys[idx];
+    const unsigned i = key >> lgN, j = key & maskN;
+    const unsigned qi = (p.s1 * i) & maskN, qj = (p.s2 * j) & maskN;
+    const unsigned ui = (qi + hw) >> lgw, uj = (qj + hw) >> lgw;
+    const unsigned oi = (qi - (ui << lgw)) & maskN, oj = (qj - (uj << lgw)) & maskN;
+    const T gain = freq[oi] * freq[oj];
+    const C ph = tw[(p.t1 * i + p.t2 * j) & maskN];
+    const C z = spec[(size_t)l * B * B + (size_t)(ui & maskB) * B + (uj & maskB)];
+    const bool ok = (double)fabs(gain) >= gain_floor;
+    C v = cmul(z, ph);
+    if (ok) { v.x = v.x / gain; v.y = v.y / gain; }
+    else v = mk<T>(0, 0);
+    vals[(size_t)l * stride + idx] = v;
+    usable[(size_t)l * stride + idx] = ok ? 1 : 0;
+  }
+}
+
+// B == N estimation shortcut: the all-pass window has gain 1 at every
+// coordinate (freq = delta, offset 0) and Z_l[sigma*i, sigma*j] * phase_l
+// equals x_hat[i, j] for every permutation (Lemma 1), so every loop's
+// estimate is x_hat[i, j]: read it once.
+template <typename T>
+__global__ void k_estimate_dense(const cplx<T>* __restrict__ xhat, const int32_t* __restrict__ keys,
+                                 const unsigned* __restrict__ m_dev, bool usable_all,
+                                 cplx<T>* __restrict__ med, T* __restrict__ mags,
+                                 uint8_t* __restrict__ alive, unsigned long long* __restrict__ peak) {
+  const long m = *m_dev;
+  unsigned long long best = 0ull;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < m;
+       i += (long)gridDim.x * blockDim.x) {
+    const cplx<T> v = xhat[(uint32_t)keys[i]];
+    med[i] = v;
+    alive[i] = usable_all ? 1 : 0;
+    const T a = usable_all ? cabs_(v) : (T)-1;
+    mags[i] = a;
+    if (usable_all) {
+      const unsigned long long k = fkey(a);
+      best = k > best ? k : best;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+    best = t > best ? t : best;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(peak, best);
+}
+
+template <typename T>
+__device__ __forceinline__ void isort(T* a, int n) {
+  for (int i = 1; i < n; ++i) {
+    const T v = a[i];
+    int j = i - 1;
+    while (j >= 0 && a[j] > v) { a[j + 1] = a[j]; --j; }
+    a[j + 1] = v;
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ T median_sorted(const T* a, int n) {
+  return (n & 1) ? a[n / 2] : (a[n / 2 - 1] + a[n / 2]) / (T)2;
+}
+
+// componentwise median over usable loops; dead coordinates get mag = -1
+template <typename T>
+__global__ void k_median(const cplx<T>* __restrict__ vals, const uint8_t* __restrict__ usable,
+                         int nloops, long stride, const unsigned* __restrict__ m_dev,
+                         cplx<T>* __restrict__ med, T* __restrict__ mags,
+                         uint8_t* __restrict__ alive, unsigned* __restrict__ alive_count,
+                         unsigned long long* __restrict__ peak) {
+  const long m = *m_dev;
+  unsigned cnt_alive = 0;
+  unsigned long long best = 0ull;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < m;
+       i += (long)gridDim.x * blockDim.x) {
+    T re[kMaxLoops], im[kMaxLoops];
+    int c = 0;
+    for (int l = 0; l < nloops; ++l) {
+      if (usable[(size_t)l * stride + i]) {
+        const cplx<T> v = vals[(size_t)l * stride + i];
+        re[c] = v.x;
+        im[c] = v.y;
+        ++c;
+      }
+    }
+    if (c == 0) {
+      alive[i] = 0;
+      mags[i] = (T)-1;
+      med[i] = mk<T>(0, 0);
+      continue;
+    }
+    isort(re, c);
+    isort(im, c);
+    const cplx<T> v = mk<T>(median_sorted(re, c), median_sorted(im, c));
+    med[i] = v;
+    alive[i] = 1;
+    const T a = cabs_(v);
+    mags[i] = a;
+    ++cnt_alive;
+    const unsigned long long k = fkey(a);
+    best = k > best ? k : best;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    cnt_alive += __shfl_xor_sync(0xffffffffu, cnt_alive, o);
+    unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+    best = t > best ? t : best;
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (cnt_alive) atomicAdd(alive_count, cnt_alive);
+    atomicMax(peak, best);
+  }
+}
+
+// Final keep-bitmask: alive, selected by top-k (sel bits, or all when no cut),
+// and |med| >= prune_rel * peak (when prune_rel > 0).
+template <typename T>
+__global__ void k_final_bits(const T* __restrict__ mags, const uint8_t* __restrict__ alive,
+                             const uint32_t* __restrict__ sel_bits, long m,
+                             const unsigned long long* __restrict__ peak, double prune_rel,
+                             uint32_t* __restrict__ bits, unsigned* __restrict__ blk_counts) {
+  __shared__ unsigned s_warp[32];
+  const long w = (long)blockIdx.x * kCmpWords + threadIdx.x;
+  const long wps = words_for(m);
+  const double floor_v = prune_rel > 0 ? prune_rel * fkey_inv(*peak) : -1.0;
+  uint32_t word = 0;
+  if (w < wps) {
+    const uint32_t sel = sel_bits ? sel_bits[w] : 0xffffffffu;
+    for (int b = 0; b < 32; ++b) {
+      const long i = w * 32 + b;
+      if (i < m && alive[i] && ((sel >> b) & 1u)) {
+        if (prune_rel <= 0 || (double)mags[i] >= floor_v) word |= 1u << b;
+      }
+    }
+    bits[w] = word;
+  }
+  const unsigned pre = block_excl_scan256(__popc(word), s_warp);
+  if (threadIdx.x == kCmpThreads - 1) blk_counts[blockIdx.x] = pre + __popc(word);
+}
+
+// gather the kept entries (positions from compaction) into (i, j) and values
+template <typename T>
+__global__ void k_gather_out(const int32_t* __restrict__ pos, const unsigned* __restrict__ count,
+                             const int32_t* __restrict__ keys, const cplx<T>* __restrict__ med,
+                             int lgN, int64_t* __restrict__ out_ij, cplx<T>* __restrict__ out_v) {
+  const long n = *count;
+  const unsigned maskN = (1u << lgN) - 1u;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
+       i += (long)gridDim.x * blockDim.x) {
+    const int32_t p = pos[i];
+    const unsigned key = (unsigned)keys[p];
+    out_ij[2 * i] = key >> lgN;
+    out_ij[2 * i + 1] = key & maskN;
+    out_v[i] = med[p];
+  }
+}
+
+}  // namespace sfft

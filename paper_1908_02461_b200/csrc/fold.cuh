@@ -1,0 +1,297 @@
+// K1 — fused permute + window + fold into B x B buckets.
+// Replaces the gather/window/reshape-sum of binned_spectrum
+// (/root/reference/pkg/src/sfft2d/hashing.py:308-337).
+//
+// Restatement used here.  The reference gathers
+//   block[u, v] = g[u] g[v] x[s1*u + t1, s2*v + t2]    (u, v over the support)
+// and folds u, v modulo B.  Substituting r = s1*u + t1 (a bijection mod N)
+// and using B | N, the bucket of row r is  pi1(r mod B)  with
+//   pi1(rho) = s1^-1 * (rho - t1) mod B,
+// so with natural-order weights  wr[r] = g[s1^-1 (r - t1) mod N]  (zero outside
+// the window support) the folded grid is
+//   y[pi1(rho), pi2(kappa)] = sum_{r = rho mod B} sum_{c = kappa mod B} wr[r] wc[c] x[r, c].
+// The image is therefore streamed in natural (coalesced) row-major order, rows
+// with zero weight are skipped, and NL permutations (hash loops) share one read.
+//
+// Work split: CTA (kappa-tile, rho, z).  Threads own CPT adjacent columns of a
+// tile of TW columns; a CTA visits rows rho + j*B for j in its alias chunk z
+// and every column congruent to its tile.  Row weights for the chunk are
+// staged in shared memory; per column the row sum is accumulated first, then
+// scaled by the column weight (2*NL FMA per complex element).  With Z > 1 the
+// CTAs write natural-order partials [Z][NL][B][B] that a second kernel sums in
+// a fixed order (deterministic, no float atomics) while applying pi1/pi2 —
+// fused with the whole 2D FFT when the grid fits one CTA's shared memory.
+#pragma once
+#include "common.cuh"
+#include "fft.cuh"
+
+namespace sfft {
+
+constexpr int kFoldThreads = 256;
+constexpr int kFoldMaxRows = 256;  // row aliases per chunk (smem weight tile)
+
+template <typename Tin, typename T, int CPT> struct ColLoad;
+template <> struct ColLoad<float2, float, 1> {
+  __device__ static void ld(const float2* p, float2* v) { v[0] = __ldg(p); }
+};
+template <> struct ColLoad<float2, double, 1> {
+  __device__ static void ld(const float2* p, double2* v) {
+    float2 a = __ldg(p); v[0] = make_double2(a.x, a.y);
+  }
+};
+template <> struct ColLoad<double2, double, 1> {
+  __device__ static void ld(const double2* p, double2* v) { v[0] = __ldg(p); }
+};
+template <> struct ColLoad<double2, float, 1> {
+  __device__ static void ld(const double2* p, float2* v) {
+    double2 a = __ldg(p); v[0] = make_float2((float)a.x, (float)a.y);
+  }
+};
+template <> struct ColLoad<float2, float, 2> {
+  __device__ static void ld(const float2* p, float2* v) {
+    float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = make_float2(a.x, a.y); v[1] = make_float2(a.z, a.w);
+  }
+};
+template <> struct ColLoad<float2, double, 2> {
+  __device__ static void ld(const float2* p, double2* v) {
+    float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = make_double2(a.x, a.y); v[1] = make_double2(a.z, a.w);
+  }
+};
+template <> struct ColLoad<double2, double, 2> {
+  __device__ static void ld(const double2* p, double2* v) { v[0] = __ldg(p); v[1] = __ldg(p + 1); }
+};
+template <> struct ColLoad<double2, float, 2> {
+  __device__ static void ld(const double2* p, float2* v) {
+    double2 a = __ldg(p), b = __ldg(p + 1);
+    v[0] = make_float2((float)a.x, (float)a.y); v[1] = make_float2((float)b.x, (float)b.y);
+  }
+};
+
+struct FoldGeom {
+  int lgN, lgB;
+  int TW;        // tile width in columns (threads * CPT)
+  int ktiles;    // kappa tiles per rho (B >= TW ? B / TW : 1)
+  int Z;         // row-alias chunks
+  int rpc;       // row aliases per chunk
+};
+
+template <typename Tin, typename T, int NL, int CPT>
+__global__ void __launch_bounds__(kFoldThreads)
+k_fold(const Tin* __restrict__ x, const T* __restrict__ space, PermPack pp, int nloops,
+       FoldGeom gm, cplx<T>* __restrict__ dst) {
+  using C = cplx<T>;
+  __shared__ T s_w[NL * kFoldMaxRows];
+  __shared__ int s_rows[kFoldMaxRows];
+  __shared__ int s_nnz;
+  extern __shared__ __align__(16) unsigned char smem_raw[];   // [NL][TW] reduction (B < TW)
+
+  const int N = 1 << gm.lgN, B = 1 << gm.lgB;
+  const unsigned maskN = (unsigned)N - 1u, maskB = (unsigned)B - 1u;
+  const int rho = blockIdx.y;
+  const int z = blockIdx.z;
+  const int aliases = N >> gm.lgB;
+  const int j0 = z * gm.rpc;
+  const int cnt = min(gm.rpc, aliases - j0);
+  const int tid = threadIdx.x;
+
+  // ---- row weights of this chunk, and the compacted list of useful rows
+  for (int jj = tid; jj < cnt; jj += blockDim.x) {
+    const unsigned r = (unsigned)(rho + (j0 + jj) * B);
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      T w = (T)0;
+      if (l < nloops) w = space[(pp.p[l].s1i * (r - pp.p[l].t1)) & maskN];
+      s_w[l * kFoldMaxRows + jj] = w;
+    }
+  }
+  __syncthreads();
+  if (tid < 32) {
+    int base = 0;
+    for (int c0 = 0; c0 < cnt; c0 += 32) {
+      const int jj = c0 + tid;
+      bool nz = false;
+      if (jj < cnt) {
+#pragma unroll
+        for (int l = 0; l < NL; ++l) nz |= (s_w[l * kFoldMaxRows + jj] != (T)0);
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, nz);
+      if (nz) s_rows[base + __popc(bal & ((1u << tid) - 1u))] = jj;
+      base += __popc(bal);
+    }
+    if (tid == 0) s_nnz = base;
+  }
+  __syncthreads();
+  const int nnz = s_nnz;
+
+  // ---- stream the image
+  const int cp = tid * CPT;
+  const int step = max(B, gm.TW);
+  const int cbase = (B >= gm.TW) ? blockIdx.x * gm.TW : 0;
+  const int ncb = N / step;
+  C acc[NL][CPT];
+#pragma unroll
+  for (int l = 0; l < NL; ++l)
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) acc[l][q] = mk<T>(0, 0);
+
+  if (nnz > 0) {
+    for (int m = 0; m < ncb; ++m) {
+      const int c = cbase + m * step + cp;
+      T wc[NL][CPT];
+      bool any = false;
+#pragma unroll
+      for (int l = 0; l < NL; ++l)
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+          T w = (T)0;
+          if (l < nloops) w = __ldg(space + ((pp.p[l].s2i * ((unsigned)(c + q) - pp.p[l].t2)) & maskN));
+          wc[l][q] = w;
+          any |= (w != (T)0);
+        }
+      if (!any) continue;
+      C u[NL][CPT];
+#pragma unroll
+      for (int l = 0; l < NL; ++l)
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) u[l][q] = mk<T>(0, 0);
+      const Tin* col = x + c;
+#pragma unroll 4
+      for (int i = 0; i < nnz; ++i) {
+        const int jj = s_rows[i];
+        const size_t r = (size_t)(rho + (j0 + jj) * B);
+        C v[CPT];
+        ColLoad<Tin, T, CPT>::ld(col + (r << gm.lgN), v);
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+          const T wr = s_w[l * kFoldMaxRows + jj];
+#pragma unroll
+          for (int q = 0; q < CPT; ++q) {
+            u[l][q].x = fma(wr, v[q].x, u[l][q].x);
+            u[l][q].y = fma(wr, v[q].y, u[l][q].y);
+          }
+        }
+      }
+#pragma unroll
+      for (int l = 0; l < NL; ++l)
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+          acc[l][q].x = fma(wc[l][q], u[l][q].x, acc[l][q].x);
+          acc[l][q].y = fma(wc[l][q], u[l][q].y, acc[l][q].y);
+        }
+    }
+  }
+
+  // ---- emit (rho, kappa) values
+  const size_t BB = (size_t)B * B;
+  if (B >= gm.TW) {
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      if (l >= nloops) break;
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) {
+        const unsigned kap = (unsigned)(cbase + cp + q);
+        if (gm.Z == 1) {
+          const unsigned a = (pp.p[l].s1i * ((unsigned)rho - pp.p[l].t1)) & maskB;
+          const unsigned b = (pp.p[l].s2i * (kap - pp.p[l].t2)) & maskB;
+          dst[l * BB + (size_t)a * B + b] = acc[l][q];
+        } else {
+          dst[((size_t)z * nloops + l) * BB + (size_t)rho * B + kap] = acc[l][q];
+        }
+      }
+    }
+  } else {
+    C* red = reinterpret_cast<C*>(smem_raw);
+#pragma unroll
+    for (int l = 0; l < NL; ++l)
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) red[l * gm.TW + cp + q] = acc[l][q];
+    __syncthreads();
+    const int reps = gm.TW / B;
+    for (int e = tid; e < nloops * B; e += blockDim.x) {
+      const int l = e / B;
+      const int kap = e - l * B;
+      C s = mk<T>(0, 0);
+      for (int a = 0; a < reps; ++a) s = cadd(s, red[l * gm.TW + kap + a * B]);
+      if (gm.Z == 1) {
+        const unsigned ra = (pp.p[l].s1i * ((unsigned)rho - pp.p[l].t1)) & maskB;
+        const unsigned cb = (pp.p[l].s2i * ((unsigned)kap - pp.p[l].t2)) & maskB;
+        dst[l * BB + (size_t)ra * B + cb] = s;
+      } else {
+        dst[((size_t)z * nloops + l) * BB + (size_t)rho * B + kap] = s;
+      }
+    }
+  }
+}
+
+// Sum the Z partials in fixed order and scatter to the permuted bucket grid.
+template <typename T>
+__global__ void k_fold_reduce(const cplx<T>* __restrict__ part, int Z, int nloops, int lgB,
+                              PermPack pp, cplx<T>* __restrict__ y) {
+  using C = cplx<T>;
+  const int B = 1 << lgB;
+  const size_t BB = (size_t)B * B;
+  const size_t total = BB * nloops;
+  const unsigned maskB = (unsigned)B - 1u;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total;
+       e += (size_t)gridDim.x * blockDim.x) {
+    const int l = (int)(e / BB);
+    const size_t rem = e - l * BB;
+    const unsigned rho = (unsigned)(rem >> lgB), kap = (unsigned)(rem & maskB);
+    C s = mk<T>(0, 0);
+    for (int z = 0; z < Z; ++z) s = cadd(s, part[((size_t)z * nloops + l) * BB + rem]);
+    const unsigned a = (pp.p[l].s1i * (rho - pp.p[l].t1)) & maskB;
+    const unsigned b = (pp.p[l].s2i * (kap - pp.p[l].t2)) & maskB;
+    y[l * BB + (size_t)a * B + b] = s;
+  }
+}
+
+// Small grids: reduce partials + permute + whole 2D FFT in one CTA per loop.
+template <typename T>
+__global__ void k_fold_reduce_fft_small(const cplx<T>* __restrict__ part, int Z, int nloops,
+                                        int lgB, PermPack pp, const cplx<T>* __restrict__ tw,
+                                        int lgN, cplx<T>* __restrict__ spec) {
+  using C = cplx<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* s = reinterpret_cast<C*>(smem_raw);
+  const int B = 1 << lgB;
+  const int BB = B * B;
+  const int l = blockIdx.x;
+  const unsigned maskB = (unsigned)B - 1u;
+  for (int e = threadIdx.x; e < BB; e += blockDim.x) {
+    const unsigned rho = (unsigned)(e >> lgB), kap = (unsigned)(e & (B - 1));
+    C v = mk<T>(0, 0);
+    for (int z = 0; z < Z; ++z) v = cadd(v, part[((size_t)z * nloops + l) * BB + e]);
+    const unsigned a = (pp.p[l].s1i * (rho - pp.p[l].t1)) & maskB;
+    const unsigned b = (pp.p[l].s2i * (kap - pp.p[l].t2)) & maskB;
+    s[bitrev(a, lgB) * B + bitrev(b, lgB)] = v;
+  }
+  __syncthreads();
+  fft_stages<T>(s, B, lgB, 1, B, tw, lgN);
+  fft_stages<T>(s, B, lgB, B, 1, tw, lgN);
+  C* out = spec + (size_t)l * BB;
+  for (int e = threadIdx.x; e < BB; e += blockDim.x) out[e] = s[e];
+}
+
+inline FoldGeom fold_geometry(int lgN, int lgB, int cpt) {
+  FoldGeom g;
+  g.lgN = lgN;
+  g.lgB = lgB;
+  const int N = 1 << lgN, B = 1 << lgB;
+  g.TW = min(N, kFoldThreads * cpt);
+  g.ktiles = B >= g.TW ? B / g.TW : 1;
+  const int aliases = N / B;
+  const long per_z = (long)B * g.ktiles;
+  const long target = 8L * kNumSMs;
+  int Z = (int)((target + per_z - 1) / per_z);
+  if (Z < 1) Z = 1;
+  if (Z > aliases) Z = aliases;
+  int rpc = (aliases + Z - 1) / Z;
+  if (rpc > kFoldMaxRows) rpc = kFoldMaxRows;
+  g.rpc = rpc;
+  g.Z = (aliases + rpc - 1) / rpc;
+  return g;
+}
+
+}  // namespace sfft

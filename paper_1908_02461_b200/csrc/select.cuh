@@ -1,0 +1,300 @@
+// K3 / K4 — bin selection.
+//
+//  * magnitudes |Z| (np.abs == hypot) with a per-segment peak (atomicMax on an
+//    order-preserving integer key — exact, order independent);
+//  * K4 local maxima (count_local_maxima, tuner.py:97-118): strict ">" against
+//    the 8 toroidal neighbours and ">= mag_floor * peak", peak > 0;
+//  * ordered stream compaction (bitmask + per-block counts + scan + scatter)
+//    so every emitted list is in ascending flat (row-major) order, like
+//    np.argwhere / np.unique;
+//  * K3 exact top-`num` selection (engine.py:122-127 stable argsort): MSB-first
+//    radix select on the magnitude key finds the threshold key T and how many
+//    ties at T to keep; ties are kept lowest-index first.
+//
+// Everything is segmented: `nseg` independent equal-length segments (e.g. the
+// L location loops' grids) are processed by one launch (gridDim.y = segment).
+#pragma once
+#include "common.cuh"
+
+namespace sfft {
+
+constexpr int kCmpThreads = 256;                 // threads per compaction block
+constexpr int kCmpWords = kCmpThreads;           // one 32-bit word per thread
+constexpr int kCmpElems = kCmpWords * 32;        // 8192 elements per block
+
+__host__ __device__ inline long words_for(long n) { return (n + 31) / 32; }
+__host__ __device__ inline int blocks_for(long n) { return (int)((words_for(n) + kCmpWords - 1) / kCmpWords); }
+
+// ---------------------------------------------------------------- magnitudes
+template <typename T>
+__global__ void k_mags(const cplx<T>* __restrict__ spec, long seglen, T* __restrict__ mags,
+                       unsigned long long* __restrict__ peak) {
+  const int seg = blockIdx.y;
+  const cplx<T>* s = spec + (size_t)seg * seglen;
+  T* m = mags + (size_t)seg * seglen;
+  unsigned long long best = 0ull;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < seglen;
+       e += (long)gridDim.x * blockDim.x) {
+    const T v = cabs_(s[e]);
+    m[e] = v;
+    const unsigned long long k = fkey(v);
+    best = k > best ? k : best;
+  }
+  if (peak) {
+    for (int o = 16; o > 0; o >>= 1) {
+      unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+      best = t > best ? t : best;
+    }
+    if ((threadIdx.x & 31) == 0) atomicMax(peak + seg, best);
+  }
+}
+
+// ---------------------------------------------------------------- local maxima
+template <typename T>
+__global__ void k_lmax_bits(const T* __restrict__ mags, int lgB, int nseg_stride_log /*unused*/,
+                            const unsigned long long* __restrict__ peak, double floor_rel,
+                            uint32_t* __restrict__ bits, unsigned* __restrict__ blk_counts) {
+  const int seg = blockIdx.y;
+  const int B = 1 << lgB;
+  const long BB = (long)B * B;
+  const T* m = mags + (size_t)seg * BB;
+  const long wps = words_for(BB);
+  uint32_t* sb = bits + (size_t)seg * wps;
+  const double pk = fkey_inv(peak[seg]);
+  const bool live = pk > 0.0;
+  const double fl = floor_rel * pk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long w0 = (long)blockIdx.x * kCmpWords + warp * 32;
+  unsigned cnt = 0;
+  const unsigned maskB = (unsigned)B - 1u;
+  for (int i = 0; i < 32; ++i) {
+    const long w = w0 + i;
+    const long e = w * 32 + lane;
+    bool f = false;
+    if (live && e < BB) {
+      const unsigned r = (unsigned)(e >> lgB), c = (unsigned)(e & maskB);
+      const T v = m[e];
+      if ((double)v >= fl) {
+        const unsigned rm = (r - 1u) & maskB, rp = (r + 1u) & maskB;
+        const unsigned cm = (c - 1u) & maskB, cp = (c + 1u) & maskB;
+        f = v > m[(rm << lgB) | cm] && v > m[(rm << lgB) | c] && v > m[(rm << lgB) | cp] &&
+            v > m[(r << lgB) | cm] && v > m[(r << lgB) | cp] && v > m[(rp << lgB) | cm] &&
+            v > m[(rp << lgB) | c] && v > m[(rp << lgB) | cp];
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0 && w < wps) sb[w] = bal;
+    cnt += __popc(bal);
+  }
+  __shared__ unsigned s_cnt[kCmpThreads / 32];
+  if (lane == 0) s_cnt[warp] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int i = 0; i < kCmpThreads / 32; ++i) t += s_cnt[i];
+    blk_counts[(size_t)seg * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+// G[r][c] = M[s1i*r mod N][s2i*c mod N]: the |Z| grid of a B == N pass seen
+// through the permutation (SURVEY.md §7 hard part 2: tuner passes at B = N are
+// permuted views of |x_hat|).  CTA per output row; the source row is staged in
+// shared memory so both the read and the write are coalesced.
+template <typename T>
+__global__ void k_permute_grid(const T* __restrict__ M, int lgN, unsigned s1i, unsigned s2i,
+                               T* __restrict__ G) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* row = reinterpret_cast<T*>(smem_raw);
+  const int N = 1 << lgN;
+  const unsigned maskN = (unsigned)N - 1u;
+  const unsigned r = blockIdx.x;
+  const T* src = M + ((size_t)((s1i * r) & maskN) << lgN);
+  for (int c = threadIdx.x; c < N; c += blockDim.x) row[c] = src[c];
+  __syncthreads();
+  T* dst = G + ((size_t)r << lgN);
+  for (int c = threadIdx.x; c < N; c += blockDim.x) dst[c] = row[(s2i * (unsigned)c) & maskN];
+}
+
+// ---------------------------------------------------------------- scans
+// Exclusive scan of each segment's per-block counts (one CTA per segment).
+__global__ void k_scan_blocks(const unsigned* __restrict__ counts, int nblk,
+                              unsigned* __restrict__ offsets, unsigned* __restrict__ totals) {
+  const int seg = blockIdx.x;
+  const unsigned* c = counts + (size_t)seg * nblk;
+  unsigned* o = offsets + (size_t)seg * nblk;
+  const int per = (nblk + blockDim.x - 1) / blockDim.x;
+  const int b0 = threadIdx.x * per;
+  const int b1 = min(b0 + per, nblk);
+  unsigned local = 0;
+  for (int b = b0; b < b1; ++b) local += c[b];
+  // block exclusive scan of `local`
+  __shared__ unsigned s_warp[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned inc = warp_incl_scan(local);
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    const int nw = (blockDim.x + 31) >> 5;
+    unsigned v = lane < nw ? s_warp[lane] : 0u;
+    v = warp_incl_scan(v);
+    s_warp[lane] = v;
+  }
+  __syncthreads();
+  unsigned run = inc - local + (warp ? s_warp[warp - 1] : 0u);
+  for (int b = b0; b < b1; ++b) {
+    o[b] = run;
+    run += c[b];
+  }
+  if (threadIdx.x == blockDim.x - 1 && totals) totals[seg] = run;
+  if (nblk == 0 && threadIdx.x == 0 && totals) totals[seg] = 0;
+}
+
+// Block-exclusive scan over kCmpThreads values; returns exclusive prefix.
+__device__ __forceinline__ unsigned block_excl_scan256(unsigned v, unsigned* s_warp) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned inc = warp_incl_scan(v);
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    unsigned t = lane < (kCmpThreads / 32) ? s_warp[lane] : 0u;
+    t = warp_incl_scan(t);
+    if (lane < (kCmpThreads / 32)) s_warp[lane] = t;
+  }
+  __syncthreads();
+  const unsigned r = inc - v + (warp ? s_warp[warp - 1] : 0u);
+  __syncthreads();
+  return r;
+}
+
+// Scatter the set bits of each segment to out[seg * out_stride + rank] (flat index).
+__global__ void k_compact_bits(const uint32_t* __restrict__ bits, long seglen,
+                               const unsigned* __restrict__ offsets, int32_t* __restrict__ out,
+                               long out_stride) {
+  __shared__ unsigned s_warp[32];
+  const int seg = blockIdx.y;
+  const long wps = words_for(seglen);
+  const long w = (long)blockIdx.x * kCmpWords + threadIdx.x;
+  uint32_t word = (w < wps) ? bits[(size_t)seg * wps + w] : 0u;
+  const unsigned pre = block_excl_scan256(__popc(word), s_warp);
+  unsigned pos = offsets[(size_t)seg * gridDim.x + blockIdx.x] + pre;
+  int32_t* o = out + (size_t)seg * out_stride;
+  while (word) {
+    const int b = __ffs(word) - 1;
+    word &= word - 1u;
+    o[pos++] = (int32_t)(w * 32 + b);
+  }
+}
+
+// ---------------------------------------------------------------- radix select
+struct SelState {
+  unsigned long long prefix;   // key bits fixed so far
+  unsigned long long mask;     // which bits are fixed
+  long long need;              // how many still to take among keys matching prefix
+  long long take_all;          // 1: keep the whole segment (num >= seglen)
+};
+
+template <typename T>
+__global__ void k_radix_hist(const T* __restrict__ vals, long seglen,
+                             const SelState* __restrict__ st, int shift,
+                             unsigned* __restrict__ hist) {
+  __shared__ unsigned sh[256];
+  const int seg = blockIdx.y;
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  const SelState s = st[seg];
+  if (!s.take_all) {
+    const T* v = vals + (size_t)seg * seglen;
+    for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < seglen;
+         e += (long)gridDim.x * blockDim.x) {
+      const unsigned long long k = fkey(v[e]);
+      if ((k & s.mask) == s.prefix) atomicAdd(&sh[(k >> shift) & 255u], 1u);
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 256; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist[(size_t)seg * 256 + i], sh[i]);
+}
+
+__global__ void k_radix_pick(SelState* __restrict__ st, unsigned* __restrict__ hist, int shift,
+                             int nseg) {
+  const int seg = blockIdx.x * blockDim.x + threadIdx.x;
+  if (seg >= nseg) return;
+  SelState s = st[seg];
+  unsigned* h = hist + (size_t)seg * 256;
+  if (!s.take_all) {
+    long long cum = 0;
+    for (int d = 255; d >= 0; --d) {
+      const long long c = h[d];
+      if (cum + c >= s.need) {
+        s.prefix |= (unsigned long long)d << shift;
+        s.mask |= 255ull << shift;
+        s.need -= cum;
+        break;
+      }
+      cum += c;
+    }
+    st[seg] = s;
+  }
+  for (int d = 0; d < 256; ++d) h[d] = 0;
+}
+
+// per-block count of keys equal to the threshold (for tie ranks)
+template <typename T>
+__global__ void k_tie_counts(const T* __restrict__ vals, long seglen,
+                             const SelState* __restrict__ st, unsigned* __restrict__ tie_blk) {
+  __shared__ unsigned s_warp[32];
+  const int seg = blockIdx.y;
+  const SelState s = st[seg];
+  const T* v = vals + (size_t)seg * seglen;
+  const long e0 = ((long)blockIdx.x * kCmpWords + threadIdx.x) * 32;
+  unsigned c = 0;
+  if (!s.take_all)
+    for (int b = 0; b < 32; ++b) {
+      const long e = e0 + b;
+      if (e < seglen && fkey(v[e]) == s.prefix) ++c;
+    }
+  const unsigned pre = block_excl_scan256(c, s_warp);
+  if (threadIdx.x == kCmpThreads - 1) tie_blk[(size_t)seg * gridDim.x + blockIdx.x] = pre + c;
+}
+
+// selection bitmask: key > T, or key == T with global tie rank < need
+template <typename T>
+__global__ void k_select_bits(const T* __restrict__ vals, long seglen,
+                              const SelState* __restrict__ st, const unsigned* __restrict__ tie_off,
+                              uint32_t* __restrict__ bits, unsigned* __restrict__ blk_counts) {
+  __shared__ unsigned s_warp[32];
+  const int seg = blockIdx.y;
+  const SelState s = st[seg];
+  const T* v = vals + (size_t)seg * seglen;
+  const long wps = words_for(seglen);
+  const long w = (long)blockIdx.x * kCmpWords + threadIdx.x;
+  uint32_t gt = 0, eq = 0;
+  for (int b = 0; b < 32; ++b) {
+    const long e = w * 32 + b;
+    if (e < seglen) {
+      if (s.take_all) {
+        gt |= 1u << b;
+      } else {
+        const unsigned long long k = fkey(v[e]);
+        if (k > s.prefix) gt |= 1u << b;
+        else if (k == s.prefix) eq |= 1u << b;
+      }
+    }
+  }
+  const unsigned pre = block_excl_scan256(__popc(eq), s_warp);
+  long long rank = (long long)tie_off[(size_t)seg * gridDim.x + blockIdx.x] + pre;
+  uint32_t word = gt;
+  uint32_t e2 = eq;
+  while (e2) {
+    const int b = __ffs(e2) - 1;
+    e2 &= e2 - 1u;
+    if (rank < s.need) word |= 1u << b;
+    ++rank;
+  }
+  if (w < wps) bits[(size_t)seg * wps + w] = word;
+  const unsigned tot = block_excl_scan256(__popc(word), s_warp);
+  if (threadIdx.x == kCmpThreads - 1)
+    blk_counts[(size_t)seg * gridDim.x + blockIdx.x] = tot + __popc(word);
+}
+
+}  // namespace sfft

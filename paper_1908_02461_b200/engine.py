@@ -1,0 +1,152 @@
+"""Algorithm 1 (fixed-sparsity 2D SFFT) — mirror of
+``/root/reference/pkg/src/sfft2d/engine.py`` on the sm_100a path.
+
+``sfft2d`` keeps the reference signature and result (a dict ``(i, j) ->
+complex``).  The host draws the 2L per-loop permutation streams exactly as the
+reference does (engine.py:266-268, 280) and hands them to the native
+controller ``sfft2d_sfft`` (csrc/capi.cu ``run_sfft``): one fused fold of all L
+location loops, bucket FFTs, top-2k selection, unhash + dedup vote histogram,
+threshold compaction, L estimation loops, median, top-k, prune.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from ._tensors import as_device_image
+from .hashing import (FlatWindow, WindowCache, build_flat_window, draw_permutation,
+                      is_power_of_two)
+
+__all__ = ["ConfigurationError", "SfftConfig", "default_bins", "sfft2d", "sfft2d_arrays"]
+
+
+class ConfigurationError(ValueError):
+    """Raised when a transform configuration cannot be executed (engine.py:45-46)."""
+
+
+def _nearest_pow2(v: float) -> int:
+    """Power of two nearest to v, ties to the lower one (engine.py:49-52)."""
+    lo = 1 << max(int(math.floor(math.log2(v))), 0) if v >= 1 else 1
+    return lo if (v - lo) <= (2 * lo - v) else 2 * lo
+
+
+def default_bins(n: int, k: int) -> int:
+    """Nearest power of two to sqrt(min(n, 256) * k), clamped to [4, n] (engine.py:55-66)."""
+    k = max(k, 1)
+    return max(4, min(_nearest_pow2(math.sqrt(min(n, 256) * k)), n))
+
+
+_WINDOWS = WindowCache()
+
+
+@dataclass
+class SfftConfig:
+    """Inputs of the fixed-sparsity transform (engine.py:69-119)."""
+
+    n: int
+    k: int
+    loops: int = 8
+    d_factor: int = 2
+    vote_threshold: int | None = None
+    b_bins: int | None = None
+    window_delta_pass: float = 1e-3
+    window_delta_stop: float = 1e-8
+    gain_floor: float = 1e-6
+    prune_rel: float = 1e-3
+
+    def __post_init__(self):
+        if not is_power_of_two(self.n):
+            raise ConfigurationError(f"side {self.n} is not a power of 2")
+        if self.k < 0 or self.k > self.n * self.n:
+            raise ConfigurationError(f"sparsity {self.k} out of range for n={self.n}")
+        if self.loops < 1:
+            raise ConfigurationError("loops must be >= 1")
+        if self.b_bins is None:
+            self.b_bins = default_bins(self.n, self.k)
+        b = self.b_bins
+        if not is_power_of_two(b) or b > self.n or self.n % b != 0:
+            raise ConfigurationError(f"bin count {b} must be a power of 2 dividing {self.n}")
+        if self.vote_threshold is None:
+            self.vote_threshold = (self.loops + 1) // 2
+        if not 1 <= self.vote_threshold <= self.loops:
+            raise ConfigurationError(
+                f"vote_threshold {self.vote_threshold} outside [1, {self.loops}]")
+        if self.num_kept_bins > b * b:
+            raise ConfigurationError(
+                f"d_factor*k = {self.num_kept_bins} exceeds the {b}x{b} bin budget")
+
+    @property
+    def num_kept_bins(self) -> int:
+        return max(1, self.d_factor * self.k)
+
+    def window(self, cache: WindowCache | None = None) -> FlatWindow:
+        cache = cache or _WINDOWS
+        return cache.get(self.n, self.b_bins, self.window_delta_stop, self.window_delta_pass)
+
+
+def _fetch(ctx, res, stream, precision_code):
+    """Copy the native result to host arrays (coords int64[m,2], values)."""
+    m = int(res.count)
+    ij = np.empty((m, 2), dtype=np.int64)
+    vals = np.empty(m, dtype=np.complex128 if precision_code == _native.FP64 else np.complex64)
+    if m:
+        ctx.check(ctx.lib.sfft2d_fetch_result(ctx.handle, ij.ctypes.data, vals.ctypes.data, 1,
+                                              stream))
+    if res.ordered_by_magnitude and m > 1:
+        order = np.lexsort((ij[:, 1], ij[:, 0], -np.abs(vals.astype(np.complex128))))
+        ij, vals = ij[order], vals[order]
+    return ij, vals
+
+
+def to_dict(ij: np.ndarray, vals: np.ndarray) -> dict:
+    return {(int(i), int(j)): complex(v) for (i, j), v in zip(ij.tolist(), vals.tolist())}
+
+
+def _stream(torch, device):
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def sfft2d_arrays(x, cfg: SfftConfig, rng, *, cache: WindowCache | None = None,
+                  precision: str = "fp64", device=None):
+    """``sfft2d`` returning (coords int64[m, 2], values[m]) in the reference's
+    dict order instead of a dict."""
+    torch = _native._torch()
+    img = as_device_image(x, device, upload=False)
+    if img.n != cfg.n:
+        raise ConfigurationError(f"config built for n={cfg.n}, signal has n={img.n}")
+    prec = _native.precision_code(precision)
+    rng = np.random.default_rng(rng)
+    loop_rngs = [np.random.default_rng(int(rng.integers(2**63))) for _ in range(2 * cfg.loops)]
+    perms = [draw_permutation(cfg.n, g) for g in loop_rngs]
+    ctx = _native.context(img.device)
+    ctx.ensure_tables(cfg.n, cfg.window_delta_pass, cfg.window_delta_stop)
+    ccfg = _native.SfftCfg(cfg.n, cfg.k, cfg.loops, cfg.d_factor, cfg.vote_threshold, cfg.b_bins,
+                           cfg.window_delta_pass, cfg.window_delta_stop, cfg.gain_floor,
+                           cfg.prune_rel)
+    res = _native.ResultC()
+    with torch.cuda.device(img.device):
+        st = _stream(torch, img.device)
+        if img.tensor is not None:
+            ptr, on_host = img.tensor.data_ptr(), 0
+        else:
+            ptr, on_host = img.host.ctypes.data, 1
+        ctx.check(ctx.lib.sfft2d_sfft(ctx.handle, ptr, img.dtype_code, on_host, ctypes.byref(ccfg),
+                                      _native.perm_array(perms), prec, st, ctypes.byref(res)))
+        return _fetch(ctx, res, st, prec)
+
+
+def sfft2d(x, cfg: SfftConfig, rng, *, cache: WindowCache | None = None,
+           precision: str = "fp64", device=None) -> dict:
+    """Full Algorithm 1 on the GPU: location loops, vote, estimation loops,
+    median, top-k, prune (engine.py:256-284).  ``rng``: seed or Generator."""
+    return to_dict(*sfft2d_arrays(x, cfg, rng, cache=cache, precision=precision, device=device))
+
+
+def build_window(cfg: SfftConfig) -> FlatWindow:
+    return build_flat_window(cfg.n, cfg.b_bins, cfg.window_delta_stop,
+                             delta_pass=cfg.window_delta_pass)

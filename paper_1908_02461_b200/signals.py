@@ -1,0 +1,129 @@
+"""Synthetic k-sparse-spectrum workloads and the average-L1 error metric.
+
+The reference ships only a noiseless unit-spike generator
+(``/root/reference/pkg/src/sfft2d/signals.py:42-65``).  BASELINE.json's configs
+need noise, log-uniform magnitudes and a clustered low-frequency block
+(SURVEY.md D3, §8(d) "D-in"), so the workload is defined here, once:
+
+* ``k`` coefficients at distinct (row, col) positions.  A fraction
+  ``cluster_frac`` of them is placed in the wrap-around DC block
+  ``{-side/2 .. side/2-1}^2 mod n`` (c5), the rest uniformly over the grid.
+* magnitude 1 (``"unit"``) or log-uniform in ``mag_range``; phase U[0, 2pi).
+* image = inverse 2D DFT of that spectrum with the ``1/n^2`` convention
+  (``corefft.py:112-118``), computed with ``np.fft.ifft2``.
+* optional complex Gaussian noise with total variance
+  ``mean|x_clean|^2 * 10^(-snr_db/10)``, split evenly between re and im.
+
+Everything is drawn from one ``np.random.default_rng(seed)`` stream, so a seed
+fully determines the image (same numpy on the dev container and the GPU box).
+This is host-side workload tooling, not part of the transform.
+"""
+
+from __future__ import annotations
+
+import hashlib
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = ["SparseImage", "sparse_image", "planted_image", "error_metric", "image_digest"]
+
+
+@dataclass(frozen=True)
+class SparseImage:
+    n: int
+    k: int
+    seed: int
+    x: np.ndarray                 # (n, n) complex64 / complex128
+    rows: np.ndarray              # int64[k]
+    cols: np.ndarray              # int64[k]
+    coeffs: np.ndarray            # complex128[k]
+
+    @property
+    def truth(self) -> dict:
+        return {(int(i), int(j)): complex(c) for i, j, c in zip(self.rows, self.cols, self.coeffs)}
+
+
+def _is_pow2(v: int) -> bool:
+    return v >= 1 and (v & (v - 1)) == 0
+
+
+def sparse_image(
+    n: int,
+    k: int,
+    seed: int,
+    *,
+    snr_db: float | None = None,
+    magnitude: str = "unit",
+    mag_range: tuple[float, float] = (0.1, 10.0),
+    cluster_frac: float = 0.0,
+    cluster_side: int = 64,
+    dtype=np.complex64,
+) -> SparseImage:
+    """Seeded k-sparse-spectrum image, optionally noisy (see module docstring)."""
+    if not _is_pow2(n):
+        raise ValueError(f"side {n} is not a power of 2")
+    if k < 0 or k > n * n:
+        raise ValueError(f"sparsity {k} out of range for side {n}")
+    rng = np.random.default_rng(seed)
+    n_clu = int(round(cluster_frac * k)) if cluster_frac > 0 else 0
+    side = min(cluster_side, n)
+    if n_clu > side * side:
+        raise ValueError("cluster block too small for the clustered fraction")
+    picked: list[int] = []
+    if n_clu:
+        half = side // 2
+        local = rng.choice(side * side, size=n_clu, replace=False)
+        ci = (local // side - half) % n
+        cj = (local % side - half) % n
+        picked.extend((ci * n + cj).tolist())
+    taken = set(picked)
+    need = k - n_clu
+    while need > 0:
+        draw = rng.choice(n * n, size=need, replace=False)
+        for f in draw.tolist():
+            if f not in taken and need > 0:
+                taken.add(f)
+                picked.append(f)
+                need -= 1
+    flat = np.asarray(picked, dtype=np.int64)
+    rows, cols = flat // n, flat % n
+    phases = rng.uniform(0.0, 2.0 * np.pi, size=k)
+    if magnitude == "unit":
+        mags = np.ones(k)
+    elif magnitude == "loguniform":
+        lo, hi = np.log(mag_range[0]), np.log(mag_range[1])
+        mags = np.exp(rng.uniform(lo, hi, size=k))
+    else:
+        raise ValueError(f"unknown magnitude law {magnitude!r}")
+    coeffs = mags * np.exp(1j * phases)
+    spec = np.zeros((n, n), dtype=np.complex128)
+    spec[rows, cols] = coeffs
+    x = np.fft.ifft2(spec)
+    del spec
+    if snr_db is not None:
+        power = float(np.mean(np.abs(x) ** 2))
+        sd = np.sqrt(power * 10.0 ** (-snr_db / 10.0) / 2.0)
+        x += sd * rng.standard_normal((n, n))
+        x += 1j * sd * rng.standard_normal((n, n))
+    return SparseImage(n, k, seed, np.ascontiguousarray(x.astype(dtype)), rows, cols, coeffs)
+
+
+def planted_image(n: int, k: int, seed: int) -> SparseImage:
+    """Noiseless unit-magnitude complex128 image (config c1's workload shape)."""
+    return sparse_image(n, k, seed, snr_db=None, dtype=np.complex128)
+
+
+def error_metric(approx: dict, exact: dict, k: int) -> float:
+    """Average L1 spectral error (1/k) * sum |approx - exact| over the union of
+    supports, absent entries reading as zero (``signals.py:68-85``)."""
+    keys = set(approx) | set(exact)
+    total = sum(abs(approx.get(key, 0.0) - exact.get(key, 0.0)) for key in keys)
+    if k <= 0:
+        return 0.0 if total == 0.0 else float("inf")
+    return float(total) / k
+
+
+def image_digest(x: np.ndarray) -> str:
+    """sha256 of the raw bytes; golden fixtures pin regenerated inputs with it."""
+    return hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest()
