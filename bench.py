@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""Benchmark: 2D ATSFFT transforms/s at N=4096, k=100 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[2], "c3"): one 4096 x 4096 complex64 image per
+rank per step whose spectrum has k=100 unit-magnitude random-phase coefficients
+at distinct uniform positions plus complex Gaussian noise at 20 dB SNR
+(seeded synthetic input, paper_1908_02461_b200.signals.sparse_image; the
+reference ships no dataset).  A step is one full ``atsfft2d`` (TunerConfig()
+defaults, est_loops=8): the adaptive tuning passes, the vote histogram, the
+estimation loops, median, top-k and prune.
+
+Legs printed on ONE JSON line (rank 0):
+  value     transforms/s, image resident in HBM, CUDA events on the launch
+            stream over exactly --steps steps (barrier + sync both sides, max
+            over ranks).  The 134 MB image and the ~1 GB per-transform working
+            set exceed the 126 MB L2, so no explicit flush is needed.
+  e2e       the same metric through the public API with the image in pinned
+            HOST memory: the host->device copy and the result download are
+            inside the timed region.
+  roofline  dominant kernel: algorithmic bytes per launch / CUDA-event launch
+            time from the library's per-launch profiler (a separate
+            instrumented pass over the same steps), against MEASURED_PEAKS.json.
+  cpu_baseline  the numpy oracle port (oracle/sfft_oracle.py, pocketfft FFTs)
+            on one full c3 transform on one host core (rank 0, N=1).
+``--impl reference`` times that oracle port instead (the reference is a pure
+Python package that cannot travel to the GPU box; oracle/ restates it), on all
+host cores via a process pool, and prints the same line with impl=reference.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "2D ATSFFT transforms/sec at N=4096,k=100; achieved HBM GB/s vs B200 peak"
+UNIT = "transforms/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--k", type=int, default=100)
+    ap.add_argument("--snr", type=float, default=20.0)
+    ap.add_argument("--est-loops", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=3)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def workload(args, rank):
+    from paper_1908_02461_b200.signals import sparse_image
+    return sparse_image(args.n, args.k, 7 + rank, snr_db=args.snr)
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        try:
+            fd, self.path = tempfile.mkstemp(suffix=".csv")
+            os.close(fd)
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.QUERY}", "--format=csv,noheader,nounits",
+                 "-lms", "200", "-i", str(self.dev)], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self) -> dict | None:
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.fh.close()
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [v.strip() for v in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = max(smax, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def kernel_traffic():
+    path = os.path.join(ROOT, "profiles", "kernel_traffic.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return {}
+
+
+def cpu_baseline(x, args):
+    from oracle import sfft_oracle as O
+    O.FAST = True
+    t0 = time.perf_counter()
+    O.atsfft(x, O.TunerParams(), args.est_loops, 11)
+    dt = time.perf_counter() - t0
+    return {"value": 1.0 / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"one full ATSFFT transform of the c3 image ({args.n}^2 c64, k={args.k}, "
+                      f"{args.snr:g} dB, est_loops={args.est_loops}) by the numpy oracle port "
+                      f"(pocketfft FFTs), 1 thread, {dt:.1f} s"}
+
+
+# ---------------------------------------------------------------- reference arm
+def _ref_worker(args_tuple):
+    import numpy as np  # noqa: F811
+    from oracle import sfft_oracle as O
+    O.FAST = True
+    x, est_loops, seed = args_tuple
+    t0 = time.perf_counter()
+    O.atsfft(x, O.TunerParams(), est_loops, seed)
+    return time.perf_counter() - t0
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import multiprocessing as mp
+    img = workload(args, 0)
+    cores = os.cpu_count() or 1
+    procs = max(1, min(cores, 16))
+    steps = max(1, min(args.steps, 2))
+    warm = 1 if args.warmup > 0 else 0
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        for _ in range(warm):
+            pool.map(_ref_worker, [(img.x, args.est_loops, 11)] * procs)
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            pool.map(_ref_worker, [(img.x, args.est_loops, 11)] * procs)
+        dt = time.perf_counter() - t0
+    value = steps * procs / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": steps, "requested_steps": args.steps, "warmup": warm,
+        "ms_per_step": dt / steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"c3: ATSFFT {args.n}x{args.n} c64, k={args.k}, {args.snr:g} dB, "
+                               f"est_loops={args.est_loops}", "parallelism": f"{procs} host processes"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
+                         "sample": f"{steps} step(s) x {procs} concurrent full c3 transforms of the "
+                                   f"numpy oracle port (pocketfft FFTs), one per process"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://", world_size=world, rank=rank)
+    dev = torch.device("cuda", local)
+    import paper_1908_02461_b200 as P
+    from paper_1908_02461_b200 import _native
+
+    img = workload(args, rank)
+    x_dev = torch.from_numpy(img.x).to(dev)
+    cfg = P.TunerConfig()
+    ctx = _native.context(local)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(x):
+        return P.atsfft2d_arrays(x, cfg, args.est_loops, 11, precision=args.precision)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # warm-up (also builds tables / workspace)
+    for _ in range(max(args.warmup, 1)):
+        (ij, vals), state = step(x_dev)
+    torch.cuda.synchronize()
+    parity = None
+    gold = os.path.join(ROOT, "tests", "golden", "c3_ats.npz")
+    if rank == 0 and args.n == 4096 and args.k == 100 and args.snr == 20.0 and os.path.exists(gold):
+        g = np.load(gold)
+        ref = {tuple(c) for c in g["coords"].tolist()}
+        parity = {"support_equal_to_reference": ref == {tuple(c) for c in ij.tolist()},
+                  "coefficients": int(len(ij)),
+                  "trajectory_equal": [(b, c) for b, c, _ in state.history] ==
+                                      [(int(b), int(c)) for b, c in g["hist"][:, :2]]}
+
+    # ---- timed region: value (image resident in HBM)
+    vis = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
+    sampler = ClockSampler(int(vis[local]) if len(vis) > local and vis[local].isdigit() else local)
+    launches = 0
+    barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(x_dev)
+        launches += ctx.last_launches
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * args.steps / (ms_max / 1e3)
+
+    # ---- e2e: pinned host image, H2D + result D2H inside the region
+    e2e = None
+    if not args.no_e2e:
+        host = torch.empty((args.n, args.n), dtype=torch.complex64, pin_memory=True)
+        host.copy_(torch.from_numpy(img.x))
+        xh = host.numpy()
+        P.atsfft2d(xh, cfg, args.est_loops, 11, precision=args.precision)
+        barrier()
+        torch.cuda.synchronize()
+        d2h = 0
+        e0.record(stream)
+        for _ in range(args.steps):
+            out, st = P.atsfft2d(xh, cfg, args.est_loops, 11, precision=args.precision)
+            d2h += len(out) * (16 + (16 if args.precision == "fp64" else 8))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        nperm = cfg.iters(args.n) + 2 + args.est_loops
+        e2e = {"value": world * args.steps / (float(t.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": args.n * args.n * 8 + nperm * 48,
+               "d2h_bytes_per_step": d2h // max(args.steps, 1)}
+
+    # ---- kernel-level roofline (instrumented pass, same workload)
+    ctx.set_profiling(True)
+    nprof = max(1, min(args.profile_steps, args.steps))
+    pe0 = torch.cuda.Event(enable_timing=True)
+    pe1 = torch.cuda.Event(enable_timing=True)
+    pe0.record(stream)
+    for _ in range(nprof):
+        step(x_dev)
+    pe1.record(stream)
+    torch.cuda.synchronize()
+    rep = ctx.profile_report()
+    ctx.set_profiling(False)
+    prof_ms = pe0.elapsed_time(pe1)
+    peak, peak_kind = peaks()
+    top = max(rep.items(), key=lambda kv: kv[1][1]) if rep else None
+    roofline = None
+    if top:
+        name, (cnt, tms, tbytes) = top
+        achieved = (tbytes / cnt) / (tms / cnt / 1e3) / 1e9
+        traffic = kernel_traffic().get(name)
+        roofline = {"bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak,
+                    "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": traffic, "alg_bytes_per_launch": tbytes / cnt,
+                    "launches_per_step": cnt / nprof, "avg_launch_us": tms / cnt * 1e3,
+                    "share_of_step": tms / prof_ms}
+    kernels = {k: {"launches_per_step": v[0] / nprof, "ms_per_step": v[1] / nprof,
+                   "GBps": (v[2] / v[1] / 1e6) if v[1] > 0 else None}
+               for k, v in sorted(rep.items(), key=lambda kv: -kv[1][1])[:8]}
+
+    # ---- dense cuFFT of the same image, for context only
+    torch.cuda.synchronize()
+    xc = x_dev.to(torch.complex64)
+    for _ in range(3):
+        torch.fft.fft2(xc)
+    c0 = torch.cuda.Event(enable_timing=True)
+    c1 = torch.cuda.Event(enable_timing=True)
+    c0.record(stream)
+    for _ in range(10):
+        torch.fft.fft2(xc)
+    c1.record(stream)
+    torch.cuda.synchronize()
+    cufft_ms = c0.elapsed_time(c1) / 10
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(img.x, args)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if args.precision == "fp32" else "f64", "data": "synthetic",
+            "config": {"workload": f"c3: ATSFFT {args.n}x{args.n} complex64, k={args.k}, "
+                                   f"{args.snr:g} dB SNR, TunerConfig() defaults, est_loops="
+                                   f"{args.est_loops}, one image per rank per step",
+                       "precision": args.precision, "l2": "inputs larger than L2 (134 MB image)",
+                       "parallelism": f"independent transforms, {world} rank(s)"},
+            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+            "gpu_launches": launches, "kernels": kernels,
+            "context": {"cufft_dense_fft2_c64_ms": cufft_ms,
+                        "detected_k": state.detected_k, "passes": state.passes,
+                        "trajectory": [b for b, _, _ in state.history]},
+            "parity": parity,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -148,6 +148,14 @@ int sfft2d_fetch_result(sfft2d_ctx* ctx, int64_t* ij, void* values, int dst_on_h
 int sfft2d_fetch_votes(sfft2d_ctx* ctx, int32_t* keys, int32_t* tallies, int dst_on_host,
                        void* stream);
 
+/* Kernel-level profiling: when enabled, every kernel launch is bracketed by
+ * a CUDA event pair on its launching stream and tagged with its algorithmic
+ * bytes.  The report synchronises the device and returns
+ * lines "name launches total_ms total_bytes" (then clears the records); the
+ * return value is the report length (negative status on error).          */
+int sfft2d_ctx_set_profiling(sfft2d_ctx* ctx, int enable);
+int64_t sfft2d_ctx_profile_report(sfft2d_ctx* ctx, char* buf, int64_t buflen);
+
 /* ---- building blocks (device pointers, stream-ordered, no host sync) ---- */
 
 /* binned_spectrum (hashing.py:308-337) for `nloops` permutations sharing one

@@ -27,7 +27,8 @@ EXPORTS = (
     "sfft2d_abi_version", "sfft2d_ctx_create", "sfft2d_ctx_destroy", "sfft2d_ctx_last_error",
     "sfft2d_ctx_set_tables", "sfft2d_sfft", "sfft2d_atsfft", "sfft2d_detect_sparsity",
     "sfft2d_fetch_result", "sfft2d_fetch_votes", "sfft2d_binned_spectrum", "sfft2d_fft2d",
-    "sfft2d_local_maxima", "sfft2d_top_bins",
+    "sfft2d_local_maxima", "sfft2d_top_bins", "sfft2d_ctx_set_profiling",
+    "sfft2d_ctx_profile_report",
 )
 
 
@@ -105,6 +106,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "sfft2d_fft2d": ([vp, vp, i32, i32, i32, i32, vp], i32),
             "sfft2d_local_maxima": ([vp, vp, i32, dbl, i32, P(i64), vp, i64, vp], i32),
             "sfft2d_top_bins": ([vp, vp, i32, i32, i64, i32, vp, vp], i32),
+            "sfft2d_ctx_set_profiling": ([vp, i32], i32),
+            "sfft2d_ctx_profile_report": ([vp, ctypes.c_char_p, i64], i64),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)
@@ -139,6 +142,7 @@ class Context:
                 raise RuntimeError(f"sfft2d_ctx_create failed with status {rc}")
         self.handle = h
         self._tables: set = set()
+        self.last_launches = 0
         self._lock = threading.Lock()
 
     def error(self) -> str:
@@ -155,6 +159,22 @@ class Context:
             from .engine import ConfigurationError
             raise ConfigurationError(msg)
         raise StatusError(f"sfft2d status {rc}: {msg}")
+
+    def set_profiling(self, enable: bool):
+        self.check(self.lib.sfft2d_ctx_set_profiling(self.handle, 1 if enable else 0))
+
+    def profile_report(self) -> dict:
+        """{kernel: (launches, total_ms, total_algorithmic_bytes)} since enabling."""
+        n = self.lib.sfft2d_ctx_profile_report(self.handle, None, 0)
+        if n < 0:
+            self.check(int(n))
+        buf = ctypes.create_string_buffer(int(n) + 1)
+        self.lib.sfft2d_ctx_profile_report(self.handle, buf, n + 1)
+        out = {}
+        for line in buf.value.decode().splitlines():
+            name, cnt, ms, by = line.split()
+            out[name] = (int(cnt), float(ms), float(by))
+        return out
 
     def ensure_tables(self, n: int, delta_pass: float, delta_stop: float):
         key = (n, float(delta_pass), float(delta_stop))

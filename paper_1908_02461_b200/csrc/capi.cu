@@ -57,6 +57,7 @@ struct DevTables {
   void* space[2] = {nullptr, nullptr};
   void* freq[2] = {nullptr, nullptr};
   void* tw[2] = {nullptr, nullptr};
+  std::vector<int> support;  // samples per axis with nonzero window weight, per log2(B)
 };
 
 }  // namespace
@@ -74,6 +75,17 @@ struct sfft2d_ctx {
   long long votes_count = 0;
   bool has_votes = false;
   int launches = 0;
+  // optional per-launch profiling (CUDA events on the launching stream)
+  bool profiling = false;
+  bool prof_open = false;
+  struct ProfRec {
+    const char* name;
+    double bytes;
+    cudaEvent_t a, b;
+  };
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_used = 0;
 };
 
 namespace {
@@ -97,9 +109,36 @@ void* ws(sfft2d_ctx* c, const char* name, size_t bytes) {
   return e.first;
 }
 
-void post(sfft2d_ctx* c, const char* what) {
+cudaEvent_t next_event(sfft2d_ctx* c) {
+  if (c->ev_used == c->ev_pool.size()) {
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "cudaEventCreate");
+    c->ev_pool.push_back(e);
+  }
+  return c->ev_pool[c->ev_used++];
+}
+
+// pre/post bracket every kernel launch: count it, check the launch, and when
+// profiling record an event pair on the launching stream with the launch's
+// algorithmic bytes (SURVEY.md §8(d) accounting).
+void pre(sfft2d_ctx* c, cudaStream_t st) {
+  if (!c->profiling) return;
+  cudaEvent_t a = next_event(c);
+  ck(cudaEventRecord(a, st), "cudaEventRecord");
+  c->prof.push_back({nullptr, 0.0, a, nullptr});
+  c->prof_open = true;
+}
+
+void post(sfft2d_ctx* c, const char* what, cudaStream_t st, double bytes) {
   ++c->launches;
   ck(cudaGetLastError(), what);
+  if (!c->profiling || !c->prof_open) return;
+  cudaEvent_t b = next_event(c);
+  ck(cudaEventRecord(b, st), "cudaEventRecord");
+  c->prof.back().name = what;
+  c->prof.back().bytes = bytes;
+  c->prof.back().b = b;
+  c->prof_open = false;
 }
 
 template <typename K>
@@ -199,6 +238,55 @@ __global__ void k_iota_segments(int32_t* out, long seglen, int nseg) {
     out[e] = (int32_t)(e % seglen);
 }
 
+// In-place 2D FFT of `ngrids` contiguous B x B grids (csrc/fft.cuh kernels).
+template <typename T>
+void fft_grids(sfft2d_ctx* c, cplx<T>* grids, int lgB, int ngrids, const cplx<T>* tw, int lgN,
+               cudaStream_t st) {
+  using C = cplx<T>;
+  const int B = 1 << lgB;
+  const size_t gbytes = (size_t)B * B * sizeof(C);
+  const double rw = 2.0 * gbytes * ngrids;
+  if (gbytes <= (size_t)kSmall2DBytes) {
+    const int threads = B * B / 4 >= 256 ? 256 : (B * B / 4 >= 32 ? B * B / 4 : 32);
+    pre(c, st);
+    k_fft2d_small<T><<<ngrids, threads, gbytes, st>>>(grids, lgB, tw, lgN);
+    post(c, "k_fft2d_small", st, rw);
+    return;
+  }
+  const int rpc = fft_rows_per_cta<T>(B);
+  const int cpc = fft_cols_per_cta<T>(B);
+  if (!rpc || !cpc) fail(SFFT2D_ERR_UNSUPPORTED, "bucket grid too large for the shared-memory FFT");
+  const long nrows = (long)ngrids * B;
+  pre(c, st);
+  k_fft_rows<T, C><<<(unsigned)((nrows + rpc - 1) / rpc), 256, (size_t)rpc * B * sizeof(C), st>>>(
+      (const C*)nullptr, grids, lgB, nrows, rpc, tw, lgN);
+  post(c, "k_fft_rows", st, rw);
+  pre(c, st);
+  k_fft_cols<T><<<(unsigned)(ngrids * (B / cpc)), 256, (size_t)cpc * B * sizeof(C), st>>>(
+      grids, lgB, cpc, tw, lgN);
+  post(c, "k_fft_cols", st, rw);
+}
+
+// Dense forward 2D FFT of the N x N input image (type Tin) into `out`.
+template <typename T, typename Tin>
+void dense_fft(sfft2d_ctx* c, const Tin* x, cplx<T>* out, int lgN, const cplx<T>* tw,
+               cudaStream_t st) {
+  using C = cplx<T>;
+  const int N = 1 << lgN;
+  const int rpc = fft_rows_per_cta<T>(N);
+  const int cpc = fft_cols_per_cta<T>(N);
+  if (!rpc || !cpc) fail(SFFT2D_ERR_UNSUPPORTED, "image side too large for the shared-memory FFT");
+  const double nn = (double)N * N;
+  pre(c, st);
+  k_fft_rows<T, Tin><<<(unsigned)((N + rpc - 1) / rpc), 256, (size_t)rpc * N * sizeof(C), st>>>(
+      x, out, lgN, N, rpc, tw, lgN);
+  post(c, "k_fft_rows_dense", st, nn * (sizeof(Tin) + sizeof(C)));
+  pre(c, st);
+  k_fft_cols<T><<<(unsigned)(N / cpc), 256, (size_t)cpc * N * sizeof(C), st>>>(out, lgN, cpc, tw,
+                                                                               lgN);
+  post(c, "k_fft_cols", st, 2 * nn * sizeof(C));
+}
+
 // Fold (+window, +permutation) and bucket FFT for `nloops` permutations.
 template <typename T, typename Tin>
 void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTables& tb,
@@ -222,23 +310,28 @@ void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTable
     const size_t dyn = (B < gm.TW) ? (size_t)nlt * gm.TW * sizeof(C) : 0;
     C* out = spec + (size_t)g0 * BB;
     C* dst = (gm.Z == 1) ? out : (C*)ws(c, "fold_part", (size_t)gm.Z * g * BB * sizeof(C));
+    // algorithmic bytes: the S(B)^2 support samples + the grid(s)/partials written
+    const double sup = (double)tb.support[lgB];
+    const double fold_bytes =
+        sup * sup * sizeof(Tin) + (double)gm.Z * g * BB * sizeof(C);
+    pre(c, st);
     if (g == 1)
       k_fold<Tin, T, 1, 2><<<grid, threads, dyn, st>>>(x, space, pp, g, gm, dst);
     else
       k_fold<Tin, T, kMaxFoldLoops, 1><<<grid, threads, dyn, st>>>(x, space, pp, g, gm, dst);
-    post(c, "k_fold");
+    post(c, "k_fold", st, fold_bytes);
     if (gm.Z == 1) {
-      ck(launch_fft2d<T>(out, lgB, g, tw, lgN, st), "fft2d");
-      c->launches += (BB * sizeof(C) <= (size_t)kSmall2DBytes) ? 1 : 2;
+      fft_grids<T>(c, out, lgB, g, tw, lgN, st);
     } else if (BB * sizeof(C) <= (size_t)kSmall2DBytes) {
+      pre(c, st);
       k_fold_reduce_fft_small<T><<<g, 256, BB * sizeof(C), st>>>(dst, gm.Z, g, lgB, pp, tw, lgN,
                                                                   out);
-      post(c, "k_fold_reduce_fft_small");
+      post(c, "k_fold_reduce_fft_small", st, (double)(gm.Z + 1) * g * BB * sizeof(C));
     } else {
+      pre(c, st);
       k_fold_reduce<T><<<grid_for((long long)BB * g), 256, 0, st>>>(dst, gm.Z, g, lgB, pp, out);
-      post(c, "k_fold_reduce");
-      ck(launch_fft2d<T>(out, lgB, g, tw, lgN, st), "fft2d");
-      c->launches += 2;
+      post(c, "k_fold_reduce", st, (double)(gm.Z + 1) * g * BB * sizeof(C));
+      fft_grids<T>(c, out, lgB, g, tw, lgN, st);
     }
   }
 }
@@ -248,10 +341,12 @@ void compact(sfft2d_ctx* c, const uint32_t* bits, const unsigned* cnts, long seg
              int32_t* out, long out_stride, unsigned* total_dev, cudaStream_t st) {
   const int nblk = blocks_for(seglen);
   unsigned* offs = (unsigned*)ws(c, "cmp_off", (size_t)nblk * nseg * sizeof(unsigned));
+  pre(c, st);
   k_scan_blocks<<<nseg, 1024, 0, st>>>(cnts, nblk, offs, total_dev);
-  post(c, "k_scan_blocks");
+  post(c, "k_scan_blocks", st, 0);
+  pre(c, st);
   k_compact_bits<<<dim3(nblk, nseg), kCmpThreads, 0, st>>>(bits, seglen, offs, out, out_stride);
-  post(c, "k_compact_bits");
+  post(c, "k_compact_bits", st, 0);
 }
 
 // Local maxima of one B x B magnitude grid -> row-major flat list; returns count.
@@ -263,8 +358,9 @@ unsigned local_maxima_dev(sfft2d_ctx* c, const T* mags, int lgB, const unsigned 
   uint32_t* bits = (uint32_t*)ws(c, "lm_bits", words_for(BB) * 4);
   unsigned* cnts = (unsigned*)ws(c, "lm_cnt", (size_t)nblk * 4);
   unsigned* tot = (unsigned*)ws(c, "lm_tot", 16);
+  pre(c, st);
   k_lmax_bits<T><<<dim3(nblk, 1), kCmpThreads, 0, st>>>(mags, lgB, 0, peak, floor_rel, bits, cnts);
-  post(c, "k_lmax_bits");
+  post(c, "k_lmax_bits", st, (double)BB * sizeof(T) + BB / 8.0);
   compact(c, bits, cnts, BB, 1, out, 0, tot, st);
   return read_u32(c, tot, st);
 }
@@ -276,26 +372,37 @@ void topk_bits(sfft2d_ctx* c, const T* vals, long seglen, int nseg, long long nu
   SelState* sst = (SelState*)ws(c, "sel_state", (size_t)nseg * sizeof(SelState));
   unsigned* hist = (unsigned*)ws(c, "sel_hist", (size_t)nseg * 256 * sizeof(unsigned));
   ck(cudaMemsetAsync(hist, 0, (size_t)nseg * 256 * sizeof(unsigned), st), "memset");
+  pre(c, st);
   k_sel_init<<<(nseg + 127) / 128, 128, 0, st>>>(sst, nseg, num, seglen);
-  post(c, "k_sel_init");
+  post(c, "k_sel_init", st, 0);
   const int nblk = blocks_for(seglen);
   if (num < seglen) {
     unsigned hb = (unsigned)std::max<long long>(1, std::min<long long>(256, (seglen + 4095) / 4096));
     for (int shift = 56; shift >= 0; shift -= 8) {
+      pre(c, st);
       k_radix_hist<T><<<dim3(hb, nseg), 256, 0, st>>>(vals, seglen, sst, shift, hist);
-      post(c, "k_radix_hist");
+      post(c, "k_radix_hist", st, 0);
+      pre(c, st);
       k_radix_pick<<<(nseg + 31) / 32, 32, 0, st>>>(sst, hist, shift, nseg);
-      post(c, "k_radix_pick");
+      post(c, "k_radix_pick", st, 0);
     }
   }
   unsigned* tie_blk = (unsigned*)ws(c, "sel_tie", (size_t)nblk * nseg * sizeof(unsigned));
   unsigned* tie_off = (unsigned*)ws(c, "sel_tieoff", (size_t)nblk * nseg * sizeof(unsigned));
+  pre(c, st);
   k_tie_counts<T><<<dim3(nblk, nseg), kCmpThreads, 0, st>>>(vals, seglen, sst, tie_blk);
-  post(c, "k_tie_counts");
+  post(c, "k_tie_counts", st, 0);
+  pre(c, st);
   k_scan_blocks<<<nseg, 1024, 0, st>>>(tie_blk, nblk, tie_off, nullptr);
-  post(c, "k_scan_blocks");
+  post(c, "k_scan_blocks", st, 0);
+  pre(c, st);
   k_select_bits<T><<<dim3(nblk, nseg), kCmpThreads, 0, st>>>(vals, seglen, sst, tie_off, bits, cnts);
-  post(c, "k_select_bits");
+  post(c, "k_select_bits", st, 0);
+}
+
+size_t hist_bytes(long nkeys, int mode) {
+  if (mode == kVoteAdd32) return (size_t)nkeys * 4;
+  return (size_t)((nkeys + 31) / 32) * 32;  // bytes, padded to whole 32-key groups
 }
 
 // keys (ascending) of histogram entries >= thr; returns the count (synchronises).
@@ -304,23 +411,18 @@ unsigned hist_compact(sfft2d_ctx* c, const uint32_t* hist, long nkeys, int mode,
   const int nblk = blocks_for(nkeys);
   uint32_t* bits = (uint32_t*)ws(c, "hc_bits", words_for(nkeys) * 4);
   unsigned* cnts = (unsigned*)ws(c, "hc_cnt", (size_t)nblk * 4);
+  pre(c, st);
   k_hist_bits<<<nblk, kCmpThreads, 0, st>>>(hist, nkeys, mode, thr, bits, cnts);
-  post(c, "k_hist_bits");
+  post(c, "k_hist_bits", st, (double)hist_bytes(nkeys, mode) + nkeys / 8.0);
   compact(c, bits, cnts, nkeys, 1, keys, 0, total_dev, st);
   return read_u32(c, total_dev, st);
 }
 
-size_t hist_bytes(long nkeys, int mode) {
-  if (mode == kVoteAdd32) return (size_t)nkeys * 4;
-  return (size_t)((nkeys + 31) / 32) * 32;  // bytes, padded to whole 32-key groups
-}
 
 template <typename T, typename Tin>
 void dense_xhat(sfft2d_ctx* c, const Tin* x, int lgN, const DevTables& tb, cplx<T>* xhat,
                 cudaStream_t st) {
-  ck(launch_dense_fft2d<T, Tin>(x, xhat, lgN, (const cplx<T>*)tb.tw[prec_of<T>()], st),
-     "dense fft2d");
-  c->launches += 2;
+  dense_fft<T, Tin>(c, x, xhat, lgN, (const cplx<T>*)tb.tw[prec_of<T>()], st);
 }
 
 // K6 + K7 + output compaction, shared by both algorithms.
@@ -342,9 +444,10 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
   if (dense) {
     // gain = freq[0]^2 = 1 for the all-pass window (hashing.py:228-246)
     const bool usable_all = 1.0 >= gain_floor;
+    pre(c, st);
     k_estimate_dense<T><<<grid_for(m), 256, 0, st>>>(xhat, keys, m_dev, usable_all, med, mags,
                                                       alive, peak);
-    post(c, "k_estimate_dense");
+    post(c, "k_estimate_dense", st, 0);
     n_alive = usable_all ? (long long)m : 0;
   } else {
     if (L > kMaxLoops) fail(SFFT2D_ERR_UNSUPPORTED, "more than 64 estimation loops");
@@ -355,13 +458,15 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
     C* vals = (C*)ws(c, "vals", (size_t)L * m * sizeof(C));
     uint8_t* usable = (uint8_t*)ws(c, "usable", (size_t)L * m);
     const T* freq = (const T*)tb.freq[P] + ((size_t)lgB << lgN);
+    pre(c, st);
     k_estimate<T><<<grid_for((long long)m * L), 256, 0, st>>>(
         grids, L, keys, m_dev, dp, lgN, lgB, freq, (const C*)tb.tw[P], gain_floor, vals, usable,
         (long)m);
-    post(c, "k_estimate");
+    post(c, "k_estimate", st, 0);
+    pre(c, st);
     k_median<T><<<grid_for(m, 128), 128, 0, st>>>(vals, usable, L, (long)m, m_dev, med, mags,
                                                    alive, alive_cnt, peak);
-    post(c, "k_median");
+    post(c, "k_median", st, 0);
     n_alive = read_u32(c, alive_cnt, st);
   }
   res->n_candidates = m;
@@ -381,8 +486,9 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
   }
   uint32_t* fb = (uint32_t*)ws(c, "fin_bits", words_for(m) * 4);
   unsigned* fc = (unsigned*)ws(c, "fin_cnt", (size_t)nblk * 4);
+  pre(c, st);
   k_final_bits<T><<<nblk, kCmpThreads, 0, st>>>(mags, alive, sel, (long)m, peak, prune_rel, fb, fc);
-  post(c, "k_final_bits");
+  post(c, "k_final_bits", st, 0);
   int32_t* pos = (int32_t*)ws(c, "fin_pos", (size_t)m * 4);
   unsigned* tot = (unsigned*)ws(c, "fin_tot", 16);
   compact(c, fb, fc, (long)m, 1, pos, 0, tot, st);
@@ -390,8 +496,9 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
   int64_t* oij = (int64_t*)ws(c, "out_ij", (size_t)count * 16);
   C* ov = (C*)ws(c, "out_v", (size_t)count * sizeof(C));
   if (count) {
+    pre(c, st);
     k_gather_out<T><<<grid_for(count), 256, 0, st>>>(pos, tot, keys, med, lgN, oij, ov);
-    post(c, "k_gather_out");
+    post(c, "k_gather_out", st, 0);
   }
   res->count = count;
   res->ordered_by_magnitude = cut ? 1 : 0;
@@ -448,8 +555,9 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   ck(cudaMemsetAsync(hist, 0, hist_bytes(nkeys, mode), st), "memset hist");
   unsigned* finite = (unsigned*)ws(c, "finite", 16);
   ck(cudaMemsetAsync(finite, 0, 16, st), "memset");
+  pre(c, st);
   k_check_finite<Tin><<<grid_for(nkeys, 256, kNumSMs * 8), 256, 0, st>>>(x, nkeys, finite);
-  post(c, "k_check_finite");
+  post(c, "k_check_finite", st, (double)nkeys * sizeof(Tin));
   bool finite_checked = false;
 
   std::memset(S, 0, sizeof(*S));
@@ -477,17 +585,19 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       M = (T*)ws(c, "xmag", (size_t)nkeys * sizeof(T));
       peakM = (unsigned long long*)ws(c, "xpeak", 16);
       ck(cudaMemsetAsync(peakM, 0, 16, st), "memset");
+      pre(c, st);
       k_mags<T><<<dim3(grid_for(nkeys, 256, kNumSMs * 8), 1), 256, 0, st>>>(xhat, nkeys, M, peakM);
-      post(c, "k_mags");
+      post(c, "k_mags", st, (double)nkeys * (sizeof(C) + sizeof(T)));
     }
   };
 
   auto vote_list = [&](int pi, int lgb, long long count) {
     const int w = n >> lgb;
     const long long len = (w == 1) ? 3 : std::min<long long>(w + 2, n);
+    pre(c, st);
     k_vote<<<dim3(grid_for(count * len * len, 256, kNumSMs * 8), 1), 256, 0, st>>>(
         maxlist, 0, nullptr, (long)count, dp + pi, lgN, lgb, 1, mode, 0, hist);
-    post(c, "k_vote");
+    post(c, "k_vote", st, (double)count * len * len * 4.0 + count * 4.0);
   };
 
   auto run_pass = [&](int bb) -> long long {
@@ -500,8 +610,9 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     if (bb == n) {
       ensure_xhat(true);
       T* G = (T*)ws(c, "grid_mag", (size_t)nkeys * sizeof(T));
+      pre(c, st);
       k_permute_grid<T><<<n, 256, (size_t)n * sizeof(T), st>>>(M, lgN, p.s1i, p.s2i, G);
-      post(c, "k_permute_grid");
+      post(c, "k_permute_grid", st, 2.0 * nkeys * sizeof(T));
       lmag = G;
       peak = peakM;
     } else {
@@ -511,9 +622,10 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       T* mg = (T*)ws(c, "grid_mag", BB * sizeof(T));
       unsigned long long* pk = (unsigned long long*)ws(c, "gpeak", 16);
       ck(cudaMemsetAsync(pk, 0, 16, st), "memset");
+      pre(c, st);
       k_mags<T><<<dim3(grid_for((long long)BB, 256, kNumSMs * 8), 1), 256, 0, st>>>(spec, (long)BB,
                                                                                    mg, pk);
-      post(c, "k_mags");
+      post(c, "k_mags", st, (double)BB * (sizeof(C) + sizeof(T)));
       lmag = mg;
       peak = pk;
     }
@@ -621,8 +733,9 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     if (have_votes) {
       nv = hist_compact(c, hist, nkeys, mode, 1u, keys, kt, st);
       int32_t* tal = (int32_t*)ws(c, "tallies", (size_t)std::max(nv, 1u) * 4);
+      pre(c, st);
       k_gather_tallies<<<grid_for(nv), 256, 0, st>>>(hist, mode, keys, kt, tal);
-      post(c, "k_gather_tallies");
+      post(c, "k_gather_tallies", st, 0);
     }
     S->n_votes = nv;
     S->perms_used = pidx;
@@ -692,19 +805,22 @@ void run_sfft(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, const s
   const long nkeys = (long)n * n;
   unsigned* finite = (unsigned*)ws(c, "finite", 16);
   ck(cudaMemsetAsync(finite, 0, 16, st), "memset");
+  pre(c, st);
   k_check_finite<Tin><<<grid_for(nkeys, 256, kNumSMs * 8), 256, 0, st>>>(x, nkeys, finite);
-  post(c, "k_check_finite");
+  post(c, "k_check_finite", st, (double)nkeys * sizeof(Tin));
 
   // location loops: L grids from one read of x, top-num bins per grid
   C* grids = (C*)ws(c, "loc_grids", (size_t)L * BB * sizeof(C));
   fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, hp.data(), L, grids, st);
   T* mags = (T*)ws(c, "loc_mags", (size_t)L * BB * sizeof(T));
+  pre(c, st);
   k_mags<T><<<dim3(grid_for(BB, 256, 1024), L), 256, 0, st>>>(grids, BB, mags, nullptr);
-  post(c, "k_mags");
+  post(c, "k_mags", st, 0);
   int32_t* bins = (int32_t*)ws(c, "loc_bins", (size_t)L * num * 4);
   if (num >= BB) {
+    pre(c, st);
     k_iota_segments<<<grid_for(BB * L), 256, 0, st>>>(bins, BB, L);
-    post(c, "k_iota_segments");
+    post(c, "k_iota_segments", st, 0);
   } else {
     const int nblk = blocks_for(BB);
     uint32_t* sb = (uint32_t*)ws(c, "loc_selbits", (size_t)L * words_for(BB) * 4);
@@ -724,21 +840,24 @@ void run_sfft(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, const s
   int cmode = kVoteOrBit;
   const uint32_t* chist = hist;
   if (L <= 8) {
+    pre(c, st);
     k_vote<<<dim3(grid_for(per, 256, kNumSMs * 8), L), 256, 0, st>>>(bins, (long)num, nullptr, (long)num, dp,
                                                                    lgN, lgb, 1, kVoteOrBit, 0, hist);
-    post(c, "k_vote");
+    post(c, "k_vote", st, 0);
   } else {
     uint32_t* counts = (uint32_t*)ws(c, "hist_cnt", hist_bytes(nkeys, kVoteAdd8));
     ck(cudaMemsetAsync(counts, 0, hist_bytes(nkeys, kVoteAdd8), st), "memset");
     const long nw = (long)(hist_bytes(nkeys, kVoteAdd8) / 4);
     for (int g0 = 0; g0 < L; g0 += 8) {
       const int g = std::min(8, L - g0);
+      pre(c, st);
       k_vote<<<dim3(grid_for(per, 256, kNumSMs * 8), g), 256, 0, st>>>(
           bins + (size_t)g0 * num, (long)num, nullptr, (long)num, dp + g0, lgN, lgb, 1, kVoteOrBit,
           0, hist);
-      post(c, "k_vote");
+      post(c, "k_vote", st, 0);
+      pre(c, st);
       k_mask_to_counts<<<grid_for(nw, 256, kNumSMs * 8), 256, 0, st>>>(hist, counts, nw);
-      post(c, "k_mask_to_counts");
+      post(c, "k_mask_to_counts", st, 0);
     }
     cmode = kVoteAdd8;
     chist = counts;
@@ -847,6 +966,7 @@ void sfft2d_ctx_destroy(sfft2d_ctx* c) {
       cudaFree(t.tw[p]);
     }
   if (c->pinned) cudaFreeHost(c->pinned);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
   delete c;
 }
 
@@ -876,8 +996,56 @@ int sfft2d_ctx_set_tables(sfft2d_ctx* c, int n, double dpass, double dstop, cons
     up(space, rows, &t.space[SFFT2D_FP64], &t.space[SFFT2D_FP32]);
     up(freq, rows, &t.freq[SFFT2D_FP64], &t.freq[SFFT2D_FP32]);
     up(twiddle, (size_t)2 * n, &t.tw[SFFT2D_FP64], &t.tw[SFFT2D_FP32]);
+    t.support.assign(t.lgn + 1, n);
+    for (int lb = 0; lb <= t.lgn; ++lb) {
+      int nz = 0;
+      for (int i = 0; i < n; ++i) nz += space[(size_t)lb * n + i] != 0.0;
+      t.support[lb] = nz;
+    }
     c->tables.push_back(t);
   });
+}
+
+int sfft2d_ctx_set_profiling(sfft2d_ctx* c, int enable) {
+  return guarded(c, [&] {
+    c->profiling = enable != 0;
+    c->prof.clear();
+    c->ev_used = 0;
+    c->prof_open = false;
+  });
+}
+
+int64_t sfft2d_ctx_profile_report(sfft2d_ctx* c, char* buf, int64_t buflen) {
+  std::string out;
+  int rc = guarded(c, [&] {
+    ck(cudaDeviceSynchronize(), "sync");
+    std::map<std::string, std::pair<long long, std::pair<double, double>>> agg;
+    for (auto& r : c->prof) {
+      if (!r.name || !r.b) continue;
+      float ms = 0.f;
+      ck(cudaEventElapsedTime(&ms, r.a, r.b), "cudaEventElapsedTime");
+      auto& e = agg[r.name];
+      e.first += 1;
+      e.second.first += ms;
+      e.second.second += r.bytes;
+    }
+    for (auto& kv : agg) {
+      char line[256];
+      snprintf(line, sizeof(line), "%s %lld %.6f %.0f\n", kv.first.c_str(), kv.second.first,
+               kv.second.second.first, kv.second.second.second);
+      out += line;
+    }
+    c->prof.clear();
+    c->ev_used = 0;
+    c->prof_open = false;
+  });
+  if (rc != SFFT2D_OK) return rc;
+  if (buf && buflen > 0) {
+    const size_t n = std::min<size_t>(out.size(), (size_t)buflen - 1);
+    memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return (int64_t)out.size();
 }
 
 int sfft2d_sfft(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host,
@@ -1003,9 +1171,8 @@ int sfft2d_fft2d(sfft2d_ctx* c, void* grids, int b, int count, int n_table, int 
     cudaStream_t st = (cudaStream_t)stream;
     dispatch_prec(precision, [&](auto t) {
       using T = decltype(t);
-      ck(launch_fft2d<T>((cplx<T>*)grids, ilog2(b), count, (const cplx<T>*)tb.tw[prec_of<T>()],
-                         tb.lgn, st),
-         "fft2d");
+      fft_grids<T>(c, (cplx<T>*)grids, ilog2(b), count, (const cplx<T>*)tb.tw[prec_of<T>()],
+                   tb.lgn, st);
     });
   });
 }
@@ -1021,8 +1188,9 @@ int sfft2d_local_maxima(sfft2d_ctx* c, const void* grid, int b, double mag_floor
       T* mg = (T*)ws(c, "api_mag", BB * sizeof(T));
       unsigned long long* pk = (unsigned long long*)ws(c, "api_peak", 16);
       ck(cudaMemsetAsync(pk, 0, 16, st), "memset");
+      pre(c, st);
       k_mags<T><<<dim3(grid_for(BB, 256, 1024), 1), 256, 0, st>>>((const cplx<T>*)grid, BB, mg, pk);
-      post(c, "k_mags");
+      post(c, "k_mags", st, 0);
       int32_t* tmp = (int32_t*)ws(c, "api_lm", (size_t)(BB / 4 + 64) * 4);
       const long long cnt = local_maxima_dev<T>(c, mg, ilog2(b), pk, mag_floor, tmp, st);
       if (count) *count = cnt;
@@ -1043,12 +1211,14 @@ int sfft2d_top_bins(sfft2d_ctx* c, const void* grids, int b, int nseg, int64_t n
       const long BB = (long)b * b;
       if (num > BB) fail(SFFT2D_ERR_VALUE, "num exceeds the number of bins");
       T* mg = (T*)ws(c, "api_mag", (size_t)nseg * BB * sizeof(T));
+      pre(c, st);
       k_mags<T><<<dim3(grid_for(BB, 256, 1024), nseg), 256, 0, st>>>((const cplx<T>*)grids, BB, mg,
                                                                      nullptr);
-      post(c, "k_mags");
+      post(c, "k_mags", st, 0);
       if (num >= BB) {
+        pre(c, st);
         k_iota_segments<<<grid_for(BB * nseg), 256, 0, st>>>(out_flat, BB, nseg);
-        post(c, "k_iota_segments");
+        post(c, "k_iota_segments", st, 0);
         return;
       }
       const int nblk = blocks_for(BB);

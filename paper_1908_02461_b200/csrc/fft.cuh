@@ -177,45 +177,4 @@ inline int fft_rows_per_cta(int B) {
   return r;
 }
 
-// In-place 2D FFT of `ngrids` contiguous B x B grids.
-template <typename T>
-inline cudaError_t launch_fft2d(cplx<T>* grids, int lgB, int ngrids, const cplx<T>* tw, int lgN,
-                                cudaStream_t st) {
-  using C = cplx<T>;
-  const int B = 1 << lgB;
-  const size_t gbytes = (size_t)B * B * sizeof(C);
-  if (gbytes <= (size_t)kSmall2DBytes) {
-    int threads = B * B / 4 >= 256 ? 256 : (B * B / 4 >= 32 ? B * B / 4 : 32);
-    k_fft2d_small<T><<<ngrids, threads, gbytes, st>>>(grids, lgB, tw, lgN);
-    return cudaGetLastError();
-  }
-  const int rpc = fft_rows_per_cta<T>(B);
-  const int cpc = fft_cols_per_cta<T>(B);
-  if (!rpc || !cpc) return cudaErrorInvalidConfiguration;
-  const long nrows = (long)ngrids * B;
-  const size_t rsm = (size_t)rpc * B * sizeof(C);
-  k_fft_rows<T, C><<<(unsigned)((nrows + rpc - 1) / rpc), 256, rsm, st>>>(
-      (const C*)nullptr, grids, lgB, nrows, rpc, tw, lgN);
-  const size_t csm = (size_t)cpc * B * sizeof(C);
-  k_fft_cols<T><<<(unsigned)(ngrids * (B / cpc)), 256, csm, st>>>(grids, lgB, cpc, tw, lgN);
-  return cudaGetLastError();
-}
-
-// Dense forward 2D FFT of an N x N input image into `out` (N x N, type T).
-template <typename T, typename Tin>
-inline cudaError_t launch_dense_fft2d(const Tin* x, cplx<T>* out, int lgN, const cplx<T>* tw,
-                                      cudaStream_t st) {
-  using C = cplx<T>;
-  const int N = 1 << lgN;
-  const int rpc = fft_rows_per_cta<T>(N);
-  const int cpc = fft_cols_per_cta<T>(N);
-  if (!rpc || !cpc) return cudaErrorInvalidConfiguration;
-  const size_t rsm = (size_t)rpc * N * sizeof(C);
-  k_fft_rows<T, Tin><<<(unsigned)((N + rpc - 1) / rpc), 256, rsm, st>>>(x, out, lgN, N, rpc, tw,
-                                                                        lgN);
-  const size_t csm = (size_t)cpc * N * sizeof(C);
-  k_fft_cols<T><<<(unsigned)(N / cpc), 256, csm, st>>>(out, lgN, cpc, tw, lgN);
-  return cudaGetLastError();
-}
-
 }  // namespace sfft

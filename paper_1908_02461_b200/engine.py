@@ -137,6 +137,7 @@ def sfft2d_arrays(x, cfg: SfftConfig, rng, *, cache: WindowCache | None = None,
             ptr, on_host = img.host.ctypes.data, 1
         ctx.check(ctx.lib.sfft2d_sfft(ctx.handle, ptr, img.dtype_code, on_host, ctypes.byref(ccfg),
                                       _native.perm_array(perms), prec, st, ctypes.byref(res)))
+        ctx.last_launches = int(res.gpu_launches)
         return _fetch(ctx, res, st, prec)
 
 

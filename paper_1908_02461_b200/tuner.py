@@ -195,6 +195,7 @@ def _run_ats(x, cfg: TunerConfig, est_loops: int, rng, precision, device, estima
                                                 prec, st, ctypes.byref(sc))
         stream_p.consume(int(sc.perms_used))
         ctx.check(rc)
+        ctx.last_launches = int(res.gpu_launches)
         state = _state(sc)
         if not estimate:
             nv = int(sc.n_votes)
