@@ -165,11 +165,10 @@ class Context:
 
     def profile_report(self) -> dict:
         """{kernel: (launches, total_ms, total_algorithmic_bytes)} since enabling."""
-        n = self.lib.sfft2d_ctx_profile_report(self.handle, None, 0)
+        buf = ctypes.create_string_buffer(1 << 20)
+        n = self.lib.sfft2d_ctx_profile_report(self.handle, buf, len(buf))
         if n < 0:
             self.check(int(n))
-        buf = ctypes.create_string_buffer(int(n) + 1)
-        self.lib.sfft2d_ctx_profile_report(self.handle, buf, n + 1)
         out = {}
         for line in buf.value.decode().splitlines():
             name, cnt, ms, by = line.split()
