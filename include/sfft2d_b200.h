@@ -82,6 +82,7 @@ typedef struct {
   int64_t hist_count[SFFT2D_MAX_HISTORY];
   double hist_ratio[SFFT2D_MAX_HISTORY];
   int32_t hist_has_ratio[SFFT2D_MAX_HISTORY];
+  double hist_us[SFFT2D_MAX_HISTORY];   /* host wall time of each pass (diagnostic) */
   int32_t converged;
   int64_t detected_k;
   int32_t b_detect, b_estimate, vote_passes;

@@ -59,6 +59,7 @@ class TunerStateC(ctypes.Structure):
                 ("hist_count", ctypes.c_int64 * MAX_HISTORY),
                 ("hist_ratio", ctypes.c_double * MAX_HISTORY),
                 ("hist_has_ratio", ctypes.c_int32 * MAX_HISTORY),
+                ("hist_us", ctypes.c_double * MAX_HISTORY),
                 ("converged", ctypes.c_int32), ("detected_k", ctypes.c_int64),
                 ("b_detect", ctypes.c_int32), ("b_estimate", ctypes.c_int32),
                 ("vote_passes", ctypes.c_int32), ("perms_used", ctypes.c_int32),

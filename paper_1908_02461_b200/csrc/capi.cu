@@ -9,6 +9,7 @@
 #include "../../include/sfft2d_b200.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -181,6 +182,9 @@ void allow_all_T() {
   allow_smem(k_fftcB<T, true, true>);
   allow_smem(k_lmax_rows<T, false>);
   allow_smem(k_lmax_rows<T, true>);
+  allow_smem(k_lmax_rows<T, false, true>);
+  allow_smem(k_lmax_rows<T, true, true>);
+  allow_smem(k_small_pass<T>);
 }
 
 const DevTables& find_tables(sfft2d_ctx* c, int n, double dpass, double dstop) {
@@ -324,7 +328,7 @@ void fft2d_grids(sfft2d_ctx* c, cplx<T>* grids, int lgB, int ngrids, const cplx<
 // optional |x_hat| + peak.  `scratch` holds the row-pass result.
 template <typename T, typename Tin>
 void dense_fft(sfft2d_ctx* c, const Tin* x, cplx<T>* out, T* mags, unsigned long long* peak,
-               int lgN, const cplx<T>* tw, cudaStream_t st) {
+               int lgN, const cplx<T>* tw, cudaStream_t st, unsigned* nonfinite = nullptr) {
   using C = cplx<T>;
   const int N = 1 << lgN;
   const FftPlan2D pl = plan_fft2d<T>(lgN);
@@ -334,7 +338,7 @@ void dense_fft(sfft2d_ctx* c, const Tin* x, cplx<T>* out, T* mags, unsigned long
   C* scratch = (C*)ws(c, "fft_scratch", (size_t)N * N * sizeof(C));
   pre(c, st);
   k_fftr<T, Tin, true, false><<<(unsigned)(N / pl.rows_per_cta), pl.row_threads, pl.smem_row,
-                                st>>>(x, scratch, nullptr, nullptr, lgN, 2 * lgN, tw, lgN);
+                                st>>>(x, scratch, nullptr, nullptr, lgN, 2 * lgN, tw, lgN, nonfinite);
   post(c, "k_fftr_dense", st, nn * (sizeof(Tin) + sizeof(C)));
   const double wb = nn * sizeof(C) + (mags ? nn * sizeof(T) : 0);
   if (pl.four_step) {
@@ -360,6 +364,41 @@ void dense_fft(sfft2d_ctx* c, const Tin* x, cplx<T>* out, T* mags, unsigned long
           scratch, out, nullptr, nullptr, lgN, pl.lgccB, tw, lgN);
     post(c, "k_fftc", st, nn * sizeof(C) + wb);
   }
+}
+
+// One fold launch for g <= 8 loops; returns where the result lives:
+// natural-order partials [Z][g][B][B] (Z > 1) or the permuted grids (Z == 1).
+struct FoldOut {
+  void* data;
+  int Z;
+};
+
+template <typename T, typename Tin>
+FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTables& tb,
+                    const Perm* hp, int g, void* y_direct, cudaStream_t st) {
+  using C = cplx<T>;
+  const int B = 1 << lgB;
+  const size_t BB = (size_t)B * B;
+  const T* space = (const T*)tb.space[prec_of<T>()] + ((size_t)lgB << lgN);
+  PermPack pp;
+  std::memset(&pp, 0, sizeof(pp));
+  for (int i = 0; i < g; ++i) pp.p[i] = hp[i];
+  const int cpt = (g == 1) ? 2 : 1;
+  const FoldGeom gm = fold_geometry(lgN, lgB, cpt);
+  const int threads = gm.TW / cpt;
+  const dim3 grid(gm.ktiles, B, gm.Z);
+  const int nlt = (g == 1) ? 1 : kMaxFoldLoops;
+  const size_t dyn = (B < gm.TW) ? (size_t)nlt * gm.TW * sizeof(C) : 0;
+  C* dst = (gm.Z == 1) ? (C*)y_direct : (C*)ws(c, "fold_part", (size_t)gm.Z * g * BB * sizeof(C));
+  const double sup = (double)tb.support[lgB];
+  const double fold_bytes = sup * sup * sizeof(Tin) + (double)gm.Z * g * BB * sizeof(C);
+  pre(c, st);
+  if (g == 1)
+    k_fold<Tin, T, 1, 2><<<grid, threads, dyn, st>>>(x, space, pp, g, gm, dst);
+  else
+    k_fold<Tin, T, kMaxFoldLoops, 1><<<grid, threads, dyn, st>>>(x, space, pp, g, gm, dst);
+  post(c, "k_fold", st, fold_bytes);
+  return FoldOut{dst, gm.Z};
 }
 
 // Fold (+window, +permutation) and bucket FFT for `nloops` permutations.
@@ -452,13 +491,14 @@ unsigned local_maxima_dev(sfft2d_ctx* c, const T* mags, int lgB, const unsigned 
   unsigned* cnts = (unsigned*)ws(c, "lm_cnt", (size_t)nblk * 4);
   unsigned* tot = (unsigned*)ws(c, "lm_tot", 16);
   if (B >= 32) {
-    const int unit = B >= kCmpElems ? 1 : kCmpElems / B;      // rows per 8192-bin block
-    int rb = (int)((96 * 1024) / ((size_t)B * sizeof(T))) - 2;
-    rb = std::max(unit, (rb / unit) * unit);
-    if (rb > B) rb = B;
+    // tile = rb output rows (+2 halo rows staged in smem); ~B/128 rows so that
+    // small grids still spread over many SMs, capped by shared memory
+    const int smem_rows = (int)((96 * 1024) / ((size_t)B * sizeof(T)));
+    int rb = std::max(1, std::min(B / 128, smem_rows - 2));
+    while (B % rb) --rb;
     const size_t sm = (size_t)(rb + 2) * B * sizeof(T);
     if (sm > kMaxDynSmem) fail(SFFT2D_ERR_UNSUPPORTED, "grid too large for the local-maximum tile");
-    if ((size_t)rb * B > (size_t)32 * kCmpElems) rb = 32 * kCmpElems / B;
+    ck(cudaMemsetAsync(cnts, 0, (size_t)nblk * 4, st), "memset");
     pre(c, st);
     if (perm)
       k_lmax_rows<T, true><<<B / rb, 512, sm, st>>>(mags, lgB, s1, s2, rb, peak, floor_rel, bits, cnts);
@@ -473,6 +513,29 @@ unsigned local_maxima_dev(sfft2d_ctx* c, const T* mags, int lgB, const unsigned 
   }
   compact(c, bits, cnts, BB, 1, out, 0, tot, st);
   return read_u32(c, tot, st);
+}
+
+// Tuner local maxima: unordered list + device count (no host sync).
+template <typename T>
+void lmax_tuner(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long long* peak,
+                double floor_rel, int32_t* list, unsigned* count, cudaStream_t st, bool perm,
+                unsigned s1, unsigned s2) {
+  const int B = 1 << lgB;
+  const int smem_rows = (int)((96 * 1024) / ((size_t)B * sizeof(T)));
+  int rb = std::max(1, std::min(B / 128, smem_rows - 2));
+  while (B % rb) --rb;
+  const size_t sm = (size_t)(rb + 2) * B * sizeof(T) + (size_t)rb * B / 32 * sizeof(unsigned);
+  if (sm > kMaxDynSmem) fail(SFFT2D_ERR_UNSUPPORTED, "grid too large for the local-maximum tile");
+  ck(cudaMemsetAsync(count, 0, sizeof(unsigned), st), "memset");
+  const double by = (double)B * B * sizeof(T);
+  pre(c, st);
+  if (perm)
+    k_lmax_rows<T, true, true><<<B / rb, 512, sm, st>>>(mags, lgB, s1, s2, rb, peak, floor_rel,
+                                                        nullptr, nullptr, list, count);
+  else
+    k_lmax_rows<T, false, true><<<B / rb, 512, sm, st>>>(mags, lgB, 1, 1, rb, peak, floor_rel,
+                                                         nullptr, nullptr, list, count);
+  post(c, "k_lmax_rows", st, by);
 }
 
 // Exact top-`num` selection bitmask per segment (ties -> lowest index).
@@ -531,9 +594,10 @@ unsigned hist_compact(sfft2d_ctx* c, const uint32_t* hist, long nkeys, int mode,
 
 template <typename T, typename Tin>
 void dense_xhat(sfft2d_ctx* c, const Tin* x, int lgN, const DevTables& tb, cplx<T>* xhat, T* mags,
-                unsigned long long* peak, cudaStream_t st) {
+                unsigned long long* peak, cudaStream_t st, unsigned* nonfinite = nullptr) {
   if (peak) ck(cudaMemsetAsync(peak, 0, sizeof(unsigned long long), st), "memset");
-  dense_fft<T, Tin>(c, x, xhat, mags, peak, lgN, (const cplx<T>*)tb.tw[prec_of<T>()], st);
+  dense_fft<T, Tin>(c, x, xhat, mags, peak, lgN, (const cplx<T>*)tb.tw[prec_of<T>()], st,
+                    nonfinite);
 }
 
 // K6 + K7 + output compaction, shared by both algorithms.
@@ -664,12 +728,11 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   const int mode = (4 * (max_iters + 2) <= 255) ? kVoteAdd8 : kVoteAdd32;
   uint32_t* hist = (uint32_t*)ws(c, "hist", hist_bytes(nkeys, mode));
   ck(cudaMemsetAsync(hist, 0, hist_bytes(nkeys, mode), st), "memset hist");
+  // NaN/Inf check (as_complex_matrix, corefft.py:49-50): fused into the dense
+  // FFT's row pass when the trajectory reaches B = N, else one pass at the end
   unsigned* finite = (unsigned*)ws(c, "finite", 16);
   ck(cudaMemsetAsync(finite, 0, 16, st), "memset");
-  pre(c, st);
-  k_check_finite<Tin><<<grid_for(nkeys, 256, kNumSMs * 8), 256, 0, st>>>(x, nkeys, finite);
-  post(c, "k_check_finite", st, (double)nkeys * sizeof(Tin));
-  bool finite_checked = false;
+  bool finite_scanned = false;
 
   std::memset(S, 0, sizeof(*S));
   int b = std::max(4, std::min(cf.b0, n));
@@ -693,7 +756,8 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
         M = (T*)ws(c, "xmag", (size_t)nkeys * sizeof(T));
         peakM = (unsigned long long*)ws(c, "xpeak", 16);
       }
-      dense_xhat<T, Tin>(c, x, lgN, tb, xhat, M, peakM, st);   // |x_hat| + peak fused
+      dense_xhat<T, Tin>(c, x, lgN, tb, xhat, M, peakM, st, finite);   // |x_hat|, peak, NaN check
+      finite_scanned = true;
       xhat_ready = true;
     }
     if (need_mags && !M) {
@@ -704,13 +768,16 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     }
   };
 
-  auto vote_list = [&](int pi, int lgb, long long count) {
+  unsigned* cnt_dev = (unsigned*)ws(c, "lm_count", 16);
+  // vote on the maxima list of the pass just run; queued before the host
+  // sync, with the vote budget (tuner.py:165,175) applied on the device
+  auto vote_list = [&](int pi, int lgb, long long budget_dev) {
     const int w = n >> lgb;
     const long long len = (w == 1) ? 3 : std::min<long long>(w + 2, n);
     pre(c, st);
-    k_vote<<<dim3(grid_for(count * len * len, 256, kNumSMs * 8), 1), 256, 0, st>>>(
-        maxlist, 0, nullptr, (long)count, dp + pi, lgN, lgb, 1, mode, 0, hist);
-    post(c, "k_vote", st, (double)count * len * len * 4.0 + count * 4.0);
+    k_vote<<<dim3(kNumSMs * 2, 1), 256, 0, st>>>(maxlist, 0, cnt_dev, 0, dp + pi, lgN, lgb, 1, mode,
+                                                 0, hist, budget_dev);
+    post(c, "k_vote", st, (double)len * len * 4.0);
   };
 
   auto run_pass = [&](int bb) -> long long {
@@ -718,37 +785,45 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     const int pi = pidx++;
     const Perm& p = hp[pi];
     const int lgb = ilog2(bb);
-    long long count;
+    const size_t BB = (size_t)bb * bb;
     if (bb == n) {
       // B = N: |Z_p[k1, k2]| = |x_hat[s1i k1, s2i k2]| — one dense FFT serves every pass
       ensure_xhat(true);
-      count = local_maxima_dev<T>(c, M, lgb, peakM, cf.mag_floor, maxlist, st, true, p.s1i, p.s2i);
+      lmax_tuner<T>(c, M, lgb, peakM, cf.mag_floor, maxlist, cnt_dev, st, true, p.s1i, p.s2i);
+    } else if (BB * sizeof(C) <= (size_t)kSmall2DBytes) {
+      C* y = (C*)ws(c, "fold_y", BB * sizeof(C));
+      const FoldOut fo = fold_launch<T, Tin>(c, x, lgN, lgb, tb, &p, 1, y, st);
+      pre(c, st);
+      k_small_pass<T><<<1, 1024, BB * (sizeof(C) + sizeof(T)), st>>>(
+          (const C*)fo.data, fo.Z, fo.Z == 1, lgb, p, (const C*)tb.tw[prec_of<T>()], lgN,
+          cf.mag_floor, maxlist, cnt_dev);
+      post(c, "k_small_pass", st, (double)(fo.Z + 1) * BB * sizeof(C));
     } else {
-      const size_t BB = (size_t)bb * bb;
       T* mg = (T*)ws(c, "grid_mag", BB * sizeof(T));
       unsigned long long* pk = (unsigned long long*)ws(c, "gpeak", 16);
       fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, &p, 1, (C*)nullptr, mg, pk, st);
-      count = local_maxima_dev<T>(c, mg, lgb, pk, cf.mag_floor, maxlist, st);
+      lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, maxlist, cnt_dev, st, false, 1, 1);
     }
-    if (!finite_checked) {
-      finite_checked = true;
-      if (read_u32(c, finite, st)) fail(SFFT2D_ERR_VALUE, "matrix contains NaN or Inf");
-    }
+    vote_list(pi, lgb, budget);
+    const long long count = read_u32(c, cnt_dev, st);
     last_valid = true;
     last_b = bb;
     last_pi = pi;
     last_count = count;
     const long long w = n / bb;
-    if (count > 0 && count * (w + 2) * (w + 2) <= budget) {
+    if (count > 0 && count * (w + 2) * (w + 2) <= budget) {   // host mirror of the device test
       ++vote_passes;
       have_votes = true;
-      vote_list(pi, lgb, count);
     }
     return count;
   };
 
+  auto t_pass = std::chrono::steady_clock::now();
   auto push = [&](int bb, long long cnt, double r, bool has) {
     const int i = S->passes++;
+    const auto now = std::chrono::steady_clock::now();
+    S->hist_us[i] = std::chrono::duration<double, std::micro>(now - t_pass).count();
+    t_pass = now;
     S->hist_bins[i] = bb;
     S->hist_count[i] = cnt;
     S->hist_ratio[i] = has ? r : NAN;
@@ -812,6 +887,15 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     bdet = 0;
     for (int i = 0; i < S->passes; ++i) bdet = std::max(bdet, S->hist_bins[i]);
   }
+  if (!finite_scanned) {
+    pre(c, st);
+    k_check_finite<Tin><<<grid_for(nkeys, 256, kNumSMs * 8), 256, 0, st>>>(x, nkeys, finite);
+    post(c, "k_check_finite", st, (double)nkeys * sizeof(Tin));
+  }
+  if (read_u32(c, finite, st)) {
+    std::memset(S, 0, sizeof(*S));
+    fail(SFFT2D_ERR_VALUE, "matrix contains NaN or Inf");
+  }
   S->converged = converged ? 1 : 0;
   S->detected_k = maxc;
   S->b_detect = bdet;
@@ -819,7 +903,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   if (!have_votes && last_valid && maxc > 0) {
     // every pass exceeded the vote budget: fall back to the final pass (tuner.py:228-234)
     if (last_count > 0) {
-      vote_list(last_pi, ilog2(last_b), last_count);
+      vote_list(last_pi, ilog2(last_b), 0);   // cnt_dev still holds the last pass's count
       have_votes = true;
     }
     vote_passes = 1;

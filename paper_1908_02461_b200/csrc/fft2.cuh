@@ -223,16 +223,22 @@ __device__ __forceinline__ void fft_tile(cplx<T>* s, int lgL, int nseq_lg, int r
 
 // Row pass: CTA = `rows` rows of length L (blockDim = rows * L / 16).
 template <typename T, typename Tin, bool WC, bool WM>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(512, (sizeof(T) == 4) ? 2 : 1)
 k_fftr(const Tin* src, cplx<T>* dst, T* __restrict__ mags, unsigned long long* __restrict__ peak,
-       int lgL, int grid_lg, const cplx<T>* __restrict__ tw, int lgN) {
+       int lgL, int grid_lg, const cplx<T>* __restrict__ tw, int lgN,
+       unsigned* __restrict__ nonfinite = nullptr) {
   using C = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* s = reinterpret_cast<C*>(smem_raw);
   const int rows_lg = __ffs((blockDim.x * 16) >> lgL) - 1;
   const size_t e0 = ((size_t)blockIdx.x << rows_lg) << lgL;
   unsigned long long best = 0;
-  auto ld = [&](int seq, int u) { return load_c<T>(src + e0 + ((size_t)seq << lgL) + u); };
+  bool bad = false;
+  auto ld = [&](int seq, int u) {
+    const Tin w = src[e0 + ((size_t)seq << lgL) + u];
+    if (nonfinite) bad |= !isfinite(w.x) || !isfinite(w.y);   // as_complex_matrix check
+    return mk<T>((T)w.x, (T)w.y);
+  };
   auto st = [&](int seq, int k, C v) {
     const size_t o = e0 + ((size_t)seq << lgL) + k;
     if (WC) dst[o] = v;
@@ -243,12 +249,13 @@ k_fftr(const Tin* src, cplx<T>* dst, T* __restrict__ mags, unsigned long long* _
     }
   };
   fft_tile<T, false>(s, lgL, rows_lg, pad_row(1 << lgL), tw, lgN, ld, st);
+  if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
   if (WM && peak) flush_peak(best, peak + (e0 >> grid_lg));
 }
 
 // Column pass for L <= 512: CTA = `cc` adjacent columns of one grid (W = L).
 template <typename T, bool WC, bool WM>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(512, (sizeof(T) == 4) ? 2 : 1)
 k_fftc(const cplx<T>* src, cplx<T>* dst, T* __restrict__ mags,
        unsigned long long* __restrict__ peak, int lgL, int lgcc, const cplx<T>* __restrict__ tw,
        int lgN) {
@@ -275,7 +282,7 @@ k_fftc(const cplx<T>* src, cplx<T>* dst, T* __restrict__ mags,
 // Four-step column pass A (in place): length-L1 DFTs over rows n2 + L2*n1, then
 // twiddle by W_L^{n2 k1}; grid = (column tiles, n2, grid index).
 template <typename T>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(512, (sizeof(T) == 4) ? 2 : 1)
 k_fftcA(cplx<T>* data, int lgL1, int lgL2, int lgcc, const cplx<T>* __restrict__ tw, int lgN) {
   using C = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -294,7 +301,7 @@ k_fftcA(cplx<T>* data, int lgL1, int lgL2, int lgcc, const cplx<T>* __restrict__
 
 // Four-step column pass B: length-L2 DFTs over rows L2*k1 + n2 -> row k1 + L1*k2.
 template <typename T, bool WC, bool WM>
-__global__ void __launch_bounds__(512)
+__global__ void __launch_bounds__(512, (sizeof(T) == 4) ? 2 : 1)
 k_fftcB(const cplx<T>* __restrict__ src, cplx<T>* __restrict__ dst, T* __restrict__ mags,
         unsigned long long* __restrict__ peak, int lgL1, int lgL2, int lgcc,
         const cplx<T>* __restrict__ tw, int lgN) {

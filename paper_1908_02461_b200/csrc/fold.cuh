@@ -289,6 +289,74 @@ __global__ void __launch_bounds__(1024) k_fold_reduce_fft_small(const cplx<T>* _
   for (int e = threadIdx.x; e < BB; e += blockDim.x) out[e] = s[e];
 }
 
+// Tuner pass for small grids (B*B*sizeof(C) <= kSmall2DBytes), one CTA:
+// reduce the fold partials (or take the already permuted grid), 2D FFT in
+// shared memory, |Z| and its peak, strict 8-neighbour toroidal maxima above
+// floor_rel * peak, appended (unordered) to `list` with the count in `count`.
+template <typename T>
+__global__ void __launch_bounds__(1024)
+k_small_pass(const cplx<T>* __restrict__ part, int Z, bool permuted, int lgB, Perm p,
+             const cplx<T>* __restrict__ tw, int lgN, double floor_rel,
+             int32_t* __restrict__ list, unsigned* __restrict__ count) {
+  using C = cplx<T>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* s = reinterpret_cast<C*>(smem_raw);
+  const int B = 1 << lgB, BB = B * B;
+  T* m = reinterpret_cast<T*>(s + BB);
+  __shared__ unsigned long long s_peak;
+  __shared__ unsigned s_n;
+  if (threadIdx.x == 0) { s_peak = 0; s_n = 0; }
+  const unsigned maskB = (unsigned)B - 1u;
+  for (int e = threadIdx.x; e < BB; e += blockDim.x) {
+    unsigned a = (unsigned)(e >> lgB), b = (unsigned)(e & (B - 1));
+    C v;
+    if (permuted) {
+      v = part[e];
+    } else {
+      v = sum_partials(part + e, (size_t)BB, Z);
+      a = (p.s1i * (a - p.t1)) & maskB;
+      b = (p.s2i * (b - p.t2)) & maskB;
+    }
+    s[bitrev(a, lgB) * B + bitrev(b, lgB)] = v;
+  }
+  __syncthreads();
+  fft_stages<T>(s, B, lgB, 1, B, tw, lgN);
+  fft_stages<T>(s, B, lgB, B, 1, tw, lgN);
+  unsigned long long best = 0;
+  for (int e = threadIdx.x; e < BB; e += blockDim.x) {
+    const T v = cabs_(s[e]);
+    m[e] = v;
+    const unsigned long long k = fkey(v);
+    best = k > best ? k : best;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+    best = t > best ? t : best;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(&s_peak, best);
+  __syncthreads();
+  const double pk = fkey_inv(s_peak);
+  const double fl = floor_rel * pk;
+  for (int e0 = 0; e0 < BB; e0 += blockDim.x) {
+    const int e = e0 + threadIdx.x;
+    bool f = false;
+    if (pk > 0.0 && e < BB) {
+      const unsigned r = (unsigned)(e >> lgB), c = (unsigned)(e & (B - 1));
+      const T v = m[e];
+      if ((double)v >= fl) {
+        const unsigned rm = (r - 1u) & maskB, rp = (r + 1u) & maskB;
+        const unsigned cm = (c - 1u) & maskB, cp = (c + 1u) & maskB;
+        f = v > m[(rm << lgB) | cm] && v > m[(rm << lgB) | c] && v > m[(rm << lgB) | cp] &&
+            v > m[(r << lgB) | cm] && v > m[(r << lgB) | cp] && v > m[(rp << lgB) | cm] &&
+            v > m[(rp << lgB) | c] && v > m[(rp << lgB) | cp];
+      }
+    }
+    if (f) list[atomicAdd(&s_n, 1u)] = e;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *count = s_n;
+}
+
 inline FoldGeom fold_geometry(int lgN, int lgB, int cpt) {
   FoldGeom g;
   g.lgN = lgN;

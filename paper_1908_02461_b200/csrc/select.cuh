@@ -104,15 +104,22 @@ __global__ void k_lmax_bits(const T* __restrict__ mags, int lgB, int nseg_stride
 // a tuner pass seen through the permutation (|Z_p[k1,k2]| = |x_hat[s1i k1,
 // s2i k2]|, SURVEY.md §7 hard part 2) without materialising the permuted
 // grid.  Output: one bit per bin (row-major) and a count per 8192-bin block.
-template <typename T, bool PERM>
+//
+// UNORDERED (tuner passes): instead of bits + block counts, maxima are
+// appended to `list` through one warp-aggregated atomicAdd on `count` per
+// 32-bin word — the tuner only feeds them to the vote histogram, where order
+// does not matter, and the count is order independent.
+template <typename T, bool PERM, bool UNORDERED = false>
 __global__ void __launch_bounds__(512)
 k_lmax_rows(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, int rb,
             const unsigned long long* __restrict__ peak, double floor_rel,
-            uint32_t* __restrict__ bits, unsigned* __restrict__ blk_counts) {
+            uint32_t* __restrict__ bits, unsigned* __restrict__ blk_counts,
+            int32_t* __restrict__ list = nullptr, unsigned* __restrict__ count = nullptr) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* S = reinterpret_cast<T*>(smem_raw);
   __shared__ unsigned s_cnt[32];
   const int B = 1 << lgB;
+  unsigned* s_words = reinterpret_cast<unsigned*>(S + ((size_t)(rb + 2) << lgB));  // UNORDERED only
   const unsigned mask = (unsigned)B - 1u;
   const int r0 = blockIdx.x * rb;
   for (int i = threadIdx.x; i < 32; i += blockDim.x) s_cnt[i] = 0;
@@ -131,37 +138,73 @@ k_lmax_rows(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, int rb,
   const bool live = pk > 0.0;
   const double fl = floor_rel * pk;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const int words_per_row = B >= 32 ? B >> 5 : 1;
-  const long wtot = (long)rb * words_per_row;
+  const int wpr_lg = lgB - 5;                              // words per row = B / 32 (B >= 32)
+  const int wtot = rb << wpr_lg;
   const size_t word0 = ((size_t)r0 << lgB) >> 5;
-  for (long w = warp; w < wtot; w += nwarps) {
-    const int i = (int)(w / words_per_row) + 1;           // smem row of the centre
-    const int c = (int)(w % words_per_row) * 32 + lane;
+  const int blk_first = (int)((word0 * 32) / kCmpElems);
+  for (int w = warp; w < wtot; w += nwarps) {
+    const int i = (w >> wpr_lg) + 1;                       // smem row of the centre
+    const unsigned c = ((unsigned)(w & ((1 << wpr_lg) - 1)) << 5) + lane;
     bool f = false;
-    if (live && c < B) {
-      const unsigned cm = ((unsigned)c - 1u) & mask, cp = ((unsigned)c + 1u) & mask;
+    if (live) {
+      const unsigned cm = (c - 1u) & mask, cp = (c + 1u) & mask;
       const unsigned q0 = PERM ? (s2 * cm) & mask : cm;
-      const unsigned q1 = PERM ? (s2 * (unsigned)c) & mask : (unsigned)c;
+      const unsigned q1 = PERM ? (s2 * c) & mask : c;
       const unsigned q2 = PERM ? (s2 * cp) & mask : cp;
-      const T* up = S + ((size_t)(i - 1) << lgB);
-      const T* md = S + ((size_t)i << lgB);
-      const T* dn = S + ((size_t)(i + 1) << lgB);
+      const T* md = S + (i << lgB);
       const T v = md[q1];
-      if ((double)v >= fl)
+      if ((double)v >= fl) {
+        const T* up = md - B;
+        const T* dn = md + B;
         f = v > up[q0] && v > up[q1] && v > up[q2] && v > md[q0] && v > md[q2] && v > dn[q0] &&
             v > dn[q1] && v > dn[q2];
+      }
     }
     const unsigned bal = __ballot_sync(0xffffffffu, f);
-    if (lane == 0) {
+    if (UNORDERED) {
+      if (lane == 0) s_words[w] = bal;
+    } else if (lane == 0) {
       bits[word0 + w] = bal;
-      if (bal) atomicAdd(&s_cnt[(int)((w * 32) >> 13)], (unsigned)__popc(bal));
+      if (bal) atomicAdd(&s_cnt[(int)(((word0 + w) * 32) / kCmpElems) - blk_first], (unsigned)__popc(bal));
     }
   }
+  if (UNORDERED) {
+    // CTA-level aggregation: scan the tile's ballot words, ONE global atomic
+    __syncthreads();
+    const int per = (wtot + blockDim.x - 1) / blockDim.x;
+    const int w0 = threadIdx.x * per, w1 = min(w0 + per, wtot);
+    unsigned mine = 0;
+    for (int w = w0; w < w1; ++w) mine += __popc(s_words[w]);
+    __shared__ unsigned s_wsum[32];
+    __shared__ unsigned s_base;
+    unsigned inc = warp_incl_scan(mine);
+    if (lane == 31) s_wsum[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      unsigned t = lane < nwarps ? s_wsum[lane] : 0u;
+      t = warp_incl_scan(t);
+      s_wsum[lane] = t;
+      if (lane == 31) s_base = t ? atomicAdd(count, t) : 0u;
+    }
+    __syncthreads();
+    unsigned pos = s_base + inc - mine + (warp ? s_wsum[warp - 1] : 0u);
+    for (int w = w0; w < w1; ++w) {
+      unsigned b = s_words[w];
+      while (b) {
+        const int k = __ffs(b) - 1;
+        b &= b - 1u;
+        list[pos++] = (int32_t)((word0 + w) * 32 + k);
+      }
+    }
+    return;
+  }
   __syncthreads();
-  const long elems = (long)rb << lgB;
-  const int nblk = (int)((elems + kCmpElems - 1) / kCmpElems);
-  const size_t blk0 = ((size_t)r0 << lgB) / kCmpElems;
-  for (int i = threadIdx.x; i < nblk; i += blockDim.x) blk_counts[blk0 + i] = s_cnt[i];
+  // per-8192-bin block counts (blk_counts zeroed by the caller; a tile may
+  // cover part of a block or several blocks)
+  const size_t first = ((size_t)r0 << lgB), last = first + ((size_t)rb << lgB) - 1;
+  const int nblk = (int)(last / kCmpElems - first / kCmpElems + 1);
+  for (int i = threadIdx.x; i < nblk; i += blockDim.x)
+    if (s_cnt[i]) atomicAdd(&blk_counts[first / kCmpElems + i], s_cnt[i]);
 }
 
 // G[r][c] = M[s1i*r mod N][s2i*c mod N]: the |Z| grid of a B == N pass seen

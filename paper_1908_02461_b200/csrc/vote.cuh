@@ -22,9 +22,12 @@ enum VoteMode { kVoteOrBit = 0, kVoteAdd8 = 1, kVoteAdd32 = 2 };
 
 // bins: flat bin indices (bi*B + bj) per segment, `counts[seg]` valid entries
 // (or uniform `count` when counts == nullptr); one permutation per segment.
+// budget > 0: skip the whole segment when nb * len^2 > budget (the tuner's
+// vote budget, tuner.py:165,175, evaluated on the device so the vote can be
+// queued before the host learns the count).
 __global__ void k_vote(const int32_t* __restrict__ bins, long seg_stride, const unsigned* counts,
                        long count, const Perm* __restrict__ perms, int lgN, int lgB, int expand,
-                       int mode, int bit0, uint32_t* __restrict__ hist) {
+                       int mode, int bit0, uint32_t* __restrict__ hist, long long budget = 0) {
   const int seg = blockIdx.y;
   const long nb = counts ? (long)counts[seg] : count;
   const int N = 1 << lgN;
@@ -40,6 +43,7 @@ __global__ void k_vote(const int32_t* __restrict__ bins, long seg_stride, const 
   }
   const long per = (long)len * len;
   const long total = nb * per;
+  if (budget > 0 && total > budget) return;
   const Perm p = perms[seg];
   const int32_t* sb = bins + seg * seg_stride;
   const unsigned bitv = 1u << ((bit0 + seg) & 7);

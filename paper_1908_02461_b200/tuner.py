@@ -88,9 +88,11 @@ def _state(sc: _native.TunerStateC) -> TunerState:
     for i in range(sc.passes):
         r = float(sc.hist_ratio[i]) if sc.hist_has_ratio[i] else None
         hist.append((int(sc.hist_bins[i]), int(sc.hist_count[i]), r))
-    return TunerState(history=hist, converged=bool(sc.converged), detected_k=int(sc.detected_k),
-                      b_detect=int(sc.b_detect), b_estimate=int(sc.b_estimate),
-                      vote_passes=int(sc.vote_passes))
+    st = TunerState(history=hist, converged=bool(sc.converged), detected_k=int(sc.detected_k),
+                    b_detect=int(sc.b_detect), b_estimate=int(sc.b_estimate),
+                    vote_passes=int(sc.vote_passes))
+    st.pass_us = [float(sc.hist_us[i]) for i in range(sc.passes)]   # diagnostic, not compared
+    return st
 
 
 def update_bins(b: int, r: float, cfg: TunerConfig, n: int) -> int:
