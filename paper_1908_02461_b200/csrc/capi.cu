@@ -794,7 +794,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       C* y = (C*)ws(c, "fold_y", BB * sizeof(C));
       const FoldOut fo = fold_launch<T, Tin>(c, x, lgN, lgb, tb, &p, 1, y, st);
       pre(c, st);
-      k_small_pass<T><<<1, 1024, BB * (sizeof(C) + sizeof(T)), st>>>(
+      k_small_pass<T><<<1, 1024, BB * (sizeof(C) + sizeof(T)) + bb * sizeof(C), st>>>(
           (const C*)fo.data, fo.Z, fo.Z == 1, lgb, p, (const C*)tb.tw[prec_of<T>()], lgN,
           cf.mag_floor, maxlist, cnt_dev);
       post(c, "k_small_pass", st, (double)(fo.Z + 1) * BB * sizeof(C));

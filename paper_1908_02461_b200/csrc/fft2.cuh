@@ -41,6 +41,19 @@ __device__ __forceinline__ C mul_negi(C a) {  // a * (-i)
   C z; z.x = a.y; z.y = -a.x; return z;
 }
 
+// v[r] *= w^r for r = 1..R-1 from one table twiddle w: powers by repeated
+// squaring / products (<= 3 roundings deep), instead of R-1 table loads.
+template <typename T, int R>
+__device__ __forceinline__ void twiddle_powers(cplx<T>* v, cplx<T> w) {
+  using C = cplx<T>;
+  C p[16];
+  p[1] = w;
+#pragma unroll
+  for (int r = 2; r < R; ++r) p[r] = (r & 1) ? cmul(p[r - 1], w) : cmul(p[r >> 1], p[r >> 1]);
+#pragma unroll
+  for (int r = 1; r < R; ++r) v[r] = cmul(v[r], p[r]);
+}
+
 // forward R-point DFT in registers (natural order in and out), R in {2,4,8,16}
 template <typename T, int R>
 __device__ __forceinline__ void dft_reg(cplx<T>* v) {
@@ -103,10 +116,7 @@ __device__ __forceinline__ void stockham_pass(cplx<T>* s, int lgL, int rs, int l
     const int it = threadIdx.x + q * blockDim.x;
     const int row = it >> per_lg, j = it & (per - 1);
     const int jm = j & (Ns - 1);
-    if (lgNs > 0) {
-#pragma unroll
-      for (int r = 1; r < R; ++r) v[q * R + r] = cmul(v[q * R + r], __ldg(tw + ((jm * r) << tsh)));
-    }
+    if (lgNs > 0) twiddle_powers<T, R>(&v[q * R], __ldg(tw + (jm << tsh)));
     dft_reg<T, R>(&v[q * R]);
     C* sr = s + row * rs;
     const int base = ((j >> lgNs) << (lgNs + LGR)) + jm;
@@ -168,8 +178,7 @@ __device__ __forceinline__ void stockham_last(const cplx<T>* s, int lgL, int rs,
     const C* sr = s + seq * rs;
 #pragma unroll
     for (int r = 0; r < R; ++r) v[q * R + r] = sr[padi(j + r * per)];
-#pragma unroll
-    for (int r = 1; r < R; ++r) v[q * R + r] = cmul(v[q * R + r], __ldg(tw + ((j * r) << tsh)));
+    twiddle_powers<T, R>(&v[q * R], __ldg(tw + (j << tsh)));
     dft_reg<T, R>(&v[q * R]);
 #pragma unroll
     for (int r = 0; r < R; ++r) st(seq, j + r * per, v[q * R + r]);

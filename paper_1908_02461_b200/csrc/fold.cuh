@@ -307,21 +307,40 @@ k_small_pass(const cplx<T>* __restrict__ part, int Z, bool permuted, int lgB, Pe
   __shared__ unsigned s_n;
   if (threadIdx.x == 0) { s_peak = 0; s_n = 0; }
   const unsigned maskB = (unsigned)B - 1u;
-  for (int e = threadIdx.x; e < BB; e += blockDim.x) {
-    unsigned a = (unsigned)(e >> lgB), b = (unsigned)(e & (B - 1));
+  // tpe threads per bin split the Z partials (fixed combination order:
+  // deterministic); a shuffle tree joins the slices
+  const int tpe_lg = BB >= (int)blockDim.x ? 0 : min(5, __ffs(blockDim.x / BB) - 1);
+  const int tpe = 1 << tpe_lg;
+  const int zs = (Z + tpe - 1) >> tpe_lg;
+  for (int t = threadIdx.x; t < (BB << tpe_lg); t += blockDim.x) {
+    const int e = t >> tpe_lg, sl = t & (tpe - 1);
     C v;
     if (permuted) {
       v = part[e];
     } else {
-      v = sum_partials(part + e, (size_t)BB, Z);
-      a = (p.s1i * (a - p.t1)) & maskB;
-      b = (p.s2i * (b - p.t2)) & maskB;
+      const int z0 = sl * zs;
+      const int zn = max(0, min(zs, Z - z0));
+      v = sum_partials(part + (size_t)z0 * BB + e, (size_t)BB, zn);
     }
-    s[bitrev(a, lgB) * B + bitrev(b, lgB)] = v;
+    for (int o = 1; o < tpe; o <<= 1) {
+      const C u = mk<T>(__shfl_down_sync(0xffffffffu, v.x, o), __shfl_down_sync(0xffffffffu, v.y, o));
+      v = cadd(v, u);
+    }
+    if (sl == 0) {
+      unsigned a = (unsigned)(e >> lgB), b = (unsigned)(e & (B - 1));
+      if (!permuted) {
+        a = (p.s1i * (a - p.t1)) & maskB;
+        b = (p.s2i * (b - p.t2)) & maskB;
+      }
+      s[bitrev(a, lgB) * B + bitrev(b, lgB)] = v;
+    }
   }
+  // twiddles of a length-B transform, W_B^k = tw[k * N / B], staged in smem
+  C* tws = reinterpret_cast<C*>(m + BB);
+  for (int k = threadIdx.x; k < B; k += blockDim.x) tws[k] = tw[k << (lgN - lgB)];
   __syncthreads();
-  fft_stages<T>(s, B, lgB, 1, B, tw, lgN);
-  fft_stages<T>(s, B, lgB, B, 1, tw, lgN);
+  fft_stages<T>(s, B, lgB, 1, B, tws, lgB);
+  fft_stages<T>(s, B, lgB, B, 1, tws, lgB);
   unsigned long long best = 0;
   for (int e = threadIdx.x; e < BB; e += blockDim.x) {
     const T v = cabs_(s[e]);
@@ -346,12 +365,18 @@ k_small_pass(const cplx<T>* __restrict__ part, int Z, bool permuted, int lgB, Pe
       if ((double)v >= fl) {
         const unsigned rm = (r - 1u) & maskB, rp = (r + 1u) & maskB;
         const unsigned cm = (c - 1u) & maskB, cp = (c + 1u) & maskB;
-        f = v > m[(rm << lgB) | cm] && v > m[(rm << lgB) | c] && v > m[(rm << lgB) | cp] &&
-            v > m[(r << lgB) | cm] && v > m[(r << lgB) | cp] && v > m[(rp << lgB) | cm] &&
-            v > m[(rp << lgB) | c] && v > m[(rp << lgB) | cp];
+        f = (v > m[(rm << lgB) | cm]) & (v > m[(rm << lgB) | c]) & (v > m[(rm << lgB) | cp]) &
+            (v > m[(r << lgB) | cm]) & (v > m[(r << lgB) | cp]) & (v > m[(rp << lgB) | cm]) &
+            (v > m[(rp << lgB) | c]) & (v > m[(rp << lgB) | cp]);
       }
     }
-    if (f) list[atomicAdd(&s_n, 1u)] = e;
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (bal) {
+      unsigned base = 0;
+      if ((threadIdx.x & 31) == 0) base = atomicAdd(&s_n, (unsigned)__popc(bal));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (f) list[base + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = e;
+    }
   }
   __syncthreads();
   if (threadIdx.x == 0) *count = s_n;

@@ -125,9 +125,10 @@ k_lmax_rows(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, int rb,
   for (int i = threadIdx.x; i < 32; i += blockDim.x) s_cnt[i] = 0;
   const int nrow = rb + 2;
   constexpr int V = 16 / sizeof(T);            // elements per 16-byte chunk
-  const int chunks = B / V;
-  for (int e = threadIdx.x; e < nrow * chunks; e += blockDim.x) {
-    const int i = e / chunks, q = e - i * chunks;
+  const int ch_lg = lgB - (sizeof(T) == 4 ? 2 : 1);
+  const int chunks = 1 << ch_lg;
+  for (int e = threadIdx.x; e < (nrow << ch_lg); e += blockDim.x) {
+    const int i = e >> ch_lg, q = e & (chunks - 1);
     const unsigned r = (unsigned)(r0 - 1 + i) & mask;
     const unsigned sr = PERM ? (s1 * r) & mask : r;
     cp_async16(S + ((size_t)i << lgB) + q * V, M + ((size_t)sr << lgB) + q * V);
@@ -137,35 +138,49 @@ k_lmax_rows(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, int rb,
   const double pk = fkey_inv(*peak);
   const bool live = pk > 0.0;
   const double fl = floor_rel * pk;
+  // v >= fl (float64, tuner.py:111) <=> v >= fl rounded up to T, for T-valued v
+  const T flT = sizeof(T) == 4 ? (T)__double2float_ru(fl) : (T)fl;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const int wpr_lg = lgB - 5;                              // words per row = B / 32 (B >= 32)
+  const int wpr_lg = lgB - 5;                              // 32-bin words per row (B >= 32)
   const int wtot = rb << wpr_lg;
   const size_t word0 = ((size_t)r0 << lgB) >> 5;
   const int blk_first = (int)((word0 * 32) / kCmpElems);
-  for (int w = warp; w < wtot; w += nwarps) {
-    const int i = (w >> wpr_lg) + 1;                       // smem row of the centre
-    const unsigned c = ((unsigned)(w & ((1 << wpr_lg) - 1)) << 5) + lane;
-    bool f = false;
-    if (live) {
-      const unsigned cm = (c - 1u) & mask, cp = (c + 1u) & mask;
-      const unsigned q0 = PERM ? (s2 * cm) & mask : cm;
-      const unsigned q1 = PERM ? (s2 * c) & mask : c;
-      const unsigned q2 = PERM ? (s2 * cp) & mask : cp;
-      const T* md = S + (i << lgB);
-      const T v = md[q1];
-      if ((double)v >= fl) {
-        const T* up = md - B;
-        const T* dn = md + B;
-        f = v > up[q0] && v > up[q1] && v > up[q2] && v > md[q0] && v > md[q2] && v > dn[q0] &&
-            v > dn[q1] && v > dn[q2];
+  // A warp owns a 32-column strip and walks down the tile's rows with a
+  // 3-row register window; horizontal neighbours come from lane shuffles
+  // (lanes 0/31 load their outside neighbour), so a bin costs ~1 LDS.
+  auto row_vals = [&](int i, unsigned c, unsigned qm, unsigned q, unsigned qp, T& l, T& m, T& r) {
+    const T* row = S + (i << lgB);
+    m = row[q];
+    l = __shfl_up_sync(0xffffffffu, m, 1);
+    r = __shfl_down_sync(0xffffffffu, m, 1);
+    if (lane == 0) l = row[qm];
+    if (lane == 31) r = row[qp];
+  };
+  for (int strip = warp; strip < (1 << wpr_lg); strip += nwarps) {
+    const unsigned c = ((unsigned)strip << 5) + lane;
+    const unsigned cm = (c - 1u) & mask, cp = (c + 1u) & mask;
+    const unsigned q1 = PERM ? (s2 * c) & mask : c;
+    const unsigned q0 = PERM ? (s2 * cm) & mask : cm;
+    const unsigned q2 = PERM ? (s2 * cp) & mask : cp;
+    T ul, um, ur, ml, mm, mr, dl, dm, dr;
+    row_vals(0, c, q0, q1, q2, ul, um, ur);
+    row_vals(1, c, q0, q1, q2, ml, mm, mr);
+    for (int i = 1; i <= rb; ++i) {
+      row_vals(i + 1, c, q0, q1, q2, dl, dm, dr);
+      // branch-free: every comparison evaluated, combined bitwise
+      const bool f = live & (mm >= flT) & (mm > ul) & (mm > um) & (mm > ur) & (mm > ml) &
+                     (mm > mr) & (mm > dl) & (mm > dm) & (mm > dr);
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      const int w = ((i - 1) << wpr_lg) + strip;
+      if (UNORDERED) {
+        if (lane == 0) s_words[w] = bal;
+      } else if (lane == 0) {
+        bits[word0 + w] = bal;
+        if (bal)
+          atomicAdd(&s_cnt[(int)(((word0 + w) * 32) / kCmpElems) - blk_first], (unsigned)__popc(bal));
       }
-    }
-    const unsigned bal = __ballot_sync(0xffffffffu, f);
-    if (UNORDERED) {
-      if (lane == 0) s_words[w] = bal;
-    } else if (lane == 0) {
-      bits[word0 + w] = bal;
-      if (bal) atomicAdd(&s_cnt[(int)(((word0 + w) * 32) / kCmpElems) - blk_first], (unsigned)__popc(bal));
+      ul = ml; um = mm; ur = mr;
+      ml = dl; mm = dm; mr = dr;
     }
   }
   if (UNORDERED) {
