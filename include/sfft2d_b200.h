@@ -132,12 +132,27 @@ int sfft2d_atsfft(sfft2d_ctx* ctx, const void* x, int x_dtype, int x_on_host, in
                   int n_perms, int precision, void* stream, sfft2d_result* res,
                   sfft2d_tuner_state* state);
 
+/* Same as sfft2d_atsfft, but each permutation is drawn on demand from a numpy
+ * Generator's bit generator (`numpy.random.Generator.bit_generator.ctypes.
+ * bit_generator`, a bitgen_t*) with numpy's own bounded-integer routine
+ * (libnpyrandom random_bounded_uint64_fill), consuming the stream exactly like
+ * the reference's draw_permutation calls (hashing.py:72-80, tuner.py:170,277):
+ * the caller's Generator ends in the same state as after the reference.     */
+int sfft2d_atsfft_bitgen(sfft2d_ctx* ctx, const void* x, int x_dtype, int x_on_host, int n,
+                         const sfft2d_tuner_config* cfg, int est_loops, void* numpy_bitgen,
+                         int precision, void* stream, sfft2d_result* res,
+                         sfft2d_tuner_state* state);
+
 /* detect_sparsity (tuner.py:142-241): tuning loop + votes only; fetch the
  * (coordinate, tally) pairs with sfft2d_fetch_votes.                      */
 int sfft2d_detect_sparsity(sfft2d_ctx* ctx, const void* x, int x_dtype, int x_on_host, int n,
                            const sfft2d_tuner_config* cfg, const sfft2d_perm* perms,
                            int n_perms, int precision, void* stream,
                            sfft2d_tuner_state* state);
+
+int sfft2d_detect_sparsity_bitgen(sfft2d_ctx* ctx, const void* x, int x_dtype, int x_on_host,
+                                  int n, const sfft2d_tuner_config* cfg, void* numpy_bitgen,
+                                  int precision, void* stream, sfft2d_tuner_state* state);
 
 /* Copy the last transform's recovered spectrum: ij int64[count][2], values
  * complex (float2 for FP32, double2 for FP64)[count], row-major (i, j) order. */

@@ -28,7 +28,7 @@ EXPORTS = (
     "sfft2d_ctx_set_tables", "sfft2d_sfft", "sfft2d_atsfft", "sfft2d_detect_sparsity",
     "sfft2d_fetch_result", "sfft2d_fetch_votes", "sfft2d_binned_spectrum", "sfft2d_fft2d",
     "sfft2d_local_maxima", "sfft2d_top_bins", "sfft2d_ctx_set_profiling",
-    "sfft2d_ctx_profile_report",
+    "sfft2d_ctx_profile_report", "sfft2d_atsfft_bitgen", "sfft2d_detect_sparsity_bitgen",
 )
 
 
@@ -100,6 +100,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                P(ResultC), P(TunerStateC)], i32),
             "sfft2d_detect_sparsity": ([vp, vp, i32, i32, i32, P(TunerCfg), P(Perm), i32, i32, vp,
                                         P(TunerStateC)], i32),
+            "sfft2d_atsfft_bitgen": ([vp, vp, i32, i32, i32, P(TunerCfg), i32, vp, i32, vp,
+                                      P(ResultC), P(TunerStateC)], i32),
+            "sfft2d_detect_sparsity_bitgen": ([vp, vp, i32, i32, i32, P(TunerCfg), vp, i32, vp,
+                                               P(TunerStateC)], i32),
             "sfft2d_fetch_result": ([vp, vp, vp, i32, vp], i32),
             "sfft2d_fetch_votes": ([vp, vp, vp, i32, vp], i32),
             "sfft2d_binned_spectrum": ([vp, vp, i32, i32, i32, P(Perm), i32, dbl, dbl, i32, vp, vp],

@@ -26,10 +26,20 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(s) <= t for s in sources())
 
 
+def npyrandom_dir() -> str:
+    """numpy's static bounded-integer library (the code behind Generator.integers)."""
+    import numpy
+    d = os.path.join(os.path.dirname(numpy.__file__), "random", "lib")
+    if not os.path.exists(os.path.join(d, "libnpyrandom.a")):
+        raise RuntimeError(f"libnpyrandom.a not found under {d}")
+    return d
+
+
 def build(force: bool = False, verbose: bool = True) -> str:
     if not force and up_to_date():
         return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT + ".tmp", os.path.join(SRC, "capi.cu")]
+    cmd = [NVCC, *FLAGS, "-o", OUT + ".tmp", os.path.join(SRC, "capi.cu"),
+           "-L" + npyrandom_dir(), "-lnpyrandom", "-Xlinker", "--exclude-libs,ALL"]
     if verbose:
         print(" ".join(cmd), flush=True)
     subprocess.run(cmd, check=True)

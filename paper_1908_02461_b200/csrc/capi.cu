@@ -29,6 +29,12 @@
 
 using namespace sfft;
 
+// numpy's bounded-integer routine (numpy/random/lib/libnpyrandom.a, the code
+// behind Generator.integers): drawing through it on the caller's own bitgen_t
+// reproduces draw_permutation's stream consumption exactly (hashing.py:72-80).
+extern "C" void random_bounded_uint64_fill(void* bitgen_state, uint64_t off, uint64_t rng,
+                                           intptr_t cnt, bool use_masked, uint64_t* out);
+
 namespace {
 
 struct SfftError {
@@ -70,6 +76,7 @@ struct sfft2d_ctx {
   std::vector<DevTables> tables;
   std::map<std::string, std::pair<void*, size_t>> bufs;
   unsigned* pinned = nullptr;  // small host scratch for counts
+  Perm* perm_pinned = nullptr; // staging for permutations drawn on demand
   // last results
   long long res_count = 0;
   int res_prec = SFFT2D_FP64;
@@ -200,6 +207,8 @@ const DevTables& find_twiddles(sfft2d_ctx* c, int n) {
   fail(SFFT2D_ERR_STATE, "no twiddle table registered for n=" + std::to_string(n));
 }
 
+constexpr int kPermPinned = 1024;
+
 Perm to_perm(const sfft2d_perm& p, int n) {
   const long long m = n;
   auto md = [m](long long v) { return (uint32_t)(((v % m) + m) % m); };
@@ -212,6 +221,58 @@ Perm to_perm(const sfft2d_perm& p, int n) {
   q.s2i = md(p.sigma2_inv);
   return q;
 }
+
+uint32_t inv_pow2(uint32_t s, uint32_t mask) {  // s odd: s^-1 mod 2^k by Newton iteration
+  uint32_t x = s;
+  for (int i = 0; i < 5; ++i) x *= 2u - s * x;
+  return x & mask;
+}
+
+// Permutations for a transform: from a caller array, or drawn on demand from a
+// numpy bitgen_t*.  Drawn permutations are staged in pinned memory and copied
+// to the device array in stream order.
+struct PermSource {
+  const sfft2d_perm* arr = nullptr;
+  int n_arr = 0;
+  void* bitgen = nullptr;
+  int n = 0;
+  std::vector<Perm> hp;
+  Perm* pinned = nullptr;
+  Perm* dev = nullptr;
+  int cap = 0;
+
+  const Perm& get(int i, cudaStream_t st) {
+    if (i >= cap) fail(SFFT2D_ERR_VALUE, "permutation list exhausted");
+    while ((int)hp.size() <= i) {
+      Perm q;
+      const int k = (int)hp.size();
+      if (bitgen) {
+        uint64_t v[4] = {0, 0, 0, 0};
+        if (n > 1) {
+          random_bounded_uint64_fill(bitgen, 0, (uint64_t)(n / 2 - 1), 1, false, &v[0]);
+          random_bounded_uint64_fill(bitgen, 0, (uint64_t)(n / 2 - 1), 1, false, &v[1]);
+        }
+        random_bounded_uint64_fill(bitgen, 0, (uint64_t)(n - 1), 1, false, &v[2]);
+        random_bounded_uint64_fill(bitgen, 0, (uint64_t)(n - 1), 1, false, &v[3]);
+        const uint32_t mask = (uint32_t)n - 1u;
+        q.s1 = n > 1 ? (uint32_t)(2 * v[0] + 1) : 1u;
+        q.s2 = n > 1 ? (uint32_t)(2 * v[1] + 1) : 1u;
+        q.t1 = (uint32_t)v[2];
+        q.t2 = (uint32_t)v[3];
+        q.s1i = inv_pow2(q.s1, mask);
+        q.s2i = inv_pow2(q.s2, mask);
+      } else {
+        if (k >= n_arr) fail(SFFT2D_ERR_VALUE, "permutation list exhausted");
+        q = to_perm(arr[k], n);
+      }
+      hp.push_back(q);
+      pinned[k] = q;
+      ck(cudaMemcpyAsync(dev + k, pinned + k, sizeof(Perm), cudaMemcpyHostToDevice, st), "H2D perm");
+    }
+    return hp[i];
+  }
+  int used() const { return (int)hp.size(); }
+};
 
 unsigned read_u32(sfft2d_ctx* c, const unsigned* dev, cudaStream_t st) {
   ck(cudaMemcpyAsync(c->pinned, dev, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H");
@@ -708,7 +769,7 @@ int update_bins(int b, double r, const sfft2d_tuner_config& cf, int n) {
 
 template <typename T, typename Tin>
 void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, int est_loops,
-             const sfft2d_perm* perms, int n_perms, cudaStream_t st, bool do_estimate,
+             const sfft2d_perm* perms, int n_perms, void* bitgen, cudaStream_t st, bool do_estimate,
              sfft2d_result* res, sfft2d_tuner_state* S) {
   using C = cplx<T>;
   const int lgN = ilog2(n);
@@ -718,12 +779,17 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     fail(SFFT2D_ERR_UNSUPPORTED, "max_tuning_iters too large for the history buffer");
   if (!is_pow2(cf.b0)) fail(SFFT2D_ERR_CONFIG, "b0 is not a power of 2");
   const int L = std::max(est_loops, 1);
-  std::vector<Perm> hp(n_perms);
-  for (int i = 0; i < n_perms; ++i) hp[i] = to_perm(perms[i], n);
-  Perm* dp = (Perm*)ws(c, "perms", (size_t)std::max(n_perms, 1) * sizeof(Perm));
-  if (n_perms)
-    ck(cudaMemcpyAsync(dp, hp.data(), (size_t)n_perms * sizeof(Perm), cudaMemcpyHostToDevice, st),
-       "H2D perms");
+  PermSource ps;
+  ps.arr = perms;
+  ps.n_arr = n_perms;
+  ps.bitgen = bitgen;
+  ps.n = n;
+  ps.cap = max_iters + 2 + L;
+  ps.hp.reserve(ps.cap);
+  ps.pinned = c->perm_pinned;
+  if (ps.cap > kPermPinned) fail(SFFT2D_ERR_UNSUPPORTED, "too many permutations");
+  ps.dev = (Perm*)ws(c, "perms", (size_t)ps.cap * sizeof(Perm));
+  Perm* dp = ps.dev;
   const long nkeys = (long)n * n;
   const int mode = (4 * (max_iters + 2) <= 255) ? kVoteAdd8 : kVoteAdd32;
   uint32_t* hist = (uint32_t*)ws(c, "hist", hist_bytes(nkeys, mode));
@@ -781,9 +847,8 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   };
 
   auto run_pass = [&](int bb) -> long long {
-    if (pidx >= n_perms) fail(SFFT2D_ERR_VALUE, "permutation list exhausted");
     const int pi = pidx++;
-    const Perm& p = hp[pi];
+    const Perm p = ps.get(pi, st);
     const int lgb = ilog2(bb);
     const size_t BB = (size_t)bb * bb;
     if (bb == n) {
@@ -953,10 +1018,10 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
                                 " exceeds the " + std::to_string(best) + "x" +
                                 std::to_string(best) + " bin budget");
   }
-  if (pidx + L > n_perms) fail(SFFT2D_ERR_VALUE, "permutation list exhausted");
+  for (int i = 0; i < L; ++i) ps.get(pidx + i, st);
   const bool dense = (best == n);
   if (dense) ensure_xhat(false);
-  estimate_and_select<T, Tin>(c, x, lgN, ilog2(best), tb, hp.data() + pidx, dp + pidx, L, keys, m,
+  estimate_and_select<T, Tin>(c, x, lgN, ilog2(best), tb, ps.hp.data() + pidx, dp + pidx, L, keys, m,
                               kt, k, cf.gain_floor, cf.prune_rel, dense, xhat, st, res);
   pidx += L;
   S->perms_used = pidx;
@@ -1121,6 +1186,7 @@ int sfft2d_ctx_create(int device, sfft2d_ctx** out) {
   c->device = device;
   int rc = guarded(c, [&] {
     ck(cudaMallocHost(&c->pinned, 4096), "cudaMallocHost");
+    ck(cudaMallocHost(&c->perm_pinned, kPermPinned * sizeof(Perm)), "cudaMallocHost");
     allow_all_T<float>();
     allow_all_T<double>();
   });
@@ -1146,6 +1212,7 @@ void sfft2d_ctx_destroy(sfft2d_ctx* c) {
       cudaFree(t.tw[p]);
     }
   if (c->pinned) cudaFreeHost(c->pinned);
+  if (c->perm_pinned) cudaFreeHost(c->perm_pinned);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   delete c;
 }
@@ -1251,10 +1318,10 @@ int sfft2d_sfft(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host,
   });
 }
 
-int sfft2d_atsfft(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host, int n,
-                  const sfft2d_tuner_config* cfg, int est_loops, const sfft2d_perm* perms,
-                  int n_perms, int precision, void* stream, sfft2d_result* res,
-                  sfft2d_tuner_state* state) {
+static int atsfft_impl(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host, int n,
+                       const sfft2d_tuner_config* cfg, int est_loops, const sfft2d_perm* perms,
+                       int n_perms, void* bitgen, int precision, void* stream, sfft2d_result* res,
+                       sfft2d_tuner_state* state) {
   return guarded(c, [&] {
     if (!cfg || !res || !state || !x || (n_perms > 0 && !perms)) fail(SFFT2D_ERR_VALUE, "null argument");
     check_side(n);
@@ -1266,7 +1333,8 @@ int sfft2d_atsfft(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host, int 
     dispatch(x_dtype, precision, [&](auto t, auto tin) {
       using T = decltype(t);
       using Tin = decltype(tin);
-      run_ats<T, Tin>(c, (const Tin*)xd, n, *cfg, est_loops, perms, n_perms, st, true, res, state);
+      run_ats<T, Tin>(c, (const Tin*)xd, n, *cfg, est_loops, perms, n_perms, bitgen, st, true, res,
+                      state);
     });
     res->precision = precision;
     res->gpu_launches = c->launches;
@@ -1275,9 +1343,9 @@ int sfft2d_atsfft(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host, int 
   });
 }
 
-int sfft2d_detect_sparsity(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host, int n,
-                           const sfft2d_tuner_config* cfg, const sfft2d_perm* perms, int n_perms,
-                           int precision, void* stream, sfft2d_tuner_state* state) {
+static int detect_impl(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host, int n,
+                       const sfft2d_tuner_config* cfg, const sfft2d_perm* perms, int n_perms,
+                       void* bitgen, int precision, void* stream, sfft2d_tuner_state* state) {
   return guarded(c, [&] {
     if (!cfg || !state || !x || (n_perms > 0 && !perms)) fail(SFFT2D_ERR_VALUE, "null argument");
     check_side(n);
@@ -1290,9 +1358,42 @@ int sfft2d_detect_sparsity(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_h
     dispatch(x_dtype, precision, [&](auto t, auto tin) {
       using T = decltype(t);
       using Tin = decltype(tin);
-      run_ats<T, Tin>(c, (const Tin*)xd, n, *cfg, 0, perms, n_perms, st, false, &dummy, state);
+      run_ats<T, Tin>(c, (const Tin*)xd, n, *cfg, 0, perms, n_perms, bitgen, st, false, &dummy,
+                      state);
     });
   });
+}
+
+int sfft2d_atsfft(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host, int n,
+                  const sfft2d_tuner_config* cfg, int est_loops, const sfft2d_perm* perms,
+                  int n_perms, int precision, void* stream, sfft2d_result* res,
+                  sfft2d_tuner_state* state) {
+  return atsfft_impl(c, x, x_dtype, x_on_host, n, cfg, est_loops, perms, n_perms, nullptr,
+                     precision, stream, res, state);
+}
+
+int sfft2d_atsfft_bitgen(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host, int n,
+                         const sfft2d_tuner_config* cfg, int est_loops, void* numpy_bitgen,
+                         int precision, void* stream, sfft2d_result* res,
+                         sfft2d_tuner_state* state) {
+  if (!numpy_bitgen) return SFFT2D_ERR_VALUE;
+  return atsfft_impl(c, x, x_dtype, x_on_host, n, cfg, est_loops, nullptr, 0, numpy_bitgen,
+                     precision, stream, res, state);
+}
+
+int sfft2d_detect_sparsity(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host, int n,
+                           const sfft2d_tuner_config* cfg, const sfft2d_perm* perms, int n_perms,
+                           int precision, void* stream, sfft2d_tuner_state* state) {
+  return detect_impl(c, x, x_dtype, x_on_host, n, cfg, perms, n_perms, nullptr, precision, stream,
+                     state);
+}
+
+int sfft2d_detect_sparsity_bitgen(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host, int n,
+                                  const sfft2d_tuner_config* cfg, void* numpy_bitgen,
+                                  int precision, void* stream, sfft2d_tuner_state* state) {
+  if (!numpy_bitgen) return SFFT2D_ERR_VALUE;
+  return detect_impl(c, x, x_dtype, x_on_host, n, cfg, nullptr, 0, numpy_bitgen, precision, stream,
+                     state);
 }
 
 int sfft2d_fetch_result(sfft2d_ctx* c, int64_t* ij, void* values, int dst_on_host, void* stream) {

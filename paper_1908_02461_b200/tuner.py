@@ -8,14 +8,13 @@ the host controller applies the ratio rule / cycle guard / confirmation
 passes of tuner.py:182-226 between passes (one host sync per pass).
 
 Permutations come from the caller's Generator in the reference order: the
-native controller receives enough pre-drawn permutations from a copy of the
-Generator, and the caller's Generator is then advanced by exactly the number
-the reference would have consumed.
+native controller draws them on demand through the Generator's bitgen_t with
+numpy's own bounded-integer routine, so the caller's Generator advances
+exactly as under the reference.
 """
 
 from __future__ import annotations
 
-import copy
 import ctypes
 import math
 from dataclasses import dataclass, field
@@ -149,37 +148,22 @@ def _is_tensor(x) -> bool:
     return is_torch_tensor(x)
 
 
-class _PermStream:
-    """Pre-draws permutations from a copy of the caller's Generator and can
-    rewind the caller's Generator to "exactly `used` draws consumed"."""
-
-    def __init__(self, gen: np.random.Generator, n: int, count: int):
-        self.gen = gen
-        shadow = copy.deepcopy(gen)
-        self.states = [shadow.bit_generator.state]
-        self.perms = []
-        for _ in range(count):
-            self.perms.append(draw_permutation(n, shadow))
-            self.states.append(shadow.bit_generator.state)
-
-    def consume(self, used: int):
-        self.gen.bit_generator.state = self.states[max(0, min(used, len(self.perms)))]
-
-
 def _run_ats(x, cfg: TunerConfig, est_loops: int, rng, precision, device, estimate: bool):
     torch = _native._torch()
     img = as_device_image(x, device, upload=False)
     n = img.n
     prec = _native.precision_code(precision)
+    # The native controller draws each permutation on demand from this
+    # Generator's own bit generator with numpy's bounded-integer routine, so a
+    # caller's Generator advances exactly as under the reference.
     gen = np.random.default_rng(rng)
-    need = cfg.iters(n) + 2 + (max(est_loops, 1) if estimate else 0)
-    stream_p = _PermStream(gen, n, need)
+    snapshot = gen.bit_generator.state if isinstance(rng, np.random.Generator) else None
+    bitgen = gen.bit_generator.ctypes.bit_generator.value
     ctx = _native.context(img.device)
     ctx.ensure_tables(n, cfg.window_delta_pass, cfg.window_delta_stop)
     ccfg = cfg._c()
     sc = _native.TunerStateC()
     res = _native.ResultC()
-    parr = _native.perm_array(stream_p.perms)
     with torch.cuda.device(img.device):
         st = _stream(torch, img.device)
         if img.tensor is not None:
@@ -187,15 +171,15 @@ def _run_ats(x, cfg: TunerConfig, est_loops: int, rng, precision, device, estima
         else:
             ptr, on_host = img.host.ctypes.data, 1
         if estimate:
-            rc = ctx.lib.sfft2d_atsfft(ctx.handle, ptr, img.dtype_code, on_host, n,
-                                       ctypes.byref(ccfg), int(est_loops), parr,
-                                       len(stream_p.perms), prec, st, ctypes.byref(res),
-                                       ctypes.byref(sc))
+            rc = ctx.lib.sfft2d_atsfft_bitgen(ctx.handle, ptr, img.dtype_code, on_host, n,
+                                              ctypes.byref(ccfg), int(est_loops), bitgen, prec, st,
+                                              ctypes.byref(res), ctypes.byref(sc))
         else:
-            rc = ctx.lib.sfft2d_detect_sparsity(ctx.handle, ptr, img.dtype_code, on_host, n,
-                                                ctypes.byref(ccfg), parr, len(stream_p.perms),
-                                                prec, st, ctypes.byref(sc))
-        stream_p.consume(int(sc.perms_used))
+            rc = ctx.lib.sfft2d_detect_sparsity_bitgen(ctx.handle, ptr, img.dtype_code, on_host, n,
+                                                       ctypes.byref(ccfg), bitgen, prec, st,
+                                                       ctypes.byref(sc))
+        if rc == _native.ERR_VALUE and snapshot is not None:
+            gen.bit_generator.state = snapshot   # the reference validates x before drawing
         ctx.check(rc)
         ctx.last_launches = int(res.gpu_launches)
         state = _state(sc)

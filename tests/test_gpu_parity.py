@@ -274,3 +274,31 @@ def test_atsfft_random_noisy_vs_oracle(seed):
     out, state = P.atsfft2d(img.x, P.TunerConfig(), 8, 200 + seed)
     assert [(b, c) for b, c, _ in state.history] == [(b, c) for b, c, _ in ostate["history"]]
     _close_values(out, O.as_dict((cs, vs)), TOL["fp64"])
+
+
+def test_atsfft_nan_leaves_generator_untouched():
+    x = P.sparse_image(128, 4, 1, snr_db=20.0).x.copy()
+    x[5, 7] = np.inf
+    g = np.random.default_rng(3)
+    before = g.bit_generator.state
+    with pytest.raises(ValueError, match="NaN or Inf"):
+        P.atsfft2d(x, P.TunerConfig(), 8, g)
+    assert g.bit_generator.state == before
+
+
+def test_atsfft_generator_advance_on_configuration_error():
+    # detected_k large vs the clamped estimation grid: reference raises after detection
+    img = P.sparse_image(64, 40, 2, snr_db=5.0)
+    g1, g2 = np.random.default_rng(8), np.random.default_rng(8)
+    try:
+        O.atsfft(img.x, O.TunerParams(), 8, g2)
+        ref_err = None
+    except ValueError as e:
+        ref_err = e
+    try:
+        P.atsfft2d(img.x, P.TunerConfig(), 8, g1)
+        err = None
+    except ValueError as e:
+        err = e
+    assert (ref_err is None) == (err is None)
+    assert g1.integers(1 << 40) == g2.integers(1 << 40)
