@@ -106,6 +106,8 @@ int sfft2d_abi_version(void);
 int sfft2d_ctx_create(int device, sfft2d_ctx** out);
 void sfft2d_ctx_destroy(sfft2d_ctx* ctx);
 const char* sfft2d_ctx_last_error(const sfft2d_ctx* ctx);
+/* host time the last transform spent blocked in stream synchronisation (us) */
+double sfft2d_ctx_sync_us(const sfft2d_ctx* ctx);
 
 /* Register host-built tables for side n and window tolerances
  * (WindowCache.get, hashing.py:249-261):

@@ -9,6 +9,7 @@
 #include "../../include/sfft2d_b200.h"
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -84,6 +85,16 @@ struct sfft2d_ctx {
   long long votes_count = 0;
   bool has_votes = false;
   int launches = 0;
+  double sync_us = 0;   // host time blocked in stream synchronisation (diagnostic)
+  // zero-copy count publication (tuner passes) and the side stream for votes
+  unsigned* mapped_h = nullptr;
+  unsigned* mapped_d = nullptr;
+  unsigned* done_d = nullptr;
+  unsigned done_base = 0;
+  unsigned seq = 0;
+  cudaStream_t vote_st = nullptr;
+  cudaEvent_t ev_lmax = nullptr;
+  cudaEvent_t ev_vote[2] = {nullptr, nullptr};
   // optional per-launch profiling (CUDA events on the launching stream)
   bool profiling = false;
   bool prof_open = false;
@@ -276,8 +287,40 @@ struct PermSource {
 
 unsigned read_u32(sfft2d_ctx* c, const unsigned* dev, cudaStream_t st) {
   ck(cudaMemcpyAsync(c->pinned, dev, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H");
+  const auto t0 = std::chrono::steady_clock::now();
   ck(cudaStreamSynchronize(st), "sync");
+  c->sync_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
   return c->pinned[0];
+}
+
+// Prepare a count publication for a launch of `grid` CTAs.
+Publish make_publish(sfft2d_ctx* c, unsigned grid) {
+  Publish p;
+  p.done = c->done_d;
+  c->done_base += grid;
+  p.target = c->done_base;
+  p.slot = c->mapped_d;
+  p.seq = ++c->seq;
+  return p;
+}
+
+// Spin on the mapped slot until the launch published `seq`; returns the count.
+unsigned wait_published(sfft2d_ctx* c, unsigned seq, cudaStream_t st) {
+  const auto t0 = std::chrono::steady_clock::now();
+  volatile unsigned* h = c->mapped_h;
+  for (unsigned long spin = 0;; ++spin) {
+    if (h[0] == seq) {
+      std::atomic_thread_fence(std::memory_order_acquire);
+      const unsigned v = h[1];
+      c->sync_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+      return v;
+    }
+    if ((spin & 1023) == 1023) {
+      const cudaError_t e = cudaStreamQuery(st);
+      if (e != cudaErrorNotReady && e != cudaSuccess) ck(e, "tuner pass");
+      if (e == cudaSuccess && h[0] != seq) fail(SFFT2D_ERR_CUDA, "count publication lost");
+    }
+  }
 }
 
 unsigned grid_for(long long work, int per_block = 256, int cap = kNumSMs * 16) {
@@ -436,7 +479,8 @@ struct FoldOut {
 
 template <typename T, typename Tin>
 FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTables& tb,
-                    const Perm* hp, int g, void* y_direct, cudaStream_t st) {
+                    const Perm* hp, int g, void* y_direct, cudaStream_t st,
+                    unsigned long long* zero_peak = nullptr) {
   using C = cplx<T>;
   const int B = 1 << lgB;
   const size_t BB = (size_t)B * B;
@@ -450,14 +494,29 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
   const dim3 grid(gm.ktiles, B, gm.Z);
   const int nlt = (g == 1) ? 1 : kMaxFoldLoops;
   const size_t dyn = (B < gm.TW) ? (size_t)nlt * gm.TW * sizeof(C) : 0;
-  C* dst = (gm.Z == 1) ? (C*)y_direct : (C*)ws(c, "fold_part", (size_t)gm.Z * g * BB * sizeof(C));
   const double sup = (double)tb.support[lgB];
+  if (g == 1 && B >= 512 && lgN - lgB <= 5 && y_direct) {
+    // wide single-loop fold, permuted grid written directly
+    const double by = sup * sup * sizeof(Tin) + (double)BB * sizeof(C);
+    const int rh = B >= 2048 ? 4 : (B >= 1024 ? 2 : 1);
+    const dim3 grid_w(B / 512, B / rh);
+    pre(c, st);
+    if (rh == 4)
+      k_fold_wide<Tin, T, 4><<<grid_w, 256, 0, st>>>(x, space, pp.p[0], lgN, lgB, (C*)y_direct, zero_peak);
+    else if (rh == 2)
+      k_fold_wide<Tin, T, 2><<<grid_w, 256, 0, st>>>(x, space, pp.p[0], lgN, lgB, (C*)y_direct, zero_peak);
+    else
+      k_fold_wide<Tin, T, 1><<<grid_w, 256, 0, st>>>(x, space, pp.p[0], lgN, lgB, (C*)y_direct, zero_peak);
+    post(c, "k_fold", st, by);
+    return FoldOut{y_direct, 1};
+  }
+  C* dst = (gm.Z == 1) ? (C*)y_direct : (C*)ws(c, "fold_part", (size_t)gm.Z * g * BB * sizeof(C));
   const double fold_bytes = sup * sup * sizeof(Tin) + (double)gm.Z * g * BB * sizeof(C);
   pre(c, st);
   if (g == 1)
-    k_fold<Tin, T, 1, 2><<<grid, threads, dyn, st>>>(x, space, pp, g, gm, dst);
+    k_fold<Tin, T, 1, 2><<<grid, threads, dyn, st>>>(x, space, pp, g, gm, dst, zero_peak);
   else
-    k_fold<Tin, T, kMaxFoldLoops, 1><<<grid, threads, dyn, st>>>(x, space, pp, g, gm, dst);
+    k_fold<Tin, T, kMaxFoldLoops, 1><<<grid, threads, dyn, st>>>(x, space, pp, g, gm, dst, zero_peak);
   post(c, "k_fold", st, fold_bytes);
   return FoldOut{dst, gm.Z};
 }
@@ -476,33 +535,23 @@ void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTable
   const C* tw = (const C*)tb.tw[P];
   const size_t BB = (size_t)B * B;
   const bool small = BB * sizeof(C) <= (size_t)kSmall2DBytes;
-  if (peaks) ck(cudaMemsetAsync(peaks, 0, (size_t)nloops * sizeof(unsigned long long), st), "memset");
+  // one loop: the fold kernel zeroes the peak slot (no separate memset)
+  if (peaks && nloops > 1)
+    ck(cudaMemsetAsync(peaks, 0, (size_t)nloops * sizeof(unsigned long long), st), "memset");
   for (int g0 = 0; g0 < nloops; g0 += kMaxFoldLoops) {
     const int g = std::min(kMaxFoldLoops, nloops - g0);
     PermPack pp;
     std::memset(&pp, 0, sizeof(pp));
     for (int i = 0; i < g; ++i) pp.p[i] = hp[g0 + i];
-    const int cpt = (g == 1) ? 2 : 1;
-    const FoldGeom gm = fold_geometry(lgN, lgB, cpt);
-    const int threads = gm.TW / cpt;
-    const dim3 grid(gm.ktiles, B, gm.Z);
-    const int nlt = (g == 1) ? 1 : kMaxFoldLoops;
-    const size_t dyn = (B < gm.TW) ? (size_t)nlt * gm.TW * sizeof(C) : 0;
     C* sp = spec ? spec + (size_t)g0 * BB : nullptr;
     T* mg = mags ? mags + (size_t)g0 * BB : nullptr;
     unsigned long long* pk = peaks ? peaks + g0 : nullptr;
     // bucket grid y (permuted fold) for this group
     C* y = (small && sp) ? sp : (C*)ws(c, "fold_y", (size_t)g * BB * sizeof(C));
-    C* dst = (gm.Z == 1) ? y : (C*)ws(c, "fold_part", (size_t)gm.Z * g * BB * sizeof(C));
-    // algorithmic bytes: the S(B)^2 support samples + the grid(s)/partials written
-    const double sup = (double)tb.support[lgB];
-    const double fold_bytes = sup * sup * sizeof(Tin) + (double)gm.Z * g * BB * sizeof(C);
-    pre(c, st);
-    if (g == 1)
-      k_fold<Tin, T, 1, 2><<<grid, threads, dyn, st>>>(x, space, pp, g, gm, dst);
-    else
-      k_fold<Tin, T, kMaxFoldLoops, 1><<<grid, threads, dyn, st>>>(x, space, pp, g, gm, dst);
-    post(c, "k_fold", st, fold_bytes);
+    const FoldOut fo = fold_launch<T, Tin>(c, x, lgN, lgB, tb, hp + g0, g, y, st,
+                                           (nloops == 1) ? pk : nullptr);
+    C* dst = (C*)fo.data;
+    struct { int Z; } gm{fo.Z};
     if (small) {
       if (gm.Z == 1) {
         fft2d_grids<T>(c, y, lgB, g, tw, lgN, sp, mg, pk, st);
@@ -578,25 +627,26 @@ unsigned local_maxima_dev(sfft2d_ctx* c, const T* mags, int lgB, const unsigned 
 
 // Tuner local maxima: unordered list + device count (no host sync).
 template <typename T>
-void lmax_tuner(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long long* peak,
-                double floor_rel, int32_t* list, unsigned* count, cudaStream_t st, bool perm,
-                unsigned s1, unsigned s2) {
+unsigned lmax_tuner(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long long* peak,
+                    double floor_rel, int32_t* list, unsigned* count, cudaStream_t st, bool perm,
+                    unsigned s1, unsigned s2) {
   const int B = 1 << lgB;
   const int smem_rows = (int)((96 * 1024) / ((size_t)B * sizeof(T)));
   int rb = std::max(1, std::min(B / 128, smem_rows - 2));
   while (B % rb) --rb;
   const size_t sm = (size_t)(rb + 2) * B * sizeof(T) + (size_t)rb * B / 32 * sizeof(unsigned);
   if (sm > kMaxDynSmem) fail(SFFT2D_ERR_UNSUPPORTED, "grid too large for the local-maximum tile");
-  ck(cudaMemsetAsync(count, 0, sizeof(unsigned), st), "memset");
   const double by = (double)B * B * sizeof(T);
+  const Publish pub = make_publish(c, (unsigned)(B / rb));
   pre(c, st);
   if (perm)
     k_lmax_rows<T, true, true><<<B / rb, 512, sm, st>>>(mags, lgB, s1, s2, rb, peak, floor_rel,
-                                                        nullptr, nullptr, list, count);
+                                                        nullptr, nullptr, list, count, pub);
   else
     k_lmax_rows<T, false, true><<<B / rb, 512, sm, st>>>(mags, lgB, 1, 1, rb, peak, floor_rel,
-                                                         nullptr, nullptr, list, count);
+                                                         nullptr, nullptr, list, count, pub);
   post(c, "k_lmax_rows", st, by);
+  return pub.seq;
 }
 
 // Exact top-`num` selection bitmask per segment (ties -> lowest index).
@@ -834,16 +884,28 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     }
   };
 
-  unsigned* cnt_dev = (unsigned*)ws(c, "lm_count", 16);
-  // vote on the maxima list of the pass just run; queued before the host
-  // sync, with the vote budget (tuner.py:165,175) applied on the device
-  auto vote_list = [&](int pi, int lgb, long long budget_dev) {
+  ck(cudaMemsetAsync(c->done_d, 0, sizeof(unsigned), st), "memset");
+  c->done_base = 0;
+  // per-pass count slots (zeroed once), double-buffered maxima lists: the
+  // vote of pass k runs on the side stream while pass k+1 proceeds
+  unsigned* cnt_slots = (unsigned*)ws(c, "lm_counts", (size_t)SFFT2D_MAX_HISTORY * 4);
+  ck(cudaMemsetAsync(cnt_slots, 0, (size_t)SFFT2D_MAX_HISTORY * 4, st), "memset");
+  int32_t* maxlists[2] = {maxlist, (int32_t*)ws(c, "maxlist2", (size_t)(nkeys / 4 + 64) * 4)};
+  bool vote_pending[2] = {false, false};
+  int npass = 0;
+  int last_slot = 0;
+  auto vote_list = [&](int pi, int lgb, long long budget_dev, int slot) {
     const int w = n >> lgb;
     const long long len = (w == 1) ? 3 : std::min<long long>(w + 2, n);
-    pre(c, st);
-    k_vote<<<dim3(kNumSMs * 2, 1), 256, 0, st>>>(maxlist, 0, cnt_dev, 0, dp + pi, lgN, lgb, 1, mode,
-                                                 0, hist, budget_dev);
-    post(c, "k_vote", st, (double)len * len * 4.0);
+    ck(cudaEventRecord(c->ev_lmax, st), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(c->vote_st, c->ev_lmax, 0), "cudaStreamWaitEvent");
+    pre(c, c->vote_st);
+    k_vote<<<dim3(kNumSMs * 2, 1), 256, 0, c->vote_st>>>(maxlists[slot & 1], 0, cnt_slots + slot, 0,
+                                                        dp + pi, lgN, lgb, 1, mode, 0, hist,
+                                                        budget_dev);
+    post(c, "k_vote", c->vote_st, (double)len * len * 4.0);
+    ck(cudaEventRecord(c->ev_vote[slot & 1], c->vote_st), "cudaEventRecord");
+    vote_pending[slot & 1] = true;
   };
 
   auto run_pass = [&](int bb) -> long long {
@@ -851,30 +913,40 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     const Perm p = ps.get(pi, st);
     const int lgb = ilog2(bb);
     const size_t BB = (size_t)bb * bb;
+    const int slot = npass++;
+    if (slot >= SFFT2D_MAX_HISTORY) fail(SFFT2D_ERR_UNSUPPORTED, "too many tuner passes");
+    int32_t* ml = maxlists[slot & 1];
+    unsigned* cnt = cnt_slots + slot;
+    if (vote_pending[slot & 1])   // the vote two passes back still reads this list
+      ck(cudaStreamWaitEvent(st, c->ev_vote[slot & 1], 0), "cudaStreamWaitEvent");
+    unsigned seq;
     if (bb == n) {
       // B = N: |Z_p[k1, k2]| = |x_hat[s1i k1, s2i k2]| — one dense FFT serves every pass
       ensure_xhat(true);
-      lmax_tuner<T>(c, M, lgb, peakM, cf.mag_floor, maxlist, cnt_dev, st, true, p.s1i, p.s2i);
+      seq = lmax_tuner<T>(c, M, lgb, peakM, cf.mag_floor, ml, cnt, st, true, p.s1i, p.s2i);
     } else if (BB * sizeof(C) <= (size_t)kSmall2DBytes) {
       C* y = (C*)ws(c, "fold_y", BB * sizeof(C));
       const FoldOut fo = fold_launch<T, Tin>(c, x, lgN, lgb, tb, &p, 1, y, st);
+      const Publish pub = make_publish(c, 1);
+      seq = pub.seq;
       pre(c, st);
       k_small_pass<T><<<1, 1024, BB * (sizeof(C) + sizeof(T)) + bb * sizeof(C), st>>>(
           (const C*)fo.data, fo.Z, fo.Z == 1, lgb, p, (const C*)tb.tw[prec_of<T>()], lgN,
-          cf.mag_floor, maxlist, cnt_dev);
+          cf.mag_floor, ml, cnt, pub);
       post(c, "k_small_pass", st, (double)(fo.Z + 1) * BB * sizeof(C));
     } else {
       T* mg = (T*)ws(c, "grid_mag", BB * sizeof(T));
       unsigned long long* pk = (unsigned long long*)ws(c, "gpeak", 16);
       fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, &p, 1, (C*)nullptr, mg, pk, st);
-      lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, maxlist, cnt_dev, st, false, 1, 1);
+      seq = lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, ml, cnt, st, false, 1, 1);
     }
-    vote_list(pi, lgb, budget);
-    const long long count = read_u32(c, cnt_dev, st);
+    vote_list(pi, lgb, budget, slot);
+    const long long count = wait_published(c, seq, st);
     last_valid = true;
     last_b = bb;
     last_pi = pi;
     last_count = count;
+    last_slot = slot;
     const long long w = n / bb;
     if (count > 0 && count * (w + 2) * (w + 2) <= budget) {   // host mirror of the device test
       ++vote_passes;
@@ -968,12 +1040,15 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   if (!have_votes && last_valid && maxc > 0) {
     // every pass exceeded the vote budget: fall back to the final pass (tuner.py:228-234)
     if (last_count > 0) {
-      vote_list(last_pi, ilog2(last_b), 0);   // cnt_dev still holds the last pass's count
+      vote_list(last_pi, ilog2(last_b), 0, last_slot);   // its list and count slot are intact
       have_votes = true;
     }
     vote_passes = 1;
   }
   S->vote_passes = vote_passes;
+  // the histogram is complete once the side-stream votes are
+  ck(cudaEventRecord(c->ev_lmax, c->vote_st), "cudaEventRecord");
+  ck(cudaStreamWaitEvent(st, c->ev_lmax, 0), "cudaStreamWaitEvent");
   int32_t* keys = (int32_t*)ws(c, "keys", (size_t)nkeys * 4);
   unsigned* kt = (unsigned*)ws(c, "keys_tot", 16);
 
@@ -1179,6 +1254,8 @@ extern "C" {
 
 int sfft2d_abi_version(void) { return SFFT2D_ABI_VERSION; }
 
+double sfft2d_ctx_sync_us(const sfft2d_ctx* c) { return c ? c->sync_us : 0.0; }
+
 int sfft2d_ctx_create(int device, sfft2d_ctx** out) {
   if (!out) return SFFT2D_ERR_VALUE;
   *out = nullptr;
@@ -1187,6 +1264,15 @@ int sfft2d_ctx_create(int device, sfft2d_ctx** out) {
   int rc = guarded(c, [&] {
     ck(cudaMallocHost(&c->pinned, 4096), "cudaMallocHost");
     ck(cudaMallocHost(&c->perm_pinned, kPermPinned * sizeof(Perm)), "cudaMallocHost");
+    ck(cudaHostAlloc((void**)&c->mapped_h, 64, cudaHostAllocMapped), "cudaHostAlloc");
+    std::memset(c->mapped_h, 0, 64);
+    ck(cudaHostGetDevicePointer((void**)&c->mapped_d, c->mapped_h, 0), "cudaHostGetDevicePointer");
+    ck(cudaMalloc(&c->done_d, 64), "cudaMalloc");
+    ck(cudaMemset(c->done_d, 0, 64), "cudaMemset");
+    ck(cudaStreamCreateWithFlags(&c->vote_st, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreateWithFlags(&c->ev_lmax, cudaEventDisableTiming), "cudaEventCreate");
+    for (int i = 0; i < 2; ++i)
+      ck(cudaEventCreateWithFlags(&c->ev_vote[i], cudaEventDisableTiming), "cudaEventCreate");
     allow_all_T<float>();
     allow_all_T<double>();
   });
@@ -1213,6 +1299,12 @@ void sfft2d_ctx_destroy(sfft2d_ctx* c) {
     }
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->perm_pinned) cudaFreeHost(c->perm_pinned);
+  if (c->mapped_h) cudaFreeHost(c->mapped_h);
+  if (c->done_d) cudaFree(c->done_d);
+  if (c->vote_st) cudaStreamDestroy(c->vote_st);
+  if (c->ev_lmax) cudaEventDestroy(c->ev_lmax);
+  for (int i = 0; i < 2; ++i)
+    if (c->ev_vote[i]) cudaEventDestroy(c->ev_vote[i]);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   delete c;
 }
@@ -1328,6 +1420,7 @@ static int atsfft_impl(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host,
     cudaStream_t st = (cudaStream_t)stream;
     std::memset(res, 0, sizeof(*res));
     c->launches = 0;
+    c->sync_us = 0;
     c->has_res = false;
     const void* xd = stage_input(c, x, x_dtype, x_on_host, n, st);
     dispatch(x_dtype, precision, [&](auto t, auto tin) {

@@ -69,6 +69,32 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
+// Publish a final per-launch count to mapped (zero-copy) host memory: every
+// CTA calls this once after its contribution to *count is done; the CTA that
+// takes ticket `target - 1` of the monotonic `done` counter is the last one and
+// writes slot[1] = count, then slot[0] = seq (system-scope fences), so the
+// host can spin on seq without a stream synchronisation.
+__device__ __forceinline__ void publish_count(unsigned* count, unsigned* done, unsigned target,
+                                              volatile unsigned* slot, unsigned seq) {
+  __threadfence();
+  const unsigned t = atomicAdd(done, 1u);
+  if (t + 1u == target) {
+    __threadfence();
+    const unsigned v = atomicAdd(count, 0u);
+    slot[1] = v;
+    __threadfence_system();
+    slot[0] = seq;
+    __threadfence_system();
+  }
+}
+
+struct Publish {
+  unsigned* done;
+  unsigned target;
+  volatile unsigned* slot;
+  unsigned seq;
+};
+
 // one permutation as the kernels consume it (see hashing.py:45-80)
 struct Perm {
   uint32_t s1, s2, t1, t2, s1i, s2i;

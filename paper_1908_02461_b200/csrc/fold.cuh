@@ -80,8 +80,10 @@ struct FoldGeom {
 template <typename Tin, typename T, int NL, int CPT>
 __global__ void __launch_bounds__(kFoldThreads)
 k_fold(const Tin* __restrict__ x, const T* __restrict__ space, PermPack pp, int nloops,
-       FoldGeom gm, cplx<T>* __restrict__ dst) {
+       FoldGeom gm, cplx<T>* __restrict__ dst, unsigned long long* __restrict__ zero_peak = nullptr) {
   using C = cplx<T>;
+  if (zero_peak && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0)
+    *zero_peak = 0ull;
   __shared__ T s_w[NL * kFoldMaxRows];
   __shared__ int s_rows[kFoldMaxRows];
   __shared__ int s_nnz;
@@ -242,6 +244,73 @@ __device__ __forceinline__ C sum_partials(const C* __restrict__ p, size_t stride
   return cadd(cadd(cadd(a[0], a[1]), cadd(a[2], a[3])), cadd(cadd(a[4], a[5]), cadd(a[6], a[7])));
 }
 
+// Single-loop fold for B >= 512 (every output sums only (N/B)^2 <= 1024
+// samples): CTA = 512 columns (2 per thread, 16-byte loads) x RH consecutive
+// output rows rho; for each column alias and row alias the RH row loads are
+// independent, and row aliases are unrolled by 4, so a thread keeps 4*RH
+// 16-byte loads in flight.  Writes the permuted grid directly (Z = 1).
+template <typename Tin, typename T, int RH>
+__global__ void __launch_bounds__(256)
+k_fold_wide(const Tin* __restrict__ x, const T* __restrict__ space, Perm p, int lgN, int lgB,
+            cplx<T>* __restrict__ y, unsigned long long* __restrict__ zero_peak = nullptr) {
+  using C = cplx<T>;
+  __shared__ T s_w[RH * 32];
+  if (zero_peak && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *zero_peak = 0ull;
+  const int B = 1 << lgB;
+  const unsigned maskN = (1u << lgN) - 1u, maskB = (unsigned)B - 1u;
+  const int A = 1 << (lgN - lgB);            // aliases per axis (<= 32)
+  const int rho0 = blockIdx.y * RH;
+  const int kap = blockIdx.x * 512 + threadIdx.x * 2;
+  for (int e = threadIdx.x; e < RH * A; e += blockDim.x) {
+    const int r = e / A, j = e - r * A;
+    s_w[r * 32 + j] = space[(p.s1i * ((unsigned)(rho0 + r + (j << lgB)) - p.t1)) & maskN];
+  }
+  __syncthreads();
+  C acc[RH][2];
+#pragma unroll
+  for (int r = 0; r < RH; ++r) acc[r][0] = acc[r][1] = mk<T>(0, 0);
+  for (int i = 0; i < A; ++i) {
+    const int c = kap + (i << lgB);
+    const T wc0 = __ldg(space + ((p.s2i * ((unsigned)c - p.t2)) & maskN));
+    const T wc1 = __ldg(space + ((p.s2i * ((unsigned)c + 1u - p.t2)) & maskN));
+    C u[RH][2];
+#pragma unroll
+    for (int r = 0; r < RH; ++r) u[r][0] = u[r][1] = mk<T>(0, 0);
+    const Tin* col = x + c;
+#pragma unroll 4
+    for (int j = 0; j < A; ++j) {
+      C v[RH][2];
+#pragma unroll
+      for (int r = 0; r < RH; ++r)
+        ColLoad<Tin, T, 2>::ld(col + ((size_t)(rho0 + r + (j << lgB)) << lgN), v[r]);
+#pragma unroll
+      for (int r = 0; r < RH; ++r) {
+        const T w = s_w[r * 32 + j];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          u[r][q].x = fma(w, v[r][q].x, u[r][q].x);
+          u[r][q].y = fma(w, v[r][q].y, u[r][q].y);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < RH; ++r) {
+      acc[r][0].x = fma(wc0, u[r][0].x, acc[r][0].x);
+      acc[r][0].y = fma(wc0, u[r][0].y, acc[r][0].y);
+      acc[r][1].x = fma(wc1, u[r][1].x, acc[r][1].x);
+      acc[r][1].y = fma(wc1, u[r][1].y, acc[r][1].y);
+    }
+  }
+  const unsigned b0 = (p.s2i * ((unsigned)kap - p.t2)) & maskB;
+  const unsigned b1 = (p.s2i * ((unsigned)kap + 1u - p.t2)) & maskB;
+#pragma unroll
+  for (int r = 0; r < RH; ++r) {
+    const unsigned a = (p.s1i * ((unsigned)(rho0 + r) - p.t1)) & maskB;
+    y[(size_t)a * B + b0] = acc[r][0];
+    y[(size_t)a * B + b1] = acc[r][1];
+  }
+}
+
 // Sum the Z partials in fixed order and scatter to the permuted bucket grid.
 template <typename T>
 __global__ void k_fold_reduce(const cplx<T>* __restrict__ part, int Z, int nloops, int lgB,
@@ -297,7 +366,8 @@ template <typename T>
 __global__ void __launch_bounds__(1024)
 k_small_pass(const cplx<T>* __restrict__ part, int Z, bool permuted, int lgB, Perm p,
              const cplx<T>* __restrict__ tw, int lgN, double floor_rel,
-             int32_t* __restrict__ list, unsigned* __restrict__ count) {
+             int32_t* __restrict__ list, unsigned* __restrict__ count,
+             Publish pub = Publish{nullptr, 0, nullptr, 0}) {
   using C = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* s = reinterpret_cast<C*>(smem_raw);
@@ -379,7 +449,10 @@ k_small_pass(const cplx<T>* __restrict__ part, int Z, bool permuted, int lgB, Pe
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) *count = s_n;
+  if (threadIdx.x == 0) {
+    *count = s_n;
+    if (pub.slot) publish_count(count, pub.done, pub.target, pub.slot, pub.seq);
+  }
 }
 
 inline FoldGeom fold_geometry(int lgN, int lgB, int cpt) {

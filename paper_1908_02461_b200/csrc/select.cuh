@@ -114,7 +114,8 @@ __global__ void __launch_bounds__(512)
 k_lmax_rows(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, int rb,
             const unsigned long long* __restrict__ peak, double floor_rel,
             uint32_t* __restrict__ bits, unsigned* __restrict__ blk_counts,
-            int32_t* __restrict__ list = nullptr, unsigned* __restrict__ count = nullptr) {
+            int32_t* __restrict__ list = nullptr, unsigned* __restrict__ count = nullptr,
+            Publish pub = Publish{nullptr, 0, nullptr, 0}) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* S = reinterpret_cast<T*>(smem_raw);
   __shared__ unsigned s_cnt[32];
@@ -211,6 +212,7 @@ k_lmax_rows(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, int rb,
         list[pos++] = (int32_t)((word0 + w) * 32 + k);
       }
     }
+    if (pub.slot && threadIdx.x == 0) publish_count(count, pub.done, pub.target, pub.slot, pub.seq);
     return;
   }
   __syncthreads();

@@ -17,6 +17,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -170,6 +171,7 @@ def _run_ats(x, cfg: TunerConfig, est_loops: int, rng, precision, device, estima
             ptr, on_host = img.tensor.data_ptr(), 0
         else:
             ptr, on_host = img.host.ctypes.data, 1
+        t_call = time.perf_counter()
         if estimate:
             rc = ctx.lib.sfft2d_atsfft_bitgen(ctx.handle, ptr, img.dtype_code, on_host, n,
                                               ctypes.byref(ccfg), int(est_loops), bitgen, prec, st,
@@ -178,6 +180,7 @@ def _run_ats(x, cfg: TunerConfig, est_loops: int, rng, precision, device, estima
             rc = ctx.lib.sfft2d_detect_sparsity_bitgen(ctx.handle, ptr, img.dtype_code, on_host, n,
                                                        ctypes.byref(ccfg), bitgen, prec, st,
                                                        ctypes.byref(sc))
+        ctx.last_call_us = (time.perf_counter() - t_call) * 1e6
         if rc == _native.ERR_VALUE and snapshot is not None:
             gen.bit_generator.state = snapshot   # the reference validates x before drawing
         ctx.check(rc)

@@ -21,6 +21,13 @@ for _ in range(10):
 e1.record()
 torch.cuda.synchronize()
 print(f"ms/transform {e0.elapsed_time(e1) / 10:.3f}")
+import time
+t0 = time.perf_counter()
+out, st = P.atsfft2d(x, P.TunerConfig(), 8, 11, precision=prec)
+t_py = (time.perf_counter() - t0) * 1e6
+ctx0 = _native.context()
+print(f"python call {t_py:.0f} us, native call {ctx0.last_call_us:.0f} us, "
+      f"of which blocked in sync {ctx0.lib.sfft2d_ctx_sync_us(ctx0.handle):.0f} us")
 print("passes (B, count, host_us):")
 for (b, c, _), us in zip(st.history, st.pass_us):
     print(f"  B={b:5d} count={c:7d} {us:8.1f} us")
