@@ -195,19 +195,26 @@ class Context:
 
 
 _contexts: dict = {}
+_ctx_lock = threading.Lock()
 
 
 def context(device=None) -> Context:
+    """The calling thread's context on `device`: a context (workspace, streams,
+    tables) must not be shared by concurrent host threads, so each thread gets
+    its own — this is what lets independent transforms run concurrently."""
     torch = _torch()
     if not torch.cuda.is_available():
         raise RuntimeError("no CUDA device is available: the sm_100a path has no CPU fallback")
     if device is None:
         device = torch.cuda.current_device()
-    device = int(device)
-    ctx = _contexts.get(device)
+    key = (int(device), threading.get_ident())
+    ctx = _contexts.get(key)
     if ctx is None:
-        ctx = Context(device)
-        _contexts[device] = ctx
+        with _ctx_lock:
+            ctx = _contexts.get(key)
+            if ctx is None:
+                ctx = Context(int(device))
+                _contexts[key] = ctx
     return ctx
 
 

@@ -1,0 +1,61 @@
+"""Batched / concurrent transforms on one GPU (BASELINE.json config c4: many
+independent images).
+
+ATSFFT is a chain of small sequential tuner passes, so one transform cannot
+fill 148 SMs.  Independent images are therefore run `concurrency` at a time,
+each on its own host thread with its own native context (workspace + CUDA
+streams); ctypes releases the GIL for the duration of the native call, so the
+latency-bound passes of one image overlap the bandwidth-bound passes of
+another.  Results are exactly those of calling ``atsfft2d`` on each image.
+"""
+
+from __future__ import annotations
+
+from concurrent.futures import ThreadPoolExecutor
+
+from .engine import SfftConfig, sfft2d, sfft2d_arrays
+from .tuner import TunerConfig, atsfft2d, atsfft2d_arrays
+
+__all__ = ["atsfft2d_batch", "sfft2d_batch"]
+
+_pools: dict = {}
+
+
+def _pool(workers: int) -> ThreadPoolExecutor:
+    pool = _pools.get(workers)
+    if pool is None:
+        pool = ThreadPoolExecutor(max_workers=workers, thread_name_prefix="sfft2d")
+        _pools[workers] = pool
+    return pool
+
+
+def atsfft2d_batch(xs, cfg: TunerConfig, est_loops: int, rngs, *, concurrency: int = 4,
+                   precision: str = "fp64", device=None, arrays: bool = False):
+    """``atsfft2d`` over a batch: ``xs`` images, ``rngs`` one seed/Generator per
+    image.  Returns a list of ``(spectrum, TunerState)`` in input order
+    (``((coords, values), state)`` with ``arrays=True``)."""
+    if len(xs) != len(rngs):
+        raise ValueError("need one rng per image")
+    fn = atsfft2d_arrays if arrays else atsfft2d
+
+    def one(i):
+        return fn(xs[i], cfg, est_loops, rngs[i], precision=precision, device=device)
+
+    if concurrency <= 1 or len(xs) <= 1:
+        return [one(i) for i in range(len(xs))]
+    return list(_pool(concurrency).map(one, range(len(xs))))
+
+
+def sfft2d_batch(xs, cfg: SfftConfig, rngs, *, concurrency: int = 4, precision: str = "fp64",
+                 device=None, arrays: bool = False):
+    """``sfft2d`` over a batch of images (one rng per image), input order kept."""
+    if len(xs) != len(rngs):
+        raise ValueError("need one rng per image")
+    fn = sfft2d_arrays if arrays else sfft2d
+
+    def one(i):
+        return fn(xs[i], cfg, rngs[i], precision=precision, device=device)
+
+    if concurrency <= 1 or len(xs) <= 1:
+        return [one(i) for i in range(len(xs))]
+    return list(_pool(concurrency).map(one, range(len(xs))))

@@ -302,3 +302,15 @@ def test_atsfft_generator_advance_on_configuration_error():
         err = e
     assert (ref_err is None) == (err is None)
     assert g1.integers(1 << 40) == g2.integers(1 << 40)
+
+
+def test_batch_concurrent_equals_sequential():
+    imgs = [P.sparse_image(512, 10 + i, 40 + i, snr_db=25.0, magnitude="loguniform") for i in range(6)]
+    xs = [im.x for im in imgs]
+    seq = [P.atsfft2d(x, P.TunerConfig(), 8, 100 + i) for i, x in enumerate(xs)]
+    par = P.atsfft2d_batch(xs, P.TunerConfig(), 8, [100 + i for i in range(6)], concurrency=3)
+    for (a, sa), (b, sb) in zip(seq, par):
+        assert a == b and sa == sb
+    s1 = [P.sfft2d(x, P.SfftConfig(n=512, k=12), 7) for x in xs]
+    s2 = P.sfft2d_batch(xs, P.SfftConfig(n=512, k=12), [7] * 6, concurrency=3)
+    assert s1 == s2
