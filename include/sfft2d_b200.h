@@ -125,6 +125,22 @@ int sfft2d_sfft(sfft2d_ctx* ctx, const void* x, int x_dtype, int x_on_host,
                 const sfft2d_sfft_config* cfg, const sfft2d_perm* perms, int precision,
                 void* stream, sfft2d_result* res);
 
+/* Loop split across devices: the location phase of
+ * sfft2d for a SUBSET of the location loops (engine.py:130-145, per-loop
+ * dedup).  counts: device uint8[n*n rounded up to a multiple of 32], set to the
+ * number of these loops that voted each coordinate.  Summing the ranks'
+ * counts (an allreduce) gives the full vote histogram of engine.py:148-160.  */
+int sfft2d_sfft_votes(sfft2d_ctx* ctx, const void* x, int x_dtype, int x_on_host,
+                      const sfft2d_sfft_config* cfg, const sfft2d_perm* perms, int nloops,
+                      int precision, void* stream, void* counts);
+
+/* Vote threshold + estimation loops + median/top-k/prune from a summed count
+ * histogram (engine.py:148-160, 163-284); est_perms: cfg->loops permutations. */
+int sfft2d_sfft_from_votes(sfft2d_ctx* ctx, const void* x, int x_dtype, int x_on_host,
+                           const sfft2d_sfft_config* cfg, const void* counts,
+                           const sfft2d_perm* est_perms, int precision, void* stream,
+                           sfft2d_result* res);
+
 /* Algorithm 2 — replaces atsfft2d(x, cfg, est_loops, rng) (tuner.py:244-282).
  * perms: the shared Generator's draws in order; at least
  * iters(n) + 2 + max(est_loops, 1) of them (tuner passes, confirmation passes,

@@ -29,7 +29,7 @@ EXPORTS = (
     "sfft2d_fetch_result", "sfft2d_fetch_votes", "sfft2d_binned_spectrum", "sfft2d_fft2d",
     "sfft2d_local_maxima", "sfft2d_top_bins", "sfft2d_ctx_set_profiling",
     "sfft2d_ctx_profile_report", "sfft2d_atsfft_bitgen", "sfft2d_detect_sparsity_bitgen",
-    "sfft2d_ctx_sync_us",
+    "sfft2d_ctx_sync_us", "sfft2d_sfft_votes", "sfft2d_sfft_from_votes",
 )
 
 
@@ -114,6 +114,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "sfft2d_top_bins": ([vp, vp, i32, i32, i64, i32, vp, vp], i32),
             "sfft2d_ctx_set_profiling": ([vp, i32], i32),
             "sfft2d_ctx_sync_us": ([vp], dbl),
+            "sfft2d_sfft_votes": ([vp, vp, i32, i32, P(SfftCfg), P(Perm), i32, i32, vp, vp], i32),
+            "sfft2d_sfft_from_votes": ([vp, vp, i32, i32, P(SfftCfg), vp, P(Perm), i32, vp,
+                                        P(ResultC)], i32),
             "sfft2d_ctx_profile_report": ([vp, ctypes.c_char_p, i64], i64),
         }
         for name, (args, res) in sig.items():

@@ -495,6 +495,12 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
   const int nlt = (g == 1) ? 1 : kMaxFoldLoops;
   const size_t dyn = (B < gm.TW) ? (size_t)nlt * gm.TW * sizeof(C) : 0;
   const double sup = (double)tb.support[lgB];
+  const size_t N = (size_t)1 << lgN;
+  T* wr = (T*)ws(c, "fold_w", 2 * g * N * sizeof(T));
+  T* wc = wr + g * N;
+  pre(c, st);
+  k_fold_weights<T><<<grid_for((long long)g * N), 256, 0, st>>>(space, pp, g, lgN, wr, wc);
+  post(c, "k_fold_weights", st, 2.0 * g * N * sizeof(T));
   if (g == 1 && B >= 512 && lgN - lgB <= 5 && y_direct) {
     // wide single-loop fold, permuted grid written directly
     const double by = sup * sup * sizeof(Tin) + (double)BB * sizeof(C);
@@ -502,11 +508,11 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
     const dim3 grid_w(B / 512, B / rh);
     pre(c, st);
     if (rh == 4)
-      k_fold_wide<Tin, T, 4><<<grid_w, 256, 0, st>>>(x, space, pp.p[0], lgN, lgB, (C*)y_direct, zero_peak);
+      k_fold_wide<Tin, T, 4><<<grid_w, 256, 0, st>>>(x, wr, wc, pp.p[0], lgN, lgB, (C*)y_direct, zero_peak);
     else if (rh == 2)
-      k_fold_wide<Tin, T, 2><<<grid_w, 256, 0, st>>>(x, space, pp.p[0], lgN, lgB, (C*)y_direct, zero_peak);
+      k_fold_wide<Tin, T, 2><<<grid_w, 256, 0, st>>>(x, wr, wc, pp.p[0], lgN, lgB, (C*)y_direct, zero_peak);
     else
-      k_fold_wide<Tin, T, 1><<<grid_w, 256, 0, st>>>(x, space, pp.p[0], lgN, lgB, (C*)y_direct, zero_peak);
+      k_fold_wide<Tin, T, 1><<<grid_w, 256, 0, st>>>(x, wr, wc, pp.p[0], lgN, lgB, (C*)y_direct, zero_peak);
     post(c, "k_fold", st, by);
     return FoldOut{y_direct, 1};
   }
@@ -514,9 +520,9 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
   const double fold_bytes = sup * sup * sizeof(Tin) + (double)gm.Z * g * BB * sizeof(C);
   pre(c, st);
   if (g == 1)
-    k_fold<Tin, T, 1, 2><<<grid, threads, dyn, st>>>(x, space, pp, g, gm, dst, zero_peak);
+    k_fold<Tin, T, 1, 2><<<grid, threads, dyn, st>>>(x, wr, wc, pp, g, gm, dst, zero_peak);
   else
-    k_fold<Tin, T, kMaxFoldLoops, 1><<<grid, threads, dyn, st>>>(x, space, pp, g, gm, dst, zero_peak);
+    k_fold<Tin, T, kMaxFoldLoops, 1><<<grid, threads, dyn, st>>>(x, wr, wc, pp, g, gm, dst, zero_peak);
   post(c, "k_fold", st, fold_bytes);
   return FoldOut{dst, gm.Z};
 }
@@ -1104,95 +1110,125 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
 }
 
 // ------------------------------------------------------------------ SFFT
+// SFFT location phase (engine.py:130-160) for `nloc` loops: fold all loops
+// from one read of x, top-num bins per loop, unhash with per-loop dedup.
+// Output: a byte histogram — OR of loop bits (mode kVoteOrBit, nloc <= 8 and
+// !want_counts) or per-coordinate loop counts (mode kVoteAdd8).  Returns the mode.
 template <typename T, typename Tin>
-void run_sfft(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, const sfft2d_perm* perms,
-              cudaStream_t st, sfft2d_result* res) {
-  using C = cplx<T>;
-  const int n = cf.n;
-  const int lgN = ilog2(n);
-  const int b = cf.b_bins;
-  const int L = cf.loops;
+int sfft_location(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, const DevTables& tb,
+                  const Perm* hp, const Perm* dp, int nloc, bool want_counts, uint32_t* out,
+                  cudaStream_t st) {
+  const int n = cf.n, lgN = ilog2(n), b = cf.b_bins, lgb = ilog2(b);
+  const long BB = (long)b * b;
+  const long nkeys = (long)n * n;
+  const long long num = std::max(1LL, (long long)cf.d_factor * cf.k);
+  T* mags = (T*)ws(c, "loc_mags", (size_t)nloc * BB * sizeof(T));
+  fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, hp, nloc, (cplx<T>*)nullptr, mags, nullptr, st);
+  int32_t* bins = (int32_t*)ws(c, "loc_bins", (size_t)nloc * num * 4);
+  if (num >= BB) {
+    pre(c, st);
+    k_iota_segments<<<grid_for(BB * nloc), 256, 0, st>>>(bins, BB, nloc);
+    post(c, "k_iota_segments", st, 0);
+  } else {
+    const int nblk = blocks_for(BB);
+    uint32_t* sb = (uint32_t*)ws(c, "loc_selbits", (size_t)nloc * words_for(BB) * 4);
+    unsigned* sc = (unsigned*)ws(c, "loc_selcnt", (size_t)nloc * nblk * 4);
+    topk_bits<T>(c, mags, BB, nloc, num, sb, sc, st);
+    unsigned* tots = (unsigned*)ws(c, "loc_tot", (size_t)nloc * 4 + 16);
+    compact(c, sb, sc, BB, nloc, bins, (long)num, tots, st);
+  }
+  const size_t hb = hist_bytes(nkeys, kVoteAdd8);
+  const int w = n / b;
+  const long long len = (w == 1) ? 3 : std::min<long long>(w + 2, n);
+  const long long per = num * len * len;
+  const bool direct = nloc <= 8 && !want_counts;
+  uint32_t* masks = direct ? out : (uint32_t*)ws(c, "hist_masks", hb);
+  ck(cudaMemsetAsync(masks, 0, hb, st), "memset hist");
+  if (!direct) ck(cudaMemsetAsync(out, 0, hb, st), "memset counts");
+  const long nw = (long)(hb / 4);
+  for (int g0 = 0; g0 < nloc; g0 += 8) {
+    const int g = std::min(8, nloc - g0);
+    pre(c, st);
+    k_vote<<<dim3(grid_for(per, 256, kNumSMs * 8), g), 256, 0, st>>>(
+        bins + (size_t)g0 * num, (long)num, nullptr, (long)num, dp + g0, lgN, lgb, 1, kVoteOrBit,
+        0, masks);
+    post(c, "k_vote", st, (double)per * g * 4.0);
+    if (!direct) {
+      pre(c, st);
+      k_mask_to_counts<<<grid_for(nw, 256, kNumSMs * 8), 256, 0, st>>>(masks, out, nw);
+      post(c, "k_mask_to_counts", st, 3.0 * nw * 4);
+    }
+  }
+  return direct ? kVoteOrBit : kVoteAdd8;
+}
+
+// SFFT vote threshold + estimation (engine.py:148-160, 163-284) from a
+// histogram in `mode`; results go to the context's result buffers.
+template <typename T, typename Tin>
+void sfft_from_hist(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, const DevTables& tb,
+                    const uint32_t* hist, int mode, const Perm* hp_est, const Perm* dp_est,
+                    cudaStream_t st, sfft2d_result* res) {
+  const int n = cf.n, lgN = ilog2(n), lgb = ilog2(cf.b_bins);
+  const long nkeys = (long)n * n;
+  int32_t* keys = (int32_t*)ws(c, "keys", (size_t)nkeys * 4);
+  unsigned* kt = (unsigned*)ws(c, "keys_tot", 16);
+  const unsigned m = hist_compact(c, hist, nkeys, mode, (unsigned)cf.vote_threshold, keys, kt, st);
+  res->count = 0;
+  res->ordered_by_magnitude = 0;
+  res->n_candidates = m;
+  c->res_count = 0;
+  if (m == 0) return;
+  estimate_and_select<T, Tin>(c, x, lgN, lgb, tb, hp_est, dp_est, cf.loops, keys, m, kt, cf.k,
+                              cf.gain_floor, cf.prune_rel, false, (const cplx<T>*)nullptr, st, res);
+}
+
+void check_sfft_cfg(const sfft2d_sfft_config& cf) {
+  const int n = cf.n, b = cf.b_bins, L = cf.loops;
   if (!is_pow2(b) || b > n || n % b) fail(SFFT2D_ERR_CONFIG, "bin count must be a power of 2 dividing n");
   if (L < 1) fail(SFFT2D_ERR_CONFIG, "loops must be >= 1");
   if (cf.vote_threshold < 1 || cf.vote_threshold > L) fail(SFFT2D_ERR_CONFIG, "vote_threshold out of range");
   if (L > kMaxLoops) fail(SFFT2D_ERR_UNSUPPORTED, "more than 64 loops");
   const long long num = std::max(1LL, (long long)cf.d_factor * cf.k);
-  const int lgb = ilog2(b);
-  const long BB = (long)b * b;
-  if (num > BB) fail(SFFT2D_ERR_CONFIG, "d_factor*k exceeds the bin budget");
-  const DevTables& tb = find_tables(c, n, cf.window_delta_pass, cf.window_delta_stop);
-  std::vector<Perm> hp(2 * L);
-  for (int i = 0; i < 2 * L; ++i) hp[i] = to_perm(perms[i], n);
-  Perm* dp = (Perm*)ws(c, "perms", (size_t)2 * L * sizeof(Perm));
-  ck(cudaMemcpyAsync(dp, hp.data(), (size_t)2 * L * sizeof(Perm), cudaMemcpyHostToDevice, st),
-     "H2D perms");
-  const long nkeys = (long)n * n;
+  if (num > (long long)b * b) fail(SFFT2D_ERR_CONFIG, "d_factor*k exceeds the bin budget");
+}
+
+template <typename Tin>
+void check_finite_now(sfft2d_ctx* c, const Tin* x, long nkeys, cudaStream_t st) {
   unsigned* finite = (unsigned*)ws(c, "finite", 16);
   ck(cudaMemsetAsync(finite, 0, 16, st), "memset");
   pre(c, st);
   k_check_finite<Tin><<<grid_for(nkeys, 256, kNumSMs * 8), 256, 0, st>>>(x, nkeys, finite);
   post(c, "k_check_finite", st, (double)nkeys * sizeof(Tin));
-
-  // location loops: L grids from one read of x, top-num bins per grid
-  T* mags = (T*)ws(c, "loc_mags", (size_t)L * BB * sizeof(T));
-  fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, hp.data(), L, (C*)nullptr, mags, nullptr, st);
-  int32_t* bins = (int32_t*)ws(c, "loc_bins", (size_t)L * num * 4);
-  if (num >= BB) {
-    pre(c, st);
-    k_iota_segments<<<grid_for(BB * L), 256, 0, st>>>(bins, BB, L);
-    post(c, "k_iota_segments", st, 0);
-  } else {
-    const int nblk = blocks_for(BB);
-    uint32_t* sb = (uint32_t*)ws(c, "loc_selbits", (size_t)L * words_for(BB) * 4);
-    unsigned* sc = (unsigned*)ws(c, "loc_selcnt", (size_t)L * nblk * 4);
-    topk_bits<T>(c, mags, BB, L, num, sb, sc, st);
-    unsigned* tots = (unsigned*)ws(c, "loc_tot", (size_t)L * 4 + 16);
-    compact(c, sb, sc, BB, L, bins, (long)num, tots, st);
-  }
   if (read_u32(c, finite, st)) fail(SFFT2D_ERR_VALUE, "matrix contains NaN or Inf");
+}
 
-  // votes with per-loop dedup (bit per loop), threshold
-  uint32_t* hist = (uint32_t*)ws(c, "hist", hist_bytes(nkeys, kVoteAdd8));
-  ck(cudaMemsetAsync(hist, 0, hist_bytes(nkeys, kVoteAdd8), st), "memset hist");
-  const int w = n / b;
-  const long long len = (w == 1) ? 3 : std::min<long long>(w + 2, n);
-  const long long per = num * len * len;
-  int cmode = kVoteOrBit;
-  const uint32_t* chist = hist;
-  if (L <= 8) {
-    pre(c, st);
-    k_vote<<<dim3(grid_for(per, 256, kNumSMs * 8), L), 256, 0, st>>>(bins, (long)num, nullptr, (long)num, dp,
-                                                                   lgN, lgb, 1, kVoteOrBit, 0, hist);
-    post(c, "k_vote", st, 0);
-  } else {
-    uint32_t* counts = (uint32_t*)ws(c, "hist_cnt", hist_bytes(nkeys, kVoteAdd8));
-    ck(cudaMemsetAsync(counts, 0, hist_bytes(nkeys, kVoteAdd8), st), "memset");
-    const long nw = (long)(hist_bytes(nkeys, kVoteAdd8) / 4);
-    for (int g0 = 0; g0 < L; g0 += 8) {
-      const int g = std::min(8, L - g0);
-      pre(c, st);
-      k_vote<<<dim3(grid_for(per, 256, kNumSMs * 8), g), 256, 0, st>>>(
-          bins + (size_t)g0 * num, (long)num, nullptr, (long)num, dp + g0, lgN, lgb, 1, kVoteOrBit,
-          0, hist);
-      post(c, "k_vote", st, 0);
-      pre(c, st);
-      k_mask_to_counts<<<grid_for(nw, 256, kNumSMs * 8), 256, 0, st>>>(hist, counts, nw);
-      post(c, "k_mask_to_counts", st, 0);
-    }
-    cmode = kVoteAdd8;
-    chist = counts;
-  }
-  int32_t* keys = (int32_t*)ws(c, "keys", (size_t)nkeys * 4);
-  unsigned* kt = (unsigned*)ws(c, "keys_tot", 16);
-  const unsigned m = hist_compact(c, chist, nkeys, cmode, (unsigned)cf.vote_threshold, keys, kt, st);
-  res->count = 0;
-  res->ordered_by_magnitude = 0;
-  res->n_candidates = m;
+// Upload `count` permutations to a named device array; returns (host, device).
+std::pair<std::vector<Perm>, Perm*> upload_perms(sfft2d_ctx* c, const char* name,
+                                                 const sfft2d_perm* perms, int count, int n,
+                                                 cudaStream_t st) {
+  std::vector<Perm> hp(std::max(count, 1));
+  for (int i = 0; i < count; ++i) hp[i] = to_perm(perms[i], n);
+  Perm* dp = (Perm*)ws(c, name, hp.size() * sizeof(Perm));
+  for (int i = 0; i < count; ++i) c->perm_pinned[i] = hp[i];
+  if (count > kPermPinned) fail(SFFT2D_ERR_UNSUPPORTED, "too many permutations");
+  ck(cudaMemcpyAsync(dp, c->perm_pinned, (size_t)count * sizeof(Perm), cudaMemcpyHostToDevice, st),
+     "H2D perms");
+  ck(cudaStreamSynchronize(st), "sync");   // perm_pinned is reused by the next upload
+  return {hp, dp};
+}
+
+template <typename T, typename Tin>
+void run_sfft(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, const sfft2d_perm* perms,
+              cudaStream_t st, sfft2d_result* res) {
+  check_sfft_cfg(cf);
+  const int L = cf.loops;
+  const DevTables& tb = find_tables(c, cf.n, cf.window_delta_pass, cf.window_delta_stop);
+  auto up = upload_perms(c, "perms", perms, 2 * L, cf.n, st);
+  check_finite_now<Tin>(c, x, (long)cf.n * cf.n, st);
+  uint32_t* hist = (uint32_t*)ws(c, "hist", hist_bytes((long)cf.n * cf.n, kVoteAdd8));
+  const int mode = sfft_location<T, Tin>(c, x, cf, tb, up.first.data(), up.second, L, false, hist, st);
   res->perms_used = 2 * L;
-  c->res_count = 0;
-  if (m == 0) return;
-  estimate_and_select<T, Tin>(c, x, lgN, lgb, tb, hp.data() + L, dp + L, L, keys, m, kt, cf.k,
-                              cf.gain_floor, cf.prune_rel, false, (const C*)nullptr, st, res);
+  sfft_from_hist<T, Tin>(c, x, cf, tb, hist, mode, up.first.data() + L, up.second + L, st, res);
 }
 
 template <typename F>
@@ -1454,6 +1490,57 @@ static int detect_impl(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host,
       run_ats<T, Tin>(c, (const Tin*)xd, n, *cfg, 0, perms, n_perms, bitgen, st, false, &dummy,
                       state);
     });
+  });
+}
+
+int sfft2d_sfft_votes(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host,
+                      const sfft2d_sfft_config* cfg, const sfft2d_perm* perms, int nloops,
+                      int precision, void* stream, void* counts) {
+  return guarded(c, [&] {
+    if (!cfg || !perms || !x || !counts || nloops < 1) fail(SFFT2D_ERR_VALUE, "bad arguments");
+    check_side(cfg->n);
+    check_sfft_cfg(*cfg);
+    if (nloops > cfg->loops) fail(SFFT2D_ERR_VALUE, "more loops than the configuration");
+    cudaStream_t st = (cudaStream_t)stream;
+    c->launches = 0;
+    const void* xd = stage_input(c, x, x_dtype, x_on_host, cfg->n, st);
+    const DevTables& tb = find_tables(c, cfg->n, cfg->window_delta_pass, cfg->window_delta_stop);
+    auto up = upload_perms(c, "perms", perms, nloops, cfg->n, st);
+    dispatch(x_dtype, precision, [&](auto t, auto tin) {
+      using T = decltype(t);
+      using Tin = decltype(tin);
+      check_finite_now<Tin>(c, (const Tin*)xd, (long)cfg->n * cfg->n, st);
+      sfft_location<T, Tin>(c, (const Tin*)xd, *cfg, tb, up.first.data(), up.second, nloops, true,
+                            (uint32_t*)counts, st);
+    });
+  });
+}
+
+int sfft2d_sfft_from_votes(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host,
+                           const sfft2d_sfft_config* cfg, const void* counts,
+                           const sfft2d_perm* est_perms, int precision, void* stream,
+                           sfft2d_result* res) {
+  return guarded(c, [&] {
+    if (!cfg || !est_perms || !x || !counts || !res) fail(SFFT2D_ERR_VALUE, "bad arguments");
+    check_side(cfg->n);
+    check_sfft_cfg(*cfg);
+    cudaStream_t st = (cudaStream_t)stream;
+    std::memset(res, 0, sizeof(*res));
+    c->launches = 0;
+    c->has_res = false;
+    const void* xd = stage_input(c, x, x_dtype, x_on_host, cfg->n, st);
+    const DevTables& tb = find_tables(c, cfg->n, cfg->window_delta_pass, cfg->window_delta_stop);
+    auto up = upload_perms(c, "perms_est", est_perms, cfg->loops, cfg->n, st);
+    dispatch(x_dtype, precision, [&](auto t, auto tin) {
+      using T = decltype(t);
+      using Tin = decltype(tin);
+      sfft_from_hist<T, Tin>(c, (const Tin*)xd, *cfg, tb, (const uint32_t*)counts, kVoteAdd8,
+                             up.first.data(), up.second, st, res);
+    });
+    res->precision = precision;
+    res->gpu_launches = c->launches;
+    c->res_prec = precision;
+    c->has_res = true;
   });
 }
 

@@ -77,10 +77,27 @@ struct FoldGeom {
   int rpc;       // row aliases per chunk
 };
 
+// Natural-order window weights of this pass, wr[l][r] = g[s1i_l (r - t1_l) mod N]
+// and wc[l][c] = g[s2i_l (c - t2_l) mod N]: computed once per pass so the fold
+// reads them coalesced instead of gathering the window table per element.
+template <typename T>
+__global__ void k_fold_weights(const T* __restrict__ space, PermPack pp, int nloops, int lgN,
+                               T* __restrict__ wr, T* __restrict__ wc) {
+  const int N = 1 << lgN;
+  const unsigned maskN = (unsigned)N - 1u;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nloops * N; e += gridDim.x * blockDim.x) {
+    const int l = e >> lgN;
+    const unsigned r = (unsigned)(e & (N - 1));
+    wr[e] = space[(pp.p[l].s1i * (r - pp.p[l].t1)) & maskN];
+    wc[e] = space[(pp.p[l].s2i * (r - pp.p[l].t2)) & maskN];
+  }
+}
+
 template <typename Tin, typename T, int NL, int CPT>
 __global__ void __launch_bounds__(kFoldThreads)
-k_fold(const Tin* __restrict__ x, const T* __restrict__ space, PermPack pp, int nloops,
-       FoldGeom gm, cplx<T>* __restrict__ dst, unsigned long long* __restrict__ zero_peak = nullptr) {
+k_fold(const Tin* __restrict__ x, const T* __restrict__ wrow, const T* __restrict__ wcol,
+       PermPack pp, int nloops, FoldGeom gm, cplx<T>* __restrict__ dst,
+       unsigned long long* __restrict__ zero_peak = nullptr) {
   using C = cplx<T>;
   if (zero_peak && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0)
     *zero_peak = 0ull;
@@ -104,7 +121,7 @@ k_fold(const Tin* __restrict__ x, const T* __restrict__ space, PermPack pp, int 
 #pragma unroll
     for (int l = 0; l < NL; ++l) {
       T w = (T)0;
-      if (l < nloops) w = space[(pp.p[l].s1i * (r - pp.p[l].t1)) & maskN];
+      if (l < nloops) w = wrow[((size_t)l << gm.lgN) + r];
       s_w[l * kFoldMaxRows + jj] = w;
     }
   }
@@ -148,7 +165,7 @@ k_fold(const Tin* __restrict__ x, const T* __restrict__ space, PermPack pp, int 
 #pragma unroll
         for (int q = 0; q < CPT; ++q) {
           T w = (T)0;
-          if (l < nloops) w = __ldg(space + ((pp.p[l].s2i * ((unsigned)(c + q) - pp.p[l].t2)) & maskN));
+          if (l < nloops) w = __ldg(wcol + ((size_t)l << gm.lgN) + c + q);
           wc[l][q] = w;
           any |= (w != (T)0);
         }
@@ -251,8 +268,9 @@ __device__ __forceinline__ C sum_partials(const C* __restrict__ p, size_t stride
 // 16-byte loads in flight.  Writes the permuted grid directly (Z = 1).
 template <typename Tin, typename T, int RH>
 __global__ void __launch_bounds__(256)
-k_fold_wide(const Tin* __restrict__ x, const T* __restrict__ space, Perm p, int lgN, int lgB,
-            cplx<T>* __restrict__ y, unsigned long long* __restrict__ zero_peak = nullptr) {
+k_fold_wide(const Tin* __restrict__ x, const T* __restrict__ wrow, const T* __restrict__ wcol,
+            Perm p, int lgN, int lgB, cplx<T>* __restrict__ y,
+            unsigned long long* __restrict__ zero_peak = nullptr) {
   using C = cplx<T>;
   __shared__ T s_w[RH * 32];
   if (zero_peak && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *zero_peak = 0ull;
@@ -263,7 +281,7 @@ k_fold_wide(const Tin* __restrict__ x, const T* __restrict__ space, Perm p, int 
   const int kap = blockIdx.x * 512 + threadIdx.x * 2;
   for (int e = threadIdx.x; e < RH * A; e += blockDim.x) {
     const int r = e / A, j = e - r * A;
-    s_w[r * 32 + j] = space[(p.s1i * ((unsigned)(rho0 + r + (j << lgB)) - p.t1)) & maskN];
+    s_w[r * 32 + j] = wrow[rho0 + r + (j << lgB)];
   }
   __syncthreads();
   C acc[RH][2];
@@ -271,8 +289,8 @@ k_fold_wide(const Tin* __restrict__ x, const T* __restrict__ space, Perm p, int 
   for (int r = 0; r < RH; ++r) acc[r][0] = acc[r][1] = mk<T>(0, 0);
   for (int i = 0; i < A; ++i) {
     const int c = kap + (i << lgB);
-    const T wc0 = __ldg(space + ((p.s2i * ((unsigned)c - p.t2)) & maskN));
-    const T wc1 = __ldg(space + ((p.s2i * ((unsigned)c + 1u - p.t2)) & maskN));
+    const T wc0 = __ldg(wcol + c);
+    const T wc1 = __ldg(wcol + c + 1);
     C u[RH][2];
 #pragma unroll
     for (int r = 0; r < RH; ++r) u[r][0] = u[r][1] = mk<T>(0, 0);

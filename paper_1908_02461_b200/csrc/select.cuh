@@ -146,32 +146,37 @@ k_lmax_rows(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, int rb,
   const int wtot = rb << wpr_lg;
   const size_t word0 = ((size_t)r0 << lgB) >> 5;
   const int blk_first = (int)((word0 * 32) / kCmpElems);
-  // A warp owns a 32-column strip and walks down the tile's rows with a
-  // 3-row register window; horizontal neighbours come from lane shuffles
-  // (lanes 0/31 load their outside neighbour), so a bin costs ~1 LDS.
-  auto row_vals = [&](int i, unsigned c, unsigned qm, unsigned q, unsigned qp, T& l, T& m, T& r) {
-    const T* row = S + (i << lgB);
-    m = row[q];
-    l = __shfl_up_sync(0xffffffffu, m, 1);
-    r = __shfl_down_sync(0xffffffffu, m, 1);
-    if (lane == 0) l = row[qm];
-    if (lane == 31) r = row[qp];
-  };
+  // A warp owns a 32-column strip and walks down the tile's rows keeping the
+  // strip's own values of 3 rows in registers.  Per row it loads one value per
+  // lane and votes on the floor test; only if some lane passes are the
+  // horizontal neighbours fetched (lane shuffles, lanes 0/31 load the outside
+  // neighbour) — at B = N nearly every bin fails the floor, so a 32-bin word
+  // costs a handful of instructions.
   for (int strip = warp; strip < (1 << wpr_lg); strip += nwarps) {
     const unsigned c = ((unsigned)strip << 5) + lane;
     const unsigned cm = (c - 1u) & mask, cp = (c + 1u) & mask;
     const unsigned q1 = PERM ? (s2 * c) & mask : c;
     const unsigned q0 = PERM ? (s2 * cm) & mask : cm;
     const unsigned q2 = PERM ? (s2 * cp) & mask : cp;
-    T ul, um, ur, ml, mm, mr, dl, dm, dr;
-    row_vals(0, c, q0, q1, q2, ul, um, ur);
-    row_vals(1, c, q0, q1, q2, ml, mm, mr);
+    T um = S[q1];
+    T mm = S[B + q1];
     for (int i = 1; i <= rb; ++i) {
-      row_vals(i + 1, c, q0, q1, q2, dl, dm, dr);
-      // branch-free: every comparison evaluated, combined bitwise
-      const bool f = live & (mm >= flT) & (mm > ul) & (mm > um) & (mm > ur) & (mm > ml) &
-                     (mm > mr) & (mm > dl) & (mm > dm) & (mm > dr);
-      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      const T* dnrow = S + ((i + 1) << lgB);
+      const T dm = dnrow[q1];
+      const bool cand = live & (mm >= flT);
+      unsigned bal = 0;
+      if (__any_sync(0xffffffffu, cand)) {
+        const T* uprow = dnrow - 2 * B;
+        const T* mdrow = dnrow - B;
+        T ul = __shfl_up_sync(0xffffffffu, um, 1), ur = __shfl_down_sync(0xffffffffu, um, 1);
+        T ml = __shfl_up_sync(0xffffffffu, mm, 1), mr = __shfl_down_sync(0xffffffffu, mm, 1);
+        T dl = __shfl_up_sync(0xffffffffu, dm, 1), dr = __shfl_down_sync(0xffffffffu, dm, 1);
+        if (lane == 0) { ul = uprow[q0]; ml = mdrow[q0]; dl = dnrow[q0]; }
+        if (lane == 31) { ur = uprow[q2]; mr = mdrow[q2]; dr = dnrow[q2]; }
+        const bool f = cand & (mm > ul) & (mm > um) & (mm > ur) & (mm > ml) & (mm > mr) &
+                       (mm > dl) & (mm > dm) & (mm > dr);
+        bal = __ballot_sync(0xffffffffu, f);
+      }
       const int w = ((i - 1) << wpr_lg) + strip;
       if (UNORDERED) {
         if (lane == 0) s_words[w] = bal;
@@ -180,8 +185,8 @@ k_lmax_rows(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, int rb,
         if (bal)
           atomicAdd(&s_cnt[(int)(((word0 + w) * 32) / kCmpElems) - blk_first], (unsigned)__popc(bal));
       }
-      ul = ml; um = mm; ur = mr;
-      ml = dl; mm = dm; mr = dr;
+      um = mm;
+      mm = dm;
     }
   }
   if (UNORDERED) {
