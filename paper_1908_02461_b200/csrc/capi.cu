@@ -15,6 +15,8 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <string_view>
+#include <unordered_map>
 #include <mutex>
 #include <string>
 #include <utility>
@@ -75,7 +77,8 @@ struct sfft2d_ctx {
   int device = 0;
   std::string err;
   std::vector<DevTables> tables;
-  std::map<std::string, std::pair<void*, size_t>> bufs;
+  // named workspace buffers (names are string literals: views stay valid)
+  std::unordered_map<std::string_view, std::pair<void*, size_t>> bufs;
   unsigned* pinned = nullptr;  // small host scratch for counts
   Perm* perm_pinned = nullptr; // staging for permutations drawn on demand
   // last results
@@ -183,6 +186,8 @@ void allow_all_T() {
   allow_smem(k_fft_rows<T, double2>);
   allow_smem(k_fft_cols<T>);
   allow_smem(k_fold<float2, T, 1, 2>);
+  allow_smem(k_fold<float2, T, 1, 2, 4>);
+  allow_smem(k_fold<double2, T, 1, 2, 4>);
   allow_smem(k_fold<float2, T, 8, 1>);
   allow_smem(k_fold<double2, T, 1, 2>);
   allow_smem(k_fold<double2, T, 8, 1>);
@@ -278,9 +283,14 @@ struct PermSource {
       }
       hp.push_back(q);
       pinned[k] = q;
-      ck(cudaMemcpyAsync(dev + k, pinned + k, sizeof(Perm), cudaMemcpyHostToDevice, st), "H2D perm");
     }
     return hp[i];
+  }
+  // device copies are only needed by the estimation loops: one copy for them
+  void upload(int from, int count, cudaStream_t st) {
+    ck(cudaMemcpyAsync(dev + from, pinned + from, (size_t)count * sizeof(Perm),
+                       cudaMemcpyHostToDevice, st),
+       "H2D perms");
   }
   int used() const { return (int)hp.size(); }
 };
@@ -519,7 +529,9 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
   C* dst = (gm.Z == 1) ? (C*)y_direct : (C*)ws(c, "fold_part", (size_t)gm.Z * g * BB * sizeof(C));
   const double fold_bytes = sup * sup * sizeof(Tin) + (double)gm.Z * g * BB * sizeof(C);
   pre(c, st);
-  if (g == 1)
+  if (g == 1 && (N / std::max(B, gm.TW)) >= 4)
+    k_fold<Tin, T, 1, 2, 4><<<grid, threads, dyn, st>>>(x, wr, wc, pp, g, gm, dst, zero_peak);
+  else if (g == 1)
     k_fold<Tin, T, 1, 2><<<grid, threads, dyn, st>>>(x, wr, wc, pp, g, gm, dst, zero_peak);
   else
     k_fold<Tin, T, kMaxFoldLoops, 1><<<grid, threads, dyn, st>>>(x, wr, wc, pp, g, gm, dst, zero_peak);
@@ -900,15 +912,15 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   bool vote_pending[2] = {false, false};
   int npass = 0;
   int last_slot = 0;
-  auto vote_list = [&](int pi, int lgb, long long budget_dev, int slot) {
+  auto vote_list = [&](const Perm& pv, int lgb, long long budget_dev, int slot) {
     const int w = n >> lgb;
     const long long len = (w == 1) ? 3 : std::min<long long>(w + 2, n);
     ck(cudaEventRecord(c->ev_lmax, st), "cudaEventRecord");
     ck(cudaStreamWaitEvent(c->vote_st, c->ev_lmax, 0), "cudaStreamWaitEvent");
     pre(c, c->vote_st);
     k_vote<<<dim3(kNumSMs * 2, 1), 256, 0, c->vote_st>>>(maxlists[slot & 1], 0, cnt_slots + slot, 0,
-                                                        dp + pi, lgN, lgb, 1, mode, 0, hist,
-                                                        budget_dev);
+                                                        nullptr, lgN, lgb, 1, mode, 0, hist,
+                                                        budget_dev, pv);
     post(c, "k_vote", c->vote_st, (double)len * len * 4.0);
     ck(cudaEventRecord(c->ev_vote[slot & 1], c->vote_st), "cudaEventRecord");
     vote_pending[slot & 1] = true;
@@ -946,7 +958,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, &p, 1, (C*)nullptr, mg, pk, st);
       seq = lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, ml, cnt, st, false, 1, 1);
     }
-    vote_list(pi, lgb, budget, slot);
+    vote_list(p, lgb, budget, slot);
     const long long count = wait_published(c, seq, st);
     last_valid = true;
     last_b = bb;
@@ -1046,7 +1058,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   if (!have_votes && last_valid && maxc > 0) {
     // every pass exceeded the vote budget: fall back to the final pass (tuner.py:228-234)
     if (last_count > 0) {
-      vote_list(last_pi, ilog2(last_b), 0, last_slot);   // its list and count slot are intact
+      vote_list(ps.hp[last_pi], ilog2(last_b), 0, last_slot);   // its list and count slot are intact
       have_votes = true;
     }
     vote_passes = 1;
@@ -1100,6 +1112,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
                                 std::to_string(best) + " bin budget");
   }
   for (int i = 0; i < L; ++i) ps.get(pidx + i, st);
+  ps.upload(pidx, L, st);
   const bool dense = (best == n);
   if (dense) ensure_xhat(false);
   estimate_and_select<T, Tin>(c, x, lgN, ilog2(best), tb, ps.hp.data() + pidx, dp + pidx, L, keys, m,
@@ -1583,8 +1596,8 @@ int sfft2d_fetch_result(sfft2d_ctx* c, int64_t* ij, void* values, int dst_on_hos
     const size_t n = (size_t)c->res_count;
     if (n == 0) return;
     const size_t vb = n * (c->res_prec == SFFT2D_FP64 ? 16 : 8);
-    if (ij) ck(cudaMemcpyAsync(ij, c->bufs["out_ij"].first, n * 16, cudaMemcpyDefault, st), "copy ij");
-    if (values) ck(cudaMemcpyAsync(values, c->bufs["out_v"].first, vb, cudaMemcpyDefault, st), "copy v");
+    if (ij) ck(cudaMemcpyAsync(ij, ws(c, "out_ij", n * 16), n * 16, cudaMemcpyDefault, st), "copy ij");
+    if (values) ck(cudaMemcpyAsync(values, ws(c, "out_v", vb), vb, cudaMemcpyDefault, st), "copy v");
     if (dst_on_host) ck(cudaStreamSynchronize(st), "sync");
   });
 }
@@ -1596,9 +1609,9 @@ int sfft2d_fetch_votes(sfft2d_ctx* c, int32_t* keys, int32_t* tallies, int dst_o
     cudaStream_t st = (cudaStream_t)stream;
     const size_t n = (size_t)c->votes_count;
     if (n == 0) return;
-    if (keys) ck(cudaMemcpyAsync(keys, c->bufs["keys"].first, n * 4, cudaMemcpyDefault, st), "copy keys");
+    if (keys) ck(cudaMemcpyAsync(keys, ws(c, "keys", n * 4), n * 4, cudaMemcpyDefault, st), "copy keys");
     if (tallies)
-      ck(cudaMemcpyAsync(tallies, c->bufs["tallies"].first, n * 4, cudaMemcpyDefault, st), "copy tallies");
+      ck(cudaMemcpyAsync(tallies, ws(c, "tallies", n * 4), n * 4, cudaMemcpyDefault, st), "copy tallies");
     if (dst_on_host) ck(cudaStreamSynchronize(st), "sync");
   });
 }

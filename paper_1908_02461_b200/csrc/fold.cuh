@@ -93,7 +93,7 @@ __global__ void k_fold_weights(const T* __restrict__ space, PermPack pp, int nlo
   }
 }
 
-template <typename Tin, typename T, int NL, int CPT>
+template <typename Tin, typename T, int NL, int CPT, int MU = 1>
 __global__ void __launch_bounds__(kFoldThreads)
 k_fold(const Tin* __restrict__ x, const T* __restrict__ wrow, const T* __restrict__ wcol,
        PermPack pp, int nloops, FoldGeom gm, cplx<T>* __restrict__ dst,
@@ -156,49 +156,62 @@ k_fold(const Tin* __restrict__ x, const T* __restrict__ wrow, const T* __restric
     for (int q = 0; q < CPT; ++q) acc[l][q] = mk<T>(0, 0);
 
   if (nnz > 0) {
-    for (int m = 0; m < ncb; ++m) {
-      const int c = cbase + m * step + cp;
-      T wc[NL][CPT];
+    // MU column blocks per step: MU independent loads per row, rows unrolled
+    // by 2, so a thread keeps 2*MU 16-byte loads in flight
+    for (int m0 = 0; m0 < ncb; m0 += MU) {
+      T wc[MU][NL][CPT];
       bool any = false;
 #pragma unroll
-      for (int l = 0; l < NL; ++l)
+      for (int mu = 0; mu < MU; ++mu) {
+        const int c = cbase + (m0 + mu) * step + cp;
 #pragma unroll
-        for (int q = 0; q < CPT; ++q) {
-          T w = (T)0;
-          if (l < nloops) w = __ldg(wcol + ((size_t)l << gm.lgN) + c + q);
-          wc[l][q] = w;
-          any |= (w != (T)0);
-        }
+        for (int l = 0; l < NL; ++l)
+#pragma unroll
+          for (int q = 0; q < CPT; ++q) {
+            T w = (T)0;
+            if (l < nloops && m0 + mu < ncb) w = __ldg(wcol + ((size_t)l << gm.lgN) + c + q);
+            wc[mu][l][q] = w;
+            any |= (w != (T)0);
+          }
+      }
       if (!any) continue;
-      C u[NL][CPT];
+      C u[MU][NL][CPT];
 #pragma unroll
-      for (int l = 0; l < NL; ++l)
+      for (int mu = 0; mu < MU; ++mu)
 #pragma unroll
-        for (int q = 0; q < CPT; ++q) u[l][q] = mk<T>(0, 0);
-      const Tin* col = x + c;
-#pragma unroll 4
+        for (int l = 0; l < NL; ++l)
+#pragma unroll
+          for (int q = 0; q < CPT; ++q) u[mu][l][q] = mk<T>(0, 0);
+      const Tin* col = x + cbase + m0 * step + cp;
+#pragma unroll 2
       for (int i = 0; i < nnz; ++i) {
         const int jj = s_rows[i];
         const size_t r = (size_t)(rho + (j0 + jj) * B);
-        C v[CPT];
-        ColLoad<Tin, T, CPT>::ld(col + (r << gm.lgN), v);
+        C v[MU][CPT];
+#pragma unroll
+        for (int mu = 0; mu < MU; ++mu)
+          if (m0 + mu < ncb) ColLoad<Tin, T, CPT>::ld(col + mu * step + (r << gm.lgN), v[mu]);
 #pragma unroll
         for (int l = 0; l < NL; ++l) {
           const T wr = s_w[l * kFoldMaxRows + jj];
 #pragma unroll
-          for (int q = 0; q < CPT; ++q) {
-            u[l][q].x = fma(wr, v[q].x, u[l][q].x);
-            u[l][q].y = fma(wr, v[q].y, u[l][q].y);
-          }
+          for (int mu = 0; mu < MU; ++mu)
+#pragma unroll
+            for (int q = 0; q < CPT; ++q) {
+              u[mu][l][q].x = fma(wr, v[mu][q].x, u[mu][l][q].x);
+              u[mu][l][q].y = fma(wr, v[mu][q].y, u[mu][l][q].y);
+            }
         }
       }
 #pragma unroll
-      for (int l = 0; l < NL; ++l)
+      for (int mu = 0; mu < MU; ++mu)
 #pragma unroll
-        for (int q = 0; q < CPT; ++q) {
-          acc[l][q].x = fma(wc[l][q], u[l][q].x, acc[l][q].x);
-          acc[l][q].y = fma(wc[l][q], u[l][q].y, acc[l][q].y);
-        }
+        for (int l = 0; l < NL; ++l)
+#pragma unroll
+          for (int q = 0; q < CPT; ++q) {
+            acc[l][q].x = fma(wc[mu][l][q], u[mu][l][q].x, acc[l][q].x);
+            acc[l][q].y = fma(wc[mu][l][q], u[mu][l][q].y, acc[l][q].y);
+          }
     }
   }
 
@@ -287,37 +300,52 @@ k_fold_wide(const Tin* __restrict__ x, const T* __restrict__ wrow, const T* __re
   C acc[RH][2];
 #pragma unroll
   for (int r = 0; r < RH; ++r) acc[r][0] = acc[r][1] = mk<T>(0, 0);
-  for (int i = 0; i < A; ++i) {
-    const int c = kap + (i << lgB);
-    const T wc0 = __ldg(wcol + c);
-    const T wc1 = __ldg(wcol + c + 1);
-    C u[RH][2];
+  // two column aliases per step: 2*RH independent row loads per row alias,
+  // row aliases unrolled by 4
+  for (int i0 = 0; i0 < A; i0 += 2) {
+    const int ni = (i0 + 1 < A) ? 2 : 1;
+    T wc[2][2];
+    C u[2][RH][2];
 #pragma unroll
-    for (int r = 0; r < RH; ++r) u[r][0] = u[r][1] = mk<T>(0, 0);
-    const Tin* col = x + c;
+    for (int ii = 0; ii < 2; ++ii) {
+      const int c = kap + ((i0 + ii) << lgB);
+      wc[ii][0] = ii < ni ? __ldg(wcol + c) : (T)0;
+      wc[ii][1] = ii < ni ? __ldg(wcol + c + 1) : (T)0;
+#pragma unroll
+      for (int r = 0; r < RH; ++r) u[ii][r][0] = u[ii][r][1] = mk<T>(0, 0);
+    }
 #pragma unroll 4
     for (int j = 0; j < A; ++j) {
-      C v[RH][2];
+      C v[2][RH][2];
 #pragma unroll
-      for (int r = 0; r < RH; ++r)
-        ColLoad<Tin, T, 2>::ld(col + ((size_t)(rho0 + r + (j << lgB)) << lgN), v[r]);
+      for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+        for (int r = 0; r < RH; ++r)
+          if (ii < ni)
+            ColLoad<Tin, T, 2>::ld(x + kap + ((i0 + ii) << lgB) + ((size_t)(rho0 + r + (j << lgB)) << lgN),
+                                   v[ii][r]);
+#pragma unroll
+      for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+        for (int r = 0; r < RH; ++r) {
+          if (ii >= ni) continue;
+          const T w = s_w[r * 32 + j];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            u[ii][r][q].x = fma(w, v[ii][r][q].x, u[ii][r][q].x);
+            u[ii][r][q].y = fma(w, v[ii][r][q].y, u[ii][r][q].y);
+          }
+        }
+    }
+#pragma unroll
+    for (int ii = 0; ii < 2; ++ii)
 #pragma unroll
       for (int r = 0; r < RH; ++r) {
-        const T w = s_w[r * 32 + j];
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          u[r][q].x = fma(w, v[r][q].x, u[r][q].x);
-          u[r][q].y = fma(w, v[r][q].y, u[r][q].y);
-        }
+        acc[r][0].x = fma(wc[ii][0], u[ii][r][0].x, acc[r][0].x);
+        acc[r][0].y = fma(wc[ii][0], u[ii][r][0].y, acc[r][0].y);
+        acc[r][1].x = fma(wc[ii][1], u[ii][r][1].x, acc[r][1].x);
+        acc[r][1].y = fma(wc[ii][1], u[ii][r][1].y, acc[r][1].y);
       }
-    }
-#pragma unroll
-    for (int r = 0; r < RH; ++r) {
-      acc[r][0].x = fma(wc0, u[r][0].x, acc[r][0].x);
-      acc[r][0].y = fma(wc0, u[r][0].y, acc[r][0].y);
-      acc[r][1].x = fma(wc1, u[r][1].x, acc[r][1].x);
-      acc[r][1].y = fma(wc1, u[r][1].y, acc[r][1].y);
-    }
   }
   const unsigned b0 = (p.s2i * ((unsigned)kap - p.t2)) & maskB;
   const unsigned b1 = (p.s2i * ((unsigned)kap + 1u - p.t2)) & maskB;

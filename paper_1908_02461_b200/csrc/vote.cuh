@@ -27,7 +27,8 @@ enum VoteMode { kVoteOrBit = 0, kVoteAdd8 = 1, kVoteAdd32 = 2 };
 // queued before the host learns the count).
 __global__ void k_vote(const int32_t* __restrict__ bins, long seg_stride, const unsigned* counts,
                        long count, const Perm* __restrict__ perms, int lgN, int lgB, int expand,
-                       int mode, int bit0, uint32_t* __restrict__ hist, long long budget = 0) {
+                       int mode, int bit0, uint32_t* __restrict__ hist, long long budget = 0,
+                       Perm pval = Perm{0, 0, 0, 0, 0, 0}) {
   const int seg = blockIdx.y;
   const long nb = counts ? (long)counts[seg] : count;
   const int N = 1 << lgN;
@@ -44,7 +45,7 @@ __global__ void k_vote(const int32_t* __restrict__ bins, long seg_stride, const 
   const long per = (long)len * len;
   const long total = nb * per;
   if (budget > 0 && total > budget) return;
-  const Perm p = perms[seg];
+  const Perm p = perms ? perms[seg] : pval;   // by value for single-segment tuner votes
   const int32_t* sb = bins + seg * seg_stride;
   const unsigned bitv = 1u << ((bit0 + seg) & 7);
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
