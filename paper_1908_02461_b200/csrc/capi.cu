@@ -194,6 +194,9 @@ void allow_all_T() {
   allow_smem(k_fold_reduce_fft_small<T>);
   allow_smem(k_permute_grid<T>);
   allow_smem(k_fftr<T, C, true, false>);
+  allow_smem(k_fftr<T, C, true, false, 2>);
+  allow_smem(k_fftr<T, float2, true, false, 2>);
+  allow_smem(k_fftr<T, double2, true, false, 2>);
   allow_smem(k_fftr<T, float2, true, false>);
   allow_smem(k_fftr<T, double2, true, false>);
   allow_smem(k_fftc<T, true, false>);
@@ -405,9 +408,14 @@ void fft2d_grids(sfft2d_ctx* c, cplx<T>* grids, int lgB, int ngrids, const cplx<
   if (pl.smem_row > kMaxDynSmem || pl.row_threads > 512)
     fail(SFFT2D_ERR_UNSUPPORTED, "grid too large for the smem FFT");
   pre(c, st);
-  k_fftr<T, C, true, false><<<(unsigned)(ngrids * (B / pl.rows_per_cta)), pl.row_threads,
-                              pl.smem_row, st>>>(grids, grids, nullptr, nullptr, lgB, 2 * lgB, tw,
-                                                 lgN);
+  if (pl.row_ipt == 2)
+    k_fftr<T, C, true, false, 2><<<(unsigned)(ngrids * (B / pl.rows_per_cta)), pl.row_threads,
+                                   pl.smem_row, st>>>(grids, grids, nullptr, nullptr, lgB, 2 * lgB,
+                                                      tw, lgN);
+  else
+    k_fftr<T, C, true, false><<<(unsigned)(ngrids * (B / pl.rows_per_cta)), pl.row_threads,
+                                pl.smem_row, st>>>(grids, grids, nullptr, nullptr, lgB, 2 * lgB, tw,
+                                                   lgN);
   post(c, "k_fftr", st, 2 * gb);
   const double wbytes = (wc ? gb : 0) + (wm ? (double)BB * ngrids * sizeof(T) : 0);
   C* final_out = out;
@@ -451,8 +459,13 @@ void dense_fft(sfft2d_ctx* c, const Tin* x, cplx<T>* out, T* mags, unsigned long
   const double nn = (double)N * N;
   C* scratch = (C*)ws(c, "fft_scratch", (size_t)N * N * sizeof(C));
   pre(c, st);
-  k_fftr<T, Tin, true, false><<<(unsigned)(N / pl.rows_per_cta), pl.row_threads, pl.smem_row,
-                                st>>>(x, scratch, nullptr, nullptr, lgN, 2 * lgN, tw, lgN, nonfinite);
+  if (pl.row_ipt == 2)
+    k_fftr<T, Tin, true, false, 2><<<(unsigned)(N / pl.rows_per_cta), pl.row_threads, pl.smem_row,
+                                     st>>>(x, scratch, nullptr, nullptr, lgN, 2 * lgN, tw, lgN,
+                                           nonfinite);
+  else
+    k_fftr<T, Tin, true, false><<<(unsigned)(N / pl.rows_per_cta), pl.row_threads, pl.smem_row,
+                                  st>>>(x, scratch, nullptr, nullptr, lgN, 2 * lgN, tw, lgN, nonfinite);
   post(c, "k_fftr_dense", st, nn * (sizeof(Tin) + sizeof(C)));
   const double wb = nn * sizeof(C) + (mags ? nn * sizeof(T) : 0);
   if (pl.four_step) {

@@ -91,15 +91,15 @@ __device__ __forceinline__ void dft_reg(cplx<T>* v) {
 
 // One Stockham pass of radix 2^LGR over `rows` rows (stride rs) of length 2^lgL.
 // blockDim.x * 16 == rows * L must hold.
-template <typename T, int LGR>
+template <typename T, int LGR, int IPT = 1>
 __device__ __forceinline__ void stockham_pass(cplx<T>* s, int lgL, int rs, int lgNs,
                                               const cplx<T>* __restrict__ tw, int lgN) {
   using C = cplx<T>;
   constexpr int R = 1 << LGR;
-  constexpr int K = 16 / R;
+  constexpr int K = IPT * 16 / R;
   const int per_lg = lgL - LGR;
   const int per = 1 << per_lg;
-  C v[16];
+  C v[16 * IPT];
 #pragma unroll
   for (int q = 0; q < K; ++q) {
     const int it = threadIdx.x + q * blockDim.x;
@@ -159,16 +159,16 @@ __device__ __forceinline__ void flush_peak(unsigned long long best, unsigned lon
 // to global memory through `st(seq, k, value)`; COLMAP: consecutive threads
 // take consecutive sequences (columns) so global stores coalesce across
 // columns, else consecutive j (contiguous rows).
-template <typename T, int LGR, bool COLMAP, typename St>
+template <typename T, int LGR, bool COLMAP, int IPT, typename St>
 __device__ __forceinline__ void stockham_last(const cplx<T>* s, int lgL, int rs, int nseq_lg,
                                               const cplx<T>* __restrict__ tw, int lgN, St st) {
   using C = cplx<T>;
   constexpr int R = 1 << LGR;
-  constexpr int K = 16 / R;
+  constexpr int K = IPT * 16 / R;
   const int per_lg = lgL - LGR;
   const int per = 1 << per_lg;  // == Ns
   const int tsh = lgN - lgL;
-  C v[16];
+  C v[16 * IPT];
 #pragma unroll
   for (int q = 0; q < K; ++q) {
     const int it = threadIdx.x + q * blockDim.x;
@@ -189,49 +189,52 @@ __device__ __forceinline__ void stockham_last(const cplx<T>* s, int lgL, int rs,
 // nseq * L): pass 1 (radix 16) gathers its inputs straight from global memory
 // through `ld(seq, u)`, middle passes run in smem, the last pass stores
 // through `st`.  One smem round trip for L <= 256, two for L <= 4096.
-template <typename T, bool COLMAP, typename Ld, typename St>
+template <typename T, bool COLMAP, int IPT = 1, typename Ld, typename St>
 __device__ __forceinline__ void fft_tile(cplx<T>* s, int lgL, int nseq_lg, int rs,
                                          const cplx<T>* __restrict__ tw, int lgN, Ld ld, St st) {
   using C = cplx<T>;
   const int L = 1 << lgL;
   const int per_lg = lgL - 4;
   const int per = L >> 4;
-  int seq, j;
-  if (COLMAP) { seq = threadIdx.x & ((1 << nseq_lg) - 1); j = threadIdx.x >> nseq_lg; }
-  else { seq = threadIdx.x >> per_lg; j = threadIdx.x & (per - 1); }
-  C v[16];
 #pragma unroll
-  for (int r = 0; r < 16; ++r) v[r] = ld(seq, j + r * per);
-  dft_reg<T, 16>(v);
-  if (lgL == 4) {
+  for (int q = 0; q < IPT; ++q) {
+    const int it = threadIdx.x + q * blockDim.x;
+    int seq, j;
+    if (COLMAP) { seq = it & ((1 << nseq_lg) - 1); j = it >> nseq_lg; }
+    else { seq = it >> per_lg; j = it & (per - 1); }
+    C v[16];
 #pragma unroll
-    for (int r = 0; r < 16; ++r) st(seq, r, v[r]);
-    return;
+    for (int r = 0; r < 16; ++r) v[r] = ld(seq, j + r * per);
+    dft_reg<T, 16>(v);
+    if (lgL == 4) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) st(seq, r, v[r]);
+    } else {
+      C* sr = s + seq * rs;
+#pragma unroll
+      for (int r = 0; r < 16; ++r) sr[padi(j * 16 + r)] = v[r];
+    }
   }
-  {
-    C* sr = s + seq * rs;
-#pragma unroll
-    for (int r = 0; r < 16; ++r) sr[padi(j * 16 + r)] = v[r];
-  }
+  if (lgL == 4) return;
   __syncthreads();
   int lgNs = 4;
   // middle passes: leave exactly the last pass's bits (4, or the remainder)
   while (lgL - lgNs > 4) {
     const int rem = lgL - lgNs - 4;           // bits to spend before the final radix-16
-    if (rem >= 4) { stockham_pass<T, 4>(s, lgL, rs, lgNs, tw, lgN); lgNs += 4; }
-    else if (rem == 3) { stockham_pass<T, 3>(s, lgL, rs, lgNs, tw, lgN); lgNs += 3; }
-    else if (rem == 2) { stockham_pass<T, 2>(s, lgL, rs, lgNs, tw, lgN); lgNs += 2; }
-    else { stockham_pass<T, 1>(s, lgL, rs, lgNs, tw, lgN); lgNs += 1; }
+    if (rem >= 4) { stockham_pass<T, 4, IPT>(s, lgL, rs, lgNs, tw, lgN); lgNs += 4; }
+    else if (rem == 3) { stockham_pass<T, 3, IPT>(s, lgL, rs, lgNs, tw, lgN); lgNs += 3; }
+    else if (rem == 2) { stockham_pass<T, 2, IPT>(s, lgL, rs, lgNs, tw, lgN); lgNs += 2; }
+    else { stockham_pass<T, 1, IPT>(s, lgL, rs, lgNs, tw, lgN); lgNs += 1; }
   }
   const int last = lgL - lgNs;
-  if (last == 4) stockham_last<T, 4, COLMAP>(s, lgL, rs, nseq_lg, tw, lgN, st);
-  else if (last == 3) stockham_last<T, 3, COLMAP>(s, lgL, rs, nseq_lg, tw, lgN, st);
-  else if (last == 2) stockham_last<T, 2, COLMAP>(s, lgL, rs, nseq_lg, tw, lgN, st);
-  else stockham_last<T, 1, COLMAP>(s, lgL, rs, nseq_lg, tw, lgN, st);
+  if (last == 4) stockham_last<T, 4, COLMAP, IPT>(s, lgL, rs, nseq_lg, tw, lgN, st);
+  else if (last == 3) stockham_last<T, 3, COLMAP, IPT>(s, lgL, rs, nseq_lg, tw, lgN, st);
+  else if (last == 2) stockham_last<T, 2, COLMAP, IPT>(s, lgL, rs, nseq_lg, tw, lgN, st);
+  else stockham_last<T, 1, COLMAP, IPT>(s, lgL, rs, nseq_lg, tw, lgN, st);
 }
 
 // Row pass: CTA = `rows` rows of length L (blockDim = rows * L / 16).
-template <typename T, typename Tin, bool WC, bool WM>
+template <typename T, typename Tin, bool WC, bool WM, int IPT = 1>
 __global__ void __launch_bounds__(512, (sizeof(T) == 4) ? 2 : 1)
 k_fftr(const Tin* src, cplx<T>* dst, T* __restrict__ mags, unsigned long long* __restrict__ peak,
        int lgL, int grid_lg, const cplx<T>* __restrict__ tw, int lgN,
@@ -239,7 +242,7 @@ k_fftr(const Tin* src, cplx<T>* dst, T* __restrict__ mags, unsigned long long* _
   using C = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* s = reinterpret_cast<C*>(smem_raw);
-  const int rows_lg = __ffs((blockDim.x * 16) >> lgL) - 1;
+  const int rows_lg = __ffs((blockDim.x * 16 * IPT) >> lgL) - 1;
   const size_t e0 = ((size_t)blockIdx.x << rows_lg) << lgL;
   unsigned long long best = 0;
   bool bad = false;
@@ -257,7 +260,7 @@ k_fftr(const Tin* src, cplx<T>* dst, T* __restrict__ mags, unsigned long long* _
       emit_mag(m, best);
     }
   };
-  fft_tile<T, false>(s, lgL, rows_lg, pad_row(1 << lgL), tw, lgN, ld, st);
+  fft_tile<T, false, IPT>(s, lgL, rows_lg, pad_row(1 << lgL), tw, lgN, ld, st);
   if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
   if (WM && peak) flush_peak(best, peak + (e0 >> grid_lg));
 }
@@ -339,7 +342,7 @@ k_fftcB(const cplx<T>* __restrict__ src, cplx<T>* __restrict__ dst, T* __restric
 // ---------------------------------------------------------------- geometry
 struct FftPlan2D {
   int lgL;
-  int rows_per_cta, row_threads;       // row pass
+  int rows_per_cta, row_threads, row_ipt;   // row pass
   bool four_step;
   int lgL1, lgL2;                      // four-step split
   int lgccA, thrA, lgccB, thrB;        // column tiles (A, B) or single pass (B)
@@ -356,7 +359,8 @@ inline FftPlan2D plan_fft2d(int lgL) {
   int rows = L >= 4096 ? 1 : 4096 / L;
   if (rows > L) rows = L;
   p.rows_per_cta = rows;
-  p.row_threads = rows * L / 16;
+  p.row_ipt = (rows * L / 16 > 512) ? 2 : 1;     // L = 16384: two radix-16 groups per thread
+  p.row_threads = rows * L / 16 / p.row_ipt;
   p.smem_row = (size_t)rows * pad_row(L) * cs;
   auto tile = [&](int lgLc, int& lgcc, int& thr, size_t& sm) {
     const int Lc = 1 << lgLc;

@@ -57,6 +57,8 @@ def fixture_input(g):
             kw["snr_db"] = float(g["gen_snr"])
         if "gen_mag" in g:
             kw["magnitude"] = str(g["gen_mag"])
+        if "gen_cluster" in g:
+            kw["cluster_frac"] = float(g["gen_cluster"])
         x = sparse_image(int(g["gen_n"]), int(g["gen_k"]), int(g["gen_seed"]), **kw).x
     assert image_digest(x) == str(g["digest"]), "regenerated input does not match the fixture"
     return x

@@ -314,3 +314,24 @@ def test_batch_concurrent_equals_sequential():
     s1 = [P.sfft2d(x, P.SfftConfig(n=512, k=12), 7) for x in xs]
     s2 = P.sfft2d_batch(xs, P.SfftConfig(n=512, k=12), [7] * 6, concurrency=3)
     assert s1 == s2
+
+
+@pytest.mark.parametrize("n,precision", [(8192, "fp32"), (8192, "fp64"), (16384, "fp32")])
+def test_large_fft_sides(n, precision):
+    # B = N bucket grid with the identity permutation is the dense 2D DFT
+    rng = np.random.default_rng(n)
+    x = (rng.standard_normal((n, n), dtype=np.float32)
+         + 1j * rng.standard_normal((n, n), dtype=np.float32)).astype(np.complex64)
+    win = P.all_pass_window(n)
+    got = P.binned_spectrum(x, P.identity_permutation(n), win, n, precision=precision).spectrum
+    ref = np.fft.fft2(x.astype(np.complex128))   # float64 pocketfft (numpy 2 keeps c64 in single)
+    err = np.abs(got - ref).max() / np.abs(ref).max()
+    assert err < (1e-5 if precision == "fp32" else 1e-12), err
+
+
+def test_c5_atsfft_vs_reference():
+    g = golden("c5_ats_k64")
+    x = fixture_input(g)
+    out, state = P.atsfft2d(x, _tuner(g), int(g["est_loops"]), int(g["seed"]), precision="fp32")
+    _check_state(state, g, "c5_ats_k64", "fp32")
+    _close_values(out, _ref_dict(g), TOL["fp32"])
