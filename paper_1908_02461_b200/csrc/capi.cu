@@ -527,7 +527,7 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
   if (g == 1 && B >= 512 && lgN - lgB <= 5 && y_direct) {
     // wide single-loop fold, permuted grid written directly
     const double by = sup * sup * sizeof(Tin) + (double)BB * sizeof(C);
-    const int rh = B >= 2048 ? 4 : (B >= 1024 ? 2 : 1);
+    const int rh = B >= 1024 ? 2 : 1;   // RH=4 needs 128 registers (2 CTAs/SM)
     const dim3 grid_w(B / 512, B / rh);
     pre(c, st);
     if (rh == 4)
