@@ -306,6 +306,25 @@ unsigned read_u32(sfft2d_ctx* c, const unsigned* dev, cudaStream_t st) {
   return c->pinned[0];
 }
 
+// Launch with programmatic stream serialisation (PDL): the kernel may be
+// scheduled while its predecessor in the stream drains; it waits in pdl_wait()
+// before touching memory.  Launch errors throw.
+template <typename... KArgs, typename... Args>
+void kl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+        Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  ck(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
+}
+
 // Prepare a count publication for a launch of `grid` CTAs.
 Publish make_publish(sfft2d_ctx* c, unsigned grid) {
   Publish p;
@@ -346,6 +365,7 @@ unsigned grid_for(long long work, int per_block = 256, int cap = kNumSMs * 16) {
 // ------------------------------------------------------------------ pieces
 template <typename Tin>
 __global__ void k_check_finite(const Tin* __restrict__ x, long n, unsigned* flag) {
+  pdl_wait();
   bool bad = false;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
        i += (long)gridDim.x * blockDim.x) {
@@ -356,6 +376,7 @@ __global__ void k_check_finite(const Tin* __restrict__ x, long n, unsigned* flag
 }
 
 __global__ void k_sel_init(SelState* st, int nseg, long long num, long long seglen) {
+  pdl_wait();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s < nseg) {
     st[s].prefix = 0;
@@ -366,6 +387,7 @@ __global__ void k_sel_init(SelState* st, int nseg, long long num, long long segl
 }
 
 __global__ void k_iota_segments(int32_t* out, long seglen, int nseg) {
+  pdl_wait();
   const long total = seglen * nseg;
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
        e += (long)gridDim.x * blockDim.x)
@@ -378,8 +400,7 @@ template <typename T>
 void mags_of(sfft2d_ctx* c, const cplx<T>* spec, long seglen, int nseg, T* mags,
              unsigned long long* peaks, cudaStream_t st) {
   pre(c, st);
-  k_mags<T><<<dim3(grid_for(seglen, 256, kNumSMs * 8 / std::max(1, nseg) + 1), nseg), 256, 0, st>>>(
-      spec, seglen, mags, peaks);
+  kl(k_mags<T>, dim3(grid_for(seglen, 256, kNumSMs * 8 / std::max(1, nseg) + 1), nseg), 256, 0, st, spec, seglen, mags, peaks);
   post(c, "k_mags", st, (double)seglen * nseg * (sizeof(cplx<T>) + sizeof(T)));
 }
 
@@ -397,7 +418,7 @@ void fft2d_grids(sfft2d_ctx* c, cplx<T>* grids, int lgB, int ngrids, const cplx<
   if (BB * sizeof(C) <= (size_t)kSmall2DBytes) {
     const int threads = B * B / 4 >= 256 ? 256 : (B * B / 4 >= 32 ? B * B / 4 : 32);
     pre(c, st);
-    k_fft2d_small<T><<<ngrids, threads, BB * sizeof(C), st>>>(grids, lgB, tw, lgN);
+    kl(k_fft2d_small<T>, ngrids, threads, BB * sizeof(C), st, grids, lgB, tw, lgN);
     post(c, "k_fft2d_small", st, 2 * gb);
     if (wc && out != grids)
       ck(cudaMemcpyAsync(out, grids, BB * ngrids * sizeof(C), cudaMemcpyDeviceToDevice, st), "copy");
@@ -409,13 +430,11 @@ void fft2d_grids(sfft2d_ctx* c, cplx<T>* grids, int lgB, int ngrids, const cplx<
     fail(SFFT2D_ERR_UNSUPPORTED, "grid too large for the smem FFT");
   pre(c, st);
   if (pl.row_ipt == 2)
-    k_fftr<T, C, true, false, 2><<<(unsigned)(ngrids * (B / pl.rows_per_cta)), pl.row_threads,
-                                   pl.smem_row, st>>>(grids, grids, nullptr, nullptr, lgB, 2 * lgB,
-                                                      tw, lgN);
+    kl(k_fftr<T, C, true, false, 2>, (unsigned)(ngrids * (B / pl.rows_per_cta)), pl.row_threads, pl.smem_row, st, grids, grids, nullptr, nullptr, lgB, 2 * lgB,
+                                                      tw, lgN, (unsigned*)nullptr);
   else
-    k_fftr<T, C, true, false><<<(unsigned)(ngrids * (B / pl.rows_per_cta)), pl.row_threads,
-                                pl.smem_row, st>>>(grids, grids, nullptr, nullptr, lgB, 2 * lgB, tw,
-                                                   lgN);
+    kl(k_fftr<T, C, true, false>, (unsigned)(ngrids * (B / pl.rows_per_cta)), pl.row_threads, pl.smem_row, st, grids, grids, nullptr, nullptr, lgB, 2 * lgB, tw,
+                                                   lgN, (unsigned*)nullptr);
   post(c, "k_fftr", st, 2 * gb);
   const double wbytes = (wc ? gb : 0) + (wm ? (double)BB * ngrids * sizeof(T) : 0);
   C* final_out = out;
@@ -425,17 +444,14 @@ void fft2d_grids(sfft2d_ctx* c, cplx<T>* grids, int lgB, int ngrids, const cplx<
     constexpr bool WC = decltype(WC_)::value, WM = decltype(WM_)::value;
     if (pl.four_step) {
       pre(c, st);
-      k_fftcA<T><<<dim3(B >> pl.lgccA, 1 << pl.lgL2, ngrids), pl.thrA, pl.smem_A, st>>>(
-          grids, pl.lgL1, pl.lgL2, pl.lgccA, tw, lgN);
+      kl(k_fftcA<T>, dim3(B >> pl.lgccA, 1 << pl.lgL2, ngrids), pl.thrA, pl.smem_A, st, grids, pl.lgL1, pl.lgL2, pl.lgccA, tw, lgN);
       post(c, "k_fftcA", st, 2 * gb);
       pre(c, st);
-      k_fftcB<T, WC, WM><<<dim3(B >> pl.lgccB, 1 << pl.lgL1, ngrids), pl.thrB, pl.smem_B, st>>>(
-          grids, out, mags, peaks, pl.lgL1, pl.lgL2, pl.lgccB, tw, lgN);
+      kl(k_fftcB<T, WC, WM>, dim3(B >> pl.lgccB, 1 << pl.lgL1, ngrids), pl.thrB, pl.smem_B, st, grids, out, mags, peaks, pl.lgL1, pl.lgL2, pl.lgccB, tw, lgN);
       post(c, "k_fftcB", st, gb + wbytes);
     } else {
       pre(c, st);
-      k_fftc<T, WC, WM><<<dim3(B >> pl.lgccB, ngrids), pl.thrB, pl.smem_B, st>>>(
-          grids, out, mags, peaks, lgB, pl.lgccB, tw, lgN);
+      kl(k_fftc<T, WC, WM>, dim3(B >> pl.lgccB, ngrids), pl.thrB, pl.smem_B, st, grids, out, mags, peaks, lgB, pl.lgccB, tw, lgN);
       post(c, "k_fftc", st, gb + wbytes);
     }
   };
@@ -460,35 +476,28 @@ void dense_fft(sfft2d_ctx* c, const Tin* x, cplx<T>* out, T* mags, unsigned long
   C* scratch = (C*)ws(c, "fft_scratch", (size_t)N * N * sizeof(C));
   pre(c, st);
   if (pl.row_ipt == 2)
-    k_fftr<T, Tin, true, false, 2><<<(unsigned)(N / pl.rows_per_cta), pl.row_threads, pl.smem_row,
-                                     st>>>(x, scratch, nullptr, nullptr, lgN, 2 * lgN, tw, lgN,
+    kl(k_fftr<T, Tin, true, false, 2>, (unsigned)(N / pl.rows_per_cta), pl.row_threads, pl.smem_row, st, x, scratch, nullptr, nullptr, lgN, 2 * lgN, tw, lgN,
                                            nonfinite);
   else
-    k_fftr<T, Tin, true, false><<<(unsigned)(N / pl.rows_per_cta), pl.row_threads, pl.smem_row,
-                                  st>>>(x, scratch, nullptr, nullptr, lgN, 2 * lgN, tw, lgN, nonfinite);
+    kl(k_fftr<T, Tin, true, false>, (unsigned)(N / pl.rows_per_cta), pl.row_threads, pl.smem_row, st, x, scratch, nullptr, nullptr, lgN, 2 * lgN, tw, lgN, nonfinite);
   post(c, "k_fftr_dense", st, nn * (sizeof(Tin) + sizeof(C)));
   const double wb = nn * sizeof(C) + (mags ? nn * sizeof(T) : 0);
   if (pl.four_step) {
     pre(c, st);
-    k_fftcA<T><<<dim3(N >> pl.lgccA, 1 << pl.lgL2, 1), pl.thrA, pl.smem_A, st>>>(
-        scratch, pl.lgL1, pl.lgL2, pl.lgccA, tw, lgN);
+    kl(k_fftcA<T>, dim3(N >> pl.lgccA, 1 << pl.lgL2, 1), pl.thrA, pl.smem_A, st, scratch, pl.lgL1, pl.lgL2, pl.lgccA, tw, lgN);
     post(c, "k_fftcA", st, 2 * nn * sizeof(C));
     pre(c, st);
     if (mags)
-      k_fftcB<T, true, true><<<dim3(N >> pl.lgccB, 1 << pl.lgL1, 1), pl.thrB, pl.smem_B, st>>>(
-          scratch, out, mags, peak, pl.lgL1, pl.lgL2, pl.lgccB, tw, lgN);
+      kl(k_fftcB<T, true, true>, dim3(N >> pl.lgccB, 1 << pl.lgL1, 1), pl.thrB, pl.smem_B, st, scratch, out, mags, peak, pl.lgL1, pl.lgL2, pl.lgccB, tw, lgN);
     else
-      k_fftcB<T, true, false><<<dim3(N >> pl.lgccB, 1 << pl.lgL1, 1), pl.thrB, pl.smem_B, st>>>(
-          scratch, out, nullptr, nullptr, pl.lgL1, pl.lgL2, pl.lgccB, tw, lgN);
+      kl(k_fftcB<T, true, false>, dim3(N >> pl.lgccB, 1 << pl.lgL1, 1), pl.thrB, pl.smem_B, st, scratch, out, nullptr, nullptr, pl.lgL1, pl.lgL2, pl.lgccB, tw, lgN);
     post(c, "k_fftcB", st, nn * sizeof(C) + wb);
   } else {
     pre(c, st);
     if (mags)
-      k_fftc<T, true, true><<<dim3(N >> pl.lgccB, 1), pl.thrB, pl.smem_B, st>>>(
-          scratch, out, mags, peak, lgN, pl.lgccB, tw, lgN);
+      kl(k_fftc<T, true, true>, dim3(N >> pl.lgccB, 1), pl.thrB, pl.smem_B, st, scratch, out, mags, peak, lgN, pl.lgccB, tw, lgN);
     else
-      k_fftc<T, true, false><<<dim3(N >> pl.lgccB, 1), pl.thrB, pl.smem_B, st>>>(
-          scratch, out, nullptr, nullptr, lgN, pl.lgccB, tw, lgN);
+      kl(k_fftc<T, true, false>, dim3(N >> pl.lgccB, 1), pl.thrB, pl.smem_B, st, scratch, out, nullptr, nullptr, lgN, pl.lgccB, tw, lgN);
     post(c, "k_fftc", st, nn * sizeof(C) + wb);
   }
 }
@@ -522,7 +531,7 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
   T* wr = (T*)ws(c, "fold_w", 2 * g * N * sizeof(T));
   T* wc = wr + g * N;
   pre(c, st);
-  k_fold_weights<T><<<grid_for((long long)g * N), 256, 0, st>>>(space, pp, g, lgN, wr, wc);
+  kl(k_fold_weights<T>, grid_for((long long)g * N), 256, 0, st, space, pp, g, lgN, wr, wc);
   post(c, "k_fold_weights", st, 2.0 * g * N * sizeof(T));
   if (g == 1 && B >= 512 && lgN - lgB <= 5 && y_direct) {
     // wide single-loop fold, permuted grid written directly
@@ -531,11 +540,11 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
     const dim3 grid_w(B / 512, B / rh);
     pre(c, st);
     if (rh == 4)
-      k_fold_wide<Tin, T, 4><<<grid_w, 256, 0, st>>>(x, wr, wc, pp.p[0], lgN, lgB, (C*)y_direct, zero_peak);
+      kl(k_fold_wide<Tin, T, 4>, grid_w, 256, 0, st, x, wr, wc, pp.p[0], lgN, lgB, (C*)y_direct, zero_peak);
     else if (rh == 2)
-      k_fold_wide<Tin, T, 2><<<grid_w, 256, 0, st>>>(x, wr, wc, pp.p[0], lgN, lgB, (C*)y_direct, zero_peak);
+      kl(k_fold_wide<Tin, T, 2>, grid_w, 256, 0, st, x, wr, wc, pp.p[0], lgN, lgB, (C*)y_direct, zero_peak);
     else
-      k_fold_wide<Tin, T, 1><<<grid_w, 256, 0, st>>>(x, wr, wc, pp.p[0], lgN, lgB, (C*)y_direct, zero_peak);
+      kl(k_fold_wide<Tin, T, 1>, grid_w, 256, 0, st, x, wr, wc, pp.p[0], lgN, lgB, (C*)y_direct, zero_peak);
     post(c, "k_fold", st, by);
     return FoldOut{y_direct, 1};
   }
@@ -543,11 +552,11 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
   const double fold_bytes = sup * sup * sizeof(Tin) + (double)gm.Z * g * BB * sizeof(C);
   pre(c, st);
   if (g == 1 && (N / std::max(B, gm.TW)) >= 4)
-    k_fold<Tin, T, 1, 2, 4><<<grid, threads, dyn, st>>>(x, wr, wc, pp, g, gm, dst, zero_peak);
+    kl(k_fold<Tin, T, 1, 2, 4>, grid, threads, dyn, st, x, wr, wc, pp, g, gm, dst, zero_peak);
   else if (g == 1)
-    k_fold<Tin, T, 1, 2><<<grid, threads, dyn, st>>>(x, wr, wc, pp, g, gm, dst, zero_peak);
+    kl(k_fold<Tin, T, 1, 2>, grid, threads, dyn, st, x, wr, wc, pp, g, gm, dst, zero_peak);
   else
-    k_fold<Tin, T, kMaxFoldLoops, 1><<<grid, threads, dyn, st>>>(x, wr, wc, pp, g, gm, dst, zero_peak);
+    kl(k_fold<Tin, T, kMaxFoldLoops, 1>, grid, threads, dyn, st, x, wr, wc, pp, g, gm, dst, zero_peak);
   post(c, "k_fold", st, fold_bytes);
   return FoldOut{dst, gm.Z};
 }
@@ -588,7 +597,7 @@ void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTable
         fft2d_grids<T>(c, y, lgB, g, tw, lgN, sp, mg, pk, st);
       } else {
         pre(c, st);
-        k_fold_reduce_fft_small<T><<<g, 1024, BB * sizeof(C), st>>>(dst, gm.Z, g, lgB, pp, tw, lgN,
+        kl(k_fold_reduce_fft_small<T>, g, 1024, BB * sizeof(C), st, dst, gm.Z, g, lgB, pp, tw, lgN,
                                                                     y);
         post(c, "k_fold_reduce_fft_small", st, (double)(gm.Z + 1) * g * BB * sizeof(C));
         if (sp && sp != y)
@@ -598,7 +607,7 @@ void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTable
     } else {
       if (gm.Z != 1) {
         pre(c, st);
-        k_fold_reduce<T><<<grid_for((long long)BB * g), 256, 0, st>>>(dst, gm.Z, g, lgB, pp, y);
+        kl(k_fold_reduce<T>, grid_for((long long)BB * g), 256, 0, st, dst, gm.Z, g, lgB, pp, y);
         post(c, "k_fold_reduce", st, (double)(gm.Z + 1) * g * BB * sizeof(C));
       }
       fft2d_grids<T>(c, y, lgB, g, tw, lgN, sp, mg, pk, st);
@@ -612,10 +621,10 @@ void compact(sfft2d_ctx* c, const uint32_t* bits, const unsigned* cnts, long seg
   const int nblk = blocks_for(seglen);
   unsigned* offs = (unsigned*)ws(c, "cmp_off", (size_t)nblk * nseg * sizeof(unsigned));
   pre(c, st);
-  k_scan_blocks<<<nseg, 1024, 0, st>>>(cnts, nblk, offs, total_dev);
+  kl(k_scan_blocks, nseg, 1024, 0, st, cnts, nblk, offs, total_dev);
   post(c, "k_scan_blocks", st, 0);
   pre(c, st);
-  k_compact_bits<<<dim3(nblk, nseg), kCmpThreads, 0, st>>>(bits, seglen, offs, out, out_stride);
+  kl(k_compact_bits, dim3(nblk, nseg), kCmpThreads, 0, st, bits, seglen, offs, out, out_stride);
   post(c, "k_compact_bits", st, 0);
 }
 
@@ -642,14 +651,14 @@ unsigned local_maxima_dev(sfft2d_ctx* c, const T* mags, int lgB, const unsigned 
     ck(cudaMemsetAsync(cnts, 0, (size_t)nblk * 4, st), "memset");
     pre(c, st);
     if (perm)
-      k_lmax_rows<T, true><<<B / rb, 512, sm, st>>>(mags, lgB, s1, s2, rb, peak, floor_rel, bits, cnts);
+      kl(k_lmax_rows<T, true>, B / rb, 512, sm, st, mags, lgB, s1, s2, rb, peak, floor_rel, bits, cnts, (int32_t*)nullptr, (unsigned*)nullptr, Publish{nullptr, 0, nullptr, 0});
     else
-      k_lmax_rows<T, false><<<B / rb, 512, sm, st>>>(mags, lgB, 1, 1, rb, peak, floor_rel, bits, cnts);
+      kl(k_lmax_rows<T, false>, B / rb, 512, sm, st, mags, lgB, 1, 1, rb, peak, floor_rel, bits, cnts, (int32_t*)nullptr, (unsigned*)nullptr, Publish{nullptr, 0, nullptr, 0});
     post(c, "k_lmax_rows", st, (double)BB * sizeof(T) + BB / 8.0);
   } else {
     if (perm) fail(SFFT2D_ERR_UNSUPPORTED, "permuted local maxima need B >= 32");
     pre(c, st);
-    k_lmax_bits<T><<<dim3(nblk, 1), kCmpThreads, 0, st>>>(mags, lgB, 0, peak, floor_rel, bits, cnts);
+    kl(k_lmax_bits<T>, dim3(nblk, 1), kCmpThreads, 0, st, mags, lgB, 0, peak, floor_rel, bits, cnts);
     post(c, "k_lmax_bits", st, (double)BB * sizeof(T) + BB / 8.0);
   }
   compact(c, bits, cnts, BB, 1, out, 0, tot, st);
@@ -671,10 +680,10 @@ unsigned lmax_tuner(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long l
   const Publish pub = make_publish(c, (unsigned)(B / rb));
   pre(c, st);
   if (perm)
-    k_lmax_rows<T, true, true><<<B / rb, 512, sm, st>>>(mags, lgB, s1, s2, rb, peak, floor_rel,
+    kl(k_lmax_rows<T, true, true>, B / rb, 512, sm, st, mags, lgB, s1, s2, rb, peak, floor_rel,
                                                         nullptr, nullptr, list, count, pub);
   else
-    k_lmax_rows<T, false, true><<<B / rb, 512, sm, st>>>(mags, lgB, 1, 1, rb, peak, floor_rel,
+    kl(k_lmax_rows<T, false, true>, B / rb, 512, sm, st, mags, lgB, 1, 1, rb, peak, floor_rel,
                                                          nullptr, nullptr, list, count, pub);
   post(c, "k_lmax_rows", st, by);
   return pub.seq;
@@ -688,30 +697,30 @@ void topk_bits(sfft2d_ctx* c, const T* vals, long seglen, int nseg, long long nu
   unsigned* hist = (unsigned*)ws(c, "sel_hist", (size_t)nseg * 256 * sizeof(unsigned));
   ck(cudaMemsetAsync(hist, 0, (size_t)nseg * 256 * sizeof(unsigned), st), "memset");
   pre(c, st);
-  k_sel_init<<<(nseg + 127) / 128, 128, 0, st>>>(sst, nseg, num, seglen);
+  kl(k_sel_init, (nseg + 127) / 128, 128, 0, st, sst, nseg, num, seglen);
   post(c, "k_sel_init", st, 0);
   const int nblk = blocks_for(seglen);
   if (num < seglen) {
     unsigned hb = (unsigned)std::max<long long>(1, std::min<long long>(256, (seglen + 4095) / 4096));
     for (int shift = 56; shift >= 0; shift -= 8) {
       pre(c, st);
-      k_radix_hist<T><<<dim3(hb, nseg), 256, 0, st>>>(vals, seglen, sst, shift, hist);
+      kl(k_radix_hist<T>, dim3(hb, nseg), 256, 0, st, vals, seglen, sst, shift, hist);
       post(c, "k_radix_hist", st, 0);
       pre(c, st);
-      k_radix_pick<<<(nseg + 31) / 32, 32, 0, st>>>(sst, hist, shift, nseg);
+      kl(k_radix_pick, (nseg + 31) / 32, 32, 0, st, sst, hist, shift, nseg);
       post(c, "k_radix_pick", st, 0);
     }
   }
   unsigned* tie_blk = (unsigned*)ws(c, "sel_tie", (size_t)nblk * nseg * sizeof(unsigned));
   unsigned* tie_off = (unsigned*)ws(c, "sel_tieoff", (size_t)nblk * nseg * sizeof(unsigned));
   pre(c, st);
-  k_tie_counts<T><<<dim3(nblk, nseg), kCmpThreads, 0, st>>>(vals, seglen, sst, tie_blk);
+  kl(k_tie_counts<T>, dim3(nblk, nseg), kCmpThreads, 0, st, vals, seglen, sst, tie_blk);
   post(c, "k_tie_counts", st, 0);
   pre(c, st);
-  k_scan_blocks<<<nseg, 1024, 0, st>>>(tie_blk, nblk, tie_off, nullptr);
+  kl(k_scan_blocks, nseg, 1024, 0, st, tie_blk, nblk, tie_off, nullptr);
   post(c, "k_scan_blocks", st, 0);
   pre(c, st);
-  k_select_bits<T><<<dim3(nblk, nseg), kCmpThreads, 0, st>>>(vals, seglen, sst, tie_off, bits, cnts);
+  kl(k_select_bits<T>, dim3(nblk, nseg), kCmpThreads, 0, st, vals, seglen, sst, tie_off, bits, cnts);
   post(c, "k_select_bits", st, 0);
 }
 
@@ -727,7 +736,7 @@ unsigned hist_compact(sfft2d_ctx* c, const uint32_t* hist, long nkeys, int mode,
   uint32_t* bits = (uint32_t*)ws(c, "hc_bits", words_for(nkeys) * 4);
   unsigned* cnts = (unsigned*)ws(c, "hc_cnt", (size_t)nblk * 4);
   pre(c, st);
-  k_hist_bits<<<nblk, kCmpThreads, 0, st>>>(hist, nkeys, mode, thr, bits, cnts);
+  kl(k_hist_bits, nblk, kCmpThreads, 0, st, hist, nkeys, mode, thr, bits, cnts);
   post(c, "k_hist_bits", st, (double)hist_bytes(nkeys, mode) + nkeys / 8.0);
   compact(c, bits, cnts, nkeys, 1, keys, 0, total_dev, st);
   return read_u32(c, total_dev, st);
@@ -762,7 +771,7 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
     // gain = freq[0]^2 = 1 for the all-pass window (hashing.py:228-246)
     const bool usable_all = 1.0 >= gain_floor;
     pre(c, st);
-    k_estimate_dense<T><<<grid_for(m), 256, 0, st>>>(xhat, keys, m_dev, usable_all, med, mags,
+    kl(k_estimate_dense<T>, grid_for(m), 256, 0, st, xhat, keys, m_dev, usable_all, med, mags,
                                                       alive, peak);
     post(c, "k_estimate_dense", st, 0);
     n_alive = usable_all ? (long long)m : 0;
@@ -776,12 +785,11 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
     uint8_t* usable = (uint8_t*)ws(c, "usable", (size_t)L * m);
     const T* freq = (const T*)tb.freq[P] + ((size_t)lgB << lgN);
     pre(c, st);
-    k_estimate<T><<<grid_for((long long)m * L), 256, 0, st>>>(
-        grids, L, keys, m_dev, dp, lgN, lgB, freq, (const C*)tb.tw[P], gain_floor, vals, usable,
+    kl(k_estimate<T>, grid_for((long long)m * L), 256, 0, st, grids, L, keys, m_dev, dp, lgN, lgB, freq, (const C*)tb.tw[P], gain_floor, vals, usable,
         (long)m);
     post(c, "k_estimate", st, 0);
     pre(c, st);
-    k_median<T><<<grid_for(m, 128), 128, 0, st>>>(vals, usable, L, (long)m, m_dev, med, mags,
+    kl(k_median<T>, grid_for(m, 128), 128, 0, st, vals, usable, L, (long)m, m_dev, med, mags,
                                                    alive, alive_cnt, peak);
     post(c, "k_median", st, 0);
     n_alive = read_u32(c, alive_cnt, st);
@@ -804,7 +812,7 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
   uint32_t* fb = (uint32_t*)ws(c, "fin_bits", words_for(m) * 4);
   unsigned* fc = (unsigned*)ws(c, "fin_cnt", (size_t)nblk * 4);
   pre(c, st);
-  k_final_bits<T><<<nblk, kCmpThreads, 0, st>>>(mags, alive, sel, (long)m, peak, prune_rel, fb, fc);
+  kl(k_final_bits<T>, nblk, kCmpThreads, 0, st, mags, alive, sel, (long)m, peak, prune_rel, fb, fc);
   post(c, "k_final_bits", st, 0);
   int32_t* pos = (int32_t*)ws(c, "fin_pos", (size_t)m * 4);
   unsigned* tot = (unsigned*)ws(c, "fin_tot", 16);
@@ -814,7 +822,7 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
   C* ov = (C*)ws(c, "out_v", (size_t)count * sizeof(C));
   if (count) {
     pre(c, st);
-    k_gather_out<T><<<grid_for(count), 256, 0, st>>>(pos, tot, keys, med, lgN, oij, ov);
+    kl(k_gather_out<T>, grid_for(count), 256, 0, st, pos, tot, keys, med, lgN, oij, ov);
     post(c, "k_gather_out", st, 0);
   }
   res->count = count;
@@ -931,7 +939,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     ck(cudaEventRecord(c->ev_lmax, st), "cudaEventRecord");
     ck(cudaStreamWaitEvent(c->vote_st, c->ev_lmax, 0), "cudaStreamWaitEvent");
     pre(c, c->vote_st);
-    k_vote<<<dim3(kNumSMs * 2, 1), 256, 0, c->vote_st>>>(maxlists[slot & 1], 0, cnt_slots + slot, 0,
+    kl(k_vote, dim3(kNumSMs * 2, 1), 256, 0, c->vote_st, maxlists[slot & 1], 0, cnt_slots + slot, 0,
                                                         nullptr, lgN, lgb, 1, mode, 0, hist,
                                                         budget_dev, pv);
     post(c, "k_vote", c->vote_st, (double)len * len * 4.0);
@@ -961,8 +969,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       const Publish pub = make_publish(c, 1);
       seq = pub.seq;
       pre(c, st);
-      k_small_pass<T><<<1, 1024, BB * (sizeof(C) + sizeof(T)) + bb * sizeof(C), st>>>(
-          (const C*)fo.data, fo.Z, fo.Z == 1, lgb, p, (const C*)tb.tw[prec_of<T>()], lgN,
+      kl(k_small_pass<T>, 1, 1024, BB * (sizeof(C) + sizeof(T)) + bb * sizeof(C), st, (const C*)fo.data, fo.Z, fo.Z == 1, lgb, p, (const C*)tb.tw[prec_of<T>()], lgN,
           cf.mag_floor, ml, cnt, pub);
       post(c, "k_small_pass", st, (double)(fo.Z + 1) * BB * sizeof(C));
     } else {
@@ -1057,7 +1064,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   }
   if (!finite_scanned) {
     pre(c, st);
-    k_check_finite<Tin><<<grid_for(nkeys, 256, kNumSMs * 8), 256, 0, st>>>(x, nkeys, finite);
+    kl(k_check_finite<Tin>, grid_for(nkeys, 256, kNumSMs * 8), 256, 0, st, x, nkeys, finite);
     post(c, "k_check_finite", st, (double)nkeys * sizeof(Tin));
   }
   if (read_u32(c, finite, st)) {
@@ -1089,7 +1096,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       nv = hist_compact(c, hist, nkeys, mode, 1u, keys, kt, st);
       int32_t* tal = (int32_t*)ws(c, "tallies", (size_t)std::max(nv, 1u) * 4);
       pre(c, st);
-      k_gather_tallies<<<grid_for(nv), 256, 0, st>>>(hist, mode, keys, kt, tal);
+      kl(k_gather_tallies, grid_for(nv), 256, 0, st, hist, mode, keys, kt, tal);
       post(c, "k_gather_tallies", st, 0);
     }
     S->n_votes = nv;
@@ -1153,7 +1160,7 @@ int sfft_location(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, con
   int32_t* bins = (int32_t*)ws(c, "loc_bins", (size_t)nloc * num * 4);
   if (num >= BB) {
     pre(c, st);
-    k_iota_segments<<<grid_for(BB * nloc), 256, 0, st>>>(bins, BB, nloc);
+    kl(k_iota_segments, grid_for(BB * nloc), 256, 0, st, bins, BB, nloc);
     post(c, "k_iota_segments", st, 0);
   } else {
     const int nblk = blocks_for(BB);
@@ -1175,13 +1182,12 @@ int sfft_location(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, con
   for (int g0 = 0; g0 < nloc; g0 += 8) {
     const int g = std::min(8, nloc - g0);
     pre(c, st);
-    k_vote<<<dim3(grid_for(per, 256, kNumSMs * 8), g), 256, 0, st>>>(
-        bins + (size_t)g0 * num, (long)num, nullptr, (long)num, dp + g0, lgN, lgb, 1, kVoteOrBit,
-        0, masks);
+    kl(k_vote, dim3(grid_for(per, 256, kNumSMs * 8), g), 256, 0, st, bins + (size_t)g0 * num, (long)num, nullptr, (long)num, dp + g0, lgN, lgb, 1, kVoteOrBit,
+        0, masks, 0LL, Perm{0, 0, 0, 0, 0, 0});
     post(c, "k_vote", st, (double)per * g * 4.0);
     if (!direct) {
       pre(c, st);
-      k_mask_to_counts<<<grid_for(nw, 256, kNumSMs * 8), 256, 0, st>>>(masks, out, nw);
+      kl(k_mask_to_counts, grid_for(nw, 256, kNumSMs * 8), 256, 0, st, masks, out, nw);
       post(c, "k_mask_to_counts", st, 3.0 * nw * 4);
     }
   }
@@ -1223,7 +1229,7 @@ void check_finite_now(sfft2d_ctx* c, const Tin* x, long nkeys, cudaStream_t st) 
   unsigned* finite = (unsigned*)ws(c, "finite", 16);
   ck(cudaMemsetAsync(finite, 0, 16, st), "memset");
   pre(c, st);
-  k_check_finite<Tin><<<grid_for(nkeys, 256, kNumSMs * 8), 256, 0, st>>>(x, nkeys, finite);
+  kl(k_check_finite<Tin>, grid_for(nkeys, 256, kNumSMs * 8), 256, 0, st, x, nkeys, finite);
   post(c, "k_check_finite", st, (double)nkeys * sizeof(Tin));
   if (read_u32(c, finite, st)) fail(SFFT2D_ERR_VALUE, "matrix contains NaN or Inf");
 }
@@ -1676,7 +1682,7 @@ int sfft2d_local_maxima(sfft2d_ctx* c, const void* grid, int b, double mag_floor
       unsigned long long* pk = (unsigned long long*)ws(c, "api_peak", 16);
       ck(cudaMemsetAsync(pk, 0, 16, st), "memset");
       pre(c, st);
-      k_mags<T><<<dim3(grid_for(BB, 256, 1024), 1), 256, 0, st>>>((const cplx<T>*)grid, BB, mg, pk);
+      kl(k_mags<T>, dim3(grid_for(BB, 256, 1024), 1), 256, 0, st, (const cplx<T>*)grid, BB, mg, pk);
       post(c, "k_mags", st, 0);
       int32_t* tmp = (int32_t*)ws(c, "api_lm", (size_t)(BB / 4 + 64) * 4);
       const long long cnt = local_maxima_dev<T>(c, mg, ilog2(b), pk, mag_floor, tmp, st);
@@ -1699,12 +1705,12 @@ int sfft2d_top_bins(sfft2d_ctx* c, const void* grids, int b, int nseg, int64_t n
       if (num > BB) fail(SFFT2D_ERR_VALUE, "num exceeds the number of bins");
       T* mg = (T*)ws(c, "api_mag", (size_t)nseg * BB * sizeof(T));
       pre(c, st);
-      k_mags<T><<<dim3(grid_for(BB, 256, 1024), nseg), 256, 0, st>>>((const cplx<T>*)grids, BB, mg,
+      kl(k_mags<T>, dim3(grid_for(BB, 256, 1024), nseg), 256, 0, st, (const cplx<T>*)grids, BB, mg,
                                                                      nullptr);
       post(c, "k_mags", st, 0);
       if (num >= BB) {
         pre(c, st);
-        k_iota_segments<<<grid_for(BB * nseg), 256, 0, st>>>(out_flat, BB, nseg);
+        kl(k_iota_segments, grid_for(BB * nseg), 256, 0, st, out_flat, BB, nseg);
         post(c, "k_iota_segments", st, 0);
         return;
       }

@@ -60,6 +60,14 @@ __device__ __forceinline__ unsigned bitrev(unsigned v, int bits) {
   return bits ? (__brev(v) >> (32 - bits)) : 0u;
 }
 
+// Programmatic dependent launch: kernels are launched with programmatic stream
+// serialisation so a kernel's CTAs can be scheduled while its predecessor in
+// the stream drains; every kernel waits here, before its first global memory
+// access, until the predecessor has completed and its writes are visible.
+__device__ __forceinline__ void pdl_wait() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // 16-byte global -> shared asynchronous copy (LDGSTS), no register staging
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);

@@ -24,6 +24,7 @@ __global__ void k_estimate(const cplx<T>* __restrict__ spec, int nloops, const i
                            int lgN, int lgB, const T* __restrict__ freq,
                            const cplx<T>* __restrict__ tw, double gain_floor,
                            cplx<T>* __restrict__ vals, uint8_t* __restrict__ usable, long stride) {
+  pdl_wait();
   using C = cplx<T>;
   const long m = *m_dev;
   const int N = 1 << lgN, B = 1 << lgB;
@@ -62,6 +63,7 @@ __global__ void k_estimate_dense(const cplx<T>* __restrict__ xhat, const int32_t
                                  const unsigned* __restrict__ m_dev, bool usable_all,
                                  cplx<T>* __restrict__ med, T* __restrict__ mags,
                                  uint8_t* __restrict__ alive, unsigned long long* __restrict__ peak) {
+  pdl_wait();
   const long m = *m_dev;
   unsigned long long best = 0ull;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < m;
@@ -105,6 +107,7 @@ __global__ void k_median(const cplx<T>* __restrict__ vals, const uint8_t* __rest
                          cplx<T>* __restrict__ med, T* __restrict__ mags,
                          uint8_t* __restrict__ alive, unsigned* __restrict__ alive_count,
                          unsigned long long* __restrict__ peak) {
+  pdl_wait();
   const long m = *m_dev;
   unsigned cnt_alive = 0;
   unsigned long long best = 0ull;
@@ -155,6 +158,7 @@ __global__ void k_final_bits(const T* __restrict__ mags, const uint8_t* __restri
                              const uint32_t* __restrict__ sel_bits, long m,
                              const unsigned long long* __restrict__ peak, double prune_rel,
                              uint32_t* __restrict__ bits, unsigned* __restrict__ blk_counts) {
+  pdl_wait();
   __shared__ unsigned s_warp[32];
   const long w = (long)blockIdx.x * kCmpWords + threadIdx.x;
   const long wps = words_for(m);
@@ -179,6 +183,7 @@ template <typename T>
 __global__ void k_gather_out(const int32_t* __restrict__ pos, const unsigned* __restrict__ count,
                              const int32_t* __restrict__ keys, const cplx<T>* __restrict__ med,
                              int lgN, int64_t* __restrict__ out_ij, cplx<T>* __restrict__ out_v) {
+  pdl_wait();
   const long n = *count;
   const unsigned maskN = (1u << lgN) - 1u;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;

@@ -80,6 +80,7 @@ __device__ void fft_stages(cplx<T>* base, int count, int lgL, int es, int ss,
 template <typename T>
 __global__ void k_fft2d_small(cplx<T>* __restrict__ grids, int lgB,
                               const cplx<T>* __restrict__ tw, int lgN) {
+  pdl_wait();
   using C = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* s = reinterpret_cast<C*>(smem_raw);
@@ -102,6 +103,7 @@ template <typename T, typename Tin>
 __global__ void k_fft_rows(const Tin* __restrict__ src, cplx<T>* __restrict__ dst, int lgB,
                            long nrows, int rows_per_cta, const cplx<T>* __restrict__ tw,
                            int lgN) {
+  pdl_wait();
   using C = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* s = reinterpret_cast<C*>(smem_raw);
@@ -132,6 +134,7 @@ __global__ void k_fft_rows(const Tin* __restrict__ src, cplx<T>* __restrict__ ds
 template <typename T>
 __global__ void k_fft_cols(cplx<T>* __restrict__ grids, int lgB, int cpc,
                            const cplx<T>* __restrict__ tw, int lgN) {
+  pdl_wait();
   using C = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* s = reinterpret_cast<C*>(smem_raw);

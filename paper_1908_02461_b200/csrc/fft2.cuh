@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(512, (sizeof(T) == 4) ? 2 : 1)
 k_fftr(const Tin* src, cplx<T>* dst, T* __restrict__ mags, unsigned long long* __restrict__ peak,
        int lgL, int grid_lg, const cplx<T>* __restrict__ tw, int lgN,
        unsigned* __restrict__ nonfinite = nullptr) {
+  pdl_wait();
   using C = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* s = reinterpret_cast<C*>(smem_raw);
@@ -271,6 +272,7 @@ __global__ void __launch_bounds__(512, (sizeof(T) == 4) ? 2 : 1)
 k_fftc(const cplx<T>* src, cplx<T>* dst, T* __restrict__ mags,
        unsigned long long* __restrict__ peak, int lgL, int lgcc, const cplx<T>* __restrict__ tw,
        int lgN) {
+  pdl_wait();
   using C = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* s = reinterpret_cast<C*>(smem_raw);
@@ -296,6 +298,7 @@ k_fftc(const cplx<T>* src, cplx<T>* dst, T* __restrict__ mags,
 template <typename T>
 __global__ void __launch_bounds__(512, (sizeof(T) == 4) ? 2 : 1)
 k_fftcA(cplx<T>* data, int lgL1, int lgL2, int lgcc, const cplx<T>* __restrict__ tw, int lgN) {
+  pdl_wait();
   using C = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* s = reinterpret_cast<C*>(smem_raw);
@@ -317,6 +320,7 @@ __global__ void __launch_bounds__(512, (sizeof(T) == 4) ? 2 : 1)
 k_fftcB(const cplx<T>* __restrict__ src, cplx<T>* __restrict__ dst, T* __restrict__ mags,
         unsigned long long* __restrict__ peak, int lgL1, int lgL2, int lgcc,
         const cplx<T>* __restrict__ tw, int lgN) {
+  pdl_wait();
   using C = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* s = reinterpret_cast<C*>(smem_raw);

@@ -83,6 +83,7 @@ struct FoldGeom {
 template <typename T>
 __global__ void k_fold_weights(const T* __restrict__ space, PermPack pp, int nloops, int lgN,
                                T* __restrict__ wr, T* __restrict__ wc) {
+  pdl_wait();
   const int N = 1 << lgN;
   const unsigned maskN = (unsigned)N - 1u;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nloops * N; e += gridDim.x * blockDim.x) {
@@ -98,6 +99,7 @@ __global__ void __launch_bounds__(kFoldThreads)
 k_fold(const Tin* __restrict__ x, const T* __restrict__ wrow, const T* __restrict__ wcol,
        PermPack pp, int nloops, FoldGeom gm, cplx<T>* __restrict__ dst,
        unsigned long long* __restrict__ zero_peak = nullptr) {
+  pdl_wait();
   using C = cplx<T>;
   if (zero_peak && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0)
     *zero_peak = 0ull;
@@ -284,6 +286,7 @@ __global__ void __launch_bounds__(256)
 k_fold_wide(const Tin* __restrict__ x, const T* __restrict__ wrow, const T* __restrict__ wcol,
             Perm p, int lgN, int lgB, cplx<T>* __restrict__ y,
             unsigned long long* __restrict__ zero_peak = nullptr) {
+  pdl_wait();
   using C = cplx<T>;
   __shared__ T s_w[RH * 32];
   if (zero_peak && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *zero_peak = 0ull;
@@ -361,6 +364,7 @@ k_fold_wide(const Tin* __restrict__ x, const T* __restrict__ wrow, const T* __re
 template <typename T>
 __global__ void k_fold_reduce(const cplx<T>* __restrict__ part, int Z, int nloops, int lgB,
                               PermPack pp, cplx<T>* __restrict__ y) {
+  pdl_wait();
   using C = cplx<T>;
   const int B = 1 << lgB;
   const size_t BB = (size_t)B * B;
@@ -383,6 +387,7 @@ template <typename T>
 __global__ void __launch_bounds__(1024) k_fold_reduce_fft_small(const cplx<T>* __restrict__ part, int Z, int nloops,
                                         int lgB, PermPack pp, const cplx<T>* __restrict__ tw,
                                         int lgN, cplx<T>* __restrict__ spec) {
+  pdl_wait();
   using C = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* s = reinterpret_cast<C*>(smem_raw);

@@ -29,6 +29,7 @@ __host__ __device__ inline int blocks_for(long n) { return (int)((words_for(n) +
 template <typename T>
 __global__ void k_mags(const cplx<T>* __restrict__ spec, long seglen, T* __restrict__ mags,
                        unsigned long long* __restrict__ peak) {
+  pdl_wait();
   const int seg = blockIdx.y;
   const cplx<T>* s = spec + (size_t)seg * seglen;
   T* m = mags + (size_t)seg * seglen;
@@ -54,6 +55,7 @@ template <typename T>
 __global__ void k_lmax_bits(const T* __restrict__ mags, int lgB, int nseg_stride_log /*unused*/,
                             const unsigned long long* __restrict__ peak, double floor_rel,
                             uint32_t* __restrict__ bits, unsigned* __restrict__ blk_counts) {
+  pdl_wait();
   const int seg = blockIdx.y;
   const int B = 1 << lgB;
   const long BB = (long)B * B;
@@ -236,6 +238,7 @@ k_lmax_rows(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, int rb,
 template <typename T>
 __global__ void k_permute_grid(const T* __restrict__ M, int lgN, unsigned s1i, unsigned s2i,
                                T* __restrict__ G) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* row = reinterpret_cast<T*>(smem_raw);
   const int N = 1 << lgN;
@@ -252,6 +255,7 @@ __global__ void k_permute_grid(const T* __restrict__ M, int lgN, unsigned s1i, u
 // Exclusive scan of each segment's per-block counts (one CTA per segment).
 __global__ void k_scan_blocks(const unsigned* __restrict__ counts, int nblk,
                               unsigned* __restrict__ offsets, unsigned* __restrict__ totals) {
+  pdl_wait();
   const int seg = blockIdx.x;
   const unsigned* c = counts + (size_t)seg * nblk;
   unsigned* o = offsets + (size_t)seg * nblk;
@@ -303,6 +307,7 @@ __device__ __forceinline__ unsigned block_excl_scan256(unsigned v, unsigned* s_w
 __global__ void k_compact_bits(const uint32_t* __restrict__ bits, long seglen,
                                const unsigned* __restrict__ offsets, int32_t* __restrict__ out,
                                long out_stride) {
+  pdl_wait();
   __shared__ unsigned s_warp[32];
   const int seg = blockIdx.y;
   const long wps = words_for(seglen);
@@ -330,6 +335,7 @@ template <typename T>
 __global__ void k_radix_hist(const T* __restrict__ vals, long seglen,
                              const SelState* __restrict__ st, int shift,
                              unsigned* __restrict__ hist) {
+  pdl_wait();
   __shared__ unsigned sh[256];
   const int seg = blockIdx.y;
   for (int i = threadIdx.x; i < 256; i += blockDim.x) sh[i] = 0;
@@ -350,6 +356,7 @@ __global__ void k_radix_hist(const T* __restrict__ vals, long seglen,
 
 __global__ void k_radix_pick(SelState* __restrict__ st, unsigned* __restrict__ hist, int shift,
                              int nseg) {
+  pdl_wait();
   const int seg = blockIdx.x * blockDim.x + threadIdx.x;
   if (seg >= nseg) return;
   SelState s = st[seg];
@@ -375,6 +382,7 @@ __global__ void k_radix_pick(SelState* __restrict__ st, unsigned* __restrict__ h
 template <typename T>
 __global__ void k_tie_counts(const T* __restrict__ vals, long seglen,
                              const SelState* __restrict__ st, unsigned* __restrict__ tie_blk) {
+  pdl_wait();
   __shared__ unsigned s_warp[32];
   const int seg = blockIdx.y;
   const SelState s = st[seg];
@@ -395,6 +403,7 @@ template <typename T>
 __global__ void k_select_bits(const T* __restrict__ vals, long seglen,
                               const SelState* __restrict__ st, const unsigned* __restrict__ tie_off,
                               uint32_t* __restrict__ bits, unsigned* __restrict__ blk_counts) {
+  pdl_wait();
   __shared__ unsigned s_warp[32];
   const int seg = blockIdx.y;
   const SelState s = st[seg];

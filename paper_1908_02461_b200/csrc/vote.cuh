@@ -72,6 +72,7 @@ __global__ void k_vote(const int32_t* __restrict__ bins, long seg_stride, const 
 // Fold one group's loop-bit masks into per-coordinate loop counts (L > 8).
 __global__ void k_mask_to_counts(uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
                                  long nwords) {
+  pdl_wait();
   for (long w = blockIdx.x * (long)blockDim.x + threadIdx.x; w < nwords;
        w += (long)gridDim.x * blockDim.x) {
     const uint32_t m = masks[w];
@@ -94,6 +95,7 @@ __device__ __forceinline__ unsigned hist_value(const uint32_t* hist, size_t key,
 // bitmask of coordinates with value >= thr (block = 8192 coordinates)
 __global__ void k_hist_bits(const uint32_t* __restrict__ hist, long nkeys, int mode, unsigned thr,
                             uint32_t* __restrict__ bits, unsigned* __restrict__ blk_counts) {
+  pdl_wait();
   __shared__ unsigned s_warp[32];
   const long w = (long)blockIdx.x * kCmpWords + threadIdx.x;
   const long wps = words_for(nkeys);
@@ -129,6 +131,7 @@ __global__ void k_hist_bits(const uint32_t* __restrict__ hist, long nkeys, int m
 __global__ void k_gather_tallies(const uint32_t* __restrict__ hist, int mode,
                                  const int32_t* __restrict__ keys, const unsigned* __restrict__ m,
                                  int32_t* __restrict__ tallies) {
+  pdl_wait();
   const long n = *m;
   for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n;
        i += (long)gridDim.x * blockDim.x)

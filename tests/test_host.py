@@ -19,7 +19,7 @@ def test_library_exports_header_symbols():
     from paper_1908_02461_b200.build import build
     build()
     header = open(os.path.join(ROOT, "include", "sfft2d_b200.h")).read()
-    declared = set(re.findall(r"^\s*(?:int64_t|int|void|const char\*)\s+(sfft2d_\w+)\s*\(", header, re.M))
+    declared = set(re.findall(r"^\s*(?:int64_t|int|void|double|const char\*)\s+(sfft2d_\w+)\s*\(", header, re.M))
     assert declared == set(_native.EXPORTS)
     lib = ctypes.CDLL(_native.LIB_PATH)
     for name in declared:
