@@ -91,6 +91,10 @@ struct sfft2d_ctx {
   double sync_us = 0;   // host time blocked in stream synchronisation (diagnostic)
   // zero-copy count publication (tuner passes) and the side stream for votes
   unsigned* mapped_h = nullptr;
+  void* host_out_buf = nullptr;   // mapped pinned results (grow-only)
+  size_t host_out_cap = 0;
+  int64_t* out_ij_h = nullptr;
+  void* out_v_h = nullptr;
   unsigned* mapped_d = nullptr;
   unsigned* done_d = nullptr;
   unsigned done_base = 0;
@@ -323,6 +327,22 @@ void kl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   ck(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
+}
+
+// Mapped pinned host buffer for results (grow-only).
+void* host_out(sfft2d_ctx* c, size_t bytes) {
+  if (c->host_out_cap < bytes) {
+    if (c->host_out_buf) {
+      ck(cudaDeviceSynchronize(), "sync");
+      cudaFreeHost(c->host_out_buf);
+    }
+    c->host_out_buf = nullptr;
+    c->host_out_cap = 0;
+    const size_t cap = (bytes + bytes / 4 + 4095) & ~(size_t)4095;
+    ck(cudaHostAlloc(&c->host_out_buf, cap, cudaHostAllocMapped), "cudaHostAlloc");
+    c->host_out_cap = cap;
+  }
+  return c->host_out_buf;
 }
 
 // Prepare a count publication for a launch of `grid` CTAs.
@@ -817,14 +837,21 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
   int32_t* pos = (int32_t*)ws(c, "fin_pos", (size_t)m * 4);
   unsigned* tot = (unsigned*)ws(c, "fin_tot", 16);
   compact(c, fb, fc, (long)m, 1, pos, 0, tot, st);
+  // gather straight into mapped (zero-copy) host memory sized for the m
+  // candidates, then ONE synchronisation yields the count and the results
+  const size_t cap = (size_t)m;
+  char* outh = (char*)host_out(c, cap * (16 + sizeof(C)) + 64);
+  int64_t* oij_h = (int64_t*)outh;
+  C* ov_h = (C*)(outh + cap * 16);
+  int64_t* oij_d;
+  ck(cudaHostGetDevicePointer((void**)&oij_d, oij_h, 0), "cudaHostGetDevicePointer");
+  C* ov_d = (C*)((char*)oij_d + cap * 16);
+  pre(c, st);
+  kl(k_gather_out<T>, grid_for(m), 256, 0, st, pos, tot, keys, med, lgN, oij_d, ov_d);
+  post(c, "k_gather_out", st, 0);
   const unsigned count = read_u32(c, tot, st);
-  int64_t* oij = (int64_t*)ws(c, "out_ij", (size_t)count * 16);
-  C* ov = (C*)ws(c, "out_v", (size_t)count * sizeof(C));
-  if (count) {
-    pre(c, st);
-    kl(k_gather_out<T>, grid_for(count), 256, 0, st, pos, tot, keys, med, lgN, oij, ov);
-    post(c, "k_gather_out", st, 0);
-  }
+  c->out_ij_h = oij_h;
+  c->out_v_h = ov_h;
   res->count = count;
   res->ordered_by_magnitude = cut ? 1 : 0;
   c->res_count = count;
@@ -1067,10 +1094,15 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     kl(k_check_finite<Tin>, grid_for(nkeys, 256, kNumSMs * 8), 256, 0, st, x, nkeys, finite);
     post(c, "k_check_finite", st, (double)nkeys * sizeof(Tin));
   }
-  if (read_u32(c, finite, st)) {
-    std::memset(S, 0, sizeof(*S));
-    fail(SFFT2D_ERR_VALUE, "matrix contains NaN or Inf");
-  }
+  // the NaN/Inf flag rides along with the next synchronisation
+  ck(cudaMemcpyAsync(c->pinned + 1, finite, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H");
+  auto nan_check = [&](bool need_sync) {
+    if (need_sync) ck(cudaStreamSynchronize(st), "sync");
+    if (c->pinned[1]) {
+      std::memset(S, 0, sizeof(*S));
+      fail(SFFT2D_ERR_VALUE, "matrix contains NaN or Inf");
+    }
+  };
   S->converged = converged ? 1 : 0;
   S->detected_k = maxc;
   S->b_detect = bdet;
@@ -1094,10 +1126,13 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     unsigned nv = 0;
     if (have_votes) {
       nv = hist_compact(c, hist, nkeys, mode, 1u, keys, kt, st);
+      nan_check(false);
       int32_t* tal = (int32_t*)ws(c, "tallies", (size_t)std::max(nv, 1u) * 4);
       pre(c, st);
       kl(k_gather_tallies, grid_for(nv), 256, 0, st, hist, mode, keys, kt, tal);
       post(c, "k_gather_tallies", st, 0);
+    } else {
+      nan_check(true);
     }
     S->n_votes = nv;
     S->perms_used = pidx;
@@ -1111,12 +1146,14 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   res->n_candidates = 0;
   c->res_count = 0;
   if (maxc == 0 || !have_votes) {
+    nan_check(true);
     S->perms_used = pidx;
     res->perms_used = pidx;
     return;
   }
   const unsigned thr = (unsigned)((std::max(vote_passes, 1) + 1) / 2);
   const unsigned m = hist_compact(c, hist, nkeys, mode, thr, keys, kt, st);
+  nan_check(false);
   S->n_candidates = m;
   if (m == 0) {
     S->perms_used = pidx;
@@ -1368,6 +1405,7 @@ void sfft2d_ctx_destroy(sfft2d_ctx* c) {
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->perm_pinned) cudaFreeHost(c->perm_pinned);
   if (c->mapped_h) cudaFreeHost(c->mapped_h);
+  if (c->host_out_buf) cudaFreeHost(c->host_out_buf);
   if (c->done_d) cudaFree(c->done_d);
   if (c->vote_st) cudaStreamDestroy(c->vote_st);
   if (c->ev_lmax) cudaEventDestroy(c->ev_lmax);
@@ -1615,9 +1653,14 @@ int sfft2d_fetch_result(sfft2d_ctx* c, int64_t* ij, void* values, int dst_on_hos
     const size_t n = (size_t)c->res_count;
     if (n == 0) return;
     const size_t vb = n * (c->res_prec == SFFT2D_FP64 ? 16 : 8);
-    if (ij) ck(cudaMemcpyAsync(ij, ws(c, "out_ij", n * 16), n * 16, cudaMemcpyDefault, st), "copy ij");
-    if (values) ck(cudaMemcpyAsync(values, ws(c, "out_v", vb), vb, cudaMemcpyDefault, st), "copy v");
-    if (dst_on_host) ck(cudaStreamSynchronize(st), "sync");
+    // results already sit in mapped host memory (written by k_gather_out)
+    if (dst_on_host) {
+      if (ij) std::memcpy(ij, c->out_ij_h, n * 16);
+      if (values) std::memcpy(values, c->out_v_h, vb);
+    } else {
+      if (ij) ck(cudaMemcpyAsync(ij, c->out_ij_h, n * 16, cudaMemcpyDefault, st), "copy ij");
+      if (values) ck(cudaMemcpyAsync(values, c->out_v_h, vb, cudaMemcpyDefault, st), "copy v");
+    }
   });
 }
 
