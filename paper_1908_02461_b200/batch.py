@@ -11,8 +11,10 @@ another.  Results are exactly those of calling ``atsfft2d`` on each image.
 
 from __future__ import annotations
 
+import threading
 from concurrent.futures import ThreadPoolExecutor
 
+from . import _native
 from .engine import SfftConfig, sfft2d, sfft2d_arrays
 from .tuner import TunerConfig, atsfft2d, atsfft2d_arrays
 
@@ -29,6 +31,41 @@ def _pool(workers: int) -> ThreadPoolExecutor:
     return pool
 
 
+_local = threading.local()
+
+
+def _worker_stream(torch, device):
+    """This worker thread's own CUDA stream on `device` (the legacy default
+    stream every thread would otherwise share serialises the batch)."""
+    streams = getattr(_local, "streams", None)
+    if streams is None:
+        streams = _local.streams = {}
+    s = streams.get(device)
+    if s is None:
+        s = streams[device] = torch.cuda.Stream(device=device)
+    return s
+
+
+def _run(fn, n_items, concurrency, device):
+    """Run fn(i) for every item, `concurrency` at a time, each worker on its
+    own stream ordered after the caller's current stream."""
+    if concurrency <= 1 or n_items <= 1:
+        return [fn(i) for i in range(n_items)]
+    torch = _native._torch()
+    if not torch.cuda.is_available():
+        return list(_pool(concurrency).map(fn, range(n_items)))
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    ready = torch.cuda.current_stream(dev).record_event()
+
+    def one(i):
+        s = _worker_stream(torch, dev)
+        s.wait_event(ready)
+        with torch.cuda.stream(s):
+            return fn(i)
+
+    return list(_pool(concurrency).map(one, range(n_items)))
+
+
 def atsfft2d_batch(xs, cfg: TunerConfig, est_loops: int, rngs, *, concurrency: int = 4,
                    precision: str = "fp64", device=None, arrays: bool = False):
     """``atsfft2d`` over a batch: ``xs`` images, ``rngs`` one seed/Generator per
@@ -41,9 +78,7 @@ def atsfft2d_batch(xs, cfg: TunerConfig, est_loops: int, rngs, *, concurrency: i
     def one(i):
         return fn(xs[i], cfg, est_loops, rngs[i], precision=precision, device=device)
 
-    if concurrency <= 1 or len(xs) <= 1:
-        return [one(i) for i in range(len(xs))]
-    return list(_pool(concurrency).map(one, range(len(xs))))
+    return _run(one, len(xs), concurrency, device)
 
 
 def sfft2d_batch(xs, cfg: SfftConfig, rngs, *, concurrency: int = 4, precision: str = "fp64",
@@ -56,6 +91,4 @@ def sfft2d_batch(xs, cfg: SfftConfig, rngs, *, concurrency: int = 4, precision: 
     def one(i):
         return fn(xs[i], cfg, rngs[i], precision=precision, device=device)
 
-    if concurrency <= 1 or len(xs) <= 1:
-        return [one(i) for i in range(len(xs))]
-    return list(_pool(concurrency).map(one, range(len(xs))))
+    return _run(one, len(xs), concurrency, device)

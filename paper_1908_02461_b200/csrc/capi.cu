@@ -117,6 +117,15 @@ struct sfft2d_ctx {
 
 namespace {
 
+// Power-of-two capacities: buffers sized by data-dependent counts (candidates,
+// maxima) settle after a few calls instead of reallocating -- a cudaFree /
+// cudaFreeHost synchronises the whole device, stalling every other stream.
+size_t pow2_cap(size_t bytes) {
+  size_t cap = 4096;
+  while (cap < bytes) cap <<= 1;
+  return cap;
+}
+
 void* ws(sfft2d_ctx* c, const char* name, size_t bytes) {
   auto& e = c->bufs[name];
   if (bytes == 0) bytes = 16;
@@ -124,7 +133,7 @@ void* ws(sfft2d_ctx* c, const char* name, size_t bytes) {
     if (e.first) ck(cudaFree(e.first), "cudaFree");
     e.first = nullptr;
     e.second = 0;
-    size_t cap = (bytes + bytes / 8 + 4095) & ~(size_t)4095;
+    const size_t cap = pow2_cap(bytes);
     if (cudaMalloc(&e.first, cap) != cudaSuccess) {
       cudaGetLastError();
       e.first = nullptr;
@@ -338,7 +347,7 @@ void* host_out(sfft2d_ctx* c, size_t bytes) {
     }
     c->host_out_buf = nullptr;
     c->host_out_cap = 0;
-    const size_t cap = (bytes + bytes / 4 + 4095) & ~(size_t)4095;
+    const size_t cap = pow2_cap(bytes);
     ck(cudaHostAlloc(&c->host_out_buf, cap, cudaHostAllocMapped), "cudaHostAlloc");
     c->host_out_cap = cap;
   }

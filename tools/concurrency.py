@@ -12,7 +12,7 @@ prec = sys.argv[1] if len(sys.argv) > 1 else "fp32"
 imgs = [torch.from_numpy(P.sparse_image(4096, 100, 7 + i, snr_db=20.0).x).cuda() for i in range(8)]
 for conc in (1, 2, 3, 4, 6, 8):
     xs = [imgs[i % 8] for i in range(48)]
-    P.atsfft2d_batch(xs[:conc * 2], P.TunerConfig(), 8, [11] * (conc * 2), concurrency=conc,
+    P.atsfft2d_batch(xs, P.TunerConfig(), 8, [11] * len(xs), concurrency=conc,
                      precision=prec, arrays=True)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
