@@ -223,6 +223,7 @@ void allow_all_T() {
   allow_smem(k_lmax_rows<T, true>);
   allow_smem(k_lmax_rows<T, false, true>);
   allow_smem(k_lmax_rows<T, true, true>);
+  allow_smem(k_lmax_stream<T>);
   allow_smem(k_small_pass<T>);
 }
 
@@ -695,17 +696,35 @@ unsigned local_maxima_dev(sfft2d_ctx* c, const T* mags, int lgB, const unsigned 
 }
 
 // Tuner local maxima: unordered list + device count (no host sync).
+constexpr int kLmaxStreamMinB = 512;
+
 template <typename T>
 unsigned lmax_tuner(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long long* peak,
                     double floor_rel, int32_t* list, unsigned* count, cudaStream_t st, bool perm,
-                    unsigned s1, unsigned s2) {
+                    unsigned s1, unsigned s2, unsigned s2inv) {
   const int B = 1 << lgB;
+  const double by = (double)B * B * sizeof(T);
+  const size_t row = (size_t)B * sizeof(T);
+  const size_t wb = 16 * kWarpBuf * sizeof(int32_t);
+  if (B >= kLmaxStreamMinB && 4 * row + wb <= kMaxDynSmem) {
+    // streaming bands: ~2 CTAs per SM, a ring of row buffers per CTA
+    const int nslot = (int)std::max<size_t>(4, std::min<size_t>(8, (96 * 1024 - wb) / row));
+    const int band = (B + 2 * kNumSMs - 1) / (2 * kNumSMs);
+    const int thr = 512;
+    const int grid = (B + band - 1) / band;
+    const size_t sm = nslot * row + wb;
+    const Publish pub = make_publish(c, (unsigned)grid);
+    pre(c, st);
+    kl(k_lmax_stream<T>, grid, thr, sm, st, mags, lgB, perm ? s1 : 1u, perm ? s2 : 1u,
+       perm ? s2inv : 1u, band, nslot, peak, floor_rel, list, count, pub);
+    post(c, "k_lmax_stream", st, by);
+    return pub.seq;
+  }
   const int smem_rows = (int)((96 * 1024) / ((size_t)B * sizeof(T)));
   int rb = std::max(1, std::min(B / 128, smem_rows - 2));
   while (B % rb) --rb;
   const size_t sm = (size_t)(rb + 2) * B * sizeof(T) + (size_t)rb * B / 32 * sizeof(unsigned);
   if (sm > kMaxDynSmem) fail(SFFT2D_ERR_UNSUPPORTED, "grid too large for the local-maximum tile");
-  const double by = (double)B * B * sizeof(T);
   const Publish pub = make_publish(c, (unsigned)(B / rb));
   pre(c, st);
   if (perm)
@@ -998,7 +1017,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     if (bb == n) {
       // B = N: |Z_p[k1, k2]| = |x_hat[s1i k1, s2i k2]| — one dense FFT serves every pass
       ensure_xhat(true);
-      seq = lmax_tuner<T>(c, M, lgb, peakM, cf.mag_floor, ml, cnt, st, true, p.s1i, p.s2i);
+      seq = lmax_tuner<T>(c, M, lgb, peakM, cf.mag_floor, ml, cnt, st, true, p.s1i, p.s2i, p.s2);
     } else if (BB * sizeof(C) <= (size_t)kSmall2DBytes) {
       C* y = (C*)ws(c, "fold_y", BB * sizeof(C));
       const FoldOut fo = fold_launch<T, Tin>(c, x, lgN, lgb, tb, &p, 1, y, st);
@@ -1012,7 +1031,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       T* mg = (T*)ws(c, "grid_mag", BB * sizeof(T));
       unsigned long long* pk = (unsigned long long*)ws(c, "gpeak", 16);
       fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, &p, 1, (C*)nullptr, mg, pk, st);
-      seq = lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, ml, cnt, st, false, 1, 1);
+      seq = lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, ml, cnt, st, false, 1, 1, 1);
     }
     vote_list(p, lgb, budget, slot);
     const long long count = wait_published(c, seq, st);

@@ -419,6 +419,7 @@ k_small_pass(const cplx<T>* __restrict__ part, int Z, bool permuted, int lgB, Pe
              const cplx<T>* __restrict__ tw, int lgN, double floor_rel,
              int32_t* __restrict__ list, unsigned* __restrict__ count,
              Publish pub = Publish{nullptr, 0, nullptr, 0}) {
+  pdl_wait();
   using C = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* s = reinterpret_cast<C*>(smem_raw);

@@ -118,6 +118,7 @@ k_lmax_rows(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, int rb,
             uint32_t* __restrict__ bits, unsigned* __restrict__ blk_counts,
             int32_t* __restrict__ list = nullptr, unsigned* __restrict__ count = nullptr,
             Publish pub = Publish{nullptr, 0, nullptr, 0}) {
+  pdl_wait();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* S = reinterpret_cast<T*>(smem_raw);
   __shared__ unsigned s_cnt[32];
@@ -229,6 +230,137 @@ k_lmax_rows(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, int rb,
   const int nblk = (int)(last / kCmpElems - first / kCmpElems + 1);
   for (int i = threadIdx.x; i < nblk; i += blockDim.x)
     if (s_cnt[i]) atomicAdd(&blk_counts[first / kCmpElems + i], s_cnt[i]);
+}
+
+// cp.async group wait with a runtime depth (the PTX operand is an immediate)
+__device__ __forceinline__ void cp_async_wait_upto(int n) {
+  switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;\n" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;\n" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;\n" ::: "memory"); break;
+    case 3: asm volatile("cp.async.wait_group 3;\n" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 4;\n" ::: "memory"); break;
+  }
+}
+
+// Streaming local-maximum scan of a large tuner grid (B >= 512), unordered
+// list output — same predicate and output as k_lmax_rows<T, PERM, true>.
+// Each CTA owns a contiguous band of view rows and streams the rows it needs
+// through a ring of `nslot` shared-memory row buffers with cp.async, up to
+// nslot - 3 rows ahead of the row being tested, so HBM reads overlap the test
+// and only the two halo rows of a band are read twice.  View row r is row
+// s1*r of M.  The test walks NATURAL columns C of the staged rows, four per
+// lane with one 16-byte (two for fp64) shared load: view column c = s2i*C and
+// its view neighbours c -+ 1 are natural columns C -+ s2, so the floor test
+// of 128 bins costs a handful of warp instructions, and only bins passing it
+// fetch their 8 neighbours.  Maxima are appended to a per-warp shared buffer
+// flushed with one global atomicAdd per kWarpBuf entries.
+constexpr int kWarpBuf = 256;
+
+template <typename T>
+__device__ __forceinline__ void lds4(const T* p, T v[4]) {
+  if constexpr (sizeof(T) == 4) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  } else {
+    const double2 a = *reinterpret_cast<const double2*>(p);
+    const double2 b = *reinterpret_cast<const double2*>(p + 2);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512)
+k_lmax_stream(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, unsigned s2i, int band,
+              int nslot, const unsigned long long* __restrict__ peak, double floor_rel,
+              int32_t* __restrict__ list, unsigned* __restrict__ count, Publish pub) {
+  pdl_wait();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* ring = reinterpret_cast<T*>(smem_raw);
+  const int B = 1 << lgB;
+  const unsigned mask = (unsigned)B - 1u;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  int32_t* wbuf = reinterpret_cast<int32_t*>(ring + ((size_t)nslot << lgB)) + warp * kWarpBuf;
+  const int r0 = blockIdx.x * band;
+  const int nrow = min(band, B - r0);
+  const int nload = nrow + 2;                  // view rows r0-1 .. r0+nrow
+  constexpr int V = 16 / sizeof(T);
+  const int chunks = B / V;
+  int next_load = 0, next_slot = 0;            // ring position of the next issue
+  auto issue = [&]() {
+    if (next_load < nload) {
+      const unsigned r = (unsigned)(r0 - 1 + next_load) & mask;
+      const unsigned sr = (s1 * r) & mask;
+      T* dst = ring + ((size_t)next_slot << lgB);
+      const T* src = M + ((size_t)sr << lgB);
+      for (int q = threadIdx.x; q < chunks; q += blockDim.x) cp_async16(dst + q * V, src + q * V);
+    }
+    cp_async_commit();
+    ++next_load;
+    next_slot = next_slot + 1 == nslot ? 0 : next_slot + 1;
+  };
+  for (int t = 0; t < nslot - 1; ++t) issue();
+  // floor test in T: v >= fl (float64, tuner.py:111) <=> v >= fl rounded up
+  // to T; a zero peak (no live bins) becomes an unreachable threshold
+  const double pk = fkey_inv(*peak);
+  const double fl = floor_rel * pk;
+  T flT = sizeof(T) == 4 ? (T)__double2float_ru(fl) : (T)fl;
+  if (!(pk > 0.0))
+    flT = sizeof(T) == 4 ? (T)__int_as_float(0x7f800000) : (T)__longlong_as_double(0x7ff0000000000000ll);
+  int nbuf = 0;
+  auto flush = [&]() {
+    unsigned base = 0;
+    if (lane == 0 && nbuf) base = atomicAdd(count, (unsigned)nbuf);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (int e = lane; e < nbuf; e += 32) list[base + e] = wbuf[e];
+    __syncwarp();
+    nbuf = 0;
+  };
+  const int groups = B >> 7;                   // 128 natural columns per warp step
+  int su = 0, sm = 1, sd = 2;                  // ring slots of view rows s-1, s, s+1
+  for (int s = 0; s < nrow; ++s) {
+    cp_async_wait_upto(nslot - 4);             // loads s, s+1, s+2 have landed
+    __syncthreads();                           // ... for every thread; slot of load s-1 is free
+    issue();
+    const T* up = ring + ((size_t)su << lgB);
+    const T* md = ring + ((size_t)sm << lgB);
+    const T* dn = ring + ((size_t)sd << lgB);
+    const unsigned rowbase = (unsigned)(r0 + s) << lgB;
+    for (int g = warp; g < groups; g += nwarps) {
+      const unsigned C0 = ((unsigned)g << 7) + ((unsigned)lane << 2);
+      T m[4];
+      lds4(md + C0, m);
+      const T hi = fmax(fmax(m[0], m[1]), fmax(m[2], m[3]));
+      if (!__any_sync(0xffffffffu, hi >= flT)) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const unsigned C = C0 + j;
+        const T v = m[j];
+        bool f = v >= flT;
+        if (f) {
+          const unsigned Cl = (C - s2) & mask, Cr = (C + s2) & mask;
+          f = (v > up[Cl]) & (v > up[C]) & (v > up[Cr]) & (v > md[Cl]) & (v > md[Cr]) &
+              (v > dn[Cl]) & (v > dn[C]) & (v > dn[Cr]);
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        if (!bal) continue;
+        const int n = __popc(bal);
+        if (nbuf + n > kWarpBuf) flush();
+        if (f) wbuf[nbuf + __popc(bal & ((1u << lane) - 1u))] = (int32_t)(rowbase | ((s2i * C) & mask));
+        nbuf += n;
+      }
+    }
+    su = sm;
+    sm = sd;
+    sd = sd + 1 == nslot ? 0 : sd + 1;
+  }
+  __syncwarp();
+  flush();
+  cp_async_wait_upto(0);
+  if (pub.slot) {
+    __syncthreads();
+    if (threadIdx.x == 0) publish_count(count, pub.done, pub.target, pub.slot, pub.seq);
+  }
 }
 
 // G[r][c] = M[s1i*r mod N][s2i*c mod N]: the |Z| grid of a B == N pass seen

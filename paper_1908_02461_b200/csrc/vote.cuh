@@ -29,6 +29,7 @@ __global__ void k_vote(const int32_t* __restrict__ bins, long seg_stride, const 
                        long count, const Perm* __restrict__ perms, int lgN, int lgB, int expand,
                        int mode, int bit0, uint32_t* __restrict__ hist, long long budget = 0,
                        Perm pval = Perm{0, 0, 0, 0, 0, 0}) {
+  pdl_wait();
   const int seg = blockIdx.y;
   const long nb = counts ? (long)counts[seg] : count;
   const int N = 1 << lgN;

@@ -161,3 +161,25 @@ def test_error_metric():
     assert P.error_metric({(0, 0): 1.0}, {(0, 0): 1.0}, 1) == 0.0
     assert P.error_metric({}, {}, 0) == 0.0
     assert P.error_metric({(1, 1): 1.0}, {}, 0) == float("inf")
+
+
+def test_every_kernel_waits_on_its_predecessor():
+    """Every launch goes through cudaLaunchKernelEx with programmatic stream
+    serialization, so every kernel must execute griddepcontrol.wait
+    (pdl_wait) before touching memory its predecessor wrote."""
+    import glob
+    import re
+    csrc = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                        "paper_1908_02461_b200", "csrc")
+    missing = []
+    for path in sorted(glob.glob(os.path.join(csrc, "*.cuh")) + glob.glob(os.path.join(csrc, "*.cu"))):
+        src = open(path).read()
+        for m in re.finditer(r"__global__\b", src):
+            open_brace = src.index("{", m.end())
+            name = re.findall(r"(\w+)\s*\(", src[m.end():open_brace])
+            name = [n for n in name if n != "__launch_bounds__"]
+            body = src[open_brace:open_brace + 400]
+            first_stmt = body.split(";")[0]
+            if "pdl_wait()" not in first_stmt:
+                missing.append(f"{os.path.basename(path)}:{name[0] if name else '?'}")
+    assert not missing, missing
