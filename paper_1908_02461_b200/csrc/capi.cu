@@ -539,10 +539,17 @@ struct FoldOut {
   int Z;
 };
 
+PermPack identity_pack(int g) {
+  PermPack pp;
+  std::memset(&pp, 0, sizeof(pp));
+  for (int i = 0; i < g; ++i) pp.p[i] = Perm{1, 1, 0, 0, 1, 1};
+  return pp;
+}
+
 template <typename T, typename Tin>
 FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTables& tb,
                     const Perm* hp, int g, void* y_direct, cudaStream_t st,
-                    unsigned long long* zero_peak = nullptr) {
+                    unsigned long long* zero_peak = nullptr, bool natural = false) {
   using C = cplx<T>;
   const int B = 1 << lgB;
   const size_t BB = (size_t)B * B;
@@ -550,6 +557,9 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
   PermPack pp;
   std::memset(&pp, 0, sizeof(pp));
   for (int i = 0; i < g; ++i) pp.p[i] = hp[i];
+  // the fold kernels use their permutations only to place buckets; natural
+  // order (bucket (rho, kappa) at row rho, column kappa) is the identity
+  const PermPack po = natural ? identity_pack(g) : pp;
   const int cpt = (g == 1) ? 2 : 1;
   const FoldGeom gm = fold_geometry(lgN, lgB, cpt);
   const int threads = gm.TW / cpt;
@@ -570,11 +580,11 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
     const dim3 grid_w(B / 512, B / rh);
     pre(c, st);
     if (rh == 4)
-      kl(k_fold_wide<Tin, T, 4>, grid_w, 256, 0, st, x, wr, wc, pp.p[0], lgN, lgB, (C*)y_direct, zero_peak);
+      kl(k_fold_wide<Tin, T, 4>, grid_w, 256, 0, st, x, wr, wc, po.p[0], lgN, lgB, (C*)y_direct, zero_peak);
     else if (rh == 2)
-      kl(k_fold_wide<Tin, T, 2>, grid_w, 256, 0, st, x, wr, wc, pp.p[0], lgN, lgB, (C*)y_direct, zero_peak);
+      kl(k_fold_wide<Tin, T, 2>, grid_w, 256, 0, st, x, wr, wc, po.p[0], lgN, lgB, (C*)y_direct, zero_peak);
     else
-      kl(k_fold_wide<Tin, T, 1>, grid_w, 256, 0, st, x, wr, wc, pp.p[0], lgN, lgB, (C*)y_direct, zero_peak);
+      kl(k_fold_wide<Tin, T, 1>, grid_w, 256, 0, st, x, wr, wc, po.p[0], lgN, lgB, (C*)y_direct, zero_peak);
     post(c, "k_fold", st, by);
     return FoldOut{y_direct, 1};
   }
@@ -582,11 +592,11 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
   const double fold_bytes = sup * sup * sizeof(Tin) + (double)gm.Z * g * BB * sizeof(C);
   pre(c, st);
   if (g == 1 && (N / std::max(B, gm.TW)) >= 4)
-    kl(k_fold<Tin, T, 1, 2, 4>, grid, threads, dyn, st, x, wr, wc, pp, g, gm, dst, zero_peak);
+    kl(k_fold<Tin, T, 1, 2, 4>, grid, threads, dyn, st, x, wr, wc, po, g, gm, dst, zero_peak);
   else if (g == 1)
-    kl(k_fold<Tin, T, 1, 2>, grid, threads, dyn, st, x, wr, wc, pp, g, gm, dst, zero_peak);
+    kl(k_fold<Tin, T, 1, 2>, grid, threads, dyn, st, x, wr, wc, po, g, gm, dst, zero_peak);
   else
-    kl(k_fold<Tin, T, kMaxFoldLoops, 1>, grid, threads, dyn, st, x, wr, wc, pp, g, gm, dst, zero_peak);
+    kl(k_fold<Tin, T, kMaxFoldLoops, 1>, grid, threads, dyn, st, x, wr, wc, po, g, gm, dst, zero_peak);
   post(c, "k_fold", st, fold_bytes);
   return FoldOut{dst, gm.Z};
 }
@@ -597,7 +607,7 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
 template <typename T, typename Tin>
 void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTables& tb,
                    const Perm* hp, int nloops, cplx<T>* spec, T* mags, unsigned long long* peaks,
-                   cudaStream_t st) {
+                   cudaStream_t st, bool natural = false) {
   using C = cplx<T>;
   const int B = 1 << lgB;
   const int P = prec_of<T>();
@@ -613,13 +623,14 @@ void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTable
     PermPack pp;
     std::memset(&pp, 0, sizeof(pp));
     for (int i = 0; i < g; ++i) pp.p[i] = hp[g0 + i];
+    if (natural) pp = identity_pack(g);     // output placement only (see fold_launch)
     C* sp = spec ? spec + (size_t)g0 * BB : nullptr;
     T* mg = mags ? mags + (size_t)g0 * BB : nullptr;
     unsigned long long* pk = peaks ? peaks + g0 : nullptr;
     // bucket grid y (permuted fold) for this group
     C* y = (small && sp) ? sp : (C*)ws(c, "fold_y", (size_t)g * BB * sizeof(C));
     const FoldOut fo = fold_launch<T, Tin>(c, x, lgN, lgB, tb, hp + g0, g, y, st,
-                                           (nloops == 1) ? pk : nullptr);
+                                           (nloops == 1) ? pk : nullptr, natural);
     C* dst = (C*)fo.data;
     struct { int Z; } gm{fo.Z};
     if (small) {
@@ -1030,8 +1041,13 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     } else {
       T* mg = (T*)ws(c, "grid_mag", BB * sizeof(T));
       unsigned long long* pk = (unsigned long long*)ws(c, "gpeak", 16);
-      fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, &p, 1, (C*)nullptr, mg, pk, st);
-      seq = lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, ml, cnt, st, false, 1, 1, 1);
+      // |Z[k1,k2]| = |Y^[s1i k1, s2i k2]| for the natural-order fold Y
+      // (Z[a,b] = Y[s1 a + t1, s2 b + t2]; the tau shifts are a phase):
+      // fold without the bucket scatter, FFT Y, and test the permuted view
+      fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, &p, 1, (C*)nullptr, mg, pk, st, true);
+      const unsigned mb = (unsigned)bb - 1u;
+      seq = lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, ml, cnt, st, true, p.s1i & mb, p.s2i & mb,
+                          p.s2 & mb);
     }
     vote_list(p, lgb, budget, slot);
     const long long count = wait_published(c, seq, st);
