@@ -10,13 +10,16 @@ defaults, est_loops=8): the adaptive tuning passes, the vote histogram, the
 estimation loops, median, top-k and prune.
 
 Legs printed on ONE JSON line (rank 0):
-  value     transforms/s, image resident in HBM, CUDA events on the launch
-            stream over exactly --steps steps (barrier + sync both sides, max
-            over ranks).  The 134 MB image and the ~1 GB per-transform working
-            set exceed the 126 MB L2, so no explicit flush is needed.
-  e2e       the same metric through the public API with the image in pinned
-            HOST memory: the host->device copy and the result download are
-            inside the timed region.
+  value     transforms/s with the images resident in HBM: --steps transforms
+            per rank, --concurrency of them in flight (distinct c3 images, one
+            CUDA stream + native context per in-flight transform), CUDA events
+            on the launch stream around the whole run (barrier + sync both
+            sides, max over ranks).  The 134 MB images and the ~1 GB
+            per-transform working set exceed the 126 MB L2, so no flush.
+  latency   the same steps with one transform in flight (per-transform time).
+  e2e       the value leg through the public API with the images in pinned
+            HOST memory: every step's host->device copy and result download
+            are inside the timed region.
   roofline  dominant kernel: algorithmic bytes per launch / CUDA-event launch
             time from the library's per-launch profiler (a separate
             instrumented pass over the same steps), against MEASURED_PEAKS.json.
@@ -74,9 +77,10 @@ def dist_env():
     return world, rank, local
 
 
-def workload(args, rank):
+def workload(args, rank, j=0):
+    """c3 image j of this rank (distinct seeds: 7 + rank + 1000 j)."""
     from paper_1908_02461_b200.signals import sparse_image
-    return sparse_image(args.n, args.k, 7 + rank, snr_db=args.snr)
+    return sparse_image(args.n, args.k, 7 + rank + 1000 * j, snr_db=args.snr)
 
 
 def c4_image(i: int):
@@ -267,22 +271,35 @@ def main():
     import paper_1908_02461_b200 as P
     from paper_1908_02461_b200 import _native
 
-    img = workload(args, rank)
-    x_dev = torch.from_numpy(img.x).to(dev)
+    conc = max(1, args.concurrency)
+    imgs = [workload(args, rank, j) for j in range(conc)]
+    img = imgs[0]
+    xs_dev = [torch.from_numpy(im.x).to(dev) for im in imgs]
+    x_dev = xs_dev[0]
     cfg = P.TunerConfig()
     ctx = _native.context(local)
     stream = torch.cuda.current_stream(dev)
+    from paper_1908_02461_b200 import batch as PB
 
     def step(x):
         return P.atsfft2d_arrays(x, cfg, args.est_loops, 11, precision=args.precision)
+
+    def run_steps(items, fn, concurrency):
+        """fn(item) for every item, `concurrency` in flight (one stream and
+        native context per worker); returns the summed kernel launches."""
+        def one(i):
+            fn(items[i])
+            return _native.context(local).last_launches
+        return sum(PB._run(one, len(items), concurrency, dev))
 
     def barrier():
         if world > 1:
             dist.barrier()
 
-    # warm-up (also builds tables / workspace)
+    # warm-up (also builds tables / workspace in every worker context)
     for _ in range(max(args.warmup, 1)):
         (ij, vals), state = step(x_dev)
+    run_steps([xs_dev[i % conc] for i in range(max(args.warmup, 2 * conc))], step, conc)
     torch.cuda.synchronize()
     parity = None
     gold = os.path.join(ROOT, "tests", "golden", "c3_ats.npz")
@@ -300,54 +317,60 @@ def main():
                   "trajectory_within_tolerance": same_b and (rel <= 1e-4 if args.precision == "fp32"
                                                              else rel == 0.0)}
 
-    # ---- timed region: value (image resident in HBM)
-    vis = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
-    sampler = ClockSampler(int(vis[local]) if len(vis) > local and vis[local].isdigit() else local)
-    launches = 0
-    barrier()
-    torch.cuda.synchronize()
-    sampler.start()
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        step(x_dev)
-        launches += ctx.last_launches
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    clocks = sampler.stop()
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    value = world * args.steps / (ms_max / 1e3)
 
-    # ---- e2e: pinned host image, H2D + result D2H inside the region
-    e2e = None
-    if not args.no_e2e:
-        host = torch.empty((args.n, args.n), dtype=torch.complex64, pin_memory=True)
-        host.copy_(torch.from_numpy(img.x))
-        xh = host.numpy()
-        P.atsfft2d(xh, cfg, args.est_loops, 11, precision=args.precision)
+    def timed(items, fn, concurrency):
         barrier()
         torch.cuda.synchronize()
-        d2h = 0
         e0.record(stream)
-        for _ in range(args.steps):
-            out, st = P.atsfft2d(xh, cfg, args.est_loops, 11, precision=args.precision)
-            d2h += len(out) * (16 + (16 if args.precision == "fp64" else 8))
+        n_launch = run_steps(items, fn, concurrency)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
         t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()), n_launch
+
+    if os.environ.get("SFFT2D_TRACE_ALLOC"):
+        print("---- timed region", file=sys.stderr, flush=True)
+    # ---- timed region: value (images resident in HBM, `conc` in flight)
+    vis = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
+    sampler = ClockSampler(int(vis[local]) if len(vis) > local and vis[local].isdigit() else local)
+    sampler.start()
+    ms_max, launches = timed([xs_dev[i % conc] for i in range(args.steps)], step, conc)
+    clocks = sampler.stop()
+    value = world * args.steps / (ms_max / 1e3)
+
+    if os.environ.get("SFFT2D_TRACE_ALLOC"):
+        print("---- end of timed region", file=sys.stderr, flush=True)
+    # ---- single-transform latency: one in flight, same steps
+    lat_ms, _ = timed([x_dev] * args.steps, step, 1)
+    latency = {"ms_per_transform": lat_ms / args.steps, "transforms_per_s": world * args.steps / (lat_ms / 1e3),
+               "in_flight": 1}
+
+    # ---- e2e: pinned host images, H2D + result D2H inside the region
+    e2e = None
+    if not args.no_e2e:
+        hosts = []
+        for im in imgs:
+            h = torch.empty((args.n, args.n), dtype=torch.complex64, pin_memory=True)
+            h.copy_(torch.from_numpy(im.x))
+            hosts.append(h.numpy())
+        d2h = [0]
+
+        def step_host(xh):
+            out, _st = P.atsfft2d(xh, cfg, args.est_loops, 11, precision=args.precision)
+            d2h[0] += len(out) * (16 + (16 if args.precision == "fp64" else 8))
+
+        run_steps(hosts, step_host, conc)
+        d2h[0] = 0
+        e2e_ms, _ = timed([hosts[i % conc] for i in range(args.steps)], step_host, conc)
         nperm = cfg.iters(args.n) + 2 + args.est_loops
-        e2e = {"value": world * args.steps / (float(t.item()) / 1e3), "unit": UNIT,
+        e2e = {"value": world * args.steps / (e2e_ms / 1e3), "unit": UNIT, "in_flight": conc,
                "h2d_bytes_per_step": args.n * args.n * 8 + nperm * 48,
-               "d2h_bytes_per_step": d2h // max(args.steps, 1)}
+               "d2h_bytes_per_step": d2h[0] // max(args.steps, 1)}
 
     # ---- batched throughput (c4 sample): independent 1024^2 images, resident
     # in HBM, `--concurrency` transforms in flight on separate streams
@@ -431,10 +454,12 @@ def main():
             "dtype": "f32" if args.precision == "fp32" else "f64", "data": "synthetic",
             "config": {"workload": f"c3: ATSFFT {args.n}x{args.n} complex64, k={args.k}, "
                                    f"{args.snr:g} dB SNR, TunerConfig() defaults, est_loops="
-                                   f"{args.est_loops}, one image per rank per step",
+                                   f"{args.est_loops}, one transform per rank per step, {conc} "
+                                   f"distinct images, {conc} transforms in flight (one CUDA "
+                                   f"stream each)",
                        "precision": args.precision, "l2": "inputs larger than L2 (134 MB image)",
                        "parallelism": f"independent transforms, {world} rank(s)"},
-            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+            "e2e": e2e, "latency": latency, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
             "gpu_launches": launches, "kernels": kernels, "batched": batched,
             "context": {"cufft_dense_fft2_c64_ms": cufft_ms,
                         "detected_k": state.detected_k, "passes": state.passes,

@@ -111,6 +111,8 @@ struct sfft2d_ctx {
     cudaEvent_t a, b;
   };
   std::vector<ProfRec> prof;
+  cudaStream_t ws_st = nullptr;     // stream of the running call: workspace grows stream-ordered on it
+  cudaEvent_t ev_ws = nullptr;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
 };
@@ -130,11 +132,22 @@ void* ws(sfft2d_ctx* c, const char* name, size_t bytes) {
   auto& e = c->bufs[name];
   if (bytes == 0) bytes = 16;
   if (e.second < bytes) {
-    if (e.first) ck(cudaFree(e.first), "cudaFree");
+    // Stream-ordered growth from the device's memory pool: cudaMalloc /
+    // cudaFree would synchronise the whole device and stall every other
+    // in-flight transform.  The side (vote) stream may still read the old
+    // buffer, so the free is ordered after its pending work.
+    cudaStream_t s = c->ws_st;
+    if (e.first) {
+      ck(cudaEventRecord(c->ev_ws, c->vote_st), "cudaEventRecord");
+      ck(cudaStreamWaitEvent(s, c->ev_ws, 0), "cudaStreamWaitEvent");
+      ck(cudaFreeAsync(e.first, s), "cudaFreeAsync");
+    }
     e.first = nullptr;
     e.second = 0;
     const size_t cap = pow2_cap(bytes);
-    if (cudaMalloc(&e.first, cap) != cudaSuccess) {
+    if (getenv("SFFT2D_TRACE_ALLOC"))
+      fprintf(stderr, "[sfft2d] ctx %p workspace '%s' -> %zu bytes\n", (void*)c, name, cap);
+    if (cudaMallocAsync(&e.first, cap, s) != cudaSuccess) {
       cudaGetLastError();
       e.first = nullptr;
       fail(SFFT2D_ERR_NOMEM, std::string("cannot allocate workspace '") + name + "' of " +
@@ -219,6 +232,12 @@ void allow_all_T() {
   allow_smem(k_fftcB<T, true, false>);
   allow_smem(k_fftcB<T, false, true>);
   allow_smem(k_fftcB<T, true, true>);
+  allow_smem(k_fftc1<T, true, false, 2>);
+  allow_smem(k_fftc1<T, false, true, 2>);
+  allow_smem(k_fftc1<T, true, true, 2>);
+  allow_smem(k_fftc1<T, true, false, 1>);
+  allow_smem(k_fftc1<T, false, true, 1>);
+  allow_smem(k_fftc1<T, true, true, 1>);
   allow_smem(k_lmax_rows<T, false>);
   allow_smem(k_lmax_rows<T, true>);
   allow_smem(k_lmax_rows<T, false, true>);
@@ -348,7 +367,10 @@ void* host_out(sfft2d_ctx* c, size_t bytes) {
     }
     c->host_out_buf = nullptr;
     c->host_out_cap = 0;
-    const size_t cap = pow2_cap(bytes);
+    // pinned allocation synchronises the device: start at 32 MB (1M results)
+    const size_t cap = pow2_cap(std::max<size_t>(bytes, 32u << 20));
+    if (getenv("SFFT2D_TRACE_ALLOC"))
+      fprintf(stderr, "[sfft2d] ctx %p host_out -> %zu bytes\n", (void*)c, cap);
     ck(cudaHostAlloc(&c->host_out_buf, cap, cudaHostAllocMapped), "cudaHostAlloc");
     c->host_out_cap = cap;
   }
@@ -468,11 +490,19 @@ void fft2d_grids(sfft2d_ctx* c, cplx<T>* grids, int lgB, int ngrids, const cplx<
   post(c, "k_fftr", st, 2 * gb);
   const double wbytes = (wc ? gb : 0) + (wm ? (double)BB * ngrids * sizeof(T) : 0);
   C* final_out = out;
-  if (pl.four_step && wc && out == grids)
+  // k_fftc1 is safe in place (a CTA reads all of its columns before writing)
+  if (pl.four_step && !pl.col1 && wc && out == grids)
     out = (C*)ws(c, "fft_tmp", (size_t)BB * ngrids * sizeof(C));
   auto colB = [&](auto WC_, auto WM_) {
     constexpr bool WC = decltype(WC_)::value, WM = decltype(WM_)::value;
-    if (pl.four_step) {
+    if (pl.col1) {
+      pre(c, st);
+      if (pl.ipt1 == 2)
+        kl(k_fftc1<T, WC, WM, 2>, dim3(B >> pl.lgcc1, ngrids), pl.thr1, pl.smem_1, st, grids, out, mags, peaks, lgB, pl.lgcc1, tw, lgN);
+      else
+        kl(k_fftc1<T, WC, WM, 1>, dim3(B >> pl.lgcc1, ngrids), pl.thr1, pl.smem_1, st, grids, out, mags, peaks, lgB, pl.lgcc1, tw, lgN);
+      post(c, "k_fftc1", st, gb + wbytes);
+    } else if (pl.four_step) {
       pre(c, st);
       kl(k_fftcA<T>, dim3(B >> pl.lgccA, 1 << pl.lgL2, ngrids), pl.thrA, pl.smem_A, st, grids, pl.lgL1, pl.lgL2, pl.lgccA, tw, lgN);
       post(c, "k_fftcA", st, 2 * gb);
@@ -512,7 +542,18 @@ void dense_fft(sfft2d_ctx* c, const Tin* x, cplx<T>* out, T* mags, unsigned long
     kl(k_fftr<T, Tin, true, false>, (unsigned)(N / pl.rows_per_cta), pl.row_threads, pl.smem_row, st, x, scratch, nullptr, nullptr, lgN, 2 * lgN, tw, lgN, nonfinite);
   post(c, "k_fftr_dense", st, nn * (sizeof(Tin) + sizeof(C)));
   const double wb = nn * sizeof(C) + (mags ? nn * sizeof(T) : 0);
-  if (pl.four_step) {
+  if (pl.col1) {
+    pre(c, st);
+    if (mags && pl.ipt1 == 2)
+      kl(k_fftc1<T, true, true, 2>, dim3(N >> pl.lgcc1, 1), pl.thr1, pl.smem_1, st, scratch, out, mags, peak, lgN, pl.lgcc1, tw, lgN);
+    else if (mags)
+      kl(k_fftc1<T, true, true, 1>, dim3(N >> pl.lgcc1, 1), pl.thr1, pl.smem_1, st, scratch, out, mags, peak, lgN, pl.lgcc1, tw, lgN);
+    else if (pl.ipt1 == 2)
+      kl(k_fftc1<T, true, false, 2>, dim3(N >> pl.lgcc1, 1), pl.thr1, pl.smem_1, st, scratch, out, nullptr, nullptr, lgN, pl.lgcc1, tw, lgN);
+    else
+      kl(k_fftc1<T, true, false, 1>, dim3(N >> pl.lgcc1, 1), pl.thr1, pl.smem_1, st, scratch, out, nullptr, nullptr, lgN, pl.lgcc1, tw, lgN);
+    post(c, "k_fftc1", st, nn * sizeof(C) + wb);
+  } else if (pl.four_step) {
     pre(c, st);
     kl(k_fftcA<T>, dim3(N >> pl.lgccA, 1 << pl.lgL2, 1), pl.thrA, pl.smem_A, st, scratch, pl.lgL1, pl.lgL2, pl.lgccA, tw, lgN);
     post(c, "k_fftcA", st, 2 * nn * sizeof(C));
@@ -557,46 +598,41 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
   PermPack pp;
   std::memset(&pp, 0, sizeof(pp));
   for (int i = 0; i < g; ++i) pp.p[i] = hp[i];
-  // the fold kernels use their permutations only to place buckets; natural
-  // order (bucket (rho, kappa) at row rho, column kappa) is the identity
-  const PermPack po = natural ? identity_pack(g) : pp;
   const int cpt = (g == 1) ? 2 : 1;
-  const FoldGeom gm = fold_geometry(lgN, lgB, cpt);
+  FoldGeom gm = fold_geometry(lgN, lgB, cpt);
   const int threads = gm.TW / cpt;
   const dim3 grid(gm.ktiles, B, gm.Z);
   const int nlt = (g == 1) ? 1 : kMaxFoldLoops;
-  const size_t dyn = (B < gm.TW) ? (size_t)nlt * gm.TW * sizeof(C) : 0;
+  size_t dyn = (B < gm.TW) ? (size_t)nlt * gm.TW * sizeof(C) : 0;
+  if (((size_t)sizeof(T) << lgN) <= 32 * 1024) {   // window table staged in smem
+    gm.tab = (int)dyn;
+    dyn += (size_t)sizeof(T) << lgN;
+  }
   const double sup = (double)tb.support[lgB];
-  const size_t N = (size_t)1 << lgN;
-  T* wr = (T*)ws(c, "fold_w", 2 * g * N * sizeof(T));
-  T* wc = wr + g * N;
-  pre(c, st);
-  kl(k_fold_weights<T>, grid_for((long long)g * N), 256, 0, st, space, pp, g, lgN, wr, wc);
-  post(c, "k_fold_weights", st, 2.0 * g * N * sizeof(T));
+  // window weights are gathered from the window table inside the fold
+  // kernels; `natural` places bucket (rho, kappa) at row rho, column kappa
   if (g == 1 && B >= 512 && lgN - lgB <= 5 && y_direct) {
-    // wide single-loop fold, permuted grid written directly
+    // wide single-loop fold, grid written directly
     const double by = sup * sup * sizeof(Tin) + (double)BB * sizeof(C);
     const int rh = B >= 1024 ? 2 : 1;   // RH=4 needs 128 registers (2 CTAs/SM)
     const dim3 grid_w(B / 512, B / rh);
     pre(c, st);
-    if (rh == 4)
-      kl(k_fold_wide<Tin, T, 4>, grid_w, 256, 0, st, x, wr, wc, po.p[0], lgN, lgB, (C*)y_direct, zero_peak);
-    else if (rh == 2)
-      kl(k_fold_wide<Tin, T, 2>, grid_w, 256, 0, st, x, wr, wc, po.p[0], lgN, lgB, (C*)y_direct, zero_peak);
+    if (rh == 2)
+      kl(k_fold_wide<Tin, T, 2>, grid_w, 256, 0, st, x, space, pp.p[0], lgN, lgB, natural, (C*)y_direct, zero_peak);
     else
-      kl(k_fold_wide<Tin, T, 1>, grid_w, 256, 0, st, x, wr, wc, po.p[0], lgN, lgB, (C*)y_direct, zero_peak);
+      kl(k_fold_wide<Tin, T, 1>, grid_w, 256, 0, st, x, space, pp.p[0], lgN, lgB, natural, (C*)y_direct, zero_peak);
     post(c, "k_fold", st, by);
     return FoldOut{y_direct, 1};
   }
   C* dst = (gm.Z == 1) ? (C*)y_direct : (C*)ws(c, "fold_part", (size_t)gm.Z * g * BB * sizeof(C));
   const double fold_bytes = sup * sup * sizeof(Tin) + (double)gm.Z * g * BB * sizeof(C);
   pre(c, st);
-  if (g == 1 && (N / std::max(B, gm.TW)) >= 4)
-    kl(k_fold<Tin, T, 1, 2, 4>, grid, threads, dyn, st, x, wr, wc, po, g, gm, dst, zero_peak);
+  if (g == 1 && ((1 << lgN) / std::max(B, gm.TW)) >= 4)
+    kl(k_fold<Tin, T, 1, 2, 4>, grid, threads, dyn, st, x, space, pp, g, gm, natural, dst, zero_peak);
   else if (g == 1)
-    kl(k_fold<Tin, T, 1, 2>, grid, threads, dyn, st, x, wr, wc, po, g, gm, dst, zero_peak);
+    kl(k_fold<Tin, T, 1, 2>, grid, threads, dyn, st, x, space, pp, g, gm, natural, dst, zero_peak);
   else
-    kl(k_fold<Tin, T, kMaxFoldLoops, 1>, grid, threads, dyn, st, x, wr, wc, po, g, gm, dst, zero_peak);
+    kl(k_fold<Tin, T, kMaxFoldLoops, 1>, grid, threads, dyn, st, x, space, pp, g, gm, natural, dst, zero_peak);
   post(c, "k_fold", st, fold_bytes);
   return FoldOut{dst, gm.Z};
 }
@@ -1420,6 +1456,12 @@ int sfft2d_ctx_create(int device, sfft2d_ctx** out) {
     ck(cudaMemset(c->done_d, 0, 64), "cudaMemset");
     ck(cudaStreamCreateWithFlags(&c->vote_st, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaEventCreateWithFlags(&c->ev_lmax, cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventCreateWithFlags(&c->ev_ws, cudaEventDisableTiming), "cudaEventCreate");
+    // keep freed workspace in the device pool (no release at sync points)
+    cudaMemPool_t pool;
+    ck(cudaDeviceGetDefaultMemPool(&pool, device), "cudaDeviceGetDefaultMemPool");
+    uint64_t keep = UINT64_MAX;
+    ck(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep), "cudaMemPoolSetAttribute");
     for (int i = 0; i < 2; ++i)
       ck(cudaEventCreateWithFlags(&c->ev_vote[i], cudaEventDisableTiming), "cudaEventCreate");
     allow_all_T<float>();
@@ -1453,6 +1495,7 @@ void sfft2d_ctx_destroy(sfft2d_ctx* c) {
   if (c->done_d) cudaFree(c->done_d);
   if (c->vote_st) cudaStreamDestroy(c->vote_st);
   if (c->ev_lmax) cudaEventDestroy(c->ev_lmax);
+  if (c->ev_ws) cudaEventDestroy(c->ev_ws);
   for (int i = 0; i < 2; ++i)
     if (c->ev_vote[i]) cudaEventDestroy(c->ev_vote[i]);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -1544,6 +1587,7 @@ int sfft2d_sfft(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host,
     if (!cfg || !perms || !res || !x) fail(SFFT2D_ERR_VALUE, "null argument");
     check_side(cfg->n);
     cudaStream_t st = (cudaStream_t)stream;
+    c->ws_st = st;
     std::memset(res, 0, sizeof(*res));
     c->launches = 0;
     c->has_res = false;
@@ -1568,6 +1612,7 @@ static int atsfft_impl(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host,
     if (!cfg || !res || !state || !x || (n_perms > 0 && !perms)) fail(SFFT2D_ERR_VALUE, "null argument");
     check_side(n);
     cudaStream_t st = (cudaStream_t)stream;
+    c->ws_st = st;
     std::memset(res, 0, sizeof(*res));
     c->launches = 0;
     c->sync_us = 0;
@@ -1593,6 +1638,7 @@ static int detect_impl(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host,
     if (!cfg || !state || !x || (n_perms > 0 && !perms)) fail(SFFT2D_ERR_VALUE, "null argument");
     check_side(n);
     cudaStream_t st = (cudaStream_t)stream;
+    c->ws_st = st;
     c->launches = 0;
     c->has_votes = false;
     const void* xd = stage_input(c, x, x_dtype, x_on_host, n, st);
@@ -1616,6 +1662,7 @@ int sfft2d_sfft_votes(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host,
     check_sfft_cfg(*cfg);
     if (nloops > cfg->loops) fail(SFFT2D_ERR_VALUE, "more loops than the configuration");
     cudaStream_t st = (cudaStream_t)stream;
+    c->ws_st = st;
     c->launches = 0;
     const void* xd = stage_input(c, x, x_dtype, x_on_host, cfg->n, st);
     const DevTables& tb = find_tables(c, cfg->n, cfg->window_delta_pass, cfg->window_delta_stop);
@@ -1639,6 +1686,7 @@ int sfft2d_sfft_from_votes(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_h
     check_side(cfg->n);
     check_sfft_cfg(*cfg);
     cudaStream_t st = (cudaStream_t)stream;
+    c->ws_st = st;
     std::memset(res, 0, sizeof(*res));
     c->launches = 0;
     c->has_res = false;
@@ -1694,6 +1742,7 @@ int sfft2d_fetch_result(sfft2d_ctx* c, int64_t* ij, void* values, int dst_on_hos
   return guarded(c, [&] {
     if (!c->has_res) fail(SFFT2D_ERR_STATE, "no transform result to fetch");
     cudaStream_t st = (cudaStream_t)stream;
+    c->ws_st = st;
     const size_t n = (size_t)c->res_count;
     if (n == 0) return;
     const size_t vb = n * (c->res_prec == SFFT2D_FP64 ? 16 : 8);
@@ -1713,6 +1762,7 @@ int sfft2d_fetch_votes(sfft2d_ctx* c, int32_t* keys, int32_t* tallies, int dst_o
   return guarded(c, [&] {
     if (!c->has_votes) fail(SFFT2D_ERR_STATE, "no detection votes to fetch");
     cudaStream_t st = (cudaStream_t)stream;
+    c->ws_st = st;
     const size_t n = (size_t)c->votes_count;
     if (n == 0) return;
     if (keys) ck(cudaMemcpyAsync(keys, ws(c, "keys", n * 4), n * 4, cudaMemcpyDefault, st), "copy keys");
@@ -1733,6 +1783,7 @@ int sfft2d_binned_spectrum(sfft2d_ctx* c, const void* x, int x_dtype, int n, int
     std::vector<Perm> hp(nloops);
     for (int i = 0; i < nloops; ++i) hp[i] = to_perm(perms[i], n);
     cudaStream_t st = (cudaStream_t)stream;
+    c->ws_st = st;
     c->launches = 0;
     dispatch(x_dtype, precision, [&](auto t, auto tin) {
       using T = decltype(t);
@@ -1749,6 +1800,7 @@ int sfft2d_fft2d(sfft2d_ctx* c, void* grids, int b, int count, int n_table, int 
     if (!is_pow2(b) || b < 2 || b > n_table) fail(SFFT2D_ERR_VALUE, "bad grid side");
     const DevTables& tb = find_twiddles(c, n_table);
     cudaStream_t st = (cudaStream_t)stream;
+    c->ws_st = st;
     dispatch_prec(precision, [&](auto t) {
       using T = decltype(t);
       fft2d_grids<T>(c, (cplx<T>*)grids, ilog2(b), count, (const cplx<T>*)tb.tw[prec_of<T>()],
@@ -1762,6 +1814,7 @@ int sfft2d_local_maxima(sfft2d_ctx* c, const void* grid, int b, double mag_floor
   return guarded(c, [&] {
     if (!is_pow2(b) || b < 4) fail(SFFT2D_ERR_VALUE, "bin grid must be at least 4x4 and a power of 2");
     cudaStream_t st = (cudaStream_t)stream;
+    c->ws_st = st;
     dispatch_prec(precision, [&](auto t) {
       using T = decltype(t);
       const long BB = (long)b * b;
@@ -1786,6 +1839,7 @@ int sfft2d_top_bins(sfft2d_ctx* c, const void* grids, int b, int nseg, int64_t n
   return guarded(c, [&] {
     if (!is_pow2(b) || b < 1 || nseg < 1 || num < 1 || !out_flat) fail(SFFT2D_ERR_VALUE, "bad arguments");
     cudaStream_t st = (cudaStream_t)stream;
+    c->ws_st = st;
     dispatch_prec(precision, [&](auto t) {
       using T = decltype(t);
       const long BB = (long)b * b;

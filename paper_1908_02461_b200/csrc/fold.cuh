@@ -75,29 +75,13 @@ struct FoldGeom {
   int ktiles;    // kappa tiles per rho (B >= TW ? B / TW : 1)
   int Z;         // row-alias chunks
   int rpc;       // row aliases per chunk
+  int tab;       // byte offset of the smem copy of the window table (-1: none)
 };
-
-// Natural-order window weights of this pass, wr[l][r] = g[s1i_l (r - t1_l) mod N]
-// and wc[l][c] = g[s2i_l (c - t2_l) mod N]: computed once per pass so the fold
-// reads them coalesced instead of gathering the window table per element.
-template <typename T>
-__global__ void k_fold_weights(const T* __restrict__ space, PermPack pp, int nloops, int lgN,
-                               T* __restrict__ wr, T* __restrict__ wc) {
-  pdl_wait();
-  const int N = 1 << lgN;
-  const unsigned maskN = (unsigned)N - 1u;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < nloops * N; e += gridDim.x * blockDim.x) {
-    const int l = e >> lgN;
-    const unsigned r = (unsigned)(e & (N - 1));
-    wr[e] = space[(pp.p[l].s1i * (r - pp.p[l].t1)) & maskN];
-    wc[e] = space[(pp.p[l].s2i * (r - pp.p[l].t2)) & maskN];
-  }
-}
 
 template <typename Tin, typename T, int NL, int CPT, int MU = 1>
 __global__ void __launch_bounds__(kFoldThreads)
-k_fold(const Tin* __restrict__ x, const T* __restrict__ wrow, const T* __restrict__ wcol,
-       PermPack pp, int nloops, FoldGeom gm, cplx<T>* __restrict__ dst,
+k_fold(const Tin* __restrict__ x, const T* __restrict__ space, PermPack pp, int nloops,
+       FoldGeom gm, bool natural, cplx<T>* __restrict__ dst,
        unsigned long long* __restrict__ zero_peak = nullptr) {
   pdl_wait();
   using C = cplx<T>;
@@ -117,13 +101,24 @@ k_fold(const Tin* __restrict__ x, const T* __restrict__ wrow, const T* __restric
   const int cnt = min(gm.rpc, aliases - j0);
   const int tid = threadIdx.x;
 
+  // ---- window table in shared memory (column weights are gathered at an
+  // odd stride, which is bank-conflict free in smem but 32 sectors per warp
+  // load from L1)
+  const T* wt = space;
+  if (gm.tab >= 0) {
+    T* tsm = reinterpret_cast<T*>(smem_raw + gm.tab);
+    constexpr int V = 16 / sizeof(T);
+    for (int i = tid * V; i < N; i += blockDim.x * V)
+      *reinterpret_cast<uint4*>(tsm + i) = __ldg(reinterpret_cast<const uint4*>(space + i));
+    wt = tsm;
+  }
   // ---- row weights of this chunk, and the compacted list of useful rows
   for (int jj = tid; jj < cnt; jj += blockDim.x) {
     const unsigned r = (unsigned)(rho + (j0 + jj) * B);
 #pragma unroll
     for (int l = 0; l < NL; ++l) {
       T w = (T)0;
-      if (l < nloops) w = wrow[((size_t)l << gm.lgN) + r];
+      if (l < nloops) w = __ldg(space + ((pp.p[l].s1i * (r - pp.p[l].t1)) & maskN));
       s_w[l * kFoldMaxRows + jj] = w;
     }
   }
@@ -171,7 +166,8 @@ k_fold(const Tin* __restrict__ x, const T* __restrict__ wrow, const T* __restric
 #pragma unroll
           for (int q = 0; q < CPT; ++q) {
             T w = (T)0;
-            if (l < nloops && m0 + mu < ncb) w = __ldg(wcol + ((size_t)l << gm.lgN) + c + q);
+            if (l < nloops && m0 + mu < ncb)
+              w = wt[(pp.p[l].s2i * ((unsigned)(c + q) - pp.p[l].t2)) & maskN];
             wc[mu][l][q] = w;
             any |= (w != (T)0);
           }
@@ -227,8 +223,8 @@ k_fold(const Tin* __restrict__ x, const T* __restrict__ wrow, const T* __restric
       for (int q = 0; q < CPT; ++q) {
         const unsigned kap = (unsigned)(cbase + cp + q);
         if (gm.Z == 1) {
-          const unsigned a = (pp.p[l].s1i * ((unsigned)rho - pp.p[l].t1)) & maskB;
-          const unsigned b = (pp.p[l].s2i * (kap - pp.p[l].t2)) & maskB;
+          const unsigned a = natural ? (unsigned)rho : (pp.p[l].s1i * ((unsigned)rho - pp.p[l].t1)) & maskB;
+          const unsigned b = natural ? kap : (pp.p[l].s2i * (kap - pp.p[l].t2)) & maskB;
           dst[l * BB + (size_t)a * B + b] = acc[l][q];
         } else {
           dst[((size_t)z * nloops + l) * BB + (size_t)rho * B + kap] = acc[l][q];
@@ -249,8 +245,8 @@ k_fold(const Tin* __restrict__ x, const T* __restrict__ wrow, const T* __restric
       C s = mk<T>(0, 0);
       for (int a = 0; a < reps; ++a) s = cadd(s, red[l * gm.TW + kap + a * B]);
       if (gm.Z == 1) {
-        const unsigned ra = (pp.p[l].s1i * ((unsigned)rho - pp.p[l].t1)) & maskB;
-        const unsigned cb = (pp.p[l].s2i * ((unsigned)kap - pp.p[l].t2)) & maskB;
+        const unsigned ra = natural ? (unsigned)rho : (pp.p[l].s1i * ((unsigned)rho - pp.p[l].t1)) & maskB;
+        const unsigned cb = natural ? (unsigned)kap : (pp.p[l].s2i * ((unsigned)kap - pp.p[l].t2)) & maskB;
         dst[l * BB + (size_t)ra * B + cb] = s;
       } else {
         dst[((size_t)z * nloops + l) * BB + (size_t)rho * B + kap] = s;
@@ -283,8 +279,8 @@ __device__ __forceinline__ C sum_partials(const C* __restrict__ p, size_t stride
 // 16-byte loads in flight.  Writes the permuted grid directly (Z = 1).
 template <typename Tin, typename T, int RH>
 __global__ void __launch_bounds__(256)
-k_fold_wide(const Tin* __restrict__ x, const T* __restrict__ wrow, const T* __restrict__ wcol,
-            Perm p, int lgN, int lgB, cplx<T>* __restrict__ y,
+k_fold_wide(const Tin* __restrict__ x, const T* __restrict__ space, Perm p, int lgN, int lgB,
+            bool natural, cplx<T>* __restrict__ y,
             unsigned long long* __restrict__ zero_peak = nullptr) {
   pdl_wait();
   using C = cplx<T>;
@@ -297,7 +293,7 @@ k_fold_wide(const Tin* __restrict__ x, const T* __restrict__ wrow, const T* __re
   const int kap = blockIdx.x * 512 + threadIdx.x * 2;
   for (int e = threadIdx.x; e < RH * A; e += blockDim.x) {
     const int r = e / A, j = e - r * A;
-    s_w[r * 32 + j] = wrow[rho0 + r + (j << lgB)];
+    s_w[r * 32 + j] = __ldg(space + ((p.s1i * ((unsigned)(rho0 + r + (j << lgB)) - p.t1)) & maskN));
   }
   __syncthreads();
   C acc[RH][2];
@@ -312,8 +308,8 @@ k_fold_wide(const Tin* __restrict__ x, const T* __restrict__ wrow, const T* __re
 #pragma unroll
     for (int ii = 0; ii < 2; ++ii) {
       const int c = kap + ((i0 + ii) << lgB);
-      wc[ii][0] = ii < ni ? __ldg(wcol + c) : (T)0;
-      wc[ii][1] = ii < ni ? __ldg(wcol + c + 1) : (T)0;
+      wc[ii][0] = ii < ni ? __ldg(space + ((p.s2i * ((unsigned)c - p.t2)) & maskN)) : (T)0;
+      wc[ii][1] = ii < ni ? __ldg(space + ((p.s2i * ((unsigned)c + 1u - p.t2)) & maskN)) : (T)0;
 #pragma unroll
       for (int r = 0; r < RH; ++r) u[ii][r][0] = u[ii][r][1] = mk<T>(0, 0);
     }
@@ -350,11 +346,11 @@ k_fold_wide(const Tin* __restrict__ x, const T* __restrict__ wrow, const T* __re
         acc[r][1].y = fma(wc[ii][1], u[ii][r][1].y, acc[r][1].y);
       }
   }
-  const unsigned b0 = (p.s2i * ((unsigned)kap - p.t2)) & maskB;
-  const unsigned b1 = (p.s2i * ((unsigned)kap + 1u - p.t2)) & maskB;
+  const unsigned b0 = natural ? (unsigned)kap : (p.s2i * ((unsigned)kap - p.t2)) & maskB;
+  const unsigned b1 = natural ? (unsigned)kap + 1u : (p.s2i * ((unsigned)kap + 1u - p.t2)) & maskB;
 #pragma unroll
   for (int r = 0; r < RH; ++r) {
-    const unsigned a = (p.s1i * ((unsigned)(rho0 + r) - p.t1)) & maskB;
+    const unsigned a = natural ? (unsigned)(rho0 + r) : (p.s1i * ((unsigned)(rho0 + r) - p.t1)) & maskB;
     y[(size_t)a * B + b0] = acc[r][0];
     y[(size_t)a * B + b1] = acc[r][1];
   }
@@ -524,6 +520,7 @@ inline FoldGeom fold_geometry(int lgN, int lgB, int cpt) {
   if (rpc > kFoldMaxRows) rpc = kFoldMaxRows;
   g.rpc = rpc;
   g.Z = (aliases + rpc - 1) / rpc;
+  g.tab = -1;
   return g;
 }
 

@@ -1,0 +1,47 @@
+"""GPU timeline of c3 ATSFFT transforms from a CUPTI kernel trace
+(torch.profiler): busy vs idle time per transform and the largest gaps.
+python tools/timeline.py [fp32|fp64] [reps]"""
+import json
+import os
+import sys
+import tempfile
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+from torch.profiler import ProfilerActivity, profile  # noqa: E402
+
+import paper_1908_02461_b200 as P  # noqa: E402
+
+prec = sys.argv[1] if len(sys.argv) > 1 else "fp32"
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+img = P.sparse_image(4096, 100, 7, snr_db=20.0)
+x = torch.from_numpy(img.x).cuda()
+for _ in range(3):
+    P.atsfft2d_arrays(x, P.TunerConfig(), 8, 11, precision=prec)
+torch.cuda.synchronize()
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
+    for _ in range(reps):
+        P.atsfft2d_arrays(x, P.TunerConfig(), 8, 11, precision=prec)
+    torch.cuda.synchronize()
+path = os.path.join(tempfile.mkdtemp(), "t.json")
+prof.export_chrome_trace(path)
+ev = json.load(open(path))["traceEvents"]
+ks = sorted((e for e in ev if e.get("cat") == "kernel"), key=lambda e: e["ts"])
+mem = [e for e in ev if e.get("cat") in ("gpu_memcpy", "gpu_memset")]
+t0, t1 = ks[0]["ts"], max(e["ts"] + e["dur"] for e in ks)
+busy, end, gaps = 0.0, t0, []
+for e in ks:
+    s, d = e["ts"], e["dur"]
+    if s > end:
+        gaps.append((s - end, e["name"][:40]))
+    busy += max(0.0, s + d - max(s, end))
+    end = max(end, s + d)
+span = t1 - t0
+print(f"{len(ks) / reps:.0f} kernels/transform, span {span / reps:.1f} us/transform, "
+      f"busy {busy / reps:.1f} us ({busy / span * 100:.1f}%), idle {(span - busy) / reps:.1f} us, "
+      f"memcpy/memset ops {len(mem) / reps:.0f}/transform")
+gaps.sort(reverse=True)
+big = [g for g in gaps if g[0] > 2.0]
+print(f"gaps > 2 us: {len(big) / reps:.1f}/transform totalling {sum(g for g, _ in big) / reps:.1f} us")
+for g, nm in gaps[:12]:
+    print(f"  {g:7.1f} us before {nm}")
