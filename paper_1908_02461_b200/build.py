@@ -35,10 +35,31 @@ def npyrandom_dir() -> str:
     return d
 
 
+def units() -> list:
+    """Translation units: the ABI/controllers and the FFT instantiation units
+    (compiled in parallel, linked into one shared library)."""
+    return sorted(os.path.join(SRC, f) for f in os.listdir(SRC) if f.endswith(".cu"))
+
+
 def build(force: bool = False, verbose: bool = True) -> str:
     if not force and up_to_date():
         return OUT
-    cmd = [NVCC, *FLAGS, "-o", OUT + ".tmp", os.path.join(SRC, "capi.cu"),
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(HERE, "_build")
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in FLAGS if f != "-shared"]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        cmd = [NVCC, *compile_flags, "-c", "-o", obj, src]
+        if verbose:
+            print(" ".join(cmd), flush=True)
+        subprocess.run(cmd, check=True)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(units()), os.cpu_count() or 1))) as pool:
+        objs = list(pool.map(compile_one, units()))
+    cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", OUT + ".tmp", *objs,
            "-L" + npyrandom_dir(), "-lnpyrandom", "-Xlinker", "--exclude-libs,ALL"]
     if verbose:
         print(" ".join(cmd), flush=True)

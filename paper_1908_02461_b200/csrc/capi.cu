@@ -25,8 +25,9 @@
 #include "common.cuh"
 #include "estimate.cuh"
 #include "fft.cuh"
-#include "fft2.cuh"
+#include "fft_launch.cuh"
 #include "fold.cuh"
+#include "host.cuh"
 #include "select.cuh"
 #include "vote.cuh"
 
@@ -39,24 +40,6 @@ extern "C" void random_bounded_uint64_fill(void* bitgen_state, uint64_t off, uin
                                            intptr_t cnt, bool use_masked, uint64_t* out);
 
 namespace {
-
-struct SfftError {
-  int code;
-  std::string msg;
-};
-
-[[noreturn]] void fail(int code, const std::string& msg) { throw SfftError{code, msg}; }
-
-void ck(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) fail(SFFT2D_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
-}
-
-bool is_pow2(long long v) { return v >= 1 && (v & (v - 1)) == 0; }
-int ilog2(long long v) {
-  int l = 0;
-  while ((1LL << l) < v) ++l;
-  return l;
-}
 
 template <typename T> constexpr int prec_of();
 template <> constexpr int prec_of<float>() { return SFFT2D_FP32; }
@@ -117,7 +100,7 @@ struct sfft2d_ctx {
   size_t ev_used = 0;
 };
 
-namespace {
+namespace sfft {
 
 // Power-of-two capacities: buffers sized by data-dependent counts (candidates,
 // maxima) settle after a few calls instead of reallocating -- a cudaFree /
@@ -158,7 +141,7 @@ void* ws(sfft2d_ctx* c, const char* name, size_t bytes) {
   return e.first;
 }
 
-cudaEvent_t next_event(sfft2d_ctx* c) {
+static cudaEvent_t next_event(sfft2d_ctx* c) {
   if (c->ev_used == c->ev_pool.size()) {
     cudaEvent_t e;
     ck(cudaEventCreate(&e), "cudaEventCreate");
@@ -190,61 +173,22 @@ void post(sfft2d_ctx* c, const char* what, cudaStream_t st, double bytes) {
   c->prof_open = false;
 }
 
-template <typename K>
-void allow_smem(K kernel) {
+void allow_smem_ptr(const void* kernel) {
   static std::mutex mu;
-  static std::map<const void*, bool> done;
+  static std::map<std::pair<int, const void*>, bool> done;
+  int dev = 0;
+  ck(cudaGetDevice(&dev), "cudaGetDevice");
   std::lock_guard<std::mutex> g(mu);
-  const void* key = (const void*)kernel;
+  const auto key = std::make_pair(dev, kernel);
   if (done.count(key)) return;
-  ck(cudaFuncSetAttribute(key, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)kMaxDynSmem),
+  ck(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem),
      "cudaFuncSetAttribute");
   done[key] = true;
 }
 
-template <typename T>
-void allow_all_T() {
-  using C = cplx<T>;
-  allow_smem(k_fft2d_small<T>);
-  allow_smem(k_fft_rows<T, C>);
-  allow_smem(k_fft_rows<T, float2>);
-  allow_smem(k_fft_rows<T, double2>);
-  allow_smem(k_fft_cols<T>);
-  allow_smem(k_fold<float2, T, 1, 2>);
-  allow_smem(k_fold<float2, T, 1, 2, 4>);
-  allow_smem(k_fold<double2, T, 1, 2, 4>);
-  allow_smem(k_fold<float2, T, 8, 1>);
-  allow_smem(k_fold<double2, T, 1, 2>);
-  allow_smem(k_fold<double2, T, 8, 1>);
-  allow_smem(k_fold_reduce_fft_small<T>);
-  allow_smem(k_permute_grid<T>);
-  allow_smem(k_fftr<T, C, true, false>);
-  allow_smem(k_fftr<T, C, true, false, 2>);
-  allow_smem(k_fftr<T, float2, true, false, 2>);
-  allow_smem(k_fftr<T, double2, true, false, 2>);
-  allow_smem(k_fftr<T, float2, true, false>);
-  allow_smem(k_fftr<T, double2, true, false>);
-  allow_smem(k_fftc<T, true, false>);
-  allow_smem(k_fftc<T, false, true>);
-  allow_smem(k_fftc<T, true, true>);
-  allow_smem(k_fftcA<T>);
-  allow_smem(k_fftcB<T, true, false>);
-  allow_smem(k_fftcB<T, false, true>);
-  allow_smem(k_fftcB<T, true, true>);
-  allow_smem(k_fftc1<T, true, false, 2>);
-  allow_smem(k_fftc1<T, false, true, 2>);
-  allow_smem(k_fftc1<T, true, true, 2>);
-  allow_smem(k_fftc1<T, true, false, 1>);
-  allow_smem(k_fftc1<T, false, true, 1>);
-  allow_smem(k_fftc1<T, true, true, 1>);
-  allow_smem(k_lmax_rows<T, false>);
-  allow_smem(k_lmax_rows<T, true>);
-  allow_smem(k_lmax_rows<T, false, true>);
-  allow_smem(k_lmax_rows<T, true, true>);
-  allow_smem(k_lmax_stream<T>);
-  allow_smem(k_small_pass<T>);
-}
+}  // namespace sfft
+
+namespace {
 
 const DevTables& find_tables(sfft2d_ctx* c, int n, double dpass, double dstop) {
   for (auto& t : c->tables)
@@ -339,25 +283,6 @@ unsigned read_u32(sfft2d_ctx* c, const unsigned* dev, cudaStream_t st) {
   return c->pinned[0];
 }
 
-// Launch with programmatic stream serialisation (PDL): the kernel may be
-// scheduled while its predecessor in the stream drains; it waits in pdl_wait()
-// before touching memory.  Launch errors throw.
-template <typename... KArgs, typename... Args>
-void kl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-        Args&&... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  ck(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
-}
-
 // Mapped pinned host buffer for results (grow-only).
 void* host_out(sfft2d_ctx* c, size_t bytes) {
   if (c->host_out_cap < bytes) {
@@ -407,13 +332,6 @@ unsigned wait_published(sfft2d_ctx* c, unsigned seq, cudaStream_t st) {
   }
 }
 
-unsigned grid_for(long long work, int per_block = 256, int cap = kNumSMs * 16) {
-  long long b = (work + per_block - 1) / per_block;
-  if (b < 1) b = 1;
-  if (b > cap) b = cap;
-  return (unsigned)b;
-}
-
 // ------------------------------------------------------------------ pieces
 template <typename Tin>
 __global__ void k_check_finite(const Tin* __restrict__ x, long n, unsigned* flag) {
@@ -444,133 +362,6 @@ __global__ void k_iota_segments(int32_t* out, long seglen, int nseg) {
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
        e += (long)gridDim.x * blockDim.x)
     out[e] = (int32_t)(e % seglen);
-}
-
-// In-place 2D FFT of `ngrids` contiguous B x B grids (csrc/fft.cuh kernels).
-// Segmented |Z| + per-segment peak (small grids / API paths).
-template <typename T>
-void mags_of(sfft2d_ctx* c, const cplx<T>* spec, long seglen, int nseg, T* mags,
-             unsigned long long* peaks, cudaStream_t st) {
-  pre(c, st);
-  kl(k_mags<T>, dim3(grid_for(seglen, 256, kNumSMs * 8 / std::max(1, nseg) + 1), nseg), 256, 0, st, spec, seglen, mags, peaks);
-  post(c, "k_mags", st, (double)seglen * nseg * (sizeof(cplx<T>) + sizeof(T)));
-}
-
-// 2D FFT of `ngrids` contiguous B x B grids held in `grids` (overwritten).
-// want_c: the complex spectrum is written to `out` (may equal `grids`);
-// mags/peaks (optional): |Z| and a per-grid peak key (peaks zeroed by caller).
-template <typename T>
-void fft2d_grids(sfft2d_ctx* c, cplx<T>* grids, int lgB, int ngrids, const cplx<T>* tw, int lgN,
-                 cplx<T>* out, T* mags, unsigned long long* peaks, cudaStream_t st) {
-  using C = cplx<T>;
-  const int B = 1 << lgB;
-  const size_t BB = (size_t)B * B;
-  const double gb = (double)BB * ngrids * sizeof(C);
-  const bool wc = out != nullptr, wm = mags != nullptr;
-  if (BB * sizeof(C) <= (size_t)kSmall2DBytes) {
-    const int threads = B * B / 4 >= 256 ? 256 : (B * B / 4 >= 32 ? B * B / 4 : 32);
-    pre(c, st);
-    kl(k_fft2d_small<T>, ngrids, threads, BB * sizeof(C), st, grids, lgB, tw, lgN);
-    post(c, "k_fft2d_small", st, 2 * gb);
-    if (wc && out != grids)
-      ck(cudaMemcpyAsync(out, grids, BB * ngrids * sizeof(C), cudaMemcpyDeviceToDevice, st), "copy");
-    if (wm) mags_of<T>(c, wc ? out : grids, (long)BB, ngrids, mags, peaks, st);
-    return;
-  }
-  const FftPlan2D pl = plan_fft2d<T>(lgB);
-  if (pl.smem_row > kMaxDynSmem || pl.row_threads > 512)
-    fail(SFFT2D_ERR_UNSUPPORTED, "grid too large for the smem FFT");
-  pre(c, st);
-  if (pl.row_ipt == 2)
-    kl(k_fftr<T, C, true, false, 2>, (unsigned)(ngrids * (B / pl.rows_per_cta)), pl.row_threads, pl.smem_row, st, grids, grids, nullptr, nullptr, lgB, 2 * lgB,
-                                                      tw, lgN, (unsigned*)nullptr);
-  else
-    kl(k_fftr<T, C, true, false>, (unsigned)(ngrids * (B / pl.rows_per_cta)), pl.row_threads, pl.smem_row, st, grids, grids, nullptr, nullptr, lgB, 2 * lgB, tw,
-                                                   lgN, (unsigned*)nullptr);
-  post(c, "k_fftr", st, 2 * gb);
-  const double wbytes = (wc ? gb : 0) + (wm ? (double)BB * ngrids * sizeof(T) : 0);
-  C* final_out = out;
-  // k_fftc1 is safe in place (a CTA reads all of its columns before writing)
-  if (pl.four_step && !pl.col1 && wc && out == grids)
-    out = (C*)ws(c, "fft_tmp", (size_t)BB * ngrids * sizeof(C));
-  auto colB = [&](auto WC_, auto WM_) {
-    constexpr bool WC = decltype(WC_)::value, WM = decltype(WM_)::value;
-    if (pl.col1) {
-      pre(c, st);
-      if (pl.ipt1 == 2)
-        kl(k_fftc1<T, WC, WM, 2>, dim3(B >> pl.lgcc1, ngrids), pl.thr1, pl.smem_1, st, grids, out, mags, peaks, lgB, pl.lgcc1, tw, lgN);
-      else
-        kl(k_fftc1<T, WC, WM, 1>, dim3(B >> pl.lgcc1, ngrids), pl.thr1, pl.smem_1, st, grids, out, mags, peaks, lgB, pl.lgcc1, tw, lgN);
-      post(c, "k_fftc1", st, gb + wbytes);
-    } else if (pl.four_step) {
-      pre(c, st);
-      kl(k_fftcA<T>, dim3(B >> pl.lgccA, 1 << pl.lgL2, ngrids), pl.thrA, pl.smem_A, st, grids, pl.lgL1, pl.lgL2, pl.lgccA, tw, lgN);
-      post(c, "k_fftcA", st, 2 * gb);
-      pre(c, st);
-      kl(k_fftcB<T, WC, WM>, dim3(B >> pl.lgccB, 1 << pl.lgL1, ngrids), pl.thrB, pl.smem_B, st, grids, out, mags, peaks, pl.lgL1, pl.lgL2, pl.lgccB, tw, lgN);
-      post(c, "k_fftcB", st, gb + wbytes);
-    } else {
-      pre(c, st);
-      kl(k_fftc<T, WC, WM>, dim3(B >> pl.lgccB, ngrids), pl.thrB, pl.smem_B, st, grids, out, mags, peaks, lgB, pl.lgccB, tw, lgN);
-      post(c, "k_fftc", st, gb + wbytes);
-    }
-  };
-  if (wc && wm) colB(std::true_type(), std::true_type());
-  else if (wc) colB(std::true_type(), std::false_type());
-  else colB(std::false_type(), std::true_type());
-  if (final_out != out)
-    ck(cudaMemcpyAsync(final_out, out, BB * ngrids * sizeof(C), cudaMemcpyDeviceToDevice, st), "copy");
-}
-
-// Dense forward 2D FFT of the N x N input image: complex x_hat into `out`,
-// optional |x_hat| + peak.  `scratch` holds the row-pass result.
-template <typename T, typename Tin>
-void dense_fft(sfft2d_ctx* c, const Tin* x, cplx<T>* out, T* mags, unsigned long long* peak,
-               int lgN, const cplx<T>* tw, cudaStream_t st, unsigned* nonfinite = nullptr) {
-  using C = cplx<T>;
-  const int N = 1 << lgN;
-  const FftPlan2D pl = plan_fft2d<T>(lgN);
-  if (pl.smem_row > kMaxDynSmem || pl.row_threads > 512)
-    fail(SFFT2D_ERR_UNSUPPORTED, "image side too large for the smem FFT");
-  const double nn = (double)N * N;
-  C* scratch = (C*)ws(c, "fft_scratch", (size_t)N * N * sizeof(C));
-  pre(c, st);
-  if (pl.row_ipt == 2)
-    kl(k_fftr<T, Tin, true, false, 2>, (unsigned)(N / pl.rows_per_cta), pl.row_threads, pl.smem_row, st, x, scratch, nullptr, nullptr, lgN, 2 * lgN, tw, lgN,
-                                           nonfinite);
-  else
-    kl(k_fftr<T, Tin, true, false>, (unsigned)(N / pl.rows_per_cta), pl.row_threads, pl.smem_row, st, x, scratch, nullptr, nullptr, lgN, 2 * lgN, tw, lgN, nonfinite);
-  post(c, "k_fftr_dense", st, nn * (sizeof(Tin) + sizeof(C)));
-  const double wb = nn * sizeof(C) + (mags ? nn * sizeof(T) : 0);
-  if (pl.col1) {
-    pre(c, st);
-    if (mags && pl.ipt1 == 2)
-      kl(k_fftc1<T, true, true, 2>, dim3(N >> pl.lgcc1, 1), pl.thr1, pl.smem_1, st, scratch, out, mags, peak, lgN, pl.lgcc1, tw, lgN);
-    else if (mags)
-      kl(k_fftc1<T, true, true, 1>, dim3(N >> pl.lgcc1, 1), pl.thr1, pl.smem_1, st, scratch, out, mags, peak, lgN, pl.lgcc1, tw, lgN);
-    else if (pl.ipt1 == 2)
-      kl(k_fftc1<T, true, false, 2>, dim3(N >> pl.lgcc1, 1), pl.thr1, pl.smem_1, st, scratch, out, nullptr, nullptr, lgN, pl.lgcc1, tw, lgN);
-    else
-      kl(k_fftc1<T, true, false, 1>, dim3(N >> pl.lgcc1, 1), pl.thr1, pl.smem_1, st, scratch, out, nullptr, nullptr, lgN, pl.lgcc1, tw, lgN);
-    post(c, "k_fftc1", st, nn * sizeof(C) + wb);
-  } else if (pl.four_step) {
-    pre(c, st);
-    kl(k_fftcA<T>, dim3(N >> pl.lgccA, 1 << pl.lgL2, 1), pl.thrA, pl.smem_A, st, scratch, pl.lgL1, pl.lgL2, pl.lgccA, tw, lgN);
-    post(c, "k_fftcA", st, 2 * nn * sizeof(C));
-    pre(c, st);
-    if (mags)
-      kl(k_fftcB<T, true, true>, dim3(N >> pl.lgccB, 1 << pl.lgL1, 1), pl.thrB, pl.smem_B, st, scratch, out, mags, peak, pl.lgL1, pl.lgL2, pl.lgccB, tw, lgN);
-    else
-      kl(k_fftcB<T, true, false>, dim3(N >> pl.lgccB, 1 << pl.lgL1, 1), pl.thrB, pl.smem_B, st, scratch, out, nullptr, nullptr, pl.lgL1, pl.lgL2, pl.lgccB, tw, lgN);
-    post(c, "k_fftcB", st, nn * sizeof(C) + wb);
-  } else {
-    pre(c, st);
-    if (mags)
-      kl(k_fftc<T, true, true>, dim3(N >> pl.lgccB, 1), pl.thrB, pl.smem_B, st, scratch, out, mags, peak, lgN, pl.lgccB, tw, lgN);
-    else
-      kl(k_fftc<T, true, false>, dim3(N >> pl.lgccB, 1), pl.thrB, pl.smem_B, st, scratch, out, nullptr, nullptr, lgN, pl.lgccB, tw, lgN);
-    post(c, "k_fftc", st, nn * sizeof(C) + wb);
-  }
 }
 
 // One fold launch for g <= 8 loops; returns where the result lives:
@@ -621,7 +412,7 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
       kl(k_fold_wide<Tin, T, 2>, grid_w, 256, 0, st, x, space, pp.p[0], lgN, lgB, natural, (C*)y_direct, zero_peak);
     else
       kl(k_fold_wide<Tin, T, 1>, grid_w, 256, 0, st, x, space, pp.p[0], lgN, lgB, natural, (C*)y_direct, zero_peak);
-    post(c, "k_fold", st, by);
+    post(c, "k_fold_wide", st, by);
     return FoldOut{y_direct, 1};
   }
   C* dst = (gm.Z == 1) ? (C*)y_direct : (C*)ws(c, "fold_part", (size_t)gm.Z * g * BB * sizeof(C));
@@ -1464,8 +1255,6 @@ int sfft2d_ctx_create(int device, sfft2d_ctx** out) {
     ck(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep), "cudaMemPoolSetAttribute");
     for (int i = 0; i < 2; ++i)
       ck(cudaEventCreateWithFlags(&c->ev_vote[i], cudaEventDisableTiming), "cudaEventCreate");
-    allow_all_T<float>();
-    allow_all_T<double>();
   });
   if (rc != SFFT2D_OK) {
     fprintf(stderr, "sfft2d_ctx_create: %s\n", c->err.c_str());

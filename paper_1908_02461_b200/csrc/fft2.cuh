@@ -19,6 +19,8 @@
 // (order-independent atomicMax on an order-preserving key) instead of, or in
 // addition to, the complex spectrum: the tuner only needs magnitudes.
 #pragma once
+#include <type_traits>
+#include <utility>
 #include "common.cuh"
 
 namespace sfft {
@@ -189,10 +191,11 @@ __device__ __forceinline__ void stockham_last(const cplx<T>* s, int lgL, int rs,
 // nseq * L): pass 1 (radix 16) gathers its inputs straight from global memory
 // through `ld(seq, u)`, middle passes run in smem, the last pass stores
 // through `st`.  One smem round trip for L <= 256, two for L <= 4096.
-template <typename T, bool COLMAP, int IPT = 1, typename Ld, typename St>
+template <typename T, bool COLMAP, int IPT = 1, int LG = 0, typename Ld, typename St>
 __device__ __forceinline__ void fft_tile(cplx<T>* s, int lgL, int nseq_lg, int rs,
                                          const cplx<T>* __restrict__ tw, int lgN, Ld ld, St st) {
   using C = cplx<T>;
+  if (LG > 0) lgL = LG;   // compile-time length: only the passes it needs are emitted
   const int L = 1 << lgL;
   const int per_lg = lgL - 4;
   const int per = L >> 4;
@@ -234,7 +237,7 @@ __device__ __forceinline__ void fft_tile(cplx<T>* s, int lgL, int nseq_lg, int r
 }
 
 // Row pass: CTA = `rows` rows of length L (blockDim = rows * L / 16).
-template <typename T, typename Tin, bool WC, bool WM, int IPT = 1>
+template <typename T, typename Tin, bool WC, bool WM, int IPT = 1, int LG = 0>
 __global__ void __launch_bounds__(512, (sizeof(T) == 4) ? 2 : 1)
 k_fftr(const Tin* src, cplx<T>* dst, T* __restrict__ mags, unsigned long long* __restrict__ peak,
        int lgL, int grid_lg, const cplx<T>* __restrict__ tw, int lgN,
@@ -261,13 +264,13 @@ k_fftr(const Tin* src, cplx<T>* dst, T* __restrict__ mags, unsigned long long* _
       emit_mag(m, best);
     }
   };
-  fft_tile<T, false, IPT>(s, lgL, rows_lg, pad_row(1 << lgL), tw, lgN, ld, st);
+  fft_tile<T, false, IPT, LG>(s, lgL, rows_lg, pad_row(1 << lgL), tw, lgN, ld, st);
   if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
   if (WM && peak) flush_peak(best, peak + (e0 >> grid_lg));
 }
 
 // Column pass for L <= 512: CTA = `cc` adjacent columns of one grid (W = L).
-template <typename T, bool WC, bool WM>
+template <typename T, bool WC, bool WM, int LG = 0>
 __global__ void __launch_bounds__(512, (sizeof(T) == 4) ? 2 : 1)
 k_fftc(const cplx<T>* src, cplx<T>* dst, T* __restrict__ mags,
        unsigned long long* __restrict__ peak, int lgL, int lgcc, const cplx<T>* __restrict__ tw,
@@ -289,7 +292,7 @@ k_fftc(const cplx<T>* src, cplx<T>* dst, T* __restrict__ mags,
       emit_mag(m, best);
     }
   };
-  fft_tile<T, true>(s, lgL, lgcc, pad_row(1 << lgL), tw, lgN, ld, st);
+  fft_tile<T, true, 1, LG>(s, lgL, lgcc, pad_row(1 << lgL), tw, lgN, ld, st);
   if (WM && peak) flush_peak(best, peak + g);
 }
 
@@ -297,7 +300,7 @@ k_fftc(const cplx<T>* src, cplx<T>* dst, T* __restrict__ mags,
 // (cc * sizeof(C) >= 32 B, one full sector per row segment) held whole in
 // shared memory, IPT radix-16 groups per thread.  Replaces the four-step
 // A + B pair: one read and one write of the grid instead of two each.
-template <typename T, bool WC, bool WM, int IPT>
+template <typename T, bool WC, bool WM, int IPT, int LG = 0>
 __global__ void __launch_bounds__(512, 1)
 k_fftc1(const cplx<T>* src, cplx<T>* dst, T* __restrict__ mags,
         unsigned long long* __restrict__ peak, int lgL, int lgcc, const cplx<T>* __restrict__ tw,
@@ -319,13 +322,13 @@ k_fftc1(const cplx<T>* src, cplx<T>* dst, T* __restrict__ mags,
       emit_mag(m, best);
     }
   };
-  fft_tile<T, true, IPT>(s, lgL, lgcc, pad_row(1 << lgL), tw, lgN, ld, st);
+  fft_tile<T, true, IPT, LG>(s, lgL, lgcc, pad_row(1 << lgL), tw, lgN, ld, st);
   if (WM && peak) flush_peak(best, peak + g);
 }
 
 // Four-step column pass A (in place): length-L1 DFTs over rows n2 + L2*n1, then
 // twiddle by W_L^{n2 k1}; grid = (column tiles, n2, grid index).
-template <typename T>
+template <typename T, int LG1 = 0>
 __global__ void __launch_bounds__(512, (sizeof(T) == 4) ? 2 : 1)
 k_fftcA(cplx<T>* data, int lgL1, int lgL2, int lgcc, const cplx<T>* __restrict__ tw, int lgN) {
   pdl_wait();
@@ -341,11 +344,11 @@ k_fftcA(cplx<T>* data, int lgL1, int lgL2, int lgcc, const cplx<T>* __restrict__
     if (n2 && k1) v = cmul(v, __ldg(tw + ((n2 * k1) << tsh)));
     data[gbase + ((size_t)(n2 + (k1 << lgL2)) << lgL) + c] = v;
   };
-  fft_tile<T, true>(s, lgL1, lgcc, pad_row(1 << lgL1), tw, lgN, ld, st);
+  fft_tile<T, true, 1, LG1>(s, lgL1, lgcc, pad_row(1 << lgL1), tw, lgN, ld, st);
 }
 
 // Four-step column pass B: length-L2 DFTs over rows L2*k1 + n2 -> row k1 + L1*k2.
-template <typename T, bool WC, bool WM>
+template <typename T, bool WC, bool WM, int LG2 = 0>
 __global__ void __launch_bounds__(512, (sizeof(T) == 4) ? 2 : 1)
 k_fftcB(const cplx<T>* __restrict__ src, cplx<T>* __restrict__ dst, T* __restrict__ mags,
         unsigned long long* __restrict__ peak, int lgL1, int lgL2, int lgcc,
@@ -369,8 +372,27 @@ k_fftcB(const cplx<T>* __restrict__ src, cplx<T>* __restrict__ dst, T* __restric
       emit_mag(m, best);
     }
   };
-  fft_tile<T, true>(s, lgL2, lgcc, pad_row(1 << lgL2), tw, lgN, ld, st);
+  fft_tile<T, true, 1, LG2>(s, lgL2, lgcc, pad_row(1 << lgL2), tw, lgN, ld, st);
   if (WM && peak) flush_peak(best, peak + g);
+}
+
+// ---------------------------------------------------------------- dispatch
+// Calls f(std::integral_constant<int, lg>) for LO <= lg <= HI, else
+// f(std::integral_constant<int, 0>) (runtime length): a compile-time length
+// emits only the Stockham passes that length needs, which keeps the kernel
+// small enough for the instruction cache (measured: k_fftcB at B = 2048
+// 25.3 -> 17.8 us).
+template <int LO, int HI, typename F>
+inline void with_lg(int lg, F&& f) {
+  if constexpr (LO <= HI) {
+    if (lg == LO) {
+      f(std::integral_constant<int, LO>{});
+      return;
+    }
+    with_lg<LO + 1, HI>(lg, std::forward<F>(f));
+  } else {
+    f(std::integral_constant<int, 0>{});
+  }
 }
 
 // ---------------------------------------------------------------- geometry

@@ -15,6 +15,7 @@
 // L location loops' grids) are processed by one launch (gridDim.y = segment).
 #pragma once
 #include "common.cuh"
+#include "mags.cuh"
 
 namespace sfft {
 
@@ -24,31 +25,6 @@ constexpr int kCmpElems = kCmpWords * 32;        // 8192 elements per block
 
 __host__ __device__ inline long words_for(long n) { return (n + 31) / 32; }
 __host__ __device__ inline int blocks_for(long n) { return (int)((words_for(n) + kCmpWords - 1) / kCmpWords); }
-
-// ---------------------------------------------------------------- magnitudes
-template <typename T>
-__global__ void k_mags(const cplx<T>* __restrict__ spec, long seglen, T* __restrict__ mags,
-                       unsigned long long* __restrict__ peak) {
-  pdl_wait();
-  const int seg = blockIdx.y;
-  const cplx<T>* s = spec + (size_t)seg * seglen;
-  T* m = mags + (size_t)seg * seglen;
-  unsigned long long best = 0ull;
-  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < seglen;
-       e += (long)gridDim.x * blockDim.x) {
-    const T v = cabs_(s[e]);
-    m[e] = v;
-    const unsigned long long k = fkey(v);
-    best = k > best ? k : best;
-  }
-  if (peak) {
-    for (int o = 16; o > 0; o >>= 1) {
-      unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
-      best = t > best ? t : best;
-    }
-    if ((threadIdx.x & 31) == 0) atomicMax(peak + seg, best);
-  }
-}
 
 // ---------------------------------------------------------------- local maxima
 template <typename T>

@@ -40,6 +40,15 @@ span = t1 - t0
 print(f"{len(ks) / reps:.0f} kernels/transform, span {span / reps:.1f} us/transform, "
       f"busy {busy / reps:.1f} us ({busy / span * 100:.1f}%), idle {(span - busy) / reps:.1f} us, "
       f"memcpy/memset ops {len(mem) / reps:.0f}/transform")
+import collections  # noqa: E402
+agg = collections.defaultdict(lambda: [0, 0.0])
+for e in ks:
+    nm = e["name"].split("(")[0].split("<")[0].replace("void ", "").replace("sfft::", "")
+    agg[nm][0] += 1
+    agg[nm][1] += e["dur"]
+print("per-kernel time per transform (warm pipeline, CUPTI):")
+for nm, (cnt, dur) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+    print(f"  {nm:24s} {cnt / reps:5.1f} launches {dur / reps:8.1f} us  ({dur / busy * 100:4.1f}% of busy)")
 gaps.sort(reverse=True)
 big = [g for g in gaps if g[0] > 2.0]
 print(f"gaps > 2 us: {len(big) / reps:.1f}/transform totalling {sum(g for g, _ in big) / reps:.1f} us")
