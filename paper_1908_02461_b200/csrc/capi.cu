@@ -415,6 +415,29 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
     post(c, "k_fold_wide", st, by);
     return FoldOut{y_direct, 1};
   }
+  const int seg_cols = kRingSegBytes / (int)sizeof(Tin);
+  if (g == 1 && B < 512 && gm.TW == 512 && (1 << lgN) >= seg_cols) {
+    // TMA ring fold, 3 x 32 KB slots (2 CTAs per SM), row aliases chunked so
+    // that ~2 CTAs per SM stream rows (measured best of slots 3-6 x 1-4 CTAs
+    // per SM on c3: B = 16 15.3 -> 10.9 us, B = 256 31.6 -> 26.3 us)
+    const int nslot = 3;
+    const long target = 2L * kNumSMs;
+    FoldGeom gr = gm;
+    const int aliases = (1 << lgN) >> lgB;
+    int Z = (int)std::max(1L, std::min<long>(aliases, (target + B - 1) / B));
+    int rpc = (aliases + Z - 1) / Z;
+    if (rpc > kFoldMaxRows) rpc = kFoldMaxRows;
+    gr.rpc = rpc;
+    gr.Z = (aliases + rpc - 1) / rpc;
+    gr.ktiles = 1;
+    C* dstr = (gr.Z == 1) ? (C*)y_direct : (C*)ws(c, "fold_part", (size_t)gr.Z * BB * sizeof(C));
+    const size_t dynr = (size_t)nslot * kRingSegBytes + 512 * sizeof(C);
+    pre(c, st);
+    kl(k_fold_ring<Tin, T>, dim3(1, B, gr.Z), 256, dynr, st, x, space, pp.p[0], gr, natural, nslot,
+       dstr, zero_peak);
+    post(c, "k_fold_ring", st, sup * sup * sizeof(Tin) + (double)gr.Z * BB * sizeof(C));
+    return FoldOut{dstr, gr.Z};
+  }
   C* dst = (gm.Z == 1) ? (C*)y_direct : (C*)ws(c, "fold_part", (size_t)gm.Z * g * BB * sizeof(C));
   const double fold_bytes = sup * sup * sizeof(Tin) + (double)gm.Z * g * BB * sizeof(C);
   pre(c, st);

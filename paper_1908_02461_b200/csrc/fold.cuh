@@ -255,6 +255,151 @@ k_fold(const Tin* __restrict__ x, const T* __restrict__ space, PermPack pp, int 
   }
 }
 
+// Ring-buffered single-loop fold for B < TW (= 512 columns per tile, 256
+// threads x 2 columns): the same sums, geometry and outputs as
+// k_fold<Tin, T, 1, 2, *> (CTA (rho, chunk z), rows rho + j B of the chunk
+// with nonzero window weight), but the rows are moved by the TMA engine:
+// thread 0 streams each row's 32 KB segment into one of `nslot`
+// shared-memory slots with cp.async.bulk (completion on the slot's
+// mbarrier), so up to nslot rows per CTA are in flight without holding
+// registers; every thread then folds its 2 columns per 512-column block from
+// shared memory.  Column weights stay in registers for the whole CTA.
+constexpr int kRingSegBytes = 32 * 1024;
+
+// two adjacent complex inputs from shared memory, converted to cplx<T>
+template <typename T>
+__device__ __forceinline__ void lds_pair(const float2* p, cplx<T>* v) {
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  v[0] = mk<T>((T)a.x, (T)a.y);
+  v[1] = mk<T>((T)a.z, (T)a.w);
+}
+template <typename T>
+__device__ __forceinline__ void lds_pair(const double2* p, cplx<T>* v) {
+  const double2 a = p[0], b = p[1];
+  v[0] = mk<T>((T)a.x, (T)a.y);
+  v[1] = mk<T>((T)b.x, (T)b.y);
+}
+
+template <typename Tin, typename T>
+__global__ void __launch_bounds__(256, 1)
+k_fold_ring(const Tin* __restrict__ x, const T* __restrict__ space, Perm p, FoldGeom gm,
+            bool natural, int nslot, cplx<T>* __restrict__ dst,
+            unsigned long long* __restrict__ zero_peak = nullptr) {
+  pdl_wait();
+  using C = cplx<T>;
+  constexpr int SEGC = kRingSegBytes / (int)sizeof(Tin);   // columns per row segment
+  constexpr int NB = SEGC / 512;                            // 512-column blocks per segment
+  if (zero_peak && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) *zero_peak = 0ull;
+  __shared__ T s_w[kFoldMaxRows];
+  __shared__ int s_rows[kFoldMaxRows];
+  __shared__ int s_nnz;
+  __shared__ __align__(8) unsigned long long s_bar[8];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Tin* ring = reinterpret_cast<Tin*>(smem_raw);
+  C* red = reinterpret_cast<C*>(smem_raw + (size_t)nslot * kRingSegBytes);
+
+  const int N = 1 << gm.lgN, B = 1 << gm.lgB;
+  const unsigned maskN = (unsigned)N - 1u, maskB = (unsigned)B - 1u;
+  const int rho = blockIdx.y, z = blockIdx.z;
+  const int aliases = N >> gm.lgB;
+  const int j0 = z * gm.rpc;
+  const int cnt = min(gm.rpc, aliases - j0);
+  const int tid = threadIdx.x;
+
+  for (int jj = tid; jj < cnt; jj += blockDim.x) {
+    const unsigned r = (unsigned)(rho + (j0 + jj) * B);
+    s_w[jj] = __ldg(space + ((p.s1i * (r - p.t1)) & maskN));
+  }
+  if (tid < nslot) mbar_init(&s_bar[tid], 1);
+  mbar_fence_init();
+  __syncthreads();
+  if (tid < 32) {
+    int base = 0;
+    for (int c0 = 0; c0 < cnt; c0 += 32) {
+      const int jj = c0 + tid;
+      const bool nz = jj < cnt && s_w[jj] != (T)0;
+      const unsigned bal = __ballot_sync(0xffffffffu, nz);
+      if (nz) s_rows[base + __popc(bal & ((1u << tid) - 1u))] = jj;
+      base += __popc(bal);
+    }
+    if (tid == 0) s_nnz = base;
+  }
+  __syncthreads();
+  const int nnz = s_nnz;
+  const int cp = tid * 2;
+  C acc[2] = {mk<T>(0, 0), mk<T>(0, 0)};
+  unsigned use = 0;                        // completed uses of the ring (phase tracking)
+  for (int cg = 0; cg < N / SEGC; ++cg) {
+    T wc[NB][2];
+    bool any = false;
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const unsigned c = (unsigned)(cg * SEGC + b * 512 + cp + q);
+        wc[b][q] = __ldg(space + ((p.s2i * (c - p.t2)) & maskN));
+        any |= wc[b][q] != (T)0;
+      }
+    if (!__syncthreads_or(any)) continue;   // no column of this segment carries weight
+    C u[NB][2];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) u[b][0] = u[b][1] = mk<T>(0, 0);
+    auto issue = [&](int i) {
+      const int slot = (int)((use + i) % nslot);
+      const size_t r = (size_t)(rho + (j0 + s_rows[i]) * B);
+      mbar_expect_tx(&s_bar[slot], kRingSegBytes);
+      bulk_g2s(ring + (size_t)slot * SEGC, x + (r << gm.lgN) + (size_t)cg * SEGC, kRingSegBytes,
+               &s_bar[slot]);
+    };
+    if (tid == 0)
+      for (int i = 0; i < min(nslot, nnz); ++i) issue(i);
+    for (int i = 0; i < nnz; ++i) {
+      const unsigned k = use + i;
+      const int slot = (int)(k % nslot);
+      mbar_wait(&s_bar[slot], (k / nslot) & 1u);
+      const T wr = s_w[s_rows[i]];
+      const Tin* row = ring + (size_t)slot * SEGC;
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        C v[2];
+        lds_pair<T>(row + b * 512 + cp, v);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          u[b][q].x = fma(wr, v[q].x, u[b][q].x);
+          u[b][q].y = fma(wr, v[q].y, u[b][q].y);
+        }
+      }
+      __syncthreads();                       // every thread is done with this slot
+      if (tid == 0 && i + nslot < nnz) issue(i + nslot);
+    }
+    use += (unsigned)nnz;
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        acc[q].x = fma(wc[b][q], u[b][q].x, acc[q].x);
+        acc[q].y = fma(wc[b][q], u[b][q].y, acc[q].y);
+      }
+  }
+  // ---- column aliases within the 512-column tile -> B bucket columns
+  red[cp] = acc[0];
+  red[cp + 1] = acc[1];
+  __syncthreads();
+  const size_t BB = (size_t)B * B;
+  const int reps = 512 / B;
+  for (int kap = tid; kap < B; kap += blockDim.x) {
+    C s = mk<T>(0, 0);
+    for (int a = 0; a < reps; ++a) s = cadd(s, red[kap + a * B]);
+    if (gm.Z == 1) {
+      const unsigned ra = natural ? (unsigned)rho : (p.s1i * ((unsigned)rho - p.t1)) & maskB;
+      const unsigned cb = natural ? (unsigned)kap : (p.s2i * ((unsigned)kap - p.t2)) & maskB;
+      dst[(size_t)ra * B + cb] = s;
+    } else {
+      dst[(size_t)z * BB + (size_t)rho * B + kap] = s;
+    }
+  }
+}
+
 // Deterministic sum of Z partials with 8 independent accumulators (keeps 8
 // loads in flight; the combination order is fixed, so results are
 // reproducible bit for bit).
