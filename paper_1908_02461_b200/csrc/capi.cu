@@ -569,7 +569,8 @@ unsigned lmax_tuner(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long l
   const size_t wb = 16 * kWarpBuf * sizeof(int32_t);
   if (B >= kLmaxStreamMinB && 4 * row + wb <= kMaxDynSmem) {
     // streaming bands: ~2 CTAs per SM, a ring of row buffers per CTA
-    const int nslot = (int)std::max<size_t>(4, std::min<size_t>(8, (96 * 1024 - wb) / row));
+    int nslot = (int)std::max<size_t>(4, std::min<size_t>(8, (96 * 1024 - wb) / row));
+    if (nslot * row + wb > kMaxDynSmem) nslot = (int)((kMaxDynSmem - wb) / row);
     const int band = (B + 2 * kNumSMs - 1) / (2 * kNumSMs);
     const int thr = 512;
     const int grid = (B + band - 1) / band;

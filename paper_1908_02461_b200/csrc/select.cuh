@@ -251,7 +251,8 @@ k_lmax_stream(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, unsign
               int nslot, const unsigned long long* __restrict__ peak, double floor_rel,
               int32_t* __restrict__ list, unsigned* __restrict__ count, Publish pub) {
   pdl_wait();
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) unsigned long long s_bar[8];
   T* ring = reinterpret_cast<T*>(smem_raw);
   const int B = 1 << lgB;
   const unsigned mask = (unsigned)B - 1u;
@@ -260,22 +261,20 @@ k_lmax_stream(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, unsign
   const int r0 = blockIdx.x * band;
   const int nrow = min(band, B - r0);
   const int nload = nrow + 2;                  // view rows r0-1 .. r0+nrow
-  constexpr int V = 16 / sizeof(T);
-  const int chunks = B / V;
-  int next_load = 0, next_slot = 0;            // ring position of the next issue
-  auto issue = [&]() {
-    if (next_load < nload) {
-      const unsigned r = (unsigned)(r0 - 1 + next_load) & mask;
-      const unsigned sr = (s1 * r) & mask;
-      T* dst = ring + ((size_t)next_slot << lgB);
-      const T* src = M + ((size_t)sr << lgB);
-      for (int q = threadIdx.x; q < chunks; q += blockDim.x) cp_async16(dst + q * V, src + q * V);
-    }
-    cp_async_commit();
-    ++next_load;
-    next_slot = next_slot + 1 == nslot ? 0 : next_slot + 1;
+  const unsigned row_bytes = (unsigned)(sizeof(T) << lgB);
+  // rows arrive by TMA bulk copies issued by thread 0, one mbarrier per slot
+  auto issue = [&](int t) {                    // load t = view row r0 - 1 + t
+    const int slot = t % nslot;
+    const unsigned r = (unsigned)(r0 - 1 + t) & mask;
+    mbar_expect_tx(&s_bar[slot], row_bytes);
+    bulk_g2s(ring + ((size_t)slot << lgB), M + ((size_t)((s1 * r) & mask) << lgB), row_bytes,
+             &s_bar[slot]);
   };
-  for (int t = 0; t < nslot - 1; ++t) issue();
+  if (threadIdx.x < nslot) mbar_init(&s_bar[threadIdx.x], 1);
+  mbar_fence_init();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int t = 0; t < min(nslot, nload); ++t) issue(t);
   // floor test in T: v >= fl (float64, tuner.py:111) <=> v >= fl rounded up
   // to T; a zero peak (no live bins) becomes an unreachable threshold
   const double pk = fkey_inv(*peak);
@@ -292,12 +291,20 @@ k_lmax_stream(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, unsign
     __syncwarp();
     nbuf = 0;
   };
+  // slot of a load = load index mod nslot, tracked incrementally (no integer
+  // division per row); one phase bit per slot
+  unsigned phase = 0;
+  auto wait_slot = [&](int slot) {
+    mbar_wait(&s_bar[slot], (phase >> slot) & 1u);
+    phase ^= 1u << slot;
+  };
+  auto next = [&](int slot) { return slot + 1 == nslot ? 0 : slot + 1; };
   const int groups = B >> 7;                   // 128 natural columns per warp step
-  int su = 0, sm = 1, sd = 2;                  // ring slots of view rows s-1, s, s+1
+  int su = 0, sm = next(0), sd = next(sm);     // slots of loads s, s+1, s+2
+  wait_slot(su);
+  wait_slot(sm);
   for (int s = 0; s < nrow; ++s) {
-    cp_async_wait_upto(nslot - 4);             // loads s, s+1, s+2 have landed
-    __syncthreads();                           // ... for every thread; slot of load s-1 is free
-    issue();
+    wait_slot(sd);                             // loads s and s+1 were waited for earlier
     const T* up = ring + ((size_t)su << lgB);
     const T* md = ring + ((size_t)sm << lgB);
     const T* dn = ring + ((size_t)sd << lgB);
@@ -326,13 +333,14 @@ k_lmax_stream(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, unsign
         nbuf += n;
       }
     }
+    __syncthreads();                           // every thread is done with load s
+    if (threadIdx.x == 0 && s + nslot < nload) issue(s + nslot);
     su = sm;
     sm = sd;
-    sd = sd + 1 == nslot ? 0 : sd + 1;
+    sd = next(sd);
   }
   __syncwarp();
   flush();
-  cp_async_wait_upto(0);
   if (pub.slot) {
     __syncthreads();
     if (threadIdx.x == 0) publish_count(count, pub.done, pub.target, pub.slot, pub.seq);
