@@ -562,7 +562,9 @@ constexpr int kLmaxStreamMinB = 512;
 template <typename T>
 unsigned lmax_tuner(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long long* peak,
                     double floor_rel, int32_t* list, unsigned* count, cudaStream_t st, bool perm,
-                    unsigned s1, unsigned s2, unsigned s2inv) {
+                    unsigned s1, unsigned s2, unsigned s2inv, int32_t* cand = nullptr,
+                    unsigned* cand_count = nullptr, bool* emitted = nullptr) {
+  if (emitted) *emitted = false;
   const int B = 1 << lgB;
   const double by = (double)B * B * sizeof(T);
   const size_t row = (size_t)B * sizeof(T);
@@ -578,7 +580,8 @@ unsigned lmax_tuner(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long l
     const Publish pub = make_publish(c, (unsigned)grid);
     pre(c, st);
     kl(k_lmax_stream<T>, grid, thr, sm, st, mags, lgB, perm ? s1 : 1u, perm ? s2 : 1u,
-       perm ? s2inv : 1u, band, nslot, peak, floor_rel, list, count, pub);
+       perm ? s2inv : 1u, band, nslot, peak, floor_rel, list, count, pub, cand, cand_count);
+    if (emitted) *emitted = cand != nullptr;
     post(c, "k_lmax_stream", st, by);
     return pub.seq;
   }
@@ -864,6 +867,13 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     vote_pending[slot & 1] = true;
   };
 
+  // B = N views after the first one test only the above-floor bins of |x_hat|
+  // that the first B = N pass listed (while they are few)
+  int32_t* cand = nullptr;
+  unsigned* cand_cnt = nullptr;
+  bool cand_pending = false, cand_ready = false;
+  long long cand_n = 0;
+
   auto run_pass = [&](int bb) -> long long {
     const int pi = pidx++;
     const Perm p = ps.get(pi, st);
@@ -879,7 +889,25 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     if (bb == n) {
       // B = N: |Z_p[k1, k2]| = |x_hat[s1i k1, s2i k2]| — one dense FFT serves every pass
       ensure_xhat(true);
-      seq = lmax_tuner<T>(c, M, lgb, peakM, cf.mag_floor, ml, cnt, st, true, p.s1i, p.s2i, p.s2);
+      if (cand_ready && cand_n <= nkeys / 32) {
+        const unsigned grid = grid_for(std::max<long long>(cand_n, 1), 256, kNumSMs * 8);
+        const Publish pub = make_publish(c, grid);
+        seq = pub.seq;
+        pre(c, st);
+        kl(k_lmax_cand<T>, grid, 256, 0, st, (const T*)M, lgb, p.s1i, p.s2i, p.s1, p.s2,
+           (const int32_t*)cand, (const unsigned*)cand_cnt, ml, cnt, pub);
+        post(c, "k_lmax_cand", st, (double)cand_n * 9 * sizeof(T));
+      } else if (!cand_ready) {
+        cand = (int32_t*)ws(c, "cand", (size_t)nkeys * 4);
+        cand_cnt = (unsigned*)ws(c, "cand_cnt", 16);
+        ck(cudaMemsetAsync(cand_cnt, 0, 16, st), "memset");
+        bool emitted = false;
+        seq = lmax_tuner<T>(c, M, lgb, peakM, cf.mag_floor, ml, cnt, st, true, p.s1i, p.s2i, p.s2,
+                            cand, cand_cnt, &emitted);
+        cand_pending = emitted;
+      } else {
+        seq = lmax_tuner<T>(c, M, lgb, peakM, cf.mag_floor, ml, cnt, st, true, p.s1i, p.s2i, p.s2);
+      }
     } else if (BB * sizeof(C) <= (size_t)kSmall2DBytes) {
       C* y = (C*)ws(c, "fold_y", BB * sizeof(C));
       const FoldOut fo = fold_launch<T, Tin>(c, x, lgN, lgb, tb, &p, 1, y, st);
@@ -902,6 +930,11 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     }
     vote_list(p, lgb, budget, slot);
     const long long count = wait_published(c, seq, st);
+    if (cand_pending) {   // the candidate count rides along with the maxima count
+      cand_n = ((volatile unsigned*)c->mapped_h)[2];
+      cand_pending = false;
+      cand_ready = true;
+    }
     last_valid = true;
     last_b = bb;
     last_pi = pi;

@@ -121,12 +121,14 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 // writes slot[1] = count, then slot[0] = seq (system-scope fences), so the
 // host can spin on seq without a stream synchronisation.
 __device__ __forceinline__ void publish_count(unsigned* count, unsigned* done, unsigned target,
-                                              volatile unsigned* slot, unsigned seq) {
+                                              volatile unsigned* slot, unsigned seq,
+                                              unsigned* count2 = nullptr) {
   __threadfence();
   const unsigned t = atomicAdd(done, 1u);
   if (t + 1u == target) {
     __threadfence();
     const unsigned v = atomicAdd(count, 0u);
+    if (count2) slot[2] = atomicAdd(count2, 0u);   // optional second count (same publication)
     slot[1] = v;
     __threadfence_system();
     slot[0] = seq;

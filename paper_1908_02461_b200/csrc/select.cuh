@@ -249,7 +249,8 @@ template <typename T>
 __global__ void __launch_bounds__(512)
 k_lmax_stream(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, unsigned s2i, int band,
               int nslot, const unsigned long long* __restrict__ peak, double floor_rel,
-              int32_t* __restrict__ list, unsigned* __restrict__ count, Publish pub) {
+              int32_t* __restrict__ list, unsigned* __restrict__ count, Publish pub,
+              int32_t* __restrict__ cand = nullptr, unsigned* __restrict__ cand_count = nullptr) {
   pdl_wait();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) unsigned long long s_bar[8];
@@ -320,6 +321,16 @@ k_lmax_stream(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, unsign
         const unsigned C = C0 + j;
         const T v = m[j];
         bool f = v >= flT;
+        if (cand) {   // every above-floor bin, natural index (later views test only these)
+          const unsigned cb = __ballot_sync(0xffffffffu, f);
+          if (cb) {
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(cand_count, (unsigned)__popc(cb));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (f) cand[base + __popc(cb & ((1u << lane) - 1u))] =
+                (int32_t)((((s1 * (unsigned)(r0 + s)) & mask) << lgB) | C);
+          }
+        }
         if (f) {
           const unsigned Cl = (C - s2) & mask, Cr = (C + s2) & mask;
           f = (v > up[Cl]) & (v > up[C]) & (v > up[Cr]) & (v > md[Cl]) & (v > md[Cr]) &
@@ -341,6 +352,51 @@ k_lmax_stream(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, unsign
   }
   __syncwarp();
   flush();
+  if (pub.slot) {
+    __syncthreads();
+    if (threadIdx.x == 0) publish_count(count, pub.done, pub.target, pub.slot, pub.seq, cand_count);
+  }
+}
+
+// Local maxima of a permuted view of |x_hat| at B = N tested only at the
+// above-floor bins `cand` (natural indices R*N + C, from the first B = N
+// pass): view (r, c) = (s1i^-1 R, s2i^-1 C) has its view neighbours at the
+// natural bins (R +- s1, C +- s2) (s1, s2 = the view multipliers).  Bins below
+// the floor can never be counted, so the count equals k_lmax_stream's.
+template <typename T>
+__global__ void k_lmax_cand(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2,
+                            unsigned s1inv, unsigned s2inv, const int32_t* __restrict__ cand,
+                            const unsigned* __restrict__ cand_count,
+                            int32_t* __restrict__ list, unsigned* __restrict__ count, Publish pub) {
+  pdl_wait();
+  const unsigned mask = (1u << lgB) - 1u;
+  const unsigned n = *cand_count;
+  const int lane = threadIdx.x & 31;
+  for (unsigned e0 = blockIdx.x * blockDim.x; e0 < n; e0 += gridDim.x * blockDim.x) {
+    const unsigned e = e0 + threadIdx.x;
+    bool f = false;
+    unsigned key = 0;
+    if (e < n) {
+      const unsigned q = (unsigned)cand[e];
+      const unsigned R = q >> lgB, C = q & mask;
+      const unsigned Ru = (R - s1) & mask, Rd = (R + s1) & mask;
+      const unsigned Cl = (C - s2) & mask, Cr = (C + s2) & mask;
+      const T v = M[q];
+      const T* up = M + ((size_t)Ru << lgB);
+      const T* md = M + ((size_t)R << lgB);
+      const T* dn = M + ((size_t)Rd << lgB);
+      f = (v > up[Cl]) & (v > up[C]) & (v > up[Cr]) & (v > md[Cl]) & (v > md[Cr]) &
+          (v > dn[Cl]) & (v > dn[C]) & (v > dn[Cr]);
+      key = (((s1inv * R) & mask) << lgB) | ((s2inv * C) & mask);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (bal) {
+      unsigned base = 0;
+      if (lane == 0) base = atomicAdd(count, (unsigned)__popc(bal));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (f) list[base + __popc(bal & ((1u << lane) - 1u))] = (int32_t)key;
+    }
+  }
   if (pub.slot) {
     __syncthreads();
     if (threadIdx.x == 0) publish_count(count, pub.done, pub.target, pub.slot, pub.seq);
