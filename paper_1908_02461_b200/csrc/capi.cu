@@ -669,7 +669,8 @@ template <typename T, typename Tin>
 void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTables& tb,
                          const Perm* hp, const Perm* dp, int L, const int32_t* keys, unsigned m,
                          const unsigned* m_dev, long long k, double gain_floor, double prune_rel,
-                         bool dense, const cplx<T>* xhat, cudaStream_t st, sfft2d_result* res) {
+                         bool dense, const cplx<T>* xhat, cudaStream_t st, sfft2d_result* res,
+                         const cplx<T>* dscratch = nullptr) {
   using C = cplx<T>;
   const int P = prec_of<T>();
   C* med = (C*)ws(c, "med", (size_t)m * sizeof(C));
@@ -684,9 +685,17 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
     // gain = freq[0]^2 = 1 for the all-pass window (hashing.py:228-246)
     const bool usable_all = 1.0 >= gain_floor;
     pre(c, st);
-    kl(k_estimate_dense<T>, grid_for(m), 256, 0, st, xhat, keys, m_dev, usable_all, med, mags,
-                                                      alive, peak);
-    post(c, "k_estimate_dense", st, 0);
+    if (dscratch) {   // x_hat never stored: L2-point DFTs of the four-step scratch
+      int lgL1 = 0, lgL2 = 0;
+      dense_split(lgN, P, &lgL1, &lgL2);
+      kl(k_estimate_dense_fs<T>, grid_for((long long)m * 32, 256), 256, 0, st, dscratch, lgN, lgL1,
+         lgL2, (const C*)tb.tw[P], keys, m_dev, usable_all, med, mags, alive, peak);
+      post(c, "k_estimate_dense_fs", st, (double)m * (1 << lgL2) * sizeof(C));
+    } else {
+      kl(k_estimate_dense<T>, grid_for(m), 256, 0, st, xhat, keys, m_dev, usable_all, med, mags,
+         alive, peak);
+      post(c, "k_estimate_dense", st, 0);
+    }
     n_alive = usable_all ? (long long)m : 0;
   } else {
     if (L > kMaxLoops) fail(SFFT2D_ERR_UNSUPPORTED, "more than 64 estimation loops");
@@ -824,7 +833,25 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   int last_b = 0, last_pi = 0;
   long long last_count = 0;
 
+  // sides >= 2048: the dense FFT stops after four-step pass A (x_hat is never
+  // stored), pass B writes |x_hat| only when a B = N tuner pass needs it
+  const bool factored = dense_factored(lgN, prec_of<T>());
+  C* dscratch = nullptr;
   auto ensure_xhat = [&](bool need_mags) {
+    if (factored) {
+      const C* tw = (const C*)tb.tw[prec_of<T>()];
+      if (!dscratch) {
+        dscratch = dense_fft_front<T, Tin>(c, x, lgN, tw, st, finite);   // + NaN check
+        finite_scanned = true;
+      }
+      if (need_mags && !M) {
+        M = (T*)ws(c, "xmag", (size_t)nkeys * sizeof(T));
+        peakM = (unsigned long long*)ws(c, "xpeak", 16);
+        ck(cudaMemsetAsync(peakM, 0, 16, st), "memset");
+        dense_fft_mags<T>(c, M, peakM, lgN, tw, st);
+      }
+      return;
+    }
     if (!xhat_ready) {
       xhat = (C*)ws(c, "xhat", (size_t)nkeys * sizeof(C));
       if (need_mags) {
@@ -1101,7 +1128,8 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   const bool dense = (best == n);
   if (dense) ensure_xhat(false);
   estimate_and_select<T, Tin>(c, x, lgN, ilog2(best), tb, ps.hp.data() + pidx, dp + pidx, L, keys, m,
-                              kt, k, cf.gain_floor, cf.prune_rel, dense, xhat, st, res);
+                              kt, k, cf.gain_floor, cf.prune_rel, dense, xhat, st, res,
+                              dense ? dscratch : nullptr);
   pidx += L;
   S->perms_used = pidx;
   res->perms_used = pidx;

@@ -85,6 +85,56 @@ __global__ void k_estimate_dense(const cplx<T>* __restrict__ xhat, const int32_t
   if ((threadIdx.x & 31) == 0) atomicMax(peak, best);
 }
 
+// Same as k_estimate_dense, with x_hat[i, j] evaluated from the four-step
+// factorisation instead of read from a stored spectrum: after the row pass and
+// four-step pass A (twiddles applied), `A` row k1*L2 + n2 of column j holds
+// the inputs of the length-L2 DFT that pass B would turn into rows
+// k1 + L1*k2, so x_hat[k1 + L1 k2, j] = sum_n2 A[k1 L2 + n2, j] W_L2^(n2 k2)
+// (W_L2^e = tw[e * N / L2]).  One warp per candidate, lanes split the n2 sum.
+template <typename T>
+__global__ void k_estimate_dense_fs(const cplx<T>* __restrict__ A, int lgN, int lgL1, int lgL2,
+                                    const cplx<T>* __restrict__ tw,
+                                    const int32_t* __restrict__ keys,
+                                    const unsigned* __restrict__ m_dev, bool usable_all,
+                                    cplx<T>* __restrict__ med, T* __restrict__ mags,
+                                    uint8_t* __restrict__ alive,
+                                    unsigned long long* __restrict__ peak) {
+  pdl_wait();
+  using C = cplx<T>;
+  const long m = *m_dev;
+  const int lane = threadIdx.x & 31;
+  const long warps = (long)gridDim.x * (blockDim.x >> 5);
+  const unsigned maskN = (1u << lgN) - 1u;
+  const int L2 = 1 << lgL2;
+  const int tsh = lgN - lgL2;
+  unsigned long long best = 0ull;
+  for (long q = blockIdx.x * (long)(blockDim.x >> 5) + (threadIdx.x >> 5); q < m; q += warps) {
+    const unsigned key = (unsigned)keys[q];
+    const unsigned i = key >> lgN, j = key & maskN;
+    const unsigned k1 = i & ((1u << lgL1) - 1u), k2 = i >> lgL1;
+    C s = mk<T>(0, 0);
+    for (int n2 = lane; n2 < L2; n2 += 32) {
+      const C a = A[((size_t)((k1 << lgL2) + n2) << lgN) + j];
+      s = cadd(s, cmul(a, tw[((n2 * k2) & (L2 - 1)) << tsh]));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      s.x += __shfl_xor_sync(0xffffffffu, s.x, o);
+      s.y += __shfl_xor_sync(0xffffffffu, s.y, o);
+    }
+    if (lane == 0) {
+      med[q] = s;
+      alive[q] = usable_all ? 1 : 0;
+      const T a = usable_all ? cabs_(s) : (T)-1;
+      mags[q] = a;
+      if (usable_all) {
+        const unsigned long long k = fkey(a);
+        best = k > best ? k : best;
+      }
+    }
+  }
+  if (lane == 0 && best) atomicMax(peak, best);
+}
+
 template <typename T>
 __device__ __forceinline__ void isort(T* a, int n) {
   for (int i = 1; i < n; ++i) {

@@ -8,4 +8,21 @@ template void fft2d_grids<float>(sfft2d_ctx*, cplx<float>*, int, int, const cplx
                              float*, unsigned long long*, cudaStream_t);
 template void dense_fft<float, float2>(sfft2d_ctx*, const float2*, cplx<float>*, float*, unsigned long long*, int,
                                  const cplx<float>*, cudaStream_t, unsigned*);
+template cplx<float>* dense_fft_front<float, float2>(sfft2d_ctx*, const float2*, int, const cplx<float>*,
+                                                 cudaStream_t, unsigned*);
+template void dense_fft_mags<float>(sfft2d_ctx*, float*, unsigned long long*, int, const cplx<float>*,
+                                  cudaStream_t);
+// fp64 only: on c3 (4096^2) skipping the 268 MB complex128 x_hat write saves
+// ~70 us per transform; in fp32 pass B gains only ~6 us while the per-candidate
+// strided DFT reads cost ~13 us more (8.4K candidates x 64 scattered sectors).
+bool dense_factored(int lgN, int precision) {
+  if (precision != SFFT2D_FP64) return false;
+  const FftPlan2D pl = plan_fft2d<double>(lgN);
+  return pl.four_step && !pl.col1;
+}
+void dense_split(int lgN, int precision, int* lgL1, int* lgL2) {
+  const FftPlan2D pl = precision == SFFT2D_FP64 ? plan_fft2d<double>(lgN) : plan_fft2d<float>(lgN);
+  *lgL1 = pl.lgL1;
+  *lgL2 = pl.lgL2;
+}
 }  // namespace sfft

@@ -135,4 +135,44 @@ void dense_fft(sfft2d_ctx* c, const Tin* x, cplx<T>* out, T* mags, unsigned long
   else fft_cols<T, true, false>(c, pl, 1, scratch, out, nullptr, nullptr, tw, lgN, gb, wb, st);
 }
 
+template <typename T, typename Tin>
+cplx<T>* dense_fft_front(sfft2d_ctx* c, const Tin* x, int lgN, const cplx<T>* tw, cudaStream_t st,
+                         unsigned* nonfinite) {
+  using C = cplx<T>;
+  const int N = 1 << lgN;
+  const FftPlan2D pl = plan_fft2d<T>(lgN);
+  if (!pl.four_step || pl.col1) fail(SFFT2D_ERR_STATE, "factored dense FFT needs four-step columns");
+  if (pl.smem_row > kMaxDynSmem || pl.row_threads > 512)
+    fail(SFFT2D_ERR_UNSUPPORTED, "image side too large for the smem FFT");
+  const double nn = (double)N * N;
+  C* scratch = (C*)ws(c, "fft_scratch", (size_t)N * N * sizeof(C));
+  fft_rows<T, Tin>(c, pl, N, x, scratch, tw, lgN, nonfinite, "k_fftr_dense",
+                   nn * (sizeof(Tin) + sizeof(C)), st);
+  pre(c, st);
+  with_lg<6, 7>(pl.lgL1, [&](auto LGc) {
+    constexpr int LG1 = decltype(LGc)::value;
+    kl(k_fftcA<T, LG1>, dim3(N >> pl.lgccA, 1 << pl.lgL2, 1), pl.thrA, pl.smem_A, st, scratch,
+       pl.lgL1, pl.lgL2, pl.lgccA, tw, lgN);
+  });
+  post(c, "k_fftcA", st, 2 * nn * sizeof(C));
+  return scratch;
+}
+
+template <typename T>
+void dense_fft_mags(sfft2d_ctx* c, T* mags, unsigned long long* peak, int lgN, const cplx<T>* tw,
+                    cudaStream_t st) {
+  using C = cplx<T>;
+  const int N = 1 << lgN;
+  const FftPlan2D pl = plan_fft2d<T>(lgN);
+  const double nn = (double)N * N;
+  C* scratch = (C*)ws(c, "fft_scratch", (size_t)N * N * sizeof(C));
+  pre(c, st);
+  with_lg<5, 7>(pl.lgL2, [&](auto LGc) {
+    constexpr int LG2 = decltype(LGc)::value;
+    kl(k_fftcB<T, false, true, LG2>, dim3(N >> pl.lgccB, 1 << pl.lgL1, 1), pl.thrB, pl.smem_B, st,
+       (const C*)scratch, (C*)nullptr, mags, peak, pl.lgL1, pl.lgL2, pl.lgccB, tw, lgN);
+  });
+  post(c, "k_fftcB", st, nn * (sizeof(C) + sizeof(T)));
+}
+
 }  // namespace sfft

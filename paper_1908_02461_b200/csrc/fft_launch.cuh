@@ -27,4 +27,18 @@ template <typename T, typename Tin>
 void dense_fft(sfft2d_ctx* c, const Tin* x, cplx<T>* out, T* mags, unsigned long long* peak,
                int lgN, const cplx<T>* tw, cudaStream_t st, unsigned* nonfinite);
 
+// Factored dense FFT (sides >= 2048, four-step columns): dense_fft_front runs
+// the row pass and four-step pass A into the context's "fft_scratch" buffer
+// (returns it; nonfinite as in dense_fft); dense_fft_mags then runs pass B
+// writing only |x_hat| + peak.  x_hat itself is never written: its entries are
+// L2-point DFTs of scratch columns (k_estimate_dense_fs).
+bool dense_factored(int lgN, int precision);
+void dense_split(int lgN, int precision, int* lgL1, int* lgL2);
+template <typename T, typename Tin>
+cplx<T>* dense_fft_front(sfft2d_ctx* c, const Tin* x, int lgN, const cplx<T>* tw, cudaStream_t st,
+                         unsigned* nonfinite);
+template <typename T>
+void dense_fft_mags(sfft2d_ctx* c, T* mags, unsigned long long* peak, int lgN, const cplx<T>* tw,
+                    cudaStream_t st);
+
 }  // namespace sfft
