@@ -95,6 +95,8 @@ struct sfft2d_ctx {
   };
   std::vector<ProfRec> prof;
   cudaStream_t ws_st = nullptr;     // stream of the running call: workspace grows stream-ordered on it
+  std::chrono::steady_clock::time_point t_entry, t_sync_end;   // host-latency tracing
+  double first_launch_us = 0;
   cudaEvent_t ev_ws = nullptr;
   std::vector<cudaEvent_t> ev_pool;
   size_t ev_used = 0;
@@ -162,7 +164,8 @@ void pre(sfft2d_ctx* c, cudaStream_t st) {
 }
 
 void post(sfft2d_ctx* c, const char* what, cudaStream_t st, double bytes) {
-  ++c->launches;
+  if (++c->launches == 1)
+    c->first_launch_us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - c->t_entry).count();
   ck(cudaGetLastError(), what);
   if (!c->profiling || !c->prof_open) return;
   cudaEvent_t b = next_event(c);
@@ -279,7 +282,8 @@ unsigned read_u32(sfft2d_ctx* c, const unsigned* dev, cudaStream_t st) {
   ck(cudaMemcpyAsync(c->pinned, dev, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H");
   const auto t0 = std::chrono::steady_clock::now();
   ck(cudaStreamSynchronize(st), "sync");
-  c->sync_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+  c->t_sync_end = std::chrono::steady_clock::now();
+  c->sync_us += std::chrono::duration<double, std::micro>(c->t_sync_end - t0).count();
   return c->pinned[0];
 }
 
@@ -1483,6 +1487,7 @@ static int atsfft_impl(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host,
                        int n_perms, void* bitgen, int precision, void* stream, sfft2d_result* res,
                        sfft2d_tuner_state* state) {
   return guarded(c, [&] {
+    c->t_entry = std::chrono::steady_clock::now();
     if (!cfg || !res || !state || !x || (n_perms > 0 && !perms)) fail(SFFT2D_ERR_VALUE, "null argument");
     check_side(n);
     cudaStream_t st = (cudaStream_t)stream;
@@ -1502,6 +1507,13 @@ static int atsfft_impl(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host,
     res->gpu_launches = c->launches;
     c->res_prec = precision;
     c->has_res = true;
+    if (getenv("SFFT2D_TRACE_HOST")) {
+      const auto now = std::chrono::steady_clock::now();
+      fprintf(stderr, "[sfft2d] entry->first launch %.1f us, last sync->return %.1f us, total %.1f us\n",
+              c->first_launch_us,
+              std::chrono::duration<double, std::micro>(now - c->t_sync_end).count(),
+              std::chrono::duration<double, std::micro>(now - c->t_entry).count());
+    }
   });
 }
 
