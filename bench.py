@@ -382,21 +382,28 @@ def main():
         P.atsfft2d_batch(xs, cfg, args.est_loops, seeds, concurrency=args.concurrency,
                          precision=args.precision, arrays=True)
         torch.cuda.synchronize()
-        barrier()
-        torch.cuda.synchronize()
-        e0.record(stream)
-        P.atsfft2d_batch(xs, cfg, args.est_loops, seeds, concurrency=args.concurrency,
-                         precision=args.precision, arrays=True)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        samples = []
+        bsampler = ClockSampler(sampler.dev)
+        bsampler.start()
+        for _ in range(3):
+            barrier()
+            torch.cuda.synchronize()
+            e0.record(stream)
+            P.atsfft2d_batch(xs, cfg, args.est_loops, seeds, concurrency=args.concurrency,
+                             precision=args.precision, arrays=True)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+            if world > 1:
+                dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            samples.append(world * args.c4_images / (float(t.item()) / 1e3))
+        bclocks = bsampler.stop()
         batched = {"workload": f"c4 sample: {args.c4_images} independent 1024x1024 c64 images per "
                                "rank, k~U[20,200], log-uniform magnitudes, 25 dB, est_loops="
                                f"{args.est_loops}", "concurrency": args.concurrency,
-                   "value": world * args.c4_images / (float(t.item()) / 1e3), "unit": UNIT}
+                   "value": float(np.median(samples)), "samples": samples, "unit": UNIT,
+                   "clocks": bclocks}
         del xs
 
     # ---- kernel-level roofline (instrumented pass, same workload)
