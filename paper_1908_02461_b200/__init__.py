@@ -14,7 +14,8 @@ float64 arithmetic; ``precision="fp32"`` is the fast path.
 __version__ = "0.1.0"
 
 from .batch import atsfft2d_batch, sfft2d_batch
-from .engine import ConfigurationError, SfftConfig, default_bins, sfft2d, sfft2d_arrays
+from .engine import (ConfigurationError, SfftConfig, default_bins, estimate_once, median_combine,
+                     seek_location_once, sfft2d, sfft2d_arrays, vote_and_select)
 from .hashing import (BinGrid, FlatWindow, PermutationParams, WindowCache, all_pass_window,
                       binned_spectrum, build_flat_window, draw_permutation, hash_coord,
                       identity_permutation, mod_inverse, offset_coord, unhash_bin)
@@ -29,4 +30,5 @@ __all__ = [
     "identity_permutation", "mod_inverse", "offset_coord", "unhash_bin", "error_metric",
     "planted_image", "sparse_image", "TunerConfig", "TunerState", "atsfft2d", "atsfft2d_arrays",
     "count_local_maxima", "detect_sparsity", "update_bins", "atsfft2d_batch", "sfft2d_batch",
+    "seek_location_once", "vote_and_select", "estimate_once", "median_combine",
 ]

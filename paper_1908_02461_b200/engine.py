@@ -151,3 +151,102 @@ def sfft2d(x, cfg: SfftConfig, rng, *, cache: WindowCache | None = None,
 def build_window(cfg: SfftConfig) -> FlatWindow:
     return build_flat_window(cfg.n, cfg.b_bins, cfg.window_delta_stop,
                              delta_pass=cfg.window_delta_pass)
+
+
+# ---------------------------------------------------------------- lower level
+# The reference's per-loop building blocks (engine.py:130-225), for callers that
+# compose Algorithm 1 themselves.  The hash passes run on the GPU through the C
+# ABI; vote counting and the per-coordinate median are the same small host-side
+# bookkeeping the reference does.
+
+def _cfg_for_window(cfg: SfftConfig, window: FlatWindow) -> "_native.SfftCfg":
+    if window.n != cfg.n or window.b_bins != cfg.b_bins:
+        raise ValueError("window does not match the configuration's (n, b_bins)")
+    return _native.SfftCfg(cfg.n, cfg.k, 1, cfg.d_factor, 1, cfg.b_bins, window.delta_pass,
+                           window.delta_stop, cfg.gain_floor, cfg.prune_rel)
+
+
+def seek_location_once(x, cfg: SfftConfig, window: FlatWindow, rng, *, precision: str = "fp64",
+                       device=None):
+    """One location loop (engine.py:130-145): draw a permutation, hash,
+    keep the ``num_kept_bins`` largest bins, reverse-hash each with a
+    one-sample margin, deduplicate.  Returns the permutation and an (m, 2)
+    int64 array of candidate coordinates in row-major order."""
+    torch = _native._torch()
+    rng = np.random.default_rng(rng)
+    p = draw_permutation(cfg.n, rng)
+    img = as_device_image(x, device)
+    if img.n != cfg.n:
+        raise ConfigurationError(f"config built for n={cfg.n}, signal has n={img.n}")
+    ccfg = _cfg_for_window(cfg, window)
+    ctx = _native.context(img.device)
+    ctx.ensure_tables(cfg.n, window.delta_pass, window.delta_stop)
+    nn = cfg.n * cfg.n
+    counts = torch.zeros(((nn + 31) // 32) * 32, dtype=torch.uint8, device=img.tensor.device)
+    with torch.cuda.device(img.device):
+        st = _stream(torch, img.device)
+        ctx.check(ctx.lib.sfft2d_sfft_votes(
+            ctx.handle, img.tensor.data_ptr(), img.dtype_code, 0, ctypes.byref(ccfg),
+            _native.perm_array([p]), 1, _native.precision_code(precision), st, counts.data_ptr()))
+        keys = torch.nonzero(counts[:nn]).flatten().to(torch.int64).cpu().numpy()
+    return p, np.stack([keys // cfg.n, keys % cfg.n], axis=1)
+
+
+def vote_and_select(candidate_sets, cfg: SfftConfig) -> np.ndarray:
+    """Coordinates present in at least ``vote_threshold`` of the ``loops``
+    candidate sets, as an (m, 2) int64 array in row-major order
+    (engine.py:148-160)."""
+    if len(candidate_sets) != cfg.loops:
+        raise ValueError(f"expected {cfg.loops} candidate sets, got {len(candidate_sets)}")
+    n = cfg.n
+    flat = [np.asarray(c, dtype=np.int64).reshape(-1, 2) for c in candidate_sets]
+    keys = np.concatenate([f[:, 0] * n + f[:, 1] for f in flat]) if flat else np.empty(0, np.int64)
+    uniq, counts = np.unique(keys, return_counts=True)
+    kept = uniq[counts >= cfg.vote_threshold]
+    return np.stack([kept // n, kept % n], axis=1)
+
+
+def estimate_once(x, coords, p, window: FlatWindow, cfg: SfftConfig, *, precision: str = "fp64",
+                  device=None) -> dict:
+    """One estimation loop (engine.py:163-195): the hash pass runs on the GPU
+    (``binned_spectrum``); each coordinate reads its bin, undoes the
+    permutation's phase twist and divides by the window gain.  Coordinates
+    whose gain is below ``gain_floor`` are left out of the dict."""
+    from .hashing import binned_spectrum
+    coords = np.asarray(coords, dtype=np.int64).reshape(-1, 2)
+    if coords.size == 0:
+        return {}
+    n, b = cfg.n, cfg.b_bins
+    spec = binned_spectrum(x, p, window, b, precision=precision, device=device).spectrum
+    if not isinstance(spec, np.ndarray):
+        spec = spec.cpu().numpy()
+    w = n // b
+    qi = (p.sigma1 * coords[:, 0]) % n
+    qj = (p.sigma2 * coords[:, 1]) % n
+    ui = (qi + w // 2) // w
+    uj = (qj + w // 2) // w
+    gain = window.freq_1d[(qi - w * ui) % n] * window.freq_1d[(qj - w * uj) % n]
+    twist = np.exp(-2j * np.pi * ((p.tau1 * coords[:, 0] + p.tau2 * coords[:, 1]) % n) / n)
+    ok = np.abs(gain) >= cfg.gain_floor
+    vals = spec[ui % b, uj % b] * twist
+    return {(int(coords[m, 0]), int(coords[m, 1])): complex(vals[m] / gain[m])
+            for m in np.flatnonzero(ok)}
+
+
+def median_combine(per_loop_estimates, coords=None) -> dict:
+    """Componentwise (real, imaginary) median over the loops that produced an
+    estimate for each coordinate; coordinates with none are dropped
+    (engine.py:198-220)."""
+    if coords is None:
+        keys = list(dict.fromkeys(k for est in per_loop_estimates for k in est))
+    else:
+        keys = [(int(i), int(j)) for i, j in np.asarray(coords).reshape(-1, 2)]
+    out = {}
+    for key in keys:
+        vals = np.asarray([est[key] for est in per_loop_estimates if key in est])
+        if vals.size:
+            out[key] = complex(np.median(vals.real) + 1j * np.median(vals.imag))
+    return out
+
+
+__all__ += ["seek_location_once", "vote_and_select", "estimate_once", "median_combine"]

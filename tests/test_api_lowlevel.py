@@ -1,0 +1,94 @@
+"""The reference's lower-level Algorithm 1 building blocks (engine.py:130-220):
+``seek_location_once`` / ``estimate_once`` on the GPU against the oracle, and
+the host-side ``vote_and_select`` / ``median_combine`` against the oracle's
+restatement, plus the composed pipeline equal to ``sfft2d``."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1908_02461_b200 as P
+from oracle import sfft_oracle as O
+
+gpu = pytest.mark.gpu
+
+
+def test_vote_and_select_matches_oracle():
+    rng = np.random.default_rng(4)
+    n = 64
+    cfg = P.SfftConfig(n=n, k=3, loops=5)
+    sets = [np.stack(np.unravel_index(np.unique(rng.integers(0, n * n, 40)), (n, n)), axis=1)
+            for _ in range(cfg.loops)]
+    got = P.vote_and_select(sets, cfg)
+    want = O.vote([s[:, 0] * n + s[:, 1] for s in sets], cfg.vote_threshold)
+    np.testing.assert_array_equal(got[:, 0] * n + got[:, 1], want)
+    with pytest.raises(ValueError):
+        P.vote_and_select(sets[:-1], cfg)
+
+
+def test_median_combine_semantics():
+    ests = [{(0, 1): 1 + 1j, (2, 3): 5.0}, {(0, 1): 3 - 1j}, {(0, 1): 2 + 4j, (4, 4): -1j}]
+    out = P.median_combine(ests)
+    assert list(out) == [(0, 1), (2, 3), (4, 4)]
+    assert out[(0, 1)] == complex(2, 1) and out[(2, 3)] == 5.0 and out[(4, 4)] == -1j
+    # explicit coordinates: order kept, coordinates without estimates dropped
+    out2 = P.median_combine(ests[:2], coords=[(2, 3), (9, 9), (0, 1)])
+    assert list(out2) == [(2, 3), (0, 1)] and out2[(0, 1)] == complex(2, 0)
+
+
+@gpu
+def test_seek_location_once_matches_oracle():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    sig = P.planted_image(256, 6, 3)
+    cfg = P.SfftConfig(n=256, k=6)
+    win = P.build_flat_window(256, cfg.b_bins, cfg.window_delta_stop,
+                              delta_pass=cfg.window_delta_pass)
+    p, cand = P.seek_location_once(sig.x, cfg, win, 11)
+    gen = np.random.default_rng(11)
+    q = O.draw_perm(256, gen)
+    assert (p.sigma1, p.sigma2, p.tau1, p.tau2) == (q.s1, q.s2, q.t1, q.t2)
+    ow = O.window(256, cfg.b_bins, cfg.window_delta_stop, cfg.window_delta_pass)
+    keys = O.location_loop(O.as_c128(sig.x), O.sfft_params(256, 6), ow, q)
+    np.testing.assert_array_equal(cand[:, 0] * 256 + cand[:, 1], keys)
+
+
+@gpu
+def test_estimate_once_matches_oracle():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    img = P.sparse_image(256, 8, 5, snr_db=25.0, dtype=np.complex128)
+    cfg = P.SfftConfig(n=256, k=8)
+    win = P.build_flat_window(256, cfg.b_bins, cfg.window_delta_stop,
+                              delta_pass=cfg.window_delta_pass)
+    p = P.draw_permutation(256, np.random.default_rng(2))
+    coords = np.concatenate([np.stack([img.rows, img.cols], axis=1),
+                             np.random.default_rng(0).integers(0, 256, (40, 2))])
+    got = P.estimate_once(img.x, coords, p, win, cfg)
+    q = O.make_perm(256, p.sigma1, p.sigma2, p.tau1, p.tau2)
+    ow = O.window(256, cfg.b_bins, cfg.window_delta_stop, cfg.window_delta_pass)
+    vals, ok = O.estimate(O.as_c128(img.x), coords, q, ow, cfg.b_bins, cfg.gain_floor)
+    want = {(int(i), int(j)): complex(v) for (i, j), v, u in zip(coords, vals, ok) if u}
+    assert set(got) == set(want)
+    for key, v in want.items():
+        assert abs(got[key] - v) <= 1e-10 * max(1.0, abs(v))
+
+
+@gpu
+def test_composed_pipeline_recovers_planted_support():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    sig = P.planted_image(256, 6, 3)
+    cfg = P.SfftConfig(n=256, k=6)
+    win = P.build_flat_window(256, cfg.b_bins, cfg.window_delta_stop,
+                              delta_pass=cfg.window_delta_pass)
+    gen = np.random.default_rng(7)
+    sets = [P.seek_location_once(sig.x, cfg, win, gen)[1] for _ in range(cfg.loops)]
+    coords = P.vote_and_select(sets, cfg)
+    ests = [P.estimate_once(sig.x, coords, P.draw_permutation(256, gen), win, cfg)
+            for _ in range(cfg.loops)]
+    med = P.median_combine(ests, coords)
+    top = sorted(med, key=lambda k: -abs(med[k]))[:6]
+    assert set(top) == set(sig.truth)
+    for key in top:
+        assert abs(med[key] - sig.truth[key]) < 1e-6
