@@ -22,11 +22,13 @@ This is host-side workload tooling, not part of the transform.
 from __future__ import annotations
 
 import hashlib
+import struct
 from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["SparseImage", "sparse_image", "planted_image", "error_metric", "image_digest"]
+__all__ = ["SparseImage", "sparse_image", "planted_image", "error_metric", "image_digest",
+           "save_signal", "load_signal"]
 
 
 @dataclass(frozen=True)
@@ -127,3 +129,39 @@ def error_metric(approx: dict, exact: dict, k: int) -> float:
 def image_digest(x: np.ndarray) -> str:
     """sha256 of the raw bytes; golden fixtures pin regenerated inputs with it."""
     return hashlib.sha256(np.ascontiguousarray(x).tobytes()).hexdigest()
+
+
+# SF2D exchange format (signals.py:86-115 of the reference): a 20-byte header
+# (magic b"SF2D", n: uint32, k: uint32, seed: uint64, little endian) followed by
+# the n*n row-major samples as little-endian float64 (re, im) pairs.  The
+# ground truth is not stored.
+_SF2D_MAGIC = b"SF2D"
+_SF2D_HEADER = struct.Struct("<4sIIQ")
+
+
+def save_signal(sig: SparseImage, path) -> None:
+    """Write ``sig.x`` (any complex dtype, stored as float64 pairs) with its
+    (n, k, seed) header."""
+    x = np.ascontiguousarray(sig.x, dtype=np.complex128)
+    if x.shape != (sig.n, sig.n):
+        raise ValueError(f"signal shape {x.shape} does not match n={sig.n}")
+    with open(path, "wb") as fh:
+        fh.write(_SF2D_HEADER.pack(_SF2D_MAGIC, sig.n, sig.k, sig.seed))
+        fh.write(x.view("<f8").tobytes())
+
+
+def load_signal(path) -> SparseImage:
+    """Read an SF2D file; the truth arrays are empty (not stored)."""
+    with open(path, "rb") as fh:
+        head = fh.read(_SF2D_HEADER.size)
+        if len(head) != _SF2D_HEADER.size:
+            raise ValueError("truncated SF2D header")
+        magic, n, k, seed = _SF2D_HEADER.unpack(head)
+        if magic != _SF2D_MAGIC:
+            raise ValueError(f"bad magic {magic!r}")
+        raw = np.frombuffer(fh.read(), dtype="<f8")
+    if raw.size != 2 * n * n:
+        raise ValueError(f"payload holds {raw.size} floats, expected {2 * n * n}")
+    x = raw.view(np.complex128).reshape(n, n).copy()
+    empty = np.empty(0, dtype=np.int64)
+    return SparseImage(int(n), int(k), int(seed), x, empty, empty, np.empty(0, np.complex128))
