@@ -945,7 +945,8 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       const Publish pub = make_publish(c, 1);
       seq = pub.seq;
       pre(c, st);
-      kl(k_small_pass<T>, 1, 1024, BB * (sizeof(C) + sizeof(T)) + bb * sizeof(C), st, (const C*)fo.data, fo.Z, fo.Z == 1, lgb, p, (const C*)tb.tw[prec_of<T>()], lgN,
+      if (BB > 4 * 1024) fail(SFFT2D_ERR_UNSUPPORTED, "small pass holds at most 4 bins per thread");
+      kl(k_small_pass<T>, 1, 1024, (size_t)bb * (bb + 1) * sizeof(C) + BB * sizeof(T) + bb * sizeof(C), st, (const C*)fo.data, fo.Z, fo.Z == 1, lgb, p, (const C*)tb.tw[prec_of<T>()], lgN,
           cf.mag_floor, ml, cnt, pub);
       post(c, "k_small_pass", st, (double)(fo.Z + 1) * BB * sizeof(C));
     } else {

@@ -565,7 +565,10 @@ k_small_pass(const cplx<T>* __restrict__ part, int Z, bool permuted, int lgB, Pe
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* s = reinterpret_cast<C*>(smem_raw);
   const int B = 1 << lgB, BB = B * B;
-  T* m = reinterpret_cast<T*>(s + BB);
+  // rows padded to B + 1 elements: the column pass (stride RS) is then free
+  // of shared-memory bank conflicts (stride B put a warp on one bank)
+  const int RS = B + 1;
+  T* m = reinterpret_cast<T*>(s + (size_t)B * RS);
   __shared__ unsigned long long s_peak;
   __shared__ unsigned s_n;
   if (threadIdx.x == 0) { s_peak = 0; s_n = 0; }
@@ -575,19 +578,44 @@ k_small_pass(const cplx<T>* __restrict__ part, int Z, bool permuted, int lgB, Pe
   const int tpe_lg = BB >= (int)blockDim.x ? 0 : min(5, __ffs(blockDim.x / BB) - 1);
   const int tpe = 1 << tpe_lg;
   const int zs = (Z + tpe - 1) >> tpe_lg;
-  for (int t = threadIdx.x; t < (BB << tpe_lg); t += blockDim.x) {
-    const int e = t >> tpe_lg, sl = t & (tpe - 1);
-    C v;
-    if (permuted) {
-      v = part[e];
-    } else {
-      const int z0 = sl * zs;
-      const int zn = max(0, min(zs, Z - z0));
-      v = sum_partials(part + (size_t)z0 * BB + e, (size_t)BB, zn);
+  // up to 4 slots per thread, their partial sums loaded together (all loads
+  // in flight before the first use)
+  constexpr int kSlots = 4;
+  C vv[kSlots];
+  const int total = BB << tpe_lg;
+  const C* src[kSlots];
+  int zn[kSlots];
+  int zmax = 0;
+#pragma unroll
+  for (int u = 0; u < kSlots; ++u) {
+    const int t = threadIdx.x + u * blockDim.x;
+    vv[u] = mk<T>(0, 0);
+    zn[u] = 0;
+    src[u] = part;
+    if (t < total) {
+      const int e = t >> tpe_lg, sl = t & (tpe - 1);
+      const int z0 = permuted ? 0 : sl * zs;
+      zn[u] = permuted ? 1 : max(0, min(zs, Z - z0));
+      src[u] = part + (size_t)z0 * BB + e;
+      zmax = max(zmax, zn[u]);
     }
+  }
+  // partials in a fixed order per bin; the slots' loads are independent and
+  // the z loop is unrolled, so up to 4 x 4 loads per thread are in flight
+#pragma unroll 4
+  for (int z = 0; z < zmax; ++z)
+#pragma unroll
+    for (int u = 0; u < kSlots; ++u)
+      if (z < zn[u]) vv[u] = cadd(vv[u], src[u][(size_t)z * BB]);
+#pragma unroll
+  for (int u = 0; u < kSlots; ++u) {
+    const int t = threadIdx.x + u * blockDim.x;
+    if (t >= total) break;
+    const int e = t >> tpe_lg, sl = t & (tpe - 1);
+    C v = vv[u];
     for (int o = 1; o < tpe; o <<= 1) {
-      const C u = mk<T>(__shfl_down_sync(0xffffffffu, v.x, o), __shfl_down_sync(0xffffffffu, v.y, o));
-      v = cadd(v, u);
+      const C w = mk<T>(__shfl_down_sync(0xffffffffu, v.x, o), __shfl_down_sync(0xffffffffu, v.y, o));
+      v = cadd(v, w);
     }
     if (sl == 0) {
       unsigned a = (unsigned)(e >> lgB), b = (unsigned)(e & (B - 1));
@@ -595,18 +623,18 @@ k_small_pass(const cplx<T>* __restrict__ part, int Z, bool permuted, int lgB, Pe
         a = (p.s1i * (a - p.t1)) & maskB;
         b = (p.s2i * (b - p.t2)) & maskB;
       }
-      s[bitrev(a, lgB) * B + bitrev(b, lgB)] = v;
+      s[bitrev(a, lgB) * RS + bitrev(b, lgB)] = v;
     }
   }
   // twiddles of a length-B transform, W_B^k = tw[k * N / B], staged in smem
   C* tws = reinterpret_cast<C*>(m + BB);
   for (int k = threadIdx.x; k < B; k += blockDim.x) tws[k] = tw[k << (lgN - lgB)];
   __syncthreads();
-  fft_stages<T>(s, B, lgB, 1, B, tws, lgB);
-  fft_stages<T>(s, B, lgB, B, 1, tws, lgB);
+  fft_stages<T>(s, B, lgB, 1, RS, tws, lgB);    // rows
+  fft_stages<T>(s, B, lgB, RS, 1, tws, lgB);    // columns
   unsigned long long best = 0;
   for (int e = threadIdx.x; e < BB; e += blockDim.x) {
-    const T v = cabs_(s[e]);
+    const T v = cabs_(s[(e >> lgB) * RS + (e & (B - 1))]);
     m[e] = v;
     const unsigned long long k = fkey(v);
     best = k > best ? k : best;
