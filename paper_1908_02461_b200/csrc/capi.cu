@@ -813,9 +813,30 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   ps.dev = (Perm*)ws(c, "perms", (size_t)ps.cap * sizeof(Perm));
   Perm* dp = ps.dev;
   const long nkeys = (long)n * n;
+  const long long budget = std::max((long long)n * n / 8, 1LL << 16);   // tuner.py:165
   const int mode = (4 * (max_iters + 2) <= 255) ? kVoteAdd8 : kVoteAdd32;
   uint32_t* hist = (uint32_t*)ws(c, "hist", hist_bytes(nkeys, mode));
-  ck(cudaMemsetAsync(hist, 0, hist_bytes(nkeys, mode), st), "memset hist");
+  // deferred votes (k_vote_lazy): byte tallies, N >= 128; the histogram is
+  // only materialised (zeroed here) when a pass must vote with atomics
+  const bool lazy = mode == kVoteAdd8 && lgN >= 7;
+  bool hist_zeroed = false;
+  auto zero_hist = [&](cudaStream_t s2) {
+    if (hist_zeroed) return;
+    ck(cudaMemsetAsync(hist, 0, hist_bytes(nkeys, mode), s2), "memset hist");
+    hist_zeroed = true;
+  };
+  if (!lazy) zero_hist(st);
+  LazyPasses lp;
+  std::memset(&lp, 0, sizeof(lp));
+  lp.lgBmax = 2;
+  long long arch_cap = kLazyScan;   // entries per archived pass, bounded by the vote budget
+  for (int lb = 2; lb <= std::min(9, lgN); ++lb) {
+    const long long w = n >> lb, len = (w == 1) ? 3 : w + 2;
+    arch_cap = std::max(arch_cap, std::min((long long)1 << (2 * lb), budget / (len * len)));
+  }
+  int32_t* arch = lazy ? (int32_t*)ws(c, "vote_arch", (size_t)arch_cap * kLazyMax * 4) : nullptr;
+  long long arch_used = 0;
+  bool hist_used = false;
   // NaN/Inf check (as_complex_matrix, corefft.py:49-50): fused into the dense
   // FFT's row pass when the trajectory reaches B = N, else one pass at the end
   unsigned* finite = (unsigned*)ws(c, "finite", 16);
@@ -824,7 +845,6 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
 
   std::memset(S, 0, sizeof(*S));
   int b = std::max(4, std::min(cf.b0, n));
-  const long long budget = std::max((long long)n * n / 8, 1LL << 16);
   bool xhat_ready = false;
   C* xhat = nullptr;
   T* M = nullptr;
@@ -884,17 +904,38 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   bool vote_pending[2] = {false, false};
   int npass = 0;
   int last_slot = 0;
-  auto vote_list = [&](const Perm& pv, int lgb, long long budget_dev, int slot) {
+  // the vote of a pass is issued once the host has read its count (passes over
+  // the budget cast nothing): in deferred mode the pass's maxima list is
+  // archived for k_vote_lazy (bitmap passes B <= 512, short list passes), else
+  // one atomic per preimage coordinate into the histogram on the side stream
+  auto vote_list = [&](const Perm& pv, int lgb, int slot, long long count) {
+    if (count <= 0) return;
     const int w = n >> lgb;
     const long long len = (w == 1) ? 3 : std::min<long long>(w + 2, n);
-    ck(cudaEventRecord(c->ev_lmax, st), "cudaEventRecord");
-    ck(cudaStreamWaitEvent(c->vote_st, c->ev_lmax, 0), "cudaStreamWaitEvent");
-    pre(c, c->vote_st);
-    kl(k_vote, dim3(kNumSMs * 2, 1), 256, 0, c->vote_st, maxlists[slot & 1], 0, cnt_slots + slot, 0,
-                                                        nullptr, lgN, lgb, 1, mode, 0, hist,
-                                                        budget_dev, pv);
-    post(c, "k_vote", c->vote_st, (double)len * len * 4.0);
-    ck(cudaEventRecord(c->ev_vote[slot & 1], c->vote_st), "cudaEventRecord");
+    if (lazy && (lgb <= 9 || count <= kLazyScan) && lp.n < kLazyMax && count <= arch_cap) {
+      LazyPass& P = lp.v[lp.n++];
+      P.p = pv;
+      P.lgB = lgb;
+      P.count = (int)count;
+      P.off = arch_used;
+      if (lgb <= 9) lp.lgBmax = std::max(lp.lgBmax, lgb);
+      ck(cudaMemcpyAsync(arch + arch_used, maxlists[slot & 1], (size_t)count * 4,
+                         cudaMemcpyDeviceToDevice, st), "archive maxima");
+      arch_used += count;
+      return;
+    }
+    // profiling serialises the votes onto the main stream so every launch's
+    // event pair times that kernel alone
+    cudaStream_t vs = c->profiling ? st : c->vote_st;
+    ck(cudaStreamWaitEvent(vs, c->ev_lmax, 0), "cudaStreamWaitEvent");
+    zero_hist(vs);
+    hist_used = true;
+    const long long total = count * len * len;
+    pre(c, vs);
+    kl(k_vote, grid_for(total, 256, kNumSMs * 2), 256, 0, vs, maxlists[slot & 1], 0,
+       cnt_slots + slot, 0, nullptr, lgN, lgb, 1, mode, 0, hist, 0LL, pv);
+    post(c, "k_vote", vs, (double)total * 4.0);
+    ck(cudaEventRecord(c->ev_vote[slot & 1], vs), "cudaEventRecord");
     vote_pending[slot & 1] = true;
   };
 
@@ -960,7 +1001,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       seq = lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, ml, cnt, st, true, p.s1i & mb, p.s2i & mb,
                           p.s2 & mb);
     }
-    vote_list(p, lgb, budget, slot);
+    ck(cudaEventRecord(c->ev_lmax, st), "cudaEventRecord");   // the maxima list is complete
     const long long count = wait_published(c, seq, st);
     if (cand_pending) {   // the candidate count rides along with the maxima count
       cand_n = ((volatile unsigned*)c->mapped_h)[2];
@@ -973,7 +1014,9 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     last_count = count;
     last_slot = slot;
     const long long w = n / bb;
-    if (count > 0 && count * (w + 2) * (w + 2) <= budget) {   // host mirror of the device test
+    const long long len = (w == 1) ? 3 : std::min<long long>(w + 2, n);
+    if (count > 0 && count * len * len <= budget) {   // tuner.py:165,175
+      vote_list(p, lgb, slot, count);
       ++vote_passes;
       have_votes = true;
     }
@@ -1070,7 +1113,9 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   if (!have_votes && last_valid && maxc > 0) {
     // every pass exceeded the vote budget: fall back to the final pass (tuner.py:228-234)
     if (last_count > 0) {
-      vote_list(ps.hp[last_pi], ilog2(last_b), 0, last_slot);   // its list and count slot are intact
+      // its list and count slot are intact; the side stream must see the list
+      ck(cudaEventRecord(c->ev_lmax, st), "cudaEventRecord");
+      vote_list(ps.hp[last_pi], ilog2(last_b), last_slot, last_count);
       have_votes = true;
     }
     vote_passes = 1;
@@ -1081,10 +1126,24 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   ck(cudaStreamWaitEvent(st, c->ev_lmax, 0), "cudaStreamWaitEvent");
   int32_t* keys = (int32_t*)ws(c, "keys", (size_t)nkeys * 4);
   unsigned* kt = (unsigned*)ws(c, "keys_tot", 16);
+  // deferred votes: tallies of every archived pass, tile by tile in shared
+  // memory; either thresholded into the compaction bitmask (bits != nullptr)
+  // or written out as the histogram (the detect_sparsity API's tallies)
+  auto lazy_votes = [&](unsigned thr_, uint32_t* bits, unsigned* cnts, uint32_t* hist_out) {
+    int lgG = 13;
+    while (lgG < 15 && ((long long)1 << (lgG + 1)) * (2 * kNumSMs) <= nkeys) ++lgG;
+    const size_t smem = vote_lazy_smem(lgN, lgG, lp.lgBmax);
+    pre(c, st);
+    kl(k_vote_lazy, (unsigned)(nkeys >> lgG), 256, smem, st, (const int32_t*)arch, lp, lgN, lgG,
+       (const uint32_t*)(hist_used ? hist : nullptr), hist_out, thr_, bits, cnts);
+    post(c, "k_vote_lazy", st, (double)nkeys / 8.0 + (hist_used ? (double)nkeys : 0.0) +
+                                   (hist_out ? (double)nkeys : 0.0));
+  };
 
   if (!do_estimate) {
     unsigned nv = 0;
     if (have_votes) {
+      if (lazy) lazy_votes(0u, nullptr, nullptr, hist);
       nv = hist_compact(c, hist, nkeys, mode, 1u, keys, kt, st);
       nan_check(false);
       int32_t* tal = (int32_t*)ws(c, "tallies", (size_t)std::max(nv, 1u) * 4);
@@ -1112,7 +1171,16 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     return;
   }
   const unsigned thr = (unsigned)((std::max(vote_passes, 1) + 1) / 2);
-  const unsigned m = hist_compact(c, hist, nkeys, mode, thr, keys, kt, st);
+  unsigned m;
+  if (lazy) {
+    uint32_t* bits = (uint32_t*)ws(c, "hc_bits", words_for(nkeys) * 4);
+    unsigned* cnts = (unsigned*)ws(c, "hc_cnt", (size_t)blocks_for(nkeys) * 4);
+    lazy_votes(thr, bits, cnts, nullptr);
+    compact(c, bits, cnts, nkeys, 1, keys, 0, kt, st);
+    m = read_u32(c, kt, st);
+  } else {
+    m = hist_compact(c, hist, nkeys, mode, thr, keys, kt, st);
+  }
   nan_check(false);
   S->n_candidates = m;
   if (m == 0) {

@@ -316,10 +316,13 @@ k_lmax_stream(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, unsign
       lds4(md + C0, m);
       const T hi = fmax(fmax(m[0], m[1]), fmax(m[2], m[3]));
       if (!__any_sync(0xffffffffu, hi >= flT)) continue;
+      // the group holds a live bin: test it with lanes on consecutive columns
+      // (sub-group j = columns g*128 + j*32 + lane), so every neighbour load
+      // at C, C -+ s2 is one conflict-free 32-word wavefront
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const unsigned C = C0 + j;
-        const T v = m[j];
+        const unsigned C = ((unsigned)g << 7) + ((unsigned)j << 5) + (unsigned)lane;
+        const T v = md[C];
         bool f = v >= flT;
         if (cand) {   // every above-floor bin, natural index (later views test only these)
           const unsigned cb = __ballot_sync(0xffffffffu, f);

@@ -70,6 +70,200 @@ __global__ void k_vote(const int32_t* __restrict__ bins, long seg_stride, const 
   }
 }
 
+// Deferred tuner vote (kVoteAdd8 tallies, tuner.py:175-179, 228-240).
+// Instead of adding every voting pass into an N^2 histogram in HBM, the tuner
+// archives each pass's maxima list (a few KB) and ONE kernel at the end
+// computes the tallies of a tile of G consecutive keys (R = G / N natural rows)
+// in shared memory from all archived passes, then thresholds them straight
+// into the compaction bitmask (k_hist_bits' output) — the histogram never
+// touches HBM.  Per pass, for row i of the tile:
+//   coordinate (i, j) is in the preimage of maximum (a, b) iff t = s1 i mod N
+//   lies in T_a and v = s2 j mod N lies in T_b, where
+//   T_c = [c w - floor(w/2) - 1, c w + ceil(w/2) + 1) mod N  (expand = 1),
+// so row i gains, at every j = s2^-1 v with v in T_b, the number of maxima
+// (a, b) whose bin row a has t in T_a (at most 3 bin rows).
+//   * bitmap passes (B <= 512): the pass's B x B maxima bitmap is built in
+//     shared memory; [A] lists each row's active bin columns b with their
+//     multiplicity, [B] scatters the increments with shared atomics;
+//   * list passes (B >= 1024, at most kLazyScan maxima): every maximum's
+//     len x len preimage is tested against the tile's rows.
+// Passes with more maxima at B >= 1024 were voted into `hist_init` with
+// k_vote (one atomic per coordinate) and seed the tile.  Bytes cannot carry:
+// tallies are bounded by 4 * passes <= 255 in this mode.
+constexpr int kLazyMax = 40;        // archived passes (tuner passes + confirmations + fallback)
+constexpr int kLazyScan = 8192;     // list passes: maxima scanned by every CTA
+constexpr int kLazyMaxRows = 128;   // R = G / N, G >= 8192 keys, N >= 256... capped
+struct LazyPass {
+  Perm p;
+  int lgB;
+  int count;
+  long long off;                    // first entry in the archive
+};
+struct LazyPasses {
+  LazyPass v[kLazyMax];
+  int n;
+  int lgBmax;                       // largest B of a bitmap pass (sizes the bitmap / lists)
+};
+
+__device__ __forceinline__ void lazy_add(uint32_t* tal, unsigned key, unsigned inc) {
+  atomicAdd(&tal[key >> 2], inc << ((key & 3u) * 8u));
+}
+
+__global__ void __launch_bounds__(256) k_vote_lazy(const int32_t* __restrict__ arch, LazyPasses lp,
+                                                    int lgN, int lgG,
+                                                    const uint32_t* __restrict__ hist_init,
+                                                    uint32_t* __restrict__ hist_out, unsigned thr,
+                                                    uint32_t* __restrict__ bits,
+                                                    unsigned* __restrict__ blk_counts) {
+  pdl_wait();
+  extern __shared__ __align__(16) uint32_t sm_vote[];
+  __shared__ int s_nlist[kLazyMaxRows];
+  __shared__ unsigned s_warp[32];
+  const int N = 1 << lgN, G = 1 << lgG, R = G >> lgN;
+  const unsigned maskN = (unsigned)N - 1u;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const size_t k0 = (size_t)blockIdx.x << lgG;
+  const unsigned i0 = (unsigned)(k0 >> lgN);
+  const int Bmax = 1 << lp.lgBmax;
+  uint32_t* s_tal = sm_vote;                                   // G bytes
+  uint32_t* s_bits = s_tal + G / 4;                            // Bmax^2 bits
+  uint32_t* s_flag = s_bits + ((Bmax * Bmax + 31) / 32 + 3) / 4 * 4;
+  int* s_list = (int*)(s_flag + ((Bmax + 31) / 32 + 3) / 4 * 4);   // R x Bmax entries
+  uint4* t4 = reinterpret_cast<uint4*>(s_tal);
+  if (hist_init) {
+    const uint4* h4 = reinterpret_cast<const uint4*>(hist_init + k0 / 4);
+    for (int e = tid; e < G / 16; e += nt) t4[e] = h4[e];
+  } else {
+    for (int e = tid; e < G / 16; e += nt) t4[e] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  for (int r = tid; r < R; r += nt) s_nlist[r] = 0;
+  for (int ps = 0; ps < lp.n; ++ps) {
+    const LazyPass& P = lp.v[ps];
+    const int lgB = P.lgB, B = 1 << lgB;
+    const unsigned maskB = (unsigned)B - 1u;
+    const int lgw = lgN - lgB, w = 1 << lgw;
+    const int len = (w == 1) ? 3 : w + 2;
+    const int shiftlo = w / 2 + 1;   // floor(w/2) + expand
+    const int32_t* L = arch + P.off;
+    if (lgB <= lp.lgBmax) {
+      // ---- bitmap pass
+      const int bitwords = (B * B + 31) / 32, flagwords = (B + 31) / 32;
+      for (int e = tid; e < bitwords; e += nt) s_bits[e] = 0u;
+      for (int e = tid; e < flagwords; e += nt) s_flag[e] = 0u;
+      __syncthreads();
+      for (int e = tid; e < P.count; e += nt) {
+        const unsigned bin = (unsigned)L[e];
+        atomicOr(&s_bits[bin >> 5], 1u << (bin & 31u));
+        const unsigned a = bin >> lgB;
+        atomicOr(&s_flag[a >> 5], 1u << (a & 31u));
+      }
+      __syncthreads();
+      // [A] item (row r, 32-column chunk q): bin rows a with
+      //     t + shiftlo - len < a w <= t + shiftlo, and their maxima in the chunk
+      const int chunks = (B + 31) / 32;
+      const unsigned cmask = B >= 32 ? 0xffffffffu : ((1u << B) - 1u);
+      for (int item = tid; item < R * chunks; item += nt) {
+        const int r = item / chunks, q = item - r * chunks;
+        const unsigned t = (P.p.s1 * (i0 + (unsigned)r)) & maskN;
+        const int hi = (int)((t + (unsigned)N + (unsigned)shiftlo) >> lgw);
+        const int lo = (int)((t + (unsigned)N + (unsigned)shiftlo - (unsigned)len + (unsigned)w) >> lgw);
+        unsigned rb[3];
+        int na = 0;
+        unsigned any = 0;
+        for (int a = lo; a <= hi; ++a) {
+          const unsigned am = (unsigned)a & maskB;
+          if (!((s_flag[am >> 5] >> (am & 31u)) & 1u)) continue;
+          const unsigned bit0 = am * (unsigned)B + (unsigned)q * 32u;
+          rb[na] = B >= 32 ? s_bits[bit0 >> 5] : (s_bits[bit0 >> 5] >> (bit0 & 31u)) & cmask;
+          any |= rb[na++];
+        }
+        while (any) {
+          const int k = __ffs(any) - 1;
+          any &= any - 1u;
+          int m = 0;
+          for (int u = 0; u < na; ++u) m += (rb[u] >> k) & 1u;
+          const int slot = atomicAdd(&s_nlist[r], 1);
+          s_list[r * Bmax + slot] = ((q * 32 + k) << 8) | m;
+        }
+      }
+      __syncthreads();
+      // [B] scatter every row's increments into the tile: preimage offsets
+      // rr < w as (entry, rr) = (e >> lgw, e & (w - 1)), the two expand
+      // offsets rr = w, w + 1 separately (no integer division by len)
+      for (int r = 0; r < R; ++r) {
+        const int nl = s_nlist[r];
+        if (nl == 0) continue;
+        const int* lst = s_list + r * Bmax;
+        const unsigned rowkey = (unsigned)r << lgN;
+        const int nmain = w == 1 ? nl * 3 : nl << lgw;
+        for (int e = tid; e < nmain; e += nt) {
+          int q, rr;
+          if (w == 1) { q = e / 3; rr = e - q * 3; } else { q = e >> lgw; rr = e & (w - 1); }
+          const int ent = lst[q];
+          const unsigned v = ((unsigned)(ent >> 8) * (unsigned)w - (unsigned)shiftlo + (unsigned)rr) & maskN;
+          lazy_add(s_tal, rowkey | ((P.p.s2i * v) & maskN), (unsigned)(ent & 255));
+        }
+        if (w > 1) {
+          for (int e = tid; e < 2 * nl; e += nt) {
+            const int ent = lst[e >> 1];
+            const unsigned rr = (unsigned)w + (unsigned)(e & 1);
+            const unsigned v = ((unsigned)(ent >> 8) * (unsigned)w - (unsigned)shiftlo + rr) & maskN;
+            lazy_add(s_tal, rowkey | ((P.p.s2i * v) & maskN), (unsigned)(ent & 255));
+          }
+        }
+      }
+      __syncthreads();
+      for (int r = tid; r < R; r += nt) s_nlist[r] = 0;
+    } else {
+      // ---- list pass: the preimage rows of maximum (a, b) are s1^-1 t, t in T_a
+      for (int e = tid; e < P.count; e += nt) {
+        const unsigned bin = (unsigned)L[e];
+        const unsigned a = bin >> lgB, b = bin & maskB;
+        for (int u = 0; u < len; ++u) {
+          const unsigned t = (a * (unsigned)w - (unsigned)shiftlo + (unsigned)u) & maskN;
+          const unsigned r = ((P.p.s1i * t) & maskN) - i0;
+          if (r >= (unsigned)R) continue;
+          for (int v = 0; v < len; ++v) {
+            const unsigned tv = (b * (unsigned)w - (unsigned)shiftlo + (unsigned)v) & maskN;
+            lazy_add(s_tal, (r << lgN) | ((P.p.s2i * tv) & maskN), 1u);
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (hist_out) {
+    uint4* h4 = reinterpret_cast<uint4*>(hist_out + k0 / 4);
+    for (int e = tid; e < G / 16; e += nt) h4[e] = t4[e];
+  }
+  if (bits) {
+    // kCmpElems keys per compaction block: word tid of every block in the tile
+    for (int blk = 0; blk < G / kCmpElems; ++blk) {
+      const int wl = blk * kCmpWords + tid;   // 32 keys = 8 tally words
+      uint32_t word = 0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t h = s_tal[wl * 8 + u];
+        if (!h) continue;
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb)
+          if (((h >> (8 * bb)) & 255u) >= thr) word |= 1u << (u * 4 + bb);
+      }
+      bits[(k0 >> 5) + wl] = word;
+      const unsigned pre = block_excl_scan256(__popc(word), s_warp);
+      if (tid == kCmpThreads - 1) blk_counts[(k0 >> lgG) * (G / kCmpElems) + blk] = pre + __popc(word);
+      __syncthreads();
+    }
+  }
+}
+
+// dynamic shared memory of k_vote_lazy
+inline size_t vote_lazy_smem(int lgN, int lgG, int lgBmax) {
+  const long G = 1L << lgG, Bm = 1L << lgBmax, R = G >> lgN;
+  const long bitw = ((Bm * Bm + 31) / 32 + 3) / 4 * 4, flagw = ((Bm + 31) / 32 + 3) / 4 * 4;
+  return (size_t)(G / 4 + bitw + flagw + R * Bm) * 4;
+}
+
 // Fold one group's loop-bit masks into per-coordinate loop counts (L > 8).
 __global__ void k_mask_to_counts(uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
                                  long nwords) {
