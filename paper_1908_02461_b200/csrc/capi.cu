@@ -423,12 +423,15 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
   if (g == 1 && B < 512 && gm.TW == 512 && (1 << lgN) >= seg_cols) {
     // TMA ring fold, 3 x 32 KB slots (2 CTAs per SM), row aliases chunked so
     // that ~2 CTAs per SM stream rows (measured best of slots 3-6 x 1-4 CTAs
-    // per SM on c3: B = 16 15.3 -> 10.9 us, B = 256 31.6 -> 26.3 us)
+    // per SM on c3)
     const int nslot = 3;
+    // one wave: at most 2 CTAs per SM (floor, not ceil — a 384-CTA grid
+    // over 296 slots left a 30% tail; c3 B = 128/256: 28.5 -> 26.2 us, and
+    // B >= 256 writes its grid directly, no partials)
     const long target = 2L * kNumSMs;
     FoldGeom gr = gm;
     const int aliases = (1 << lgN) >> lgB;
-    int Z = (int)std::max(1L, std::min<long>(aliases, (target + B - 1) / B));
+    int Z = (int)std::max(1L, std::min<long>(aliases, target / B));
     int rpc = (aliases + Z - 1) / Z;
     if (rpc > kFoldMaxRows) rpc = kFoldMaxRows;
     gr.rpc = rpc;
