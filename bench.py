@@ -66,7 +66,7 @@ def parse():
     ap.add_argument("--profile-steps", type=int, default=3)
     ap.add_argument("--c4-images", type=int, default=96,
                     help="images in the batched (c4) throughput sample; 0 skips it")
-    ap.add_argument("--concurrency", type=int, default=4)
+    ap.add_argument("--concurrency", type=int, default=6)
     return ap.parse_args()
 
 

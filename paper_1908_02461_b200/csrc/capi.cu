@@ -570,7 +570,8 @@ template <typename T>
 unsigned lmax_tuner(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long long* peak,
                     double floor_rel, int32_t* list, unsigned* count, cudaStream_t st, bool perm,
                     unsigned s1, unsigned s2, unsigned s2inv, int32_t* cand = nullptr,
-                    unsigned* cand_count = nullptr, bool* emitted = nullptr) {
+                    unsigned* cand_count = nullptr, bool* emitted = nullptr,
+                    bool live_most = false) {
   if (emitted) *emitted = false;
   const int B = 1 << lgB;
   const double by = (double)B * B * sizeof(T);
@@ -586,6 +587,19 @@ unsigned lmax_tuner(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long l
     const size_t sm = nslot * row + wb;
     const Publish pub = make_publish(c, (unsigned)grid);
     pre(c, st);
+    if (live_most && !cand && B <= 4096) {
+      // most bins pass the floor: register neighbourhood windows, one warp per
+      // 128-column group (fewer threads for narrow grids)
+      const int tw = std::min(512, B / 4);
+      if (B / 128 > 16)
+        kl(k_lmax_win<T, 2>, grid, tw, sm, st, mags, lgB, perm ? s1 : 1u, perm ? s2 : 1u,
+           perm ? s2inv : 1u, band, nslot, peak, floor_rel, list, count, pub);
+      else
+        kl(k_lmax_win<T, 1>, grid, tw, sm, st, mags, lgB, perm ? s1 : 1u, perm ? s2 : 1u,
+           perm ? s2inv : 1u, band, nslot, peak, floor_rel, list, count, pub);
+      post(c, "k_lmax_win", st, by);
+      return pub.seq;
+    }
     kl(k_lmax_stream<T>, grid, thr, sm, st, mags, lgB, perm ? s1 : 1u, perm ? s2 : 1u,
        perm ? s2inv : 1u, band, nslot, peak, floor_rel, list, count, pub, cand, cand_count);
     if (emitted) *emitted = cand != nullptr;
@@ -1001,8 +1015,9 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       // fold without the bucket scatter, FFT Y, and test the permuted view
       fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, &p, 1, (C*)nullptr, mg, pk, st, true);
       const unsigned mb = (unsigned)bb - 1u;
+      // B < N: the fold aliases the noise floor into most buckets
       seq = lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, ml, cnt, st, true, p.s1i & mb, p.s2i & mb,
-                          p.s2 & mb);
+                          p.s2 & mb, nullptr, nullptr, nullptr, true);
     }
     ck(cudaEventRecord(c->ev_lmax, st), "cudaEventRecord");   // the maxima list is complete
     const long long count = wait_published(c, seq, st);

@@ -361,6 +361,124 @@ k_lmax_stream(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, unsign
   }
 }
 
+// k_lmax_stream for grids where most bins pass the floor (tuner passes at
+// B < N: the fold aliases the noise into every bucket).  Each warp owns fixed
+// column groups (128 natural columns, lanes on consecutive columns) for the
+// whole band and keeps, per tested column C, the 3 x 3 neighbourhood
+// {C - s2, C, C + s2} of the previous two view rows in registers: each new
+// view row costs 3 conflict-free shared loads per bin instead of 9, and the
+// strict 8-neighbour test runs on registers.  Same ring, floor, list and
+// publication as k_lmax_stream.  GPW = column groups per warp.
+template <typename T, int GPW>
+__global__ void __launch_bounds__(512)
+k_lmax_win(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, unsigned s2i, int band,
+           int nslot, const unsigned long long* __restrict__ peak, double floor_rel,
+           int32_t* __restrict__ list, unsigned* __restrict__ count, Publish pub) {
+  pdl_wait();
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) unsigned long long s_bar[8];
+  T* ring = reinterpret_cast<T*>(smem_raw);
+  const int B = 1 << lgB;
+  const unsigned mask = (unsigned)B - 1u;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  int32_t* wbuf = reinterpret_cast<int32_t*>(ring + ((size_t)nslot << lgB)) + warp * kWarpBuf;
+  const int r0 = blockIdx.x * band;
+  const int nrow = min(band, B - r0);
+  const int nload = nrow + 2;
+  const unsigned row_bytes = (unsigned)(sizeof(T) << lgB);
+  auto issue = [&](int t) {
+    const int slot = t % nslot;
+    const unsigned r = (unsigned)(r0 - 1 + t) & mask;
+    mbar_expect_tx(&s_bar[slot], row_bytes);
+    bulk_g2s(ring + ((size_t)slot << lgB), M + ((size_t)((s1 * r) & mask) << lgB), row_bytes,
+             &s_bar[slot]);
+  };
+  if (threadIdx.x < nslot) mbar_init(&s_bar[threadIdx.x], 1);
+  mbar_fence_init();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int t = 0; t < min(nslot, nload); ++t) issue(t);
+  const double pk = fkey_inv(*peak);
+  const double fl = floor_rel * pk;
+  T flT = sizeof(T) == 4 ? (T)__double2float_ru(fl) : (T)fl;
+  if (!(pk > 0.0))
+    flT = sizeof(T) == 4 ? (T)__int_as_float(0x7f800000) : (T)__longlong_as_double(0x7ff0000000000000ll);
+  int nbuf = 0;
+  auto flush = [&]() {
+    unsigned base = 0;
+    if (lane == 0 && nbuf) base = atomicAdd(count, (unsigned)nbuf);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (int e = lane; e < nbuf; e += 32) list[base + e] = wbuf[e];
+    __syncwarp();
+    nbuf = 0;
+  };
+  unsigned phase = 0;
+  auto wait_slot = [&](int slot) {
+    mbar_wait(&s_bar[slot], (phase >> slot) & 1u);
+    phase ^= 1u << slot;
+  };
+  auto next = [&](int slot) { return slot + 1 == nslot ? 0 : slot + 1; };
+  const int groups = B >> 7;
+  T wu[GPW][4][3], wm[GPW][4][3];
+  int su = 0, sm = next(0), sd = next(sm);
+  wait_slot(su);
+  wait_slot(sm);
+  {
+    const T* up = ring + ((size_t)su << lgB);
+    const T* md = ring + ((size_t)sm << lgB);
+#pragma unroll
+    for (int q = 0; q < GPW; ++q) {
+      const int g = warp + q * nwarps;
+      if (g >= groups) break;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const unsigned C = ((unsigned)g << 7) + ((unsigned)j << 5) + (unsigned)lane;
+        const unsigned Cl = (C - s2) & mask, Cr = (C + s2) & mask;
+        wu[q][j][0] = up[Cl]; wu[q][j][1] = up[C]; wu[q][j][2] = up[Cr];
+        wm[q][j][0] = md[Cl]; wm[q][j][1] = md[C]; wm[q][j][2] = md[Cr];
+      }
+    }
+  }
+  for (int s = 0; s < nrow; ++s) {
+    wait_slot(sd);
+    const T* dn = ring + ((size_t)sd << lgB);
+    const unsigned rowbase = (unsigned)(r0 + s) << lgB;
+#pragma unroll
+    for (int q = 0; q < GPW; ++q) {
+      const int g = warp + q * nwarps;
+      if (g >= groups) break;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const unsigned C = ((unsigned)g << 7) + ((unsigned)j << 5) + (unsigned)lane;
+        const unsigned Cl = (C - s2) & mask, Cr = (C + s2) & mask;
+        const T d0 = dn[Cl], d1 = dn[C], d2 = dn[Cr];
+        const T v = wm[q][j][1];
+        const bool f = (v >= flT) & (v > wu[q][j][0]) & (v > wu[q][j][1]) & (v > wu[q][j][2]) &
+                       (v > wm[q][j][0]) & (v > wm[q][j][2]) & (v > d0) & (v > d1) & (v > d2);
+        wu[q][j][0] = wm[q][j][0]; wu[q][j][1] = wm[q][j][1]; wu[q][j][2] = wm[q][j][2];
+        wm[q][j][0] = d0; wm[q][j][1] = d1; wm[q][j][2] = d2;
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        if (!bal) continue;
+        const int n = __popc(bal);
+        if (nbuf + n > kWarpBuf) flush();
+        if (f) wbuf[nbuf + __popc(bal & ((1u << lane) - 1u))] = (int32_t)(rowbase | ((s2i * C) & mask));
+        nbuf += n;
+      }
+    }
+    __syncthreads();                           // every thread is done with load s
+    if (threadIdx.x == 0 && s + nslot < nload) issue(s + nslot);
+    su = sm;
+    sm = sd;
+    sd = next(sd);
+  }
+  __syncwarp();
+  flush();
+  if (pub.slot) {
+    __syncthreads();
+    if (threadIdx.x == 0) publish_count(count, pub.done, pub.target, pub.slot, pub.seq);
+  }
+}
+
 // Local maxima of a permuted view of |x_hat| at B = N tested only at the
 // above-floor bins `cand` (natural indices R*N + C, from the first B = N
 // pass): view (r, c) = (s1i^-1 R, s2i^-1 C) has its view neighbours at the
