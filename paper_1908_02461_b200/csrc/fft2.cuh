@@ -142,19 +142,18 @@ __device__ __forceinline__ void stockham(cplx<T>* s, int lgL, int rs, const cplx
   }
 }
 
+// per-thread running peak in the arithmetic type (|z| >= 0 and finite
+// inputs: max in T then one order-preserving key per warp equals the max key)
 template <typename T>
-__device__ __forceinline__ void emit_mag(T m, unsigned long long& best) {
-  const unsigned long long k = fkey(m);
-  best = k > best ? k : best;
+__device__ __forceinline__ void emit_mag(T m, T& best) {
+  best = fmax(best, m);
 }
 
-__device__ __forceinline__ void flush_peak(unsigned long long best, unsigned long long* peak) {
+template <typename T>
+__device__ __forceinline__ void flush_peak(T best, unsigned long long* peak) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
-    best = t > best ? t : best;
-  }
-  if ((threadIdx.x & 31) == 0 && best) atomicMax(peak, best);
+  for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(peak, fkey(best));
 }
 
 // Last Stockham pass (radix 2^LGR, Ns = L/R) read from smem, written straight
@@ -248,7 +247,7 @@ k_fftr(const Tin* src, cplx<T>* dst, T* __restrict__ mags, unsigned long long* _
   C* s = reinterpret_cast<C*>(smem_raw);
   const int rows_lg = __ffs((blockDim.x * 16 * IPT) >> lgL) - 1;
   const size_t e0 = ((size_t)blockIdx.x << rows_lg) << lgL;
-  unsigned long long best = 0;
+  T best = 0;
   bool bad = false;
   auto ld = [&](int seq, int u) {
     const Tin w = src[e0 + ((size_t)seq << lgL) + u];
@@ -259,7 +258,7 @@ k_fftr(const Tin* src, cplx<T>* dst, T* __restrict__ mags, unsigned long long* _
     const size_t o = e0 + ((size_t)seq << lgL) + k;
     if (WC) dst[o] = v;
     if (WM) {
-      const T m = cabs_(v);
+      const T m = mag_(v);
       mags[o] = m;
       emit_mag(m, best);
     }
@@ -281,13 +280,13 @@ k_fftc(const cplx<T>* src, cplx<T>* dst, T* __restrict__ mags,
   C* s = reinterpret_cast<C*>(smem_raw);
   const size_t g = blockIdx.y;
   const size_t gbase = (g << (2 * lgL)) + ((size_t)blockIdx.x << lgcc);
-  unsigned long long best = 0;
+  T best = 0;
   auto ld = [&](int c, int u) { return src[gbase + ((size_t)u << lgL) + c]; };
   auto st = [&](int c, int k, C v) {
     const size_t o = gbase + ((size_t)k << lgL) + c;
     if (WC) dst[o] = v;
     if (WM) {
-      const T m = cabs_(v);
+      const T m = mag_(v);
       mags[o] = m;
       emit_mag(m, best);
     }
@@ -311,13 +310,13 @@ k_fftc1(const cplx<T>* src, cplx<T>* dst, T* __restrict__ mags,
   C* s = reinterpret_cast<C*>(smem_raw);
   const size_t g = blockIdx.y;
   const size_t gbase = (g << (2 * lgL)) + ((size_t)blockIdx.x << lgcc);
-  unsigned long long best = 0;
+  T best = 0;
   auto ld = [&](int c, int u) { return src[gbase + ((size_t)u << lgL) + c]; };
   auto st = [&](int c, int k, C v) {
     const size_t o = gbase + ((size_t)k << lgL) + c;
     if (WC) dst[o] = v;
     if (WM) {
-      const T m = cabs_(v);
+      const T m = mag_(v);
       mags[o] = m;
       emit_mag(m, best);
     }
@@ -361,13 +360,13 @@ k_fftcB(const cplx<T>* __restrict__ src, cplx<T>* __restrict__ dst, T* __restric
   const int k1 = blockIdx.y;
   const size_t g = blockIdx.z;
   const size_t gbase = (g << (2 * lgL)) + ((size_t)blockIdx.x << lgcc);
-  unsigned long long best = 0;
+  T best = 0;
   auto ld = [&](int c, int n2) { return src[gbase + ((size_t)((k1 << lgL2) + n2) << lgL) + c]; };
   auto st = [&](int c, int k2, C v) {
     const size_t o = gbase + ((size_t)(k1 + (k2 << lgL1)) << lgL) + c;
     if (WC) dst[o] = v;
     if (WM) {
-      const T m = cabs_(v);
+      const T m = mag_(v);
       mags[o] = m;
       emit_mag(m, best);
     }
