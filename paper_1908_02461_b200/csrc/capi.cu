@@ -385,7 +385,8 @@ PermPack identity_pack(int g) {
 template <typename T, typename Tin>
 FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTables& tb,
                     const Perm* hp, int g, void* y_direct, cudaStream_t st,
-                    unsigned long long* zero_peak = nullptr, bool natural = false) {
+                    unsigned long long* zero_peak = nullptr, bool natural = false,
+                    const Perm* spec_q = nullptr, void* spec_y = nullptr) {
   using C = cplx<T>;
   const int B = 1 << lgB;
   const size_t BB = (size_t)B * B;
@@ -406,6 +407,18 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
   const double sup = (double)tb.support[lgB];
   // window weights are gathered from the window table inside the fold
   // kernels; `natural` places bucket (rho, kappa) at row rho, column kappa
+  if (spec_q) {
+    // pass t's fold at B plus the next pass's fold at 2B from one read
+    if (!(g == 1 && B >= 512 && lgN - lgB <= 5 && lgN - lgB >= 2 && y_direct && spec_y && natural))
+      fail(SFFT2D_ERR_STATE, "speculative fold outside its geometry");
+    const T* space2 = (const T*)tb.space[prec_of<T>()] + ((size_t)(lgB + 1) << lgN);
+    const double by = sup * sup * sizeof(Tin) + 5.0 * (double)BB * sizeof(C);
+    pre(c, st);
+    kl(k_fold_wide2<Tin, T>, dim3(B / 256, B), 128, 0, st, x, space, space2, pp.p[0], *spec_q, lgN,
+       lgB, (C*)y_direct, (C*)spec_y, zero_peak);
+    post(c, "k_fold_wide2", st, by);
+    return FoldOut{y_direct, 1};
+  }
   if (g == 1 && B >= 512 && lgN - lgB <= 5 && y_direct) {
     // wide single-loop fold, grid written directly
     const double by = sup * sup * sizeof(Tin) + (double)BB * sizeof(C);
@@ -464,7 +477,8 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
 template <typename T, typename Tin>
 void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTables& tb,
                    const Perm* hp, int nloops, cplx<T>* spec, T* mags, unsigned long long* peaks,
-                   cudaStream_t st, bool natural = false) {
+                   cudaStream_t st, bool natural = false, cplx<T>* prefolded = nullptr,
+                   const Perm* spec_q = nullptr, cplx<T>* spec_y = nullptr) {
   using C = cplx<T>;
   const int B = 1 << lgB;
   const int P = prec_of<T>();
@@ -486,8 +500,16 @@ void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTable
     unsigned long long* pk = peaks ? peaks + g0 : nullptr;
     // bucket grid y (permuted fold) for this group
     C* y = (small && sp) ? sp : (C*)ws(c, "fold_y", (size_t)g * BB * sizeof(C));
-    const FoldOut fo = fold_launch<T, Tin>(c, x, lgN, lgB, tb, hp + g0, g, y, st,
-                                           (nloops == 1) ? pk : nullptr, natural);
+    FoldOut fo{y, 1};
+    if (prefolded) {   // the previous pass's speculative fold is this pass's grid
+      if (nloops != 1 || small) fail(SFFT2D_ERR_STATE, "prefolded grid for a multi-loop pass");
+      y = prefolded;
+      fo = FoldOut{y, 1};
+      if (pk) ck(cudaMemsetAsync(pk, 0, sizeof(unsigned long long), st), "memset");
+    } else {
+      fo = fold_launch<T, Tin>(c, x, lgN, lgB, tb, hp + g0, g, y, st, (nloops == 1) ? pk : nullptr,
+                               natural, spec_q, spec_y);
+    }
     C* dst = (C*)fo.data;
     struct { int Z; } gm{fo.Z};
     if (small) {
@@ -963,6 +985,10 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   bool cand_pending = false, cand_ready = false;
   long long cand_n = 0;
 
+  // speculative next-pass grid (k_fold_wide2), valid for permutation index spec_pi at spec_b
+  static const bool spec_on = getenv("SFFT2D_NO_SPEC") == nullptr;
+  int spec_pi = -1, spec_b = 0;
+  C* spec_grid = nullptr;
   auto run_pass = [&](int bb) -> long long {
     const int pi = pidx++;
     const Perm p = ps.get(pi, st);
@@ -1013,7 +1039,22 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       // |Z[k1,k2]| = |Y^[s1i k1, s2i k2]| for the natural-order fold Y
       // (Z[a,b] = Y[s1 a + t1, s2 b + t2]; the tau shifts are a phase):
       // fold without the bucket scatter, FFT Y, and test the permuted view
-      fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, &p, 1, (C*)nullptr, mg, pk, st, true);
+      // speculation: B >= 512 folds also produce the next pass's grid at 2B
+      // (its permutation is the next draw whatever the next pass is; with
+      // estimation loops to follow that draw is always made, so drawing it
+      // early leaves the caller's Generator exactly where the reference does)
+      C* pre_y = (spec_pi == pi && spec_b == bb) ? spec_grid : nullptr;
+      spec_pi = -1;
+      const Perm* sq = nullptr;
+      C* sy = nullptr;
+      if (!pre_y && spec_on && do_estimate && bb >= 512 && 2 * bb < n && lgN - lgb <= 5 &&
+          lgN - lgb >= 2) {
+        sq = &ps.get(pi + 1, st);
+        sy = spec_grid = (C*)ws(c, "spec_y", 4 * BB * sizeof(C));
+        spec_pi = pi + 1;
+        spec_b = 2 * bb;
+      }
+      fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, &p, 1, (C*)nullptr, mg, pk, st, true, pre_y, sq, sy);
       const unsigned mb = (unsigned)bb - 1u;
       // B < N: the fold aliases the noise floor into most buckets
       seq = lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, ml, cnt, st, true, p.s1i & mb, p.s2i & mb,

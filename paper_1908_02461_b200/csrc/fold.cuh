@@ -501,6 +501,113 @@ k_fold_wide(const Tin* __restrict__ x, const T* __restrict__ space, Perm p, int 
   }
 }
 
+// k_fold_wide for TWO hash passes from one read of x: pass t's natural fold
+// Y1 at B (permutation p, window `space`) and, speculatively, the next pass's
+// natural fold Y2 at 2B (permutation q, window `space2`).  The tuner almost
+// always doubles B (tuner.py:121-130, ratio > delta2), and the next pass's
+// permutation is already known (draws do not depend on B), so one HBM read of
+// the image serves both passes; if the count of pass t sends the tuner
+// elsewhere, Y2 is discarded.  Bucket row rho of Y1 collects rows
+// rho + jB; Y2's rows rho and rho + B are the even / odd j of the same rows
+// (columns likewise), so the CTA that owns Y1's (rho, kappa) owns Y2's four
+// buckets (rho + {0, B}, kappa + {0, B}).  CTA = one bucket row x 256 columns;
+// 16 row-segment loads in flight per thread (~136 registers, 3 CTAs per SM).
+template <typename Tin, typename T>
+__global__ void __launch_bounds__(128)
+k_fold_wide2(const Tin* __restrict__ x, const T* __restrict__ space, const T* __restrict__ space2,
+             Perm p, Perm q, int lgN, int lgB, cplx<T>* __restrict__ y, cplx<T>* __restrict__ y2,
+             unsigned long long* __restrict__ zero_peak) {
+  pdl_wait();
+  using C = cplx<T>;
+  __shared__ T s_w[32], s_w2[32];
+  if (zero_peak && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) *zero_peak = 0ull;
+  const int B = 1 << lgB;
+  const unsigned maskN = (1u << lgN) - 1u;
+  const int A = 1 << (lgN - lgB);            // aliases per axis (4 .. 32, even)
+  const int rho = blockIdx.y;
+  const int kap = blockIdx.x * 256 + threadIdx.x * 2;   // 128 threads x 2 columns
+  for (int j = threadIdx.x; j < A; j += blockDim.x) {
+    const unsigned r = (unsigned)(rho + (j << lgB));
+    s_w[j] = __ldg(space + ((p.s1i * (r - p.t1)) & maskN));
+    s_w2[j] = __ldg(space2 + ((q.s1i * (r - q.t1)) & maskN));
+  }
+  __syncthreads();
+  C acc[2], acc2[2][2][2];                   // acc2[column parity][row parity][column]
+#pragma unroll
+  for (int cq = 0; cq < 2; ++cq) {
+    acc[cq] = mk<T>(0, 0);
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < 2; ++b) acc2[a][b][cq] = mk<T>(0, 0);
+  }
+  for (int i0 = 0; i0 < A; i0 += 2) {         // column aliases i0 (even), i0 + 1 (odd)
+    T wc[2][2], wc2[2][2];
+    C u[2][2], u2[2][2][2];                  // [ii][cq], [ii][row parity][cq]
+#pragma unroll
+    for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+      for (int cq = 0; cq < 2; ++cq) {
+        const unsigned c = (unsigned)(kap + ((i0 + ii) << lgB) + cq);
+        wc[ii][cq] = __ldg(space + ((p.s2i * (c - p.t2)) & maskN));
+        wc2[ii][cq] = __ldg(space2 + ((q.s2i * (c - q.t2)) & maskN));
+        u[ii][cq] = mk<T>(0, 0);
+        u2[ii][0][cq] = u2[ii][1][cq] = mk<T>(0, 0);
+      }
+    // row aliases in batches of 8: all 16 row-segment loads of a batch are
+    // issued before the first FMA (A = 4 runs one half batch)
+    for (int jb = 0; jb < A; jb += 8) {
+      C v[8][2][2];                          // [row alias in batch][ii][cq]
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+        for (int ii = 0; ii < 2; ++ii)
+          if (jj < 4 || A > 4)
+            ColLoad<Tin, T, 2>::ld(x + kap + ((i0 + ii) << lgB) + ((size_t)(rho + ((jb + jj) << lgB)) << lgN),
+                                   v[jj][ii]);
+#pragma unroll
+      for (int jj = 0; jj < 8; ++jj) {
+        if (jj >= 4 && A <= 4) break;
+        const int jp = jj & 1;
+        const T w = s_w[jb + jj], w2 = s_w2[jb + jj];
+#pragma unroll
+        for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+          for (int cq = 0; cq < 2; ++cq) {
+            const C vv = v[jj][ii][cq];
+            u[ii][cq].x = fma(w, vv.x, u[ii][cq].x);
+            u[ii][cq].y = fma(w, vv.y, u[ii][cq].y);
+            u2[ii][jp][cq].x = fma(w2, vv.x, u2[ii][jp][cq].x);
+            u2[ii][jp][cq].y = fma(w2, vv.y, u2[ii][jp][cq].y);
+          }
+      }
+    }
+#pragma unroll
+    for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+      for (int cq = 0; cq < 2; ++cq) {
+        acc[cq].x = fma(wc[ii][cq], u[ii][cq].x, acc[cq].x);
+        acc[cq].y = fma(wc[ii][cq], u[ii][cq].y, acc[cq].y);
+#pragma unroll
+        for (int jp = 0; jp < 2; ++jp) {
+          acc2[ii][jp][cq].x = fma(wc2[ii][cq], u2[ii][jp][cq].x, acc2[ii][jp][cq].x);
+          acc2[ii][jp][cq].y = fma(wc2[ii][cq], u2[ii][jp][cq].y, acc2[ii][jp][cq].y);
+        }
+      }
+  }
+  y[(size_t)rho * B + kap] = acc[0];
+  y[(size_t)rho * B + kap + 1] = acc[1];
+  const size_t B2 = (size_t)B << 1;
+#pragma unroll
+  for (int ii = 0; ii < 2; ++ii)
+#pragma unroll
+    for (int jp = 0; jp < 2; ++jp) {
+      C* o = y2 + (size_t)(rho + jp * B) * B2 + kap + ii * B;
+      o[0] = acc2[ii][jp][0];
+      o[1] = acc2[ii][jp][1];
+    }
+}
+
 // Sum the Z partials in fixed order and scatter to the permuted bucket grid.
 template <typename T>
 __global__ void k_fold_reduce(const cplx<T>* __restrict__ part, int Z, int nloops, int lgB,

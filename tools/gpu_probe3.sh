@@ -14,3 +14,4 @@ for K in ${PROBE_KERNELS:-k_vote_rows k_fftc_cl}; do
   cp /tmp/$K.ncu-rep gpurun_out/ 2>/dev/null
 done
 timeout 600 python tools/concurrency.py fp32 > gpurun_out/conc.txt 2>&1
+if [ -n "${COMPARE_ENV:-}" ]; then env $COMPARE_ENV timeout 600 python tools/concurrency.py fp32 > gpurun_out/conc_compare.txt 2>&1; fi
