@@ -89,6 +89,13 @@ typedef struct {
   int32_t perms_used;       /* permutations consumed from the caller's list   */
   int64_t n_votes;          /* distinct voted coordinates (detect_sparsity)   */
   int64_t n_candidates;     /* coordinates at or above the vote threshold     */
+  int32_t perms_drawn;      /* permutations drawn from the caller's generator:
+                               the speculative fold draws the next pass's one
+                               early, so when no estimation loop follows it
+                               can exceed perms_used by one — a caller sharing
+                               the generator with the reference restores its
+                               state and redraws perms_used permutations    */
+  int32_t pad_;
 } sfft2d_tuner_state;
 
 typedef struct {

@@ -64,7 +64,8 @@ class TunerStateC(ctypes.Structure):
                 ("converged", ctypes.c_int32), ("detected_k", ctypes.c_int64),
                 ("b_detect", ctypes.c_int32), ("b_estimate", ctypes.c_int32),
                 ("vote_passes", ctypes.c_int32), ("perms_used", ctypes.c_int32),
-                ("n_votes", ctypes.c_int64), ("n_candidates", ctypes.c_int64)]
+                ("n_votes", ctypes.c_int64), ("n_candidates", ctypes.c_int64),
+                ("perms_drawn", ctypes.c_int32), ("pad_", ctypes.c_int32)]
 
 
 class ResultC(ctypes.Structure):

@@ -1214,6 +1214,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     }
     S->n_votes = nv;
     S->perms_used = pidx;
+    S->perms_drawn = (int32_t)ps.used();
     c->votes_count = nv;
     c->has_votes = true;
     return;
@@ -1226,6 +1227,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   if (maxc == 0 || !have_votes) {
     nan_check(true);
     S->perms_used = pidx;
+    S->perms_drawn = (int32_t)ps.used();
     res->perms_used = pidx;
     return;
   }
@@ -1244,6 +1246,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   S->n_candidates = m;
   if (m == 0) {
     S->perms_used = pidx;
+    S->perms_drawn = (int32_t)ps.used();
     res->perms_used = pidx;
     return;
   }
@@ -1251,6 +1254,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   const int best = S->b_estimate;
   if (std::max(1LL, 2 * k) > (long long)best * best) {
     S->perms_used = pidx;
+    S->perms_drawn = (int32_t)ps.used();
     fail(SFFT2D_ERR_CONFIG, "d_factor*k = " + std::to_string(std::max(1LL, 2 * k)) +
                                 " exceeds the " + std::to_string(best) + "x" +
                                 std::to_string(best) + " bin budget");
@@ -1264,6 +1268,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
                               dense ? dscratch : nullptr);
   pidx += L;
   S->perms_used = pidx;
+  S->perms_drawn = (int32_t)ps.used();
   res->perms_used = pidx;
 }
 

@@ -179,6 +179,19 @@ def _is_tensor(x) -> bool:
     return is_torch_tensor(x)
 
 
+def reconcile_generator(gen, snapshot, n: int, drawn: int, used: int) -> None:
+    """The speculative fold draws the next pass's permutation before the tuner
+    knows whether a next pass or an estimation loop will consume it; when none
+    did (drawn > used), put the caller's Generator where the reference leaves
+    it: back to the call's snapshot, then replay the `used` permutation draws
+    (hashing.draw_permutation = the reference's four integers() calls)."""
+    if drawn <= used:
+        return
+    gen.bit_generator.state = snapshot
+    for _ in range(used):
+        draw_permutation(n, gen)
+
+
 def _run_ats(x, cfg: TunerConfig, est_loops: int, rng, precision, device, estimate: bool):
     torch = _native._torch()
     img = as_device_image(x, device, upload=False)
@@ -211,6 +224,8 @@ def _run_ats(x, cfg: TunerConfig, est_loops: int, rng, precision, device, estima
         ctx.last_call_us = (time.perf_counter() - t_call) * 1e6
         if rc == _native.ERR_VALUE and snapshot is not None:
             gen.bit_generator.state = snapshot   # the reference validates x before drawing
+        elif rc in (_native.OK, _native.ERR_CONFIG) and snapshot is not None:
+            reconcile_generator(gen, snapshot, n, int(sc.perms_drawn), int(sc.perms_used))
         ctx.check(rc)
         ctx.last_launches = int(res.gpu_launches)
         state = _state(sc)

@@ -255,6 +255,19 @@ def test_atsfft_generator_advance_matches_oracle():
     assert g1.integers(1 << 40) == g2.integers(1 << 40)
 
 
+def test_atsfft_generator_advance_with_speculative_fold():
+    # N = 2048: B >= 512 passes fold the next pass's 2B grid early (its
+    # permutation drawn ahead); results and the caller's Generator must match
+    img = P.sparse_image(2048, 30, 71, snr_db=20.0)
+    g1, g2 = np.random.default_rng(72), np.random.default_rng(72)
+    out, state = P.atsfft2d(img.x, P.TunerConfig(), 8, g1)
+    (cs, vs), ostate = O.atsfft(img.x, O.TunerParams(), 8, g2)
+    assert [(b, c) for b, c, _ in state.history] == [(b, c) for b, c, _ in ostate["history"]]
+    assert any(b >= 512 for b, _, _ in state.history)
+    _close_values(out, O.as_dict((cs, vs)), TOL["fp64"])
+    assert g1.integers(1 << 40) == g2.integers(1 << 40)
+
+
 def test_atsfft_device_tensor_input_matches_numpy():
     import torch
     g = golden("c2_ats")

@@ -183,3 +183,24 @@ def test_every_kernel_waits_on_its_predecessor():
             if "pdl_wait()" not in first_stmt:
                 missing.append(f"{os.path.basename(path)}:{name[0] if name else '?'}")
     assert not missing, missing
+
+
+def test_generator_reconciled_after_speculative_draw():
+    # a permutation drawn ahead (speculative fold) but never consumed must not
+    # advance the caller's Generator past where the reference leaves it
+    from paper_1908_02461_b200.hashing import draw_permutation
+    from paper_1908_02461_b200.tuner import reconcile_generator
+    n, used = 4096, 11
+    g = np.random.default_rng(123)
+    snap = g.bit_generator.state
+    for _ in range(used + 1):
+        draw_permutation(n, g)
+    reconcile_generator(g, snap, n, used + 1, used)
+    ref = np.random.default_rng(123)
+    for _ in range(used):
+        draw_permutation(n, ref)
+    assert g.bit_generator.state == ref.bit_generator.state
+    # nothing to undo when every draw was consumed
+    before = g.bit_generator.state
+    reconcile_generator(g, snap, n, used, used)
+    assert g.bit_generator.state == before
