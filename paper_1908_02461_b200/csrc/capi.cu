@@ -321,10 +321,12 @@ Publish make_publish(sfft2d_ctx* c, unsigned grid) {
 unsigned wait_published(sfft2d_ctx* c, unsigned seq, cudaStream_t st) {
   const auto t0 = std::chrono::steady_clock::now();
   volatile unsigned* h = c->mapped_h;
+  volatile unsigned long long* h64 = reinterpret_cast<volatile unsigned long long*>(c->mapped_h);
   for (unsigned long spin = 0;; ++spin) {
-    if (h[0] == seq) {
+    const unsigned long long word = *h64;   // (count << 32) | seq, one device store
+    if ((unsigned)word == seq) {
       std::atomic_thread_fence(std::memory_order_acquire);
-      const unsigned v = h[1];
+      const unsigned v = (unsigned)(word >> 32);
       c->sync_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
       return v;
     }

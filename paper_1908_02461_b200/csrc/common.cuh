@@ -123,8 +123,8 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 // Publish a final per-launch count to mapped (zero-copy) host memory: every
 // CTA calls this once after its contribution to *count is done; the CTA that
 // takes ticket `target - 1` of the monotonic `done` counter is the last one and
-// writes slot[1] = count, then slot[0] = seq (system-scope fences), so the
-// host can spin on seq without a stream synchronisation.
+// writes (seq, count) as one 8-byte word into slot[0..1], so the host can spin
+// on seq without a stream synchronisation.
 __device__ __forceinline__ void publish_count(unsigned* count, unsigned* done, unsigned target,
                                               volatile unsigned* slot, unsigned seq,
                                               unsigned* count2 = nullptr) {
@@ -133,11 +133,14 @@ __device__ __forceinline__ void publish_count(unsigned* count, unsigned* done, u
   if (t + 1u == target) {
     __threadfence();
     const unsigned v = atomicAdd(count, 0u);
-    if (count2) slot[2] = atomicAdd(count2, 0u);   // optional second count (same publication)
-    slot[1] = v;
-    __threadfence_system();
-    slot[0] = seq;
-    __threadfence_system();
+    if (count2) {   // optional second count: must land before the (seq, count) word
+      slot[2] = atomicAdd(count2, 0u);
+      __threadfence_system();
+    }
+    // (seq, count) in ONE aligned 8-byte store: the host sees both or neither,
+    // so no system-scope fence (a ~2 us PCIe round trip each) is needed
+    *reinterpret_cast<volatile unsigned long long*>(slot) =
+        ((unsigned long long)v << 32) | (unsigned long long)seq;
   }
 }
 
