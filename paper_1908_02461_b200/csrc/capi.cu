@@ -330,7 +330,13 @@ unsigned wait_published(sfft2d_ctx* c, unsigned seq, cudaStream_t st) {
       c->sync_us += std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
       return v;
     }
-    if ((spin & 1023) == 1023) {
+#if defined(__x86_64__)
+    __builtin_ia32_pause();   // spin politely (sibling hyperthread, power)
+#endif
+    // error / lost-publication check: a driver call (it takes the context lock
+    // that every other in-flight transform's launches need), so only after
+    // ~65K spins (tens of us) and then every ~65K spins
+    if ((spin & 65535) == 65535) {
       const cudaError_t e = cudaStreamQuery(st);
       if (e != cudaErrorNotReady && e != cudaSuccess) ck(e, "tuner pass");
       if (e == cudaSuccess && h[0] != seq) fail(SFFT2D_ERR_CUDA, "count publication lost");
@@ -388,7 +394,7 @@ template <typename T, typename Tin>
 FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTables& tb,
                     const Perm* hp, int g, void* y_direct, cudaStream_t st,
                     unsigned long long* zero_peak = nullptr, bool natural = false,
-                    const Perm* spec_q = nullptr, void* spec_y = nullptr) {
+                    const Perm* spec_q = nullptr, void* spec_y = nullptr, int* spec_z = nullptr) {
   using C = cplx<T>;
   const int B = 1 << lgB;
   const size_t BB = (size_t)B * B;
@@ -409,8 +415,34 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
   const double sup = (double)tb.support[lgB];
   // window weights are gathered from the window table inside the fold
   // kernels; `natural` places bucket (rho, kappa) at row rho, column kappa
+  const int seg_cols0 = kRingSegBytes / (int)sizeof(Tin);
+  if (spec_q && B < 512) {
+    // TMA ring fold of pass t at B and of the next pass at 2B <= 512, one read
+    if (!(g == 1 && 2 * B <= 512 && gm.TW == 512 && (1 << lgN) >= seg_cols0 && y_direct &&
+          spec_y && natural && spec_z))
+      fail(SFFT2D_ERR_STATE, "speculative ring fold outside its geometry");
+    const T* space2 = (const T*)tb.space[prec_of<T>()] + ((size_t)(lgB + 1) << lgN);
+    const int nslot = 3;
+    FoldGeom gr = gm;
+    const int aliases = (1 << lgN) >> lgB;
+    const int Z = (int)std::max(1L, std::min<long>(aliases, 2L * kNumSMs / B));
+    int rpc = (aliases + Z - 1) / Z;
+    if (rpc > kFoldMaxRows) rpc = kFoldMaxRows;
+    gr.rpc = rpc;
+    gr.Z = (aliases + rpc - 1) / rpc;
+    gr.ktiles = 1;
+    C* dstr = (gr.Z == 1) ? (C*)y_direct : (C*)ws(c, "fold_part", (size_t)gr.Z * BB * sizeof(C));
+    const size_t dynr = (size_t)nslot * kRingSegBytes + 3 * 512 * sizeof(C);
+    pre(c, st);
+    kl(k_fold_ring2<Tin, T>, dim3(1, B, gr.Z), 256, dynr, st, x, space, space2, pp.p[0], *spec_q, gr,
+       nslot, dstr, (C*)spec_y, zero_peak);
+    post(c, "k_fold_ring2", st, sup * sup * sizeof(Tin) + 5.0 * gr.Z * BB * sizeof(C));
+    *spec_z = gr.Z;
+    return FoldOut{dstr, gr.Z};
+  }
   if (spec_q) {
     // pass t's fold at B plus the next pass's fold at 2B from one read
+    if (spec_z) *spec_z = 1;
     if (!(g == 1 && B >= 512 && lgN - lgB <= 5 && lgN - lgB >= 2 && y_direct && spec_y && natural))
       fail(SFFT2D_ERR_STATE, "speculative fold outside its geometry");
     const T* space2 = (const T*)tb.space[prec_of<T>()] + ((size_t)(lgB + 1) << lgN);
@@ -480,7 +512,8 @@ template <typename T, typename Tin>
 void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTables& tb,
                    const Perm* hp, int nloops, cplx<T>* spec, T* mags, unsigned long long* peaks,
                    cudaStream_t st, bool natural = false, cplx<T>* prefolded = nullptr,
-                   const Perm* spec_q = nullptr, cplx<T>* spec_y = nullptr) {
+                   const Perm* spec_q = nullptr, cplx<T>* spec_y = nullptr, int pre_z = 1,
+                   int* spec_z = nullptr) {
   using C = cplx<T>;
   const int B = 1 << lgB;
   const int P = prec_of<T>();
@@ -503,14 +536,14 @@ void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTable
     // bucket grid y (permuted fold) for this group
     C* y = (small && sp) ? sp : (C*)ws(c, "fold_y", (size_t)g * BB * sizeof(C));
     FoldOut fo{y, 1};
-    if (prefolded) {   // the previous pass's speculative fold is this pass's grid
+    if (prefolded) {   // the previous pass's speculative fold is this pass's grid (or partials)
       if (nloops != 1 || small) fail(SFFT2D_ERR_STATE, "prefolded grid for a multi-loop pass");
-      y = prefolded;
-      fo = FoldOut{y, 1};
+      if (pre_z == 1) y = prefolded;
+      fo = FoldOut{prefolded, pre_z};
       if (pk) ck(cudaMemsetAsync(pk, 0, sizeof(unsigned long long), st), "memset");
     } else {
       fo = fold_launch<T, Tin>(c, x, lgN, lgB, tb, hp + g0, g, y, st, (nloops == 1) ? pk : nullptr,
-                               natural, spec_q, spec_y);
+                               natural, spec_q, spec_y, spec_z);
     }
     C* dst = (C*)fo.data;
     struct { int Z; } gm{fo.Z};
@@ -989,7 +1022,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
 
   // speculative next-pass grid (k_fold_wide2), valid for permutation index spec_pi at spec_b
   static const bool spec_on = getenv("SFFT2D_NO_SPEC") == nullptr;
-  int spec_pi = -1, spec_b = 0;
+  int spec_pi = -1, spec_b = 0, spec_z = 1;
   C* spec_grid = nullptr;
   auto run_pass = [&](int bb) -> long long {
     const int pi = pidx++;
@@ -1046,17 +1079,22 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       // estimation loops to follow that draw is always made, so drawing it
       // early leaves the caller's Generator exactly where the reference does)
       C* pre_y = (spec_pi == pi && spec_b == bb) ? spec_grid : nullptr;
+      const int pre_z = spec_z;
       spec_pi = -1;
       const Perm* sq = nullptr;
       C* sy = nullptr;
-      if (!pre_y && spec_on && do_estimate && bb >= 512 && 2 * bb < n && lgN - lgb <= 5 &&
-          lgN - lgb >= 2) {
+      // ring pair (128 <= B <= 256, full-support rows) or wide pair (B >= 512)
+      const bool ring_pair = bb >= 128 && 2 * bb <= 512 && (size_t)n * sizeof(Tin) >= kRingSegBytes;
+      const bool wide_pair = bb >= 512 && lgN - lgb <= 5 && lgN - lgb >= 2;
+      if (!pre_y && spec_on && do_estimate && 2 * bb < n && (ring_pair || wide_pair)) {
         sq = &ps.get(pi + 1, st);
-        sy = spec_grid = (C*)ws(c, "spec_y", 4 * BB * sizeof(C));
+        const int zmax = ring_pair ? std::max(1, (int)(2L * kNumSMs / bb)) : 1;
+        sy = spec_grid = (C*)ws(c, "spec_y", (size_t)zmax * 4 * BB * sizeof(C));
         spec_pi = pi + 1;
         spec_b = 2 * bb;
       }
-      fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, &p, 1, (C*)nullptr, mg, pk, st, true, pre_y, sq, sy);
+      fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, &p, 1, (C*)nullptr, mg, pk, st, true, pre_y, sq, sy,
+                            pre_z, &spec_z);
       const unsigned mb = (unsigned)bb - 1u;
       // B < N: the fold aliases the noise floor into most buckets
       seq = lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, ml, cnt, st, true, p.s1i & mb, p.s2i & mb,

@@ -400,6 +400,153 @@ k_fold_ring(const Tin* __restrict__ x, const T* __restrict__ space, Perm p, Fold
   }
 }
 
+// k_fold_ring for TWO hash passes from one read (see k_fold_wide2): pass t's
+// natural fold at B < 512 (permutation p, window `space`) and the next pass's
+// at 2B <= 512 (permutation q, window `space2`).  CTA (rho, z) streams the rows
+// rho + jB of its alias chunk; for the 2B grid those rows are bucket row
+// rho + (j & 1) B.  Every bucket column of both grids is (cp + q) mod B or 2B
+// for the thread's columns cp + q (512 = 0 mod 2B), so each thread keeps
+// acc (B) and acc2[j & 1] (2B) for its two columns; the weight products
+// wr * wc are formed per row and block (no per-block row sums u[] — those
+// would not fit twice in registers).  Rows with a zero weight in both passes
+// are skipped.  Partials [Z][B][B] and [Z][2B][2B] (Z = 1: the grids).
+template <typename Tin, typename T>
+__global__ void __launch_bounds__(256)
+k_fold_ring2(const Tin* __restrict__ x, const T* __restrict__ space,
+             const T* __restrict__ space2, Perm p, Perm q, FoldGeom gm, int nslot,
+             cplx<T>* __restrict__ dst, cplx<T>* __restrict__ dst2,
+             unsigned long long* __restrict__ zero_peak = nullptr) {
+  pdl_wait();
+  using C = cplx<T>;
+  constexpr int SEGC = kRingSegBytes / (int)sizeof(Tin);
+  constexpr int NB = SEGC / 512;
+  if (zero_peak && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) *zero_peak = 0ull;
+  __shared__ T s_w[kFoldMaxRows], s_w2[kFoldMaxRows];
+  __shared__ int s_rows[kFoldMaxRows];
+  __shared__ int s_nnz;
+  __shared__ __align__(8) unsigned long long s_bar[8];
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Tin* ring = reinterpret_cast<Tin*>(smem_raw);
+  C* red = reinterpret_cast<C*>(smem_raw + (size_t)nslot * kRingSegBytes);   // 3 x 512
+
+  const int N = 1 << gm.lgN, B = 1 << gm.lgB;
+  const unsigned maskN = (unsigned)N - 1u;
+  const int rho = blockIdx.y, z = blockIdx.z;
+  const int aliases = N >> gm.lgB;
+  const int j0 = z * gm.rpc;
+  const int cnt = min(gm.rpc, aliases - j0);
+  const int tid = threadIdx.x;
+  for (int jj = tid; jj < cnt; jj += blockDim.x) {
+    const unsigned r = (unsigned)(rho + (j0 + jj) * B);
+    s_w[jj] = __ldg(space + ((p.s1i * (r - p.t1)) & maskN));
+    s_w2[jj] = __ldg(space2 + ((q.s1i * (r - q.t1)) & maskN));
+  }
+  if (tid < nslot) mbar_init(&s_bar[tid], 1);
+  mbar_fence_init();
+  __syncthreads();
+  if (tid < 32) {
+    int base = 0;
+    for (int c0 = 0; c0 < cnt; c0 += 32) {
+      const int jj = c0 + tid;
+      const bool nz = jj < cnt && (s_w[jj] != (T)0 || s_w2[jj] != (T)0);
+      const unsigned bal = __ballot_sync(0xffffffffu, nz);
+      if (nz) s_rows[base + __popc(bal & ((1u << tid) - 1u))] = jj;
+      base += __popc(bal);
+    }
+    if (tid == 0) s_nnz = base;
+  }
+  __syncthreads();
+  const int nnz = s_nnz;
+  const int cp = tid * 2;
+  C acc[2], acc2[2][2];                       // acc2[row parity][column]
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    acc[k] = mk<T>(0, 0);
+    acc2[0][k] = acc2[1][k] = mk<T>(0, 0);
+  }
+  unsigned use = 0;
+  for (int cg = 0; cg < N / SEGC; ++cg) {
+    T wc[NB][2], wc2[NB][2];
+    bool any = false;
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const unsigned c = (unsigned)(cg * SEGC + b * 512 + cp + k);
+        wc[b][k] = __ldg(space + ((p.s2i * (c - p.t2)) & maskN));
+        wc2[b][k] = __ldg(space2 + ((q.s2i * (c - q.t2)) & maskN));
+        any |= (wc[b][k] != (T)0) | (wc2[b][k] != (T)0);
+      }
+    if (!__syncthreads_or(any)) continue;
+    auto issue = [&](int i) {
+      const int slot = (int)((use + i) % nslot);
+      const size_t r = (size_t)(rho + (j0 + s_rows[i]) * B);
+      mbar_expect_tx(&s_bar[slot], kRingSegBytes);
+      bulk_g2s(ring + (size_t)slot * SEGC, x + (r << gm.lgN) + (size_t)cg * SEGC, kRingSegBytes,
+               &s_bar[slot]);
+    };
+    if (tid == 0)
+      for (int i = 0; i < min(nslot, nnz); ++i) issue(i);
+    for (int i = 0; i < nnz; ++i) {
+      const unsigned k = use + i;
+      const int slot = (int)(k % nslot);
+      mbar_wait(&s_bar[slot], (k / nslot) & 1u);
+      const int jr = s_rows[i];
+      const T wr = s_w[jr], wr2 = s_w2[jr];
+      const int par = (j0 + jr) & 1;
+      const Tin* row = ring + (size_t)slot * SEGC;
+      C t1[2] = {mk<T>(0, 0), mk<T>(0, 0)}, t2[2] = {mk<T>(0, 0), mk<T>(0, 0)};
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        C v[2];
+        lds_pair<T>(row + b * 512 + cp, v);
+#pragma unroll
+        for (int kk = 0; kk < 2; ++kk) {
+          t1[kk].x = fma(wc[b][kk], v[kk].x, t1[kk].x);
+          t1[kk].y = fma(wc[b][kk], v[kk].y, t1[kk].y);
+          t2[kk].x = fma(wc2[b][kk], v[kk].x, t2[kk].x);
+          t2[kk].y = fma(wc2[b][kk], v[kk].y, t2[kk].y);
+        }
+      }
+#pragma unroll
+      for (int kk = 0; kk < 2; ++kk) {
+        acc[kk].x = fma(wr, t1[kk].x, acc[kk].x);
+        acc[kk].y = fma(wr, t1[kk].y, acc[kk].y);
+        if (par) {
+          acc2[1][kk].x = fma(wr2, t2[kk].x, acc2[1][kk].x);
+          acc2[1][kk].y = fma(wr2, t2[kk].y, acc2[1][kk].y);
+        } else {
+          acc2[0][kk].x = fma(wr2, t2[kk].x, acc2[0][kk].x);
+          acc2[0][kk].y = fma(wr2, t2[kk].y, acc2[0][kk].y);
+        }
+      }
+      __syncthreads();                       // every thread is done with this slot
+      if (tid == 0 && i + nslot < nnz) issue(i + nslot);
+    }
+    use += (unsigned)nnz;
+  }
+  // column aliases within the 512-column tile -> bucket columns (B and 2B)
+  red[cp] = acc[0];
+  red[cp + 1] = acc[1];
+  red[512 + cp] = acc2[0][0];
+  red[512 + cp + 1] = acc2[0][1];
+  red[1024 + cp] = acc2[1][0];
+  red[1024 + cp + 1] = acc2[1][1];
+  __syncthreads();
+  const size_t BB = (size_t)B * B, B2 = (size_t)B << 1;
+  for (int kap = tid; kap < B; kap += blockDim.x) {
+    C sum = mk<T>(0, 0);
+    for (int a = 0; a < 512 / B; ++a) sum = cadd(sum, red[kap + a * B]);
+    dst[(size_t)z * BB + (size_t)rho * B + kap] = sum;
+  }
+  for (int e = tid; e < 2 * (int)B2; e += blockDim.x) {
+    const int par = e / (int)B2, kap = e - par * (int)B2;
+    C sum = mk<T>(0, 0);
+    for (int a = 0; a < 512 / (int)B2; ++a) sum = cadd(sum, red[512 * (1 + par) + kap + a * (int)B2]);
+    dst2[(size_t)z * 4 * BB + (size_t)(rho + par * B) * B2 + kap] = sum;
+  }
+}
+
 // Deterministic sum of Z partials with 8 independent accumulators (keeps 8
 // loads in flight; the combination order is fixed, so results are
 // reproducible bit for bit).
