@@ -910,6 +910,9 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   }
   int32_t* arch = lazy ? (int32_t*)ws(c, "vote_arch", (size_t)arch_cap * kLazyMax * 4) : nullptr;
   long long arch_used = 0;
+  uint32_t* bmarch = lazy ? (uint32_t*)ws(c, "vote_bm", (size_t)lazy_bm_words(std::min(9, lgN)) * kLazyMax * 4)
+                          : nullptr;
+  long long bm_used = 0;
   bool hist_used = false;
   // NaN/Inf check (as_complex_matrix, corefft.py:49-50): fused into the dense
   // FFT's row pass when the trajectory reaches B = N, else one pass at the end
@@ -992,7 +995,20 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       P.lgB = lgb;
       P.count = (int)count;
       P.off = arch_used;
-      if (lgb <= 9) lp.lgBmax = std::max(lp.lgBmax, lgb);
+      if (lgb <= 9) {
+        // bitmap pass: B x B maxima bitmap + row flags, built once here
+        lp.lgBmax = std::max(lp.lgBmax, lgb);
+        const int words = lazy_bm_words(lgb);
+        P.off = bm_used;
+        ck(cudaMemsetAsync(bmarch + bm_used, 0, (size_t)words * 4, st), "memset bitmap");
+        pre(c, st);
+        kl(k_vote_bitmap, grid_for(count, 256, kNumSMs), 256, 0, st,
+           (const int32_t*)maxlists[slot & 1], (const unsigned*)(cnt_slots + slot), lgb,
+           bmarch + bm_used);
+        post(c, "k_vote_bitmap", st, (double)count * 4.0);
+        bm_used += words;
+        return;
+      }
       ck(cudaMemcpyAsync(arch + arch_used, maxlists[slot & 1], (size_t)count * 4,
                          cudaMemcpyDeviceToDevice, st), "archive maxima");
       arch_used += count;
@@ -1233,7 +1249,8 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     while (lgG < 15 && ((long long)1 << (lgG + 1)) * (2 * kNumSMs) <= nkeys) ++lgG;
     const size_t smem = vote_lazy_smem(lgN, lgG, lp.lgBmax);
     pre(c, st);
-    kl(k_vote_lazy, (unsigned)(nkeys >> lgG), 256, smem, st, (const int32_t*)arch, lp, lgN, lgG,
+    kl(k_vote_lazy, (unsigned)(nkeys >> lgG), 256, smem, st, (const int32_t*)arch,
+       (const uint32_t*)bmarch, lp, lgN, lgG,
        (const uint32_t*)(hist_used ? hist : nullptr), hist_out, thr_, bits, cnts);
     post(c, "k_vote_lazy", st, (double)nkeys / 8.0 + (hist_used ? (double)nkeys : 0.0) +
                                    (hist_out ? (double)nkeys : 0.0));

@@ -97,8 +97,33 @@ struct LazyPass {
   Perm p;
   int lgB;
   int count;
-  long long off;                    // first entry in the archive
+  long long off;                    // list passes: first entry in the list archive;
+                                    // bitmap passes: first word of the bitmap archive
 };
+
+// words of one archived bitmap pass: B^2 bits, then B row-flag bits, each
+// padded to whole 16-byte chunks (cp.async granules)
+__host__ __device__ inline int lazy_bm_words(int lgB) {
+  const int B = 1 << lgB;
+  return (((B * B + 31) / 32 + 3) & ~3) + (((B + 31) / 32 + 3) & ~3);
+}
+
+// Archive one bitmap pass: maxima bitmap + row flags of the pass's list into a
+// zeroed region (tuner pass order; runs on the main stream after the maxima
+// kernel, one thread per maximum).
+__global__ void k_vote_bitmap(const int32_t* __restrict__ list, const unsigned* __restrict__ count_p,
+                              int lgB, uint32_t* __restrict__ bm) {
+  pdl_wait();
+  const int B = 1 << lgB;
+  uint32_t* flags = bm + (((B * B + 31) / 32 + 3) & ~3);
+  const unsigned cnt = *count_p;
+  for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += gridDim.x * blockDim.x) {
+    const unsigned bin = (unsigned)list[e];
+    atomicOr(&bm[bin >> 5], 1u << (bin & 31u));
+    const unsigned a = bin >> lgB;
+    atomicOr(&flags[a >> 5], 1u << (a & 31u));
+  }
+}
 struct LazyPasses {
   LazyPass v[kLazyMax];
   int n;
@@ -109,7 +134,8 @@ __device__ __forceinline__ void lazy_add(uint32_t* tal, unsigned key, unsigned i
   atomicAdd(&tal[key >> 2], inc << ((key & 3u) * 8u));
 }
 
-__global__ void __launch_bounds__(256) k_vote_lazy(const int32_t* __restrict__ arch, LazyPasses lp,
+__global__ void __launch_bounds__(256) k_vote_lazy(const int32_t* __restrict__ arch,
+                                                    const uint32_t* __restrict__ bmarch, LazyPasses lp,
                                                     int lgN, int lgG,
                                                     const uint32_t* __restrict__ hist_init,
                                                     uint32_t* __restrict__ hist_out, unsigned thr,
@@ -125,11 +151,26 @@ __global__ void __launch_bounds__(256) k_vote_lazy(const int32_t* __restrict__ a
   const size_t k0 = (size_t)blockIdx.x << lgG;
   const unsigned i0 = (unsigned)(k0 >> lgN);
   const int Bmax = 1 << lp.lgBmax;
+  const int bmw = lazy_bm_words(lp.lgBmax);
   uint32_t* s_tal = sm_vote;                                   // G bytes
-  uint32_t* s_bits = s_tal + G / 4;                            // Bmax^2 bits
-  uint32_t* s_flag = s_bits + ((Bmax * Bmax + 31) / 32 + 3) / 4 * 4;
-  int* s_list = (int*)(s_flag + ((Bmax + 31) / 32 + 3) / 4 * 4);   // R x Bmax entries
+  uint32_t* s_bm0 = s_tal + G / 4;                             // two bitmap buffers
+  int* s_list = (int*)(s_bm0 + 2 * bmw);                       // R x Bmax entries
   uint4* t4 = reinterpret_cast<uint4*>(s_tal);
+  // bitmap passes arrive by cp.async, the next one while the current is used
+  auto fetch = [&](int ps, int buf) {
+    const int words = lazy_bm_words(lp.v[ps].lgB);
+    const uint32_t* src = bmarch + lp.v[ps].off;
+    uint32_t* dst = s_bm0 + buf * bmw;
+    for (int e = tid * 4; e < words; e += nt * 4) cp_async16(dst + e, src + e);
+    cp_async_commit();
+  };
+  auto next_bitmap = [&](int from) {
+    for (int q = from; q < lp.n; ++q)
+      if (lp.v[q].lgB <= lp.lgBmax) return q;
+    return -1;
+  };
+  int cur = next_bitmap(0), buf = 0;
+  if (cur >= 0) fetch(cur, 0);
   if (hist_init) {
     const uint4* h4 = reinterpret_cast<const uint4*>(hist_init + k0 / 4);
     for (int e = tid; e < G / 16; e += nt) t4[e] = h4[e];
@@ -146,18 +187,14 @@ __global__ void __launch_bounds__(256) k_vote_lazy(const int32_t* __restrict__ a
     const int shiftlo = w / 2 + 1;   // floor(w/2) + expand
     const int32_t* L = arch + P.off;
     if (lgB <= lp.lgBmax) {
-      // ---- bitmap pass
-      const int bitwords = (B * B + 31) / 32, flagwords = (B + 31) / 32;
-      for (int e = tid; e < bitwords; e += nt) s_bits[e] = 0u;
-      for (int e = tid; e < flagwords; e += nt) s_flag[e] = 0u;
+      // ---- bitmap pass: its bitmap (k_vote_bitmap) is in buffer `buf`
+      asm volatile("cp.async.wait_all;\n" ::: "memory");
       __syncthreads();
-      for (int e = tid; e < P.count; e += nt) {
-        const unsigned bin = (unsigned)L[e];
-        atomicOr(&s_bits[bin >> 5], 1u << (bin & 31u));
-        const unsigned a = bin >> lgB;
-        atomicOr(&s_flag[a >> 5], 1u << (a & 31u));
-      }
-      __syncthreads();
+      const uint32_t* s_bits = s_bm0 + buf * bmw;
+      const uint32_t* s_flag = s_bits + (((B * B + 31) / 32 + 3) & ~3);
+      const int nxt = next_bitmap(ps + 1);
+      if (nxt >= 0) fetch(nxt, buf ^ 1);   // overlaps [A] and [B] of this pass
+      buf ^= 1;
       // [A] item (row r, 32-column chunk q): bin rows a with
       //     t + shiftlo - len < a w <= t + shiftlo, and their maxima in the chunk
       const int chunks = (B + 31) / 32;
@@ -187,16 +224,18 @@ __global__ void __launch_bounds__(256) k_vote_lazy(const int32_t* __restrict__ a
         }
       }
       __syncthreads();
-      // [B] scatter every row's increments into the tile: preimage offsets
-      // rr < w as (entry, rr) = (e >> lgw, e & (w - 1)), the two expand
-      // offsets rr = w, w + 1 separately (no integer division by len)
-      for (int r = 0; r < R; ++r) {
+      // [B] scatter every row's increments into the tile: the row's nt / R
+      //     threads walk its entries; preimage offsets rr < w as
+      //     (entry, rr) = (e >> lgw, e & (w - 1)), the two expand offsets
+      //     rr = w, w + 1 separately (no integer division by len)
+      {
+        const int tpr = nt / R;                 // threads per row (R <= nt, both powers of 2)
+        const int r = tid / tpr, l = tid - r * tpr;
         const int nl = s_nlist[r];
-        if (nl == 0) continue;
         const int* lst = s_list + r * Bmax;
         const unsigned rowkey = (unsigned)r << lgN;
         const int nmain = w == 1 ? nl * 3 : nl << lgw;
-        for (int e = tid; e < nmain; e += nt) {
+        for (int e = l; e < nmain; e += tpr) {
           int q, rr;
           if (w == 1) { q = e / 3; rr = e - q * 3; } else { q = e >> lgw; rr = e & (w - 1); }
           const int ent = lst[q];
@@ -204,7 +243,7 @@ __global__ void __launch_bounds__(256) k_vote_lazy(const int32_t* __restrict__ a
           lazy_add(s_tal, rowkey | ((P.p.s2i * v) & maskN), (unsigned)(ent & 255));
         }
         if (w > 1) {
-          for (int e = tid; e < 2 * nl; e += nt) {
+          for (int e = l; e < 2 * nl; e += tpr) {
             const int ent = lst[e >> 1];
             const unsigned rr = (unsigned)w + (unsigned)(e & 1);
             const unsigned v = ((unsigned)(ent >> 8) * (unsigned)w - (unsigned)shiftlo + rr) & maskN;
@@ -240,14 +279,13 @@ __global__ void __launch_bounds__(256) k_vote_lazy(const int32_t* __restrict__ a
     // kCmpElems keys per compaction block: word tid of every block in the tile
     for (int blk = 0; blk < G / kCmpElems; ++blk) {
       const int wl = blk * kCmpWords + tid;   // 32 keys = 8 tally words
+      // bytewise h >= thr (SIMD compare), byte flags packed to 4 bits per word
       uint32_t word = 0;
+      const unsigned thr4 = thr * 0x01010101u;
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const uint32_t h = s_tal[wl * 8 + u];
-        if (!h) continue;
-#pragma unroll
-        for (int bb = 0; bb < 4; ++bb)
-          if (((h >> (8 * bb)) & 255u) >= thr) word |= 1u << (u * 4 + bb);
+        const uint32_t m = __vcmpgeu4(s_tal[wl * 8 + u], thr4) & 0x01010101u;
+        word |= ((m | (m >> 7) | (m >> 14) | (m >> 21)) & 15u) << (u * 4);
       }
       bits[(k0 >> 5) + wl] = word;
       const unsigned pre = block_excl_scan256(__popc(word), s_warp);
@@ -260,8 +298,7 @@ __global__ void __launch_bounds__(256) k_vote_lazy(const int32_t* __restrict__ a
 // dynamic shared memory of k_vote_lazy
 inline size_t vote_lazy_smem(int lgN, int lgG, int lgBmax) {
   const long G = 1L << lgG, Bm = 1L << lgBmax, R = G >> lgN;
-  const long bitw = ((Bm * Bm + 31) / 32 + 3) / 4 * 4, flagw = ((Bm + 31) / 32 + 3) / 4 * 4;
-  return (size_t)(G / 4 + bitw + flagw + R * Bm) * 4;
+  return (size_t)(G / 4 + 2L * lazy_bm_words(lgBmax) + R * Bm) * 4;
 }
 
 // Fold one group's loop-bit masks into per-coordinate loop counts (L > 8).
