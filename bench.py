@@ -294,7 +294,7 @@ def main():
 
     def barrier():
         if world > 1:
-            dist.barrier()
+            dist.barrier(device_ids=[local])
 
     # warm-up (also builds tables / workspace in every worker context)
     for _ in range(max(args.warmup, 1)):
