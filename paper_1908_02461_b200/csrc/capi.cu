@@ -667,7 +667,18 @@ unsigned lmax_tuner(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long l
   int rb = std::max(1, std::min(B / 128, smem_rows - 2));
   while (B % rb) --rb;
   const size_t sm = (size_t)(rb + 2) * B * sizeof(T) + (size_t)rb * B / 32 * sizeof(unsigned);
-  if (sm > kMaxDynSmem) fail(SFFT2D_ERR_UNSUPPORTED, "grid too large for the local-maximum tile");
+  if (sm > kMaxDynSmem) {
+    // rows too long to stage (fp64 at B = 16384): test straight from global memory
+    if (!perm) fail(SFFT2D_ERR_UNSUPPORTED, "grid too large for the local-maximum tile");
+    const unsigned grid = kNumSMs * 8;
+    const Publish pub = make_publish(c, grid);
+    pre(c, st);
+    kl(k_lmax_direct<T>, grid, 256, 0, st, mags, lgB, s1, s2, inv_pow2(s1, (uint32_t)B - 1u), s2inv, peak,
+       floor_rel, list, count, pub, cand, cand_count);
+    if (emitted) *emitted = cand != nullptr;
+    post(c, "k_lmax_direct", st, by);
+    return pub.seq;
+  }
   const Publish pub = make_publish(c, (unsigned)(B / rb));
   pre(c, st);
   if (perm)

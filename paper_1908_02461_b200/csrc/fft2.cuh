@@ -21,6 +21,7 @@
 #pragma once
 #include <type_traits>
 #include <utility>
+#include <cooperative_groups.h>
 #include "common.cuh"
 
 namespace sfft {
@@ -373,6 +374,81 @@ k_fftcB(const cplx<T>* __restrict__ src, cplx<T>* __restrict__ dst, T* __restric
   };
   fft_tile<T, true, 1, LG2>(s, lgL2, lgcc, pad_row(1 << lgL2), tw, lgN, ld, st);
   if (WM && peak) flush_peak(best, peak + g);
+}
+
+// Length-2^LG transform of 2^nseq_lg sequences whose first radix-16 pass
+// gathers from global memory through ld(seq, u) (consecutive threads take
+// consecutive sequences, then consecutive j); every later pass runs in shared
+// memory and the result stays there in natural order (padded rows, stride rs).
+template <typename T, int LG, typename Ld>
+__device__ __forceinline__ void fft_tile_smem(cplx<T>* s, int nseq_lg, int rs,
+                                              const cplx<T>* __restrict__ tw, int lgN, Ld ld) {
+  using C = cplx<T>;
+  constexpr int per = (1 << LG) >> 4;
+  {
+    const int it = threadIdx.x;
+    const int seq = it & ((1 << nseq_lg) - 1), j = it >> nseq_lg;
+    C v[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = ld(seq, j + r * per);
+    dft_reg<T, 16>(v);
+    C* sr = s + seq * rs;
+#pragma unroll
+    for (int r = 0; r < 16; ++r) sr[padi(j * 16 + r)] = v[r];
+  }
+  __syncthreads();
+  int lgNs = 4;
+#pragma unroll
+  for (int pass = 0; pass < 4; ++pass) {
+    if (lgNs >= LG) break;
+    const int rem = LG - lgNs;
+    if (rem >= 4) { stockham_pass<T, 4>(s, LG, rs, lgNs, tw, lgN); lgNs += 4; }
+    else if (rem == 3) { stockham_pass<T, 3>(s, LG, rs, lgNs, tw, lgN); lgNs += 3; }
+    else if (rem == 2) { stockham_pass<T, 2>(s, LG, rs, lgNs, tw, lgN); lgNs += 2; }
+    else { stockham_pass<T, 1>(s, LG, rs, lgNs, tw, lgN); lgNs += 1; }
+  }
+}
+
+// Row pass for rows too long for one CTA's shared memory (fp64, L = 16384:
+// 278 KB padded): a 2-CTA cluster per row.  CTA q transforms the elements
+// 2u + q to E_q[k'] in its shared memory; after a cluster barrier it reads
+// E_0 and E_1 for its half of k' (the peer's through DSMEM) and writes the
+// radix-2 outputs X[k'] = E_0 + W_L^k' E_1, X[k' + L/2] = E_0 - W_L^k' E_1.
+// Complex output only (the dense row pass), with the NaN/Inf check.
+template <typename T, typename Tin, int LGM>
+__global__ void __launch_bounds__(512, 1)
+k_fftr_cl2(const Tin* __restrict__ src, cplx<T>* __restrict__ dst,
+           const cplx<T>* __restrict__ tw, int lgN, unsigned* __restrict__ nonfinite) {
+  pdl_wait();
+  namespace cg = cooperative_groups;
+  using C = cplx<T>;
+  constexpr int M = 1 << LGM;
+  constexpr int lgL = LGM + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  C* s = reinterpret_cast<C*>(smem_raw);
+  cg::cluster_group cl = cg::this_cluster();
+  const int q = (int)cl.block_rank();
+  const size_t base = (size_t)(blockIdx.x >> 1) << lgL;
+  bool bad = false;
+  auto ld = [&](int, int u) {
+    const Tin w = src[base + 2 * (size_t)u + q];
+    if (nonfinite) bad |= !isfinite(w.x) || !isfinite(w.y);
+    return mk<T>((T)w.x, (T)w.y);
+  };
+  fft_tile_smem<T, LGM>(s, 0, pad_row(M), tw, lgN, ld);
+  cl.sync();
+  const C* e0s = cl.map_shared_rank(s, 0);
+  const C* e1s = cl.map_shared_rank(s, 1);
+  const int tsh = lgN - lgL;
+  for (int kk = q * (M / 2) + threadIdx.x; kk < (q + 1) * (M / 2); kk += blockDim.x) {
+    const C e0 = e0s[padi(kk)];
+    C e1 = e1s[padi(kk)];
+    if (kk) e1 = cmul(e1, __ldg(tw + ((size_t)kk << tsh)));
+    dst[base + kk] = cadd(e0, e1);
+    dst[base + kk + M] = csub(e0, e1);
+  }
+  cl.sync();   // the peer has finished reading this CTA's shared memory
+  if (nonfinite && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(nonfinite, 1u);
 }
 
 // ---------------------------------------------------------------- dispatch

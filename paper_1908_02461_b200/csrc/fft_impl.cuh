@@ -27,6 +27,15 @@ template <typename T, typename Tin>
 void fft_rows(sfft2d_ctx* c, const FftPlan2D& pl, long nrows, const Tin* src, cplx<T>* dst,
               const cplx<T>* tw, int lgN, unsigned* nonfinite, const char* name, double bytes,
               cudaStream_t st) {
+  if (pl.smem_row > kMaxDynSmem) {
+    // fp64 L = 16384: one 2-CTA cluster per row (k_fftr_cl2)
+    if (pl.lgL != 14) fail(SFFT2D_ERR_UNSUPPORTED, "row too long for the smem FFT");
+    const size_t sm = (size_t)pad_row(1 << 13) * sizeof(cplx<T>);
+    pre(c, st);
+    klc(k_fftr_cl2<T, Tin, 13>, (unsigned)(2 * nrows), 512, sm, st, 2, src, dst, tw, lgN, nonfinite);
+    post(c, "k_fftr_cl2", st, bytes);
+    return;
+  }
   const unsigned grid = (unsigned)(nrows / pl.rows_per_cta);
   pre(c, st);
   with_lg<4, 14>(pl.lgL, [&](auto LGc) {
@@ -101,7 +110,7 @@ void fft2d_grids(sfft2d_ctx* c, cplx<T>* grids, int lgB, int ngrids, const cplx<
     return;
   }
   const FftPlan2D pl = plan_fft2d<T>(lgB);
-  if (pl.smem_row > kMaxDynSmem || pl.row_threads > 512)
+  if ((pl.smem_row > kMaxDynSmem && pl.lgL != 14) || pl.row_threads > 512)
     fail(SFFT2D_ERR_UNSUPPORTED, "grid too large for the smem FFT");
   fft_rows<T, C>(c, pl, (long)ngrids * B, grids, grids, tw, lgN, nullptr, "k_fftr", 2 * gb, st);
   const double wbytes = (wc ? gb : 0) + (wm ? (double)BB * ngrids * sizeof(T) : 0);
@@ -123,7 +132,7 @@ void dense_fft(sfft2d_ctx* c, const Tin* x, cplx<T>* out, T* mags, unsigned long
   using C = cplx<T>;
   const int N = 1 << lgN;
   const FftPlan2D pl = plan_fft2d<T>(lgN);
-  if (pl.smem_row > kMaxDynSmem || pl.row_threads > 512)
+  if ((pl.smem_row > kMaxDynSmem && pl.lgL != 14) || pl.row_threads > 512)
     fail(SFFT2D_ERR_UNSUPPORTED, "image side too large for the smem FFT");
   const double nn = (double)N * N;
   C* scratch = (C*)ws(c, "fft_scratch", (size_t)N * N * sizeof(C));
@@ -142,7 +151,7 @@ cplx<T>* dense_fft_front(sfft2d_ctx* c, const Tin* x, int lgN, const cplx<T>* tw
   const int N = 1 << lgN;
   const FftPlan2D pl = plan_fft2d<T>(lgN);
   if (!pl.four_step || pl.col1) fail(SFFT2D_ERR_STATE, "factored dense FFT needs four-step columns");
-  if (pl.smem_row > kMaxDynSmem || pl.row_threads > 512)
+  if ((pl.smem_row > kMaxDynSmem && pl.lgL != 14) || pl.row_threads > 512)
     fail(SFFT2D_ERR_UNSUPPORTED, "image side too large for the smem FFT");
   const double nn = (double)N * N;
   C* scratch = (C*)ws(c, "fft_scratch", (size_t)N * N * sizeof(C));

@@ -75,4 +75,27 @@ void kl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream
   ck(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx");
 }
 
+// kl() for a kernel launched in thread-block clusters of `cluster_x` CTAs
+// (grid.x a multiple of cluster_x), also with PDL.
+template <typename... KArgs, typename... Args>
+void klc(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+         int cluster_x, Args&&... args) {
+  if (smem > 0) allow_smem(kernel);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = (unsigned)cluster_x;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  ck(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...), "cudaLaunchKernelEx(cluster)");
+}
+
 }  // namespace sfft

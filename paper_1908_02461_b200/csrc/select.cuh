@@ -524,6 +524,65 @@ __global__ void k_lmax_cand(const T* __restrict__ M, int lgB, unsigned s1, unsig
   }
 }
 
+// Local maxima of a permuted view straight from global memory, for grids whose
+// rows do not fit the shared-memory ring (fp64 at B = 16384: 128 KB rows).
+// Every natural bin (R, C) above the floor is tested against its view
+// neighbours at the natural bins (R -+ s1, C -+ s2) (as k_lmax_cand), and is
+// optionally listed as a candidate for the later B = N views.
+template <typename T>
+__global__ void k_lmax_direct(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2,
+                              unsigned s1inv, unsigned s2inv,
+                              const unsigned long long* __restrict__ peak, double floor_rel,
+                              int32_t* __restrict__ list, unsigned* __restrict__ count, Publish pub,
+                              int32_t* __restrict__ cand, unsigned* __restrict__ cand_count) {
+  pdl_wait();
+  const unsigned mask = (1u << lgB) - 1u;
+  const size_t n = (size_t)1 << (2 * lgB);
+  const int lane = threadIdx.x & 31;
+  const double pk = fkey_inv(*peak);
+  const double fl = floor_rel * pk;
+  T flT = sizeof(T) == 4 ? (T)__double2float_ru(fl) : (T)fl;
+  if (!(pk > 0.0))
+    flT = sizeof(T) == 4 ? (T)__int_as_float(0x7f800000) : (T)__longlong_as_double(0x7ff0000000000000ll);
+  for (size_t e0 = (size_t)blockIdx.x * blockDim.x; e0 < n; e0 += (size_t)gridDim.x * blockDim.x) {
+    const size_t e = e0 + threadIdx.x;
+    const T v = e < n ? M[e] : (T)0;
+    const bool live = e < n && v >= flT;
+    if (!__any_sync(0xffffffffu, live)) continue;
+    if (cand) {
+      const unsigned cb = __ballot_sync(0xffffffffu, live);
+      unsigned b0 = 0;
+      if (lane == 0) b0 = atomicAdd(cand_count, (unsigned)__popc(cb));
+      b0 = __shfl_sync(0xffffffffu, b0, 0);
+      if (live) cand[b0 + __popc(cb & ((1u << lane) - 1u))] = (int32_t)e;
+    }
+    bool f = false;
+    unsigned key = 0;
+    if (live) {
+      const unsigned R = (unsigned)(e >> lgB), C = (unsigned)e & mask;
+      const unsigned Ru = (R - s1) & mask, Rd = (R + s1) & mask;
+      const unsigned Cl = (C - s2) & mask, Cr = (C + s2) & mask;
+      const T* up = M + ((size_t)Ru << lgB);
+      const T* md = M + ((size_t)R << lgB);
+      const T* dn = M + ((size_t)Rd << lgB);
+      f = (v > up[Cl]) & (v > up[C]) & (v > up[Cr]) & (v > md[Cl]) & (v > md[Cr]) &
+          (v > dn[Cl]) & (v > dn[C]) & (v > dn[Cr]);
+      key = (((s1inv * R) & mask) << lgB) | ((s2inv * C) & mask);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (bal) {
+      unsigned b0 = 0;
+      if (lane == 0) b0 = atomicAdd(count, (unsigned)__popc(bal));
+      b0 = __shfl_sync(0xffffffffu, b0, 0);
+      if (f) list[b0 + __popc(bal & ((1u << lane) - 1u))] = (int32_t)key;
+    }
+  }
+  if (pub.slot) {
+    __syncthreads();
+    if (threadIdx.x == 0) publish_count(count, pub.done, pub.target, pub.slot, pub.seq, cand_count);
+  }
+}
+
 // G[r][c] = M[s1i*r mod N][s2i*c mod N]: the |Z| grid of a B == N pass seen
 // through the permutation (SURVEY.md §7 hard part 2: tuner passes at B = N are
 // permuted views of |x_hat|).  CTA per output row; the source row is staged in

@@ -329,7 +329,8 @@ def test_batch_concurrent_equals_sequential():
     assert s1 == s2
 
 
-@pytest.mark.parametrize("n,precision", [(8192, "fp32"), (8192, "fp64"), (16384, "fp32")])
+@pytest.mark.parametrize("n,precision", [(8192, "fp32"), (8192, "fp64"), (16384, "fp32"),
+                                         (16384, "fp64")])
 def test_large_fft_sides(n, precision):
     # B = N bucket grid with the identity permutation is the dense 2D DFT
     rng = np.random.default_rng(n)
@@ -342,9 +343,12 @@ def test_large_fft_sides(n, precision):
     assert err < (1e-5 if precision == "fp32" else 1e-12), err
 
 
-def test_c5_atsfft_vs_reference():
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_c5_atsfft_vs_reference(precision):
+    # 16384^2: fp64 rows run as 2-CTA clusters (k_fftr_cl2), fp64 B = N local
+    # maxima straight from global memory (k_lmax_direct)
     g = golden("c5_ats_k64")
     x = fixture_input(g)
-    out, state = P.atsfft2d(x, _tuner(g), int(g["est_loops"]), int(g["seed"]), precision="fp32")
-    _check_state(state, g, "c5_ats_k64", "fp32")
-    _close_values(out, _ref_dict(g), TOL["fp32"])
+    out, state = P.atsfft2d(x, _tuner(g), int(g["est_loops"]), int(g["seed"]), precision=precision)
+    _check_state(state, g, "c5_ats_k64", precision)
+    _close_values(out, _ref_dict(g), TOL[precision])
