@@ -447,23 +447,35 @@ k_lmax_win(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, unsigned 
     for (int q = 0; q < GPW; ++q) {
       const int g = warp + q * nwarps;
       if (g >= groups) break;
+      // the four column sub-groups are tested first (a 4-bit mask per lane),
+      // then emitted with one warp scan: one ballot/scan per 128 bins
+      unsigned fm = 0;
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const unsigned C = ((unsigned)g << 7) + ((unsigned)j << 5) + (unsigned)lane;
         const unsigned Cl = (C - s2) & mask, Cr = (C + s2) & mask;
         const T d0 = dn[Cl], d1 = dn[C], d2 = dn[Cr];
         const T v = wm[q][j][1];
-        const bool f = (v >= flT) & (v > wu[q][j][0]) & (v > wu[q][j][1]) & (v > wu[q][j][2]) &
-                       (v > wm[q][j][0]) & (v > wm[q][j][2]) & (v > d0) & (v > d1) & (v > d2);
+        const T nb = fmax(fmax(fmax(wu[q][j][0], wu[q][j][1]), fmax(wu[q][j][2], wm[q][j][0])),
+                          fmax(fmax(wm[q][j][2], d0), fmax(d1, d2)));
+        fm |= ((v >= flT) & (v > nb)) ? (1u << j) : 0u;
         wu[q][j][0] = wm[q][j][0]; wu[q][j][1] = wm[q][j][1]; wu[q][j][2] = wm[q][j][2];
         wm[q][j][0] = d0; wm[q][j][1] = d1; wm[q][j][2] = d2;
-        const unsigned bal = __ballot_sync(0xffffffffu, f);
-        if (!bal) continue;
-        const int n = __popc(bal);
-        if (nbuf + n > kWarpBuf) flush();
-        if (f) wbuf[nbuf + __popc(bal & ((1u << lane) - 1u))] = (int32_t)(rowbase | ((s2i * C) & mask));
-        nbuf += n;
       }
+      if (!__any_sync(0xffffffffu, fm != 0u)) continue;
+      const unsigned cntl = (unsigned)__popc(fm);
+      const unsigned incl = warp_incl_scan(cntl);
+      const int n = (int)__shfl_sync(0xffffffffu, incl, 31);
+      if (nbuf + n > kWarpBuf) flush();
+      int pos = nbuf + (int)(incl - cntl);
+      while (fm) {
+        const int j = __ffs(fm) - 1;
+        fm &= fm - 1u;
+        const unsigned C = ((unsigned)g << 7) + ((unsigned)j << 5) + (unsigned)lane;
+        wbuf[pos++] = (int32_t)(rowbase | ((s2i * C) & mask));
+      }
+      __syncwarp();
+      nbuf += n;
     }
     __syncthreads();                           // every thread is done with load s
     if (threadIdx.x == 0 && s + nslot < nload) issue(s + nslot);
