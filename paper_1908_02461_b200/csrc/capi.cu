@@ -634,7 +634,7 @@ unsigned lmax_tuner(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long l
   const double by = (double)B * B * sizeof(T);
   const size_t row = (size_t)B * sizeof(T);
   const size_t wb = 16 * kWarpBuf * sizeof(int32_t);
-  if (B >= kLmaxStreamMinB && 4 * row + wb <= kMaxDynSmem) {
+  if ((B >= kLmaxStreamMinB || (live_most && !cand && B >= 128)) && 4 * row + wb <= kMaxDynSmem) {
     // streaming bands: ~2 CTAs per SM, a ring of row buffers per CTA
     int nslot = (int)std::max<size_t>(4, std::min<size_t>(8, (96 * 1024 - wb) / row));
     if (nslot * row + wb > kMaxDynSmem) nslot = (int)((kMaxDynSmem - wb) / row);
