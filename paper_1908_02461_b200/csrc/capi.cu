@@ -702,7 +702,11 @@ void topk_bits(sfft2d_ctx* c, const T* vals, long seglen, int nseg, long long nu
   kl(k_sel_init, (nseg + 127) / 128, 128, 0, st, sst, nseg, num, seglen);
   post(c, "k_sel_init", st, 0);
   const int nblk = blocks_for(seglen);
-  if (num < seglen) {
+  if (num < seglen && seglen <= kSelSegMax) {
+    pre(c, st);
+    kl(k_radix_select_seg<T>, nseg, 1024, 0, st, vals, seglen, sst);
+    post(c, "k_radix_select_seg", st, (double)seglen * nseg * sizeof(T) * 8);
+  } else if (num < seglen) {
     unsigned hb = (unsigned)std::max<long long>(1, std::min<long long>(256, (seglen + 4095) / 4096));
     for (int shift = 56; shift >= 0; shift -= 8) {
       pre(c, st);

@@ -742,6 +742,63 @@ __global__ void k_radix_pick(SelState* __restrict__ st, unsigned* __restrict__ h
   for (int d = 0; d < 256; ++d) h[d] = 0;
 }
 
+// All radix passes of the exact top-`need` selection of one short segment in
+// ONE CTA (segments up to kSelSegMax keys, one CTA per segment): per 8-bit
+// digit a shared histogram of the keys still matching the prefix, then warp 0
+// finds the digit holding the need-th largest key (descending warp scan).
+// Same SelState result as the k_radix_hist / k_radix_pick launch pairs, which
+// stay for long segments (16 launches -> 1 for SFFT's B x B loops).
+constexpr long kSelSegMax = 1L << 16;
+
+template <typename T>
+__global__ void __launch_bounds__(1024) k_radix_select_seg(const T* __restrict__ vals, long seglen,
+                                                           SelState* __restrict__ st) {
+  pdl_wait();
+  __shared__ unsigned sh[256];
+  __shared__ SelState s_st;
+  const int seg = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) s_st = st[seg];
+  __syncthreads();
+  if (s_st.take_all) return;
+  const T* v = vals + (size_t)seg * seglen;
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = tid; i < 256; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    const unsigned long long prefix = s_st.prefix, mask = s_st.mask;
+    for (long e = tid; e < seglen; e += blockDim.x) {
+      const unsigned long long k = fkey(v[e]);
+      if ((k & mask) == prefix) atomicAdd(&sh[(k >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    if (tid < 32) {
+      // lane l owns digits 255 - 8l .. 248 - 8l (descending)
+      unsigned c[8], lsum = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { c[i] = sh[255 - 8 * lane - i]; lsum += c[i]; }
+      const unsigned incl = warp_incl_scan(lsum);
+      const long long need = s_st.need;
+      const unsigned hit = __ballot_sync(0xffffffffu, (long long)incl >= need);
+      const int L0 = __ffs(hit) - 1;               // first lane reaching need (exists)
+      if (lane == L0) {
+        long long cum = (long long)(incl - lsum);
+        for (int i = 0; i < 8; ++i) {
+          if (cum + c[i] >= need) {
+            const unsigned d = 255u - 8u * (unsigned)lane - (unsigned)i;
+            s_st.prefix |= (unsigned long long)d << shift;
+            s_st.mask |= 255ull << shift;
+            s_st.need = need - cum;
+            break;
+          }
+          cum += c[i];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) st[seg] = s_st;
+}
+
 // per-block count of keys equal to the threshold (for tie ranks)
 template <typename T>
 __global__ void k_tie_counts(const T* __restrict__ vals, long seglen,
