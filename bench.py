@@ -33,6 +33,7 @@ host cores via a process pool, and prints the same line with impl=reference.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import subprocess
@@ -321,6 +322,7 @@ def main():
     e1 = torch.cuda.Event(enable_timing=True)
 
     def timed(items, fn, concurrency):
+        gc.collect()
         barrier()
         torch.cuda.synchronize()
         e0.record(stream)
@@ -333,6 +335,10 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item()), n_launch
 
+    # the cyclic garbage collector stays off for the timed legs: a collection
+    # pause (tens of ms over the run's Python objects) inside a ~15 ms region
+    # would halve that sample; it is re-enabled before the CPU baseline
+    gc.disable()
     if os.environ.get("SFFT2D_TRACE_ALLOC"):
         print("---- timed region", file=sys.stderr, flush=True)
     # ---- timed region: value (images resident in HBM, `conc` in flight)
@@ -386,6 +392,7 @@ def main():
         bsampler = ClockSampler(sampler.dev)
         bsampler.start()
         for _ in range(3):
+            gc.collect()
             barrier()
             torch.cuda.synchronize()
             e0.record(stream)
@@ -449,6 +456,7 @@ def main():
     torch.cuda.synchronize()
     cufft_ms = c0.elapsed_time(c1) / 10
 
+    gc.enable()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(img.x, args)
