@@ -297,9 +297,12 @@ def main():
         if world > 1:
             dist.barrier(device_ids=[local])
 
-    # warm-up (also builds tables / workspace in every worker context)
+    # warm-up (also builds tables / workspace in every worker context): every
+    # worker thread runs every distinct image once, then the usual warm-up steps
     for _ in range(max(args.warmup, 1)):
         (ij, vals), state = step(x_dev)
+    for j in range(conc):
+        PB.warm_workers(lambda j=j: step(xs_dev[j]), conc, dev)
     run_steps([xs_dev[i % conc] for i in range(max(args.warmup, 2 * conc))], step, conc)
     torch.cuda.synchronize()
     parity = None

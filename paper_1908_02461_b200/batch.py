@@ -18,7 +18,7 @@ from . import _native
 from .engine import SfftConfig, sfft2d, sfft2d_arrays
 from .tuner import TunerConfig, atsfft2d, atsfft2d_arrays
 
-__all__ = ["atsfft2d_batch", "sfft2d_batch"]
+__all__ = ["atsfft2d_batch", "sfft2d_batch", "warm_workers"]
 
 _pools: dict = {}
 
@@ -64,6 +64,32 @@ def _run(fn, n_items, concurrency, device):
             return fn(i)
 
     return list(_pool(concurrency).map(one, range(n_items)))
+
+
+def warm_workers(fn, concurrency: int, device=None) -> None:
+    """Run fn() once on EVERY worker thread of the `concurrency` pool (a barrier
+    makes the pool start all of them), so each thread's native context, pinned
+    result buffer and workspace exist before a timed or latency-sensitive batch:
+    creating them later (cudaHostAlloc, table uploads) synchronises the device
+    and stalls every transform in flight."""
+    if concurrency <= 1:
+        fn()
+        return
+    barrier = threading.Barrier(concurrency)
+    torch = _native._torch()
+    dev = None
+    if torch.cuda.is_available():
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+
+    def one(_):
+        barrier.wait()
+        if dev is None:
+            return fn()
+        s = _worker_stream(torch, dev)
+        with torch.cuda.stream(s):
+            return fn()
+
+    list(_pool(concurrency).map(one, range(concurrency)))
 
 
 def atsfft2d_batch(xs, cfg: TunerConfig, est_loops: int, rngs, *, concurrency: int = 4,

@@ -1011,16 +1011,21 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       P.count = (int)count;
       P.off = arch_used;
       if (lgb <= 9) {
-        // bitmap pass: B x B maxima bitmap + row flags, built once here
+        // bitmap pass: B x B maxima bitmap + row flags, built on the side
+        // stream (off the tuner's critical path; joined before k_vote_lazy)
         lp.lgBmax = std::max(lp.lgBmax, lgb);
         const int words = lazy_bm_words(lgb);
         P.off = bm_used;
-        ck(cudaMemsetAsync(bmarch + bm_used, 0, (size_t)words * 4, st), "memset bitmap");
-        pre(c, st);
-        kl(k_vote_bitmap, grid_for(count, 256, kNumSMs), 256, 0, st,
+        cudaStream_t vs = c->profiling ? st : c->vote_st;
+        ck(cudaStreamWaitEvent(vs, c->ev_lmax, 0), "cudaStreamWaitEvent");
+        ck(cudaMemsetAsync(bmarch + bm_used, 0, (size_t)words * 4, vs), "memset bitmap");
+        pre(c, vs);
+        kl(k_vote_bitmap, grid_for(count, 256, kNumSMs), 256, 0, vs,
            (const int32_t*)maxlists[slot & 1], (const unsigned*)(cnt_slots + slot), lgb,
            bmarch + bm_used);
-        post(c, "k_vote_bitmap", st, (double)count * 4.0);
+        post(c, "k_vote_bitmap", vs, (double)count * 4.0);
+        ck(cudaEventRecord(c->ev_vote[slot & 1], vs), "cudaEventRecord");
+        vote_pending[slot & 1] = true;   // the list slot is reused two passes later
         bm_used += words;
         return;
       }

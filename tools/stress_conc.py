@@ -13,6 +13,9 @@ conc = int(sys.argv[1]) if len(sys.argv) > 1 else 6
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
 imgs = [torch.from_numpy(P.sparse_image(4096, 100, 7 + i, snr_db=20.0).x).cuda() for i in range(8)]
 xs = [imgs[i % 8] for i in range(48)]
+from paper_1908_02461_b200 import batch as PB  # noqa: E402
+for j in range(8):
+    PB.warm_workers(lambda j=j: P.atsfft2d_arrays(imgs[j], P.TunerConfig(), 8, 11, precision="fp32"), conc)
 P.atsfft2d_batch(xs, P.TunerConfig(), 8, [11] * len(xs), concurrency=conc, precision="fp32", arrays=True)
 for r in range(reps):
     torch.cuda.synchronize()
