@@ -289,6 +289,18 @@ def test_atsfft_random_noisy_vs_oracle(seed):
     _close_values(out, O.as_dict((cs, vs)), TOL["fp64"])
 
 
+@pytest.mark.parametrize("n", [256, 512])
+def test_atsfft_wide_tallies_match_oracle(n):
+    # max_tuning_iters = 70: tallies can exceed 255, so votes take the 32-bit
+    # atomic histogram path instead of the deferred byte tiles
+    img = P.sparse_image(n, 9, 500 + n, snr_db=20.0)
+    (cs, vs), ostate = O.atsfft(img.x, O.TunerParams(max_iters=70), 8, 9)
+    out, state = P.atsfft2d(img.x, P.TunerConfig(max_tuning_iters=70), 8, 9)
+    assert [(b, c) for b, c, _ in state.history] == [(b, c) for b, c, _ in ostate["history"]]
+    assert state.vote_passes == ostate["vote_passes"]
+    _close_values(out, O.as_dict((cs, vs)), TOL["fp64"])
+
+
 def test_atsfft_nan_leaves_generator_untouched():
     x = P.sparse_image(128, 4, 1, snr_db=20.0).x.copy()
     x[5, 7] = np.inf
