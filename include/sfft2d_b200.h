@@ -152,6 +152,24 @@ int sfft2d_sfft_from_votes(sfft2d_ctx* ctx, const void* x, int x_dtype, int x_on
  * perms: the shared Generator's draws in order; at least
  * iters(n) + 2 + max(est_loops, 1) of them (tuner passes, confirmation passes,
  * estimation loops).  state->perms_used reports how many were consumed.   */
+/* The two halves of the estimation phase (engine.py:163-195 and 228-253) as
+ * separate calls, so ranks can split the estimation loops
+ * (paper_1908_02461_b200/distributed.py).  All pointers but perms are device
+ * pointers.  keys: candidate coordinates i*n + j (int32, ascending), m of them.
+ * sfft2d_estimate_loops: vals[l*m + e] = complex estimate of loop l (the
+ *   precision's complex type), usable[l*m + e] = 1 where the window gain is at
+ *   least gain_floor; B x B hash passes with perms[0..nloops).
+ * sfft2d_median_select: componentwise median over the usable loops (any loop
+ *   order), top-k cut (ties -> lowest index), prune below prune_rel * max;
+ *   results through sfft2d_fetch_result.                                   */
+int sfft2d_estimate_loops(sfft2d_ctx* ctx, const void* x, int x_dtype, int x_on_host, int n, int b,
+                          double delta_pass, double delta_stop, double gain_floor,
+                          const int32_t* keys, int64_t m, const sfft2d_perm* perms, int nloops,
+                          int precision, void* stream, void* vals, uint8_t* usable);
+int sfft2d_median_select(sfft2d_ctx* ctx, int n, const int32_t* keys, int64_t m, const void* vals,
+                         const uint8_t* usable, int nloops, int64_t k, double prune_rel,
+                         int precision, void* stream, sfft2d_result* res);
+
 int sfft2d_atsfft(sfft2d_ctx* ctx, const void* x, int x_dtype, int x_on_host, int n,
                   const sfft2d_tuner_config* cfg, int est_loops, const sfft2d_perm* perms,
                   int n_perms, int precision, void* stream, sfft2d_result* res,

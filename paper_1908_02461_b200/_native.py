@@ -30,6 +30,7 @@ EXPORTS = (
     "sfft2d_local_maxima", "sfft2d_top_bins", "sfft2d_ctx_set_profiling",
     "sfft2d_ctx_profile_report", "sfft2d_atsfft_bitgen", "sfft2d_detect_sparsity_bitgen",
     "sfft2d_ctx_sync_us", "sfft2d_sfft_votes", "sfft2d_sfft_from_votes",
+    "sfft2d_estimate_loops", "sfft2d_median_select",
 )
 
 
@@ -119,6 +120,10 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "sfft2d_sfft_from_votes": ([vp, vp, i32, i32, P(SfftCfg), vp, P(Perm), i32, vp,
                                         P(ResultC)], i32),
             "sfft2d_ctx_profile_report": ([vp, ctypes.c_char_p, i64], i64),
+            "sfft2d_estimate_loops": ([vp, vp, i32, i32, i32, i32, dbl, dbl, dbl, vp, i64, P(Perm),
+                                       i32, i32, vp, vp, vp], i32),
+            "sfft2d_median_select": ([vp, i32, vp, i64, vp, vp, i32, i64, dbl, i32, vp,
+                                      P(ResultC)], i32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)

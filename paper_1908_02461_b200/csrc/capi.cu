@@ -757,6 +757,61 @@ void dense_xhat(sfft2d_ctx* c, const Tin* x, int lgN, const DevTables& tb, cplx<
                     nonfinite);
 }
 
+// K7 tail shared by every estimation path (engine.py:228-253): from the
+// per-coordinate medians `med`, |med| `mags`, `alive` flags and the peak key,
+// the exact top-k cut (when more than k are alive), the prune against
+// prune_rel * max |med|, the ordered compaction and the gather of the
+// results into mapped host memory (one synchronisation).
+template <typename T>
+void finish_select(sfft2d_ctx* c, int lgN, const int32_t* keys, unsigned m, long long k,
+                   double prune_rel, cplx<T>* med, T* mags, uint8_t* alive,
+                   unsigned long long* peak, long long n_alive, cudaStream_t st,
+                   sfft2d_result* res) {
+  using C = cplx<T>;
+  res->n_candidates = m;
+  if (n_alive == 0) {
+    res->count = 0;
+    res->ordered_by_magnitude = 0;
+    c->res_count = 0;
+    return;
+  }
+  const bool cut = n_alive > k;
+  const int nblk = blocks_for(m);
+  uint32_t* sel = nullptr;
+  if (cut) {
+    sel = (uint32_t*)ws(c, "fsel_bits", words_for(m) * 4);
+    unsigned* scnt = (unsigned*)ws(c, "fsel_cnt", (size_t)nblk * 4);
+    topk_bits<T>(c, mags, (long)m, 1, k, sel, scnt, st);
+  }
+  uint32_t* fb = (uint32_t*)ws(c, "fin_bits", words_for(m) * 4);
+  unsigned* fc = (unsigned*)ws(c, "fin_cnt", (size_t)nblk * 4);
+  pre(c, st);
+  kl(k_final_bits<T>, nblk, kCmpThreads, 0, st, mags, alive, sel, (long)m, peak, prune_rel, fb, fc);
+  post(c, "k_final_bits", st, 0);
+  int32_t* pos = (int32_t*)ws(c, "fin_pos", (size_t)m * 4);
+  unsigned* tot = (unsigned*)ws(c, "fin_tot", 16);
+  compact(c, fb, fc, (long)m, 1, pos, 0, tot, st);
+  // gather straight into mapped (zero-copy) host memory sized for the m
+  // candidates, then ONE synchronisation yields the count and the results
+  const size_t cap = (size_t)m;
+  char* outh = (char*)host_out(c, cap * (16 + sizeof(C)) + 64);
+  int64_t* oij_h = (int64_t*)outh;
+  C* ov_h = (C*)(outh + cap * 16);
+  int64_t* oij_d;
+  ck(cudaHostGetDevicePointer((void**)&oij_d, oij_h, 0), "cudaHostGetDevicePointer");
+  C* ov_d = (C*)((char*)oij_d + cap * 16);
+  pre(c, st);
+  kl(k_gather_out<T>, grid_for(m), 256, 0, st, pos, tot, keys, med, lgN, oij_d, ov_d);
+  post(c, "k_gather_out", st, 0);
+  const unsigned count = read_u32(c, tot, st);
+  c->out_ij_h = oij_h;
+  c->out_v_h = ov_h;
+  res->count = count;
+  res->ordered_by_magnitude = cut ? 1 : 0;
+  c->res_count = count;
+}
+
+
 // K6 + K7 + output compaction, shared by both algorithms.
 template <typename T, typename Tin>
 void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTables& tb,
@@ -809,47 +864,7 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
     post(c, "k_median", st, 0);
     n_alive = read_u32(c, alive_cnt, st);
   }
-  res->n_candidates = m;
-  if (n_alive == 0) {
-    res->count = 0;
-    res->ordered_by_magnitude = 0;
-    c->res_count = 0;
-    return;
-  }
-  const bool cut = n_alive > k;
-  const int nblk = blocks_for(m);
-  uint32_t* sel = nullptr;
-  if (cut) {
-    sel = (uint32_t*)ws(c, "fsel_bits", words_for(m) * 4);
-    unsigned* scnt = (unsigned*)ws(c, "fsel_cnt", (size_t)nblk * 4);
-    topk_bits<T>(c, mags, (long)m, 1, k, sel, scnt, st);
-  }
-  uint32_t* fb = (uint32_t*)ws(c, "fin_bits", words_for(m) * 4);
-  unsigned* fc = (unsigned*)ws(c, "fin_cnt", (size_t)nblk * 4);
-  pre(c, st);
-  kl(k_final_bits<T>, nblk, kCmpThreads, 0, st, mags, alive, sel, (long)m, peak, prune_rel, fb, fc);
-  post(c, "k_final_bits", st, 0);
-  int32_t* pos = (int32_t*)ws(c, "fin_pos", (size_t)m * 4);
-  unsigned* tot = (unsigned*)ws(c, "fin_tot", 16);
-  compact(c, fb, fc, (long)m, 1, pos, 0, tot, st);
-  // gather straight into mapped (zero-copy) host memory sized for the m
-  // candidates, then ONE synchronisation yields the count and the results
-  const size_t cap = (size_t)m;
-  char* outh = (char*)host_out(c, cap * (16 + sizeof(C)) + 64);
-  int64_t* oij_h = (int64_t*)outh;
-  C* ov_h = (C*)(outh + cap * 16);
-  int64_t* oij_d;
-  ck(cudaHostGetDevicePointer((void**)&oij_d, oij_h, 0), "cudaHostGetDevicePointer");
-  C* ov_d = (C*)((char*)oij_d + cap * 16);
-  pre(c, st);
-  kl(k_gather_out<T>, grid_for(m), 256, 0, st, pos, tot, keys, med, lgN, oij_d, ov_d);
-  post(c, "k_gather_out", st, 0);
-  const unsigned count = read_u32(c, tot, st);
-  c->out_ij_h = oij_h;
-  c->out_v_h = ov_h;
-  res->count = count;
-  res->ordered_by_magnitude = cut ? 1 : 0;
-  c->res_count = count;
+  finish_select<T>(c, lgN, keys, m, k, prune_rel, med, mags, alive, peak, n_alive, st, res);
 }
 
 // ------------------------------------------------------------------ ATSFFT
@@ -1795,6 +1810,94 @@ int sfft2d_sfft_from_votes(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_h
       sfft_from_hist<T, Tin>(c, (const Tin*)xd, *cfg, tb, (const uint32_t*)counts, kVoteAdd8,
                              up.first.data(), up.second, st, res);
     });
+    res->precision = precision;
+    res->gpu_launches = c->launches;
+    c->res_prec = precision;
+    c->has_res = true;
+  });
+}
+
+// Estimation loops for caller-given candidates, and the median/selection over
+// gathered per-loop estimates: the two halves of engine.py:163-253 as separate
+// entry points, so ranks can split the estimation loops (distributed.py).
+int sfft2d_estimate_loops(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host, int n, int b,
+                          double delta_pass, double delta_stop, double gain_floor,
+                          const int32_t* keys, int64_t m, const sfft2d_perm* perms, int nloops,
+                          int precision, void* stream, void* vals, uint8_t* usable) {
+  return guarded(c, [&] {
+    if (!x || !keys || !perms || !vals || !usable || m < 0 || nloops < 1)
+      fail(SFFT2D_ERR_VALUE, "bad arguments");
+    check_side(n);
+    if (!is_pow2(b) || b > n || n % b) fail(SFFT2D_ERR_CONFIG, "bin count must be a power of 2 dividing n");
+    if (nloops > kMaxFoldLoops * 8) fail(SFFT2D_ERR_UNSUPPORTED, "too many estimation loops");
+    if (m == 0) return;
+    cudaStream_t st = (cudaStream_t)stream;
+    c->ws_st = st;
+    c->launches = 0;
+    const void* xd = stage_input(c, x, x_dtype, x_on_host, n, st);
+    const DevTables& tb = find_tables(c, n, delta_pass, delta_stop);
+    auto up = upload_perms(c, "perms_estl", perms, nloops, n, st);
+    unsigned* m_dev = (unsigned*)ws(c, "estl_m", 16);
+    const unsigned m32 = (unsigned)m;
+    ck(cudaMemcpyAsync(m_dev, &m32, 4, cudaMemcpyHostToDevice, st), "H2D m");
+    const int lgN = ilog2(n), lgB = ilog2(b);
+    dispatch(x_dtype, precision, [&](auto t, auto tin) {
+      using T = decltype(t);
+      using Tin = decltype(tin);
+      using C = cplx<T>;
+      const int P = prec_of<T>();
+      const size_t BB = (size_t)b * b;
+      C* grids = (C*)ws(c, "est_grids", (size_t)nloops * BB * sizeof(C));
+      fold_spectrum<T, Tin>(c, (const Tin*)xd, lgN, lgB, tb, up.first.data(), nloops, grids,
+                            (T*)nullptr, nullptr, st);
+      const T* freq = (const T*)tb.freq[P] + ((size_t)lgB << lgN);
+      pre(c, st);
+      kl(k_estimate<T>, grid_for((long long)m * nloops), 256, 0, st, (const C*)grids, nloops, keys,
+         (const unsigned*)m_dev, (const Perm*)up.second, lgN, lgB, freq, (const C*)tb.tw[P],
+         gain_floor, (C*)vals, usable, (long)m);
+      post(c, "k_estimate", st, 0);
+    });
+    ck(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+int sfft2d_median_select(sfft2d_ctx* c, int n, const int32_t* keys, int64_t m, const void* vals,
+                         const uint8_t* usable, int nloops, int64_t k, double prune_rel,
+                         int precision, void* stream, sfft2d_result* res) {
+  return guarded(c, [&] {
+    if (!keys || !vals || !usable || !res || m < 0 || nloops < 1) fail(SFFT2D_ERR_VALUE, "bad arguments");
+    if (nloops > kMaxLoops) fail(SFFT2D_ERR_UNSUPPORTED, "more than 64 estimation loops");
+    check_side(n);
+    cudaStream_t st = (cudaStream_t)stream;
+    c->ws_st = st;
+    std::memset(res, 0, sizeof(*res));
+    c->launches = 0;
+    c->has_res = false;
+    c->res_count = 0;
+    if (m > 0) {
+      unsigned* m_dev = (unsigned*)ws(c, "msel_m", 16);
+      const unsigned m32 = (unsigned)m;
+      ck(cudaMemcpyAsync(m_dev, &m32, 4, cudaMemcpyHostToDevice, st), "H2D m");
+      dispatch_prec(precision, [&](auto t) {
+        using T = decltype(t);
+        using C = cplx<T>;
+        C* med = (C*)ws(c, "med", (size_t)m * sizeof(C));
+        T* mags = (T*)ws(c, "emag", (size_t)m * sizeof(T));
+        uint8_t* alive = (uint8_t*)ws(c, "alive", (size_t)m);
+        unsigned long long* peak = (unsigned long long*)ws(c, "epeak", 16);
+        unsigned* alive_cnt = (unsigned*)ws(c, "ealive", 16);
+        ck(cudaMemsetAsync(peak, 0, 16, st), "memset");
+        ck(cudaMemsetAsync(alive_cnt, 0, 16, st), "memset");
+        pre(c, st);
+        kl(k_median<T>, grid_for(m, 128), 128, 0, st, (const C*)vals, usable, nloops, (long)m,
+           (const unsigned*)m_dev, med, mags, alive, alive_cnt, peak);
+        post(c, "k_median", st, 0);
+        const long long n_alive = read_u32(c, alive_cnt, st);
+        res->n_candidates = m;
+        finish_select<T>(c, ilog2(n), keys, (unsigned)m, k, prune_rel, med, mags, alive, peak,
+                         n_alive, st, res);
+      });
+    }
     res->precision = precision;
     res->gpu_launches = c->launches;
     c->res_prec = precision;

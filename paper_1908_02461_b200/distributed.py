@@ -12,8 +12,14 @@
   data-path collective; `atsfft2d_sharded` gathers the per-image results (small
   Python objects) so every rank ends with the full list in input order.
 
-ATSFFT tuner passes are strictly sequential (tuner.py:182-207) and do not
-shard; a single large ATSFFT runs on one GPU.
+* **Estimation-loop split** (Algorithm 2, `atsfft2d`; the estimation loops
+  dominate large configs such as c5, where b_estimate = 8192 and each loop is
+  a full hash pass + 8192^2 FFT): the tuner passes are strictly sequential
+  (tuner.py:182-207), so every rank runs the same detection (same generator,
+  same trajectory), then rank r estimates loops l = r, r + world, ...
+  (`sfft2d_estimate_loops`), the per-loop estimates [L, m] are merged with one
+  zero-padded sum all-reduce, and every rank takes the median / top-k / prune
+  (`sfft2d_median_select`) — the same dict as single-GPU `atsfft2d`.
 """
 
 from __future__ import annotations
@@ -29,7 +35,7 @@ from .engine import ConfigurationError, SfftConfig, _fetch, _stream, to_dict
 from .hashing import draw_permutation
 
 __all__ = ["loop_shard", "batch_shard", "merge_votes", "sfft2d_loopsplit", "atsfft2d_sharded",
-           "vote_bytes"]
+           "vote_bytes", "merge_estimates", "atsfft2d_loopsplit"]
 
 
 def _dist():
@@ -123,3 +129,82 @@ def atsfft2d_sharded(xs, cfg, est_loops: int, rngs, *, group=None, concurrency: 
         for i, r in part:
             out[i] = r
     return out
+
+
+def merge_estimates(vals, usable, group=None):
+    """Zero-padded sum all-reduce of per-loop estimates: every rank filled only
+    the rows [l] of the loops it owns (others zero), so the sum is the full
+    [L, m] table (complex values as their real view) and usable flags."""
+    dist = _dist()
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        torch = _native._torch()
+        re = torch.view_as_real(vals) if vals.is_complex() else vals
+        dist.all_reduce(re, op=dist.ReduceOp.SUM, group=group)
+        dist.all_reduce(usable, op=dist.ReduceOp.SUM, group=group)
+    return vals, usable
+
+
+def atsfft2d_loopsplit(x, cfg, est_loops: int, rng, *, group=None, precision: str = "fp64",
+                       device=None):
+    """`atsfft2d` with the estimation loops split across the ranks of `group`
+    (every rank passes the same x, cfg, est_loops and seed, and gets the same
+    (dict, TunerState) as single-GPU `atsfft2d`, tuner.py:244-282).  A
+    Generator passed as `rng` advances exactly as under the reference."""
+    from .tuner import detect_sparsity
+    torch = _native._torch()
+    dist = _dist()
+    if dist.is_available() and dist.is_initialized():
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+    else:
+        rank, world = 0, 1
+    gen = rng if isinstance(rng, np.random.Generator) else np.random.default_rng(rng)
+    img = as_device_image(x, device)
+    n = img.n
+    state, (coords, tallies) = detect_sparsity(img.tensor, cfg, gen, precision=precision,
+                                               device=img.device)
+    if state.detected_k == 0 or len(coords) == 0:
+        return {}, state
+    thr = (max(state.vote_passes, 1) + 1) // 2
+    cand = coords[tallies >= thr]
+    if len(cand) == 0:
+        return {}, state
+    ecfg = SfftConfig(n=n, k=state.detected_k, loops=max(int(est_loops), 1),
+                      b_bins=state.b_estimate, window_delta_pass=cfg.window_delta_pass,
+                      window_delta_stop=cfg.window_delta_stop, gain_floor=cfg.gain_floor,
+                      prune_rel=cfg.prune_rel)          # ConfigurationError as the reference
+    perms = [draw_permutation(n, gen) for _ in range(ecfg.loops)]
+    prec = _native.precision_code(precision)
+    L, m = ecfg.loops, len(cand)
+    if ecfg.b_bins == n:
+        # all-pass window: every loop returns x_hat[i, j] itself (gain 1, the
+        # phase twists cancel; Lemma 1), so one loop on every rank is the
+        # median of all of them up to roundoff — nothing to split
+        L, perms = 1, perms[:1]
+    dev = img.tensor.device
+    keys = torch.as_tensor((cand[:, 0] * n + cand[:, 1]).astype(np.int32), device=dev)
+    cdt = torch.complex128 if prec == _native.FP64 else torch.complex64
+    vals = torch.zeros((L, m), dtype=cdt, device=dev)
+    usable = torch.zeros((L, m), dtype=torch.uint8, device=dev)
+    mine = [0] if L == 1 else loop_shard(L, rank, world)
+    ctx = _native.context(img.device)
+    ctx.ensure_tables(n, cfg.window_delta_pass, cfg.window_delta_stop)
+    with torch.cuda.device(img.device):
+        st = _stream(torch, img.device)
+        if mine:
+            lv = torch.empty((len(mine), m), dtype=cdt, device=dev)
+            lu = torch.empty((len(mine), m), dtype=torch.uint8, device=dev)
+            ctx.check(ctx.lib.sfft2d_estimate_loops(
+                ctx.handle, img.tensor.data_ptr(), img.dtype_code, 0, n, ecfg.b_bins,
+                ecfg.window_delta_pass, ecfg.window_delta_stop, ecfg.gain_floor, keys.data_ptr(), m,
+                _native.perm_array([perms[l] for l in mine]), len(mine), prec, st,
+                lv.data_ptr(), lu.data_ptr()))
+            idx = torch.as_tensor(mine, device=dev)
+            vals.index_copy_(0, idx, lv)
+            usable.index_copy_(0, idx, lu)
+        if L > 1:
+            merge_estimates(vals, usable, group)
+        res = _native.ResultC()
+        ctx.check(ctx.lib.sfft2d_median_select(
+            ctx.handle, n, keys.data_ptr(), m, vals.data_ptr(), usable.data_ptr(), L,
+            int(state.detected_k), ecfg.prune_rel, prec, st, ctypes.byref(res)))
+        return to_dict(*_fetch(ctx, res, st, prec)), state

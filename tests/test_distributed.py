@@ -123,3 +123,75 @@ def test_loopsplit_single_gpu_equals_sfft2d():
             assert a == b
     finally:
         dist.destroy_process_group()
+
+
+def _est_case():
+    img = sparse_image(128, 5, 41, snr_db=20.0)
+    a = O.as_c128(img.x)
+    gen = np.random.default_rng(43)
+    state, (vc, vt), _ = O.detect(a, O.TunerParams(), gen)
+    thr = (max(state["vote_passes"], 1) + 1) // 2
+    coords = vc[vt >= thr]
+    ecfg = O.sfft_params(128, state["detected_k"], loops=6, b_bins=state["b_estimate"])
+    win = O.cached_window(128, ecfg.b, ecfg.dstop, ecfg.dpass)
+    perms = [O.draw_perm(128, gen) for _ in range(ecfg.loops)]
+    return a, coords, ecfg, win, perms, state
+
+
+def _worker_est(rank, world, port, out_path):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    a, coords, ecfg, win, perms, _ = _est_case()
+    vals = torch.zeros((ecfg.loops, len(coords)), dtype=torch.complex128)
+    usable = torch.zeros((ecfg.loops, len(coords)), dtype=torch.uint8)
+    for l in D.loop_shard(ecfg.loops, rank, world):   # this rank's estimation loops only
+        v, o = O.estimate(a, coords, perms[l], win, ecfg.b, ecfg.gain_floor)
+        vals[l] = torch.from_numpy(np.asarray(v, dtype=np.complex128))
+        usable[l] = torch.from_numpy(np.asarray(o, dtype=np.uint8))
+    D.merge_estimates(vals, usable)
+    if rank == 0:
+        torch.save((vals, usable), out_path)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_estimation_split_merge_matches_single_process():
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "est.pt")
+        mp.spawn(_worker_est, args=(2, _free_port(), out), nprocs=2, join=True)
+        vals, usable = torch.load(out)
+    a, coords, ecfg, win, perms, state = _est_case()
+    vl, ol = zip(*[O.estimate(a, coords, p, win, ecfg.b, ecfg.gain_floor) for p in perms])
+    np.testing.assert_array_equal(vals.numpy(), np.asarray(vl, dtype=np.complex128))
+    np.testing.assert_array_equal(usable.numpy().astype(bool), np.asarray(ol, dtype=bool))
+    # the median / top-k / prune over the merged table is the reference's result
+    got = O.median_pick(coords, list(vals.numpy()), list(usable.numpy().astype(bool)),
+                        state["detected_k"], O.TunerParams().prune_rel)
+    ref, _ = O.atsfft(a, O.TunerParams(), 6, 43)
+    assert O.as_dict(got) == O.as_dict(ref)
+
+
+@pytest.mark.gpu
+def test_atsfft_estimation_split_single_gpu_equals_atsfft2d():
+    # world size 1 through the split entry points (sfft2d_estimate_loops +
+    # sfft2d_median_select, NCCL process group): the same support and values as
+    # atsfft2d, the reference's result, and the same Generator advance
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1908_02461_b200 as P
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        for n, k, seed in ((512, 9, 3), (256, 20, 4), (1024, 50, 7)):
+            img = sparse_image(n, k, seed, snr_db=25.0)
+            g1, g2 = np.random.default_rng(seed + 50), np.random.default_rng(seed + 50)
+            a, sa = P.atsfft2d(img.x, P.TunerConfig(), 8, g1)
+            b, sb = D.atsfft2d_loopsplit(img.x, P.TunerConfig(), 8, g2)
+            assert sa == sb and set(a) == set(b)
+            ref = O.as_dict(O.atsfft(img.x, O.TunerParams(), 8, seed + 50)[0])
+            assert set(b) == set(ref)
+            vmax = max([abs(v) for v in ref.values()] + [1e-30])
+            assert all(abs(b[q] - v) <= 1e-10 * max(abs(v), 1e-3 * vmax) for q, v in ref.items())
+            assert g1.integers(1 << 40) == g2.integers(1 << 40)
+    finally:
+        dist.destroy_process_group()
