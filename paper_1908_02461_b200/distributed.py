@@ -5,9 +5,11 @@
   (engine.py:270-273).  Rank r runs loops l = r, r + world, ... through the
   C-ABI location phase (`sfft2d_sfft_votes`), which yields a per-coordinate
   count of the loops that voted it (per-loop dedup, engine.py:144).  One
-  all-reduce (sum) of that uint8 histogram is the only collective; every rank
-  then thresholds and estimates (`sfft2d_sfft_from_votes`) and returns the same
-  dict as single-GPU `sfft2d`.
+  all-reduce (sum) of that uint8 histogram merges the votes; every rank
+  thresholds it, rank r estimates ITS estimation loops
+  (`sfft2d_estimate_loops`), one zero-padded sum all-reduce merges the [L, m]
+  estimates and every rank takes the median / top-k / prune
+  (`sfft2d_median_select`): the same dict as single-GPU `sfft2d`.
 * **Batch sharding** (config c4): independent images, one shard per rank, no
   data-path collective; `atsfft2d_sharded` gathers the per-image results (small
   Python objects) so every rank ends with the full list in input order.
@@ -100,11 +102,34 @@ def sfft2d_loopsplit(x, cfg: SfftConfig, rng, *, group=None, precision: str = "f
                 _native.perm_array([perms[l] for l in mine]), len(mine), prec, st,
                 counts.data_ptr()))
         merge_votes(counts, group)
+        # estimation loops split too: candidates = coordinates voted by at
+        # least vote_threshold loops (ascending, engine.py:148-160); rank r
+        # estimates loops l = r, r + world, ...; one sum all-reduce merges the
+        # [L, m] table; every rank takes the median / top-k / prune
+        keys = torch.nonzero(counts[: cfg.n * cfg.n] >= cfg.vote_threshold).flatten().to(torch.int32)
+        m = int(keys.numel())
+        if m == 0:
+            return {}
+        est = perms[cfg.loops:]
+        cdt = torch.complex128 if prec == _native.FP64 else torch.complex64
+        vals = torch.zeros((cfg.loops, m), dtype=cdt, device=counts.device)
+        usable = torch.zeros((cfg.loops, m), dtype=torch.uint8, device=counts.device)
+        if mine:
+            lv = torch.empty((len(mine), m), dtype=cdt, device=counts.device)
+            lu = torch.empty((len(mine), m), dtype=torch.uint8, device=counts.device)
+            ctx.check(ctx.lib.sfft2d_estimate_loops(
+                ctx.handle, img.tensor.data_ptr(), img.dtype_code, 0, cfg.n, cfg.b_bins,
+                cfg.window_delta_pass, cfg.window_delta_stop, cfg.gain_floor, keys.data_ptr(), m,
+                _native.perm_array([est[l] for l in mine]), len(mine), prec, st, lv.data_ptr(),
+                lu.data_ptr()))
+            idx = torch.as_tensor(mine, device=counts.device)
+            vals.index_copy_(0, idx, lv)
+            usable.index_copy_(0, idx, lu)
+        merge_estimates(vals, usable, group)
         res = _native.ResultC()
-        ctx.check(ctx.lib.sfft2d_sfft_from_votes(
-            ctx.handle, img.tensor.data_ptr(), img.dtype_code, 0, ctypes.byref(ccfg),
-            counts.data_ptr(), _native.perm_array(perms[cfg.loops:]), prec, st,
-            ctypes.byref(res)))
+        ctx.check(ctx.lib.sfft2d_median_select(
+            ctx.handle, cfg.n, keys.data_ptr(), m, vals.data_ptr(), usable.data_ptr(), cfg.loops,
+            cfg.k, cfg.prune_rel, prec, st, ctypes.byref(res)))
         return to_dict(*_fetch(ctx, res, st, prec))
 
 
