@@ -175,7 +175,7 @@ def atsfft2d_loopsplit(x, cfg, est_loops: int, rng, *, group=None, precision: st
     (every rank passes the same x, cfg, est_loops and seed, and gets the same
     (dict, TunerState) as single-GPU `atsfft2d`, tuner.py:244-282).  A
     Generator passed as `rng` advances exactly as under the reference."""
-    from .tuner import detect_sparsity
+    from .tuner import _run_ats
     torch = _native._torch()
     dist = _dist()
     if dist.is_available() and dist.is_initialized():
@@ -185,13 +185,16 @@ def atsfft2d_loopsplit(x, cfg, est_loops: int, rng, *, group=None, precision: st
     gen = rng if isinstance(rng, np.random.Generator) else np.random.default_rng(rng)
     img = as_device_image(x, device)
     n = img.n
-    state, (coords, tallies) = detect_sparsity(img.tensor, cfg, gen, precision=precision,
-                                               device=img.device)
-    if state.detected_k == 0 or len(coords) == 0:
+    # detection with the votes left on the device (the reference's
+    # detect_sparsity, tuner.py:142-241); candidates = tally >= threshold,
+    # ascending keys i*n + j (engine.py:148-160 order)
+    state, (vkeys, vtal) = _run_ats(img.tensor, cfg, 0, gen, precision, img.device, False,
+                                    on_device=True)
+    if state.detected_k == 0 or vkeys.numel() == 0:
         return {}, state
     thr = (max(state.vote_passes, 1) + 1) // 2
-    cand = coords[tallies >= thr]
-    if len(cand) == 0:
+    keys = vkeys[vtal >= thr].contiguous()
+    if keys.numel() == 0:
         return {}, state
     ecfg = SfftConfig(n=n, k=state.detected_k, loops=max(int(est_loops), 1),
                       b_bins=state.b_estimate, window_delta_pass=cfg.window_delta_pass,
@@ -199,14 +202,13 @@ def atsfft2d_loopsplit(x, cfg, est_loops: int, rng, *, group=None, precision: st
                       prune_rel=cfg.prune_rel)          # ConfigurationError as the reference
     perms = [draw_permutation(n, gen) for _ in range(ecfg.loops)]
     prec = _native.precision_code(precision)
-    L, m = ecfg.loops, len(cand)
+    L, m = ecfg.loops, int(keys.numel())
     if ecfg.b_bins == n:
         # all-pass window: every loop returns x_hat[i, j] itself (gain 1, the
         # phase twists cancel; Lemma 1), so one loop on every rank is the
         # median of all of them up to roundoff — nothing to split
         L, perms = 1, perms[:1]
     dev = img.tensor.device
-    keys = torch.as_tensor((cand[:, 0] * n + cand[:, 1]).astype(np.int32), device=dev)
     cdt = torch.complex128 if prec == _native.FP64 else torch.complex64
     vals = torch.zeros((L, m), dtype=cdt, device=dev)
     usable = torch.zeros((L, m), dtype=torch.uint8, device=dev)

@@ -192,9 +192,10 @@ def reconcile_generator(gen, snapshot, n: int, drawn: int, used: int) -> None:
         draw_permutation(n, gen)
 
 
-def _run_ats(x, cfg: TunerConfig, est_loops: int, rng, precision, device, estimate: bool):
+def _run_ats(x, cfg: TunerConfig, est_loops: int, rng, precision, device, estimate: bool,
+             on_device: bool = False):
     torch = _native._torch()
-    img = as_device_image(x, device, upload=False)
+    img = as_device_image(x, device, upload=on_device)
     n = img.n
     prec = _native.precision_code(precision)
     # The native controller draws each permutation on demand from this
@@ -231,6 +232,13 @@ def _run_ats(x, cfg: TunerConfig, est_loops: int, rng, precision, device, estima
         state = _state(sc)
         if not estimate:
             nv = int(sc.n_votes)
+            if on_device:   # keys / tallies stay in device tensors (distributed split)
+                kd = torch.empty(max(nv, 1), dtype=torch.int32, device=img.tensor.device)
+                td = torch.empty(max(nv, 1), dtype=torch.int32, device=img.tensor.device)
+                if nv:
+                    ctx.check(ctx.lib.sfft2d_fetch_votes(ctx.handle, kd.data_ptr(), td.data_ptr(),
+                                                         0, st))
+                return state, (kd[:nv], td[:nv])
             keys = np.empty(nv, dtype=np.int32)
             tallies = np.empty(nv, dtype=np.int32)
             if nv:
