@@ -667,8 +667,10 @@ unsigned lmax_tuner(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long l
   int rb = std::max(1, std::min(B / 128, smem_rows - 2));
   while (B % rb) --rb;
   const size_t sm = (size_t)(rb + 2) * B * sizeof(T) + (size_t)rb * B / 32 * sizeof(unsigned);
-  if (sm > kMaxDynSmem) {
-    // rows too long to stage (fp64 at B = 16384): test straight from global memory
+  if (sm > kMaxDynSmem || (perm && !live_most && B >= 8192)) {
+    // rows too long to stage (fp64 at B = 16384), or a B = N view too wide for
+    // the ring (fp32 16384: one 3-row tile per SM): test straight from global
+    // memory — below-floor bins (almost all at B = N) cost one coalesced read
     if (!perm) fail(SFFT2D_ERR_UNSUPPORTED, "grid too large for the local-maximum tile");
     const unsigned grid = kNumSMs * 8;
     const Publish pub = make_publish(c, grid);
