@@ -204,3 +204,24 @@ def test_generator_reconciled_after_speculative_draw():
     before = g.bit_generator.state
     reconcile_generator(g, snap, n, used, used)
     assert g.bit_generator.state == before
+
+
+@pytest.mark.parametrize("shape", [(0, 0), (8,), (4, 8), (6, 6), (3, 3), (2, 4, 4), (1, 2)])
+def test_bad_shapes_rejected_like_reference(shape):
+    # corefft.as_complex_matrix (corefft.py:38-51): square, power-of-two sides only
+    from paper_1908_02461_b200._tensors import host_image
+    x = np.zeros(shape, dtype=np.complex64)
+    with pytest.raises(ValueError):
+        O.as_c128(x)
+    with pytest.raises(ValueError):
+        host_image(x)
+
+
+@pytest.mark.parametrize("dtype", [np.int32, np.float32, np.float64, np.complex64, np.complex128])
+def test_numeric_inputs_accepted_like_reference(dtype):
+    from paper_1908_02461_b200._tensors import host_image
+    x = (np.arange(16).reshape(4, 4) % 5).astype(dtype)
+    a, code = host_image(x)
+    ref = O.as_c128(x)
+    assert a.shape == (4, 4) and np.array_equal(a.astype(np.complex128), ref)
+    assert code == (_native.C64 if dtype == np.complex64 else _native.C128)
