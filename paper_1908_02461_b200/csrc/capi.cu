@@ -394,7 +394,8 @@ template <typename T, typename Tin>
 FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTables& tb,
                     const Perm* hp, int g, void* y_direct, cudaStream_t st,
                     unsigned long long* zero_peak = nullptr, bool natural = false,
-                    const Perm* spec_q = nullptr, void* spec_y = nullptr, int* spec_z = nullptr) {
+                    const Perm* spec_q = nullptr, void* spec_y = nullptr, int* spec_z = nullptr,
+                    bool spec_same = false) {
   using C = cplx<T>;
   const int B = 1 << lgB;
   const size_t BB = (size_t)B * B;
@@ -417,11 +418,12 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
   // kernels; `natural` places bucket (rho, kappa) at row rho, column kappa
   const int seg_cols0 = kRingSegBytes / (int)sizeof(Tin);
   if (spec_q && B < 512) {
-    // TMA ring fold of pass t at B and of the next pass at 2B <= 512, one read
-    if (!(g == 1 && 2 * B <= 512 && gm.TW == 512 && (1 << lgN) >= seg_cols0 && y_direct &&
-          spec_y && natural && spec_z))
+    // TMA ring fold of pass t at B and of the next pass at 2B <= 512 (or, for
+    // the first two tuner passes, at the same B), one read
+    if (!(g == 1 && (spec_same || 2 * B <= 512) && gm.TW == 512 && (1 << lgN) >= seg_cols0 &&
+          y_direct && spec_y && spec_z && (natural || spec_same)))
       fail(SFFT2D_ERR_STATE, "speculative ring fold outside its geometry");
-    const T* space2 = (const T*)tb.space[prec_of<T>()] + ((size_t)(lgB + 1) << lgN);
+    const T* space2 = (const T*)tb.space[prec_of<T>()] + ((size_t)(lgB + (spec_same ? 0 : 1)) << lgN);
     const int nslot = 3;
     FoldGeom gr = gm;
     const int aliases = (1 << lgN) >> lgB;
@@ -434,9 +436,14 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
     C* dstr = (gr.Z == 1) ? (C*)y_direct : (C*)ws(c, "fold_part", (size_t)gr.Z * BB * sizeof(C));
     const size_t dynr = (size_t)nslot * kRingSegBytes + 3 * 512 * sizeof(C);
     pre(c, st);
-    kl(k_fold_ring2<Tin, T>, dim3(1, B, gr.Z), 256, dynr, st, x, space, space2, pp.p[0], *spec_q, gr,
-       nslot, dstr, (C*)spec_y, zero_peak);
+    if (spec_same)
+      kl(k_fold_ring2<Tin, T, true>, dim3(1, B, gr.Z), 256, dynr, st, x, space, space2, pp.p[0],
+         *spec_q, gr, nslot, dstr, (C*)spec_y, zero_peak);
+    else
+      kl(k_fold_ring2<Tin, T>, dim3(1, B, gr.Z), 256, dynr, st, x, space, space2, pp.p[0], *spec_q,
+         gr, nslot, dstr, (C*)spec_y, zero_peak);
     post(c, "k_fold_ring2", st, sup * sup * sizeof(Tin) + 5.0 * gr.Z * BB * sizeof(C));
+    if (spec_same && gr.Z == 1) fail(SFFT2D_ERR_STATE, "same-B speculative fold needs partials");
     *spec_z = gr.Z;
     return FoldOut{dstr, gr.Z};
   }
@@ -1113,7 +1120,28 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       }
     } else if (BB * sizeof(C) <= (size_t)kSmall2DBytes) {
       C* y = (C*)ws(c, "fold_y", BB * sizeof(C));
-      const FoldOut fo = fold_launch<T, Tin>(c, x, lgN, lgb, tb, &p, 1, y, st);
+      FoldOut fo{y, 1};
+      if (spec_pi == pi && spec_b == bb) {
+        fo = FoldOut{spec_grid, spec_z};   // folded with pass 0 (same B, one read)
+        spec_pi = -1;
+      } else {
+        spec_pi = -1;
+        // the first two tuner passes share B (no ratio after pass 0) and pass 1
+        // always follows when max_iters >= 2: fold both from one read
+        const long zs = std::min<long>(n / bb, 2L * kNumSMs / bb);
+        static const bool spec0_on = getenv("SFFT2D_NO_SPEC0") == nullptr;
+        if (spec_on && spec0_on && pi == 0 && max_iters >= 2 && (size_t)n * sizeof(Tin) >= kRingSegBytes &&
+            bb < 512 && zs > 1) {
+          const Perm* sq = &ps.get(1, st);
+          spec_grid = (C*)ws(c, "spec_small", (size_t)zs * BB * sizeof(C));
+          spec_pi = 1;
+          spec_b = bb;
+          fo = fold_launch<T, Tin>(c, x, lgN, lgb, tb, &p, 1, y, st, nullptr, false, sq, spec_grid,
+                                   &spec_z, true);
+        } else {
+          fo = fold_launch<T, Tin>(c, x, lgN, lgb, tb, &p, 1, y, st);
+        }
+      }
       const Publish pub = make_publish(c, 1);
       seq = pub.seq;
       pre(c, st);

@@ -410,7 +410,10 @@ k_fold_ring(const Tin* __restrict__ x, const T* __restrict__ space, Perm p, Fold
 // wr * wc are formed per row and block (no per-block row sums u[] — those
 // would not fit twice in registers).  Rows with a zero weight in both passes
 // are skipped.  Partials [Z][B][B] and [Z][2B][2B] (Z = 1: the grids).
-template <typename Tin, typename T>
+// SAME: the second pass has the same B (the tuner's first two passes, whose
+// B does not change after a pass without a ratio, tuner.py:182-207): its rows
+// all go to bucket row rho, window `space2` = `space`.
+template <typename Tin, typename T, bool SAME = false>
 __global__ void __launch_bounds__(256)
 k_fold_ring2(const Tin* __restrict__ x, const T* __restrict__ space,
              const T* __restrict__ space2, Perm p, Perm q, FoldGeom gm, int nslot,
@@ -493,7 +496,7 @@ k_fold_ring2(const Tin* __restrict__ x, const T* __restrict__ space,
       mbar_wait(&s_bar[slot], (k / nslot) & 1u);
       const int jr = s_rows[i];
       const T wr = s_w[jr], wr2 = s_w2[jr];
-      const int par = (j0 + jr) & 1;
+      const int par = SAME ? 0 : ((j0 + jr) & 1);
       const Tin* row = ring + (size_t)slot * SEGC;
       C t1[2] = {mk<T>(0, 0), mk<T>(0, 0)}, t2[2] = {mk<T>(0, 0), mk<T>(0, 0)};
 #pragma unroll
@@ -538,6 +541,14 @@ k_fold_ring2(const Tin* __restrict__ x, const T* __restrict__ space,
     C sum = mk<T>(0, 0);
     for (int a = 0; a < 512 / B; ++a) sum = cadd(sum, red[kap + a * B]);
     dst[(size_t)z * BB + (size_t)rho * B + kap] = sum;
+  }
+  if (SAME) {
+    for (int kap = tid; kap < B; kap += blockDim.x) {
+      C sum = mk<T>(0, 0);
+      for (int a = 0; a < 512 / B; ++a) sum = cadd(sum, red[512 + kap + a * B]);
+      dst2[(size_t)z * BB + (size_t)rho * B + kap] = sum;
+    }
+    return;
   }
   for (int e = tid; e < 2 * (int)B2; e += blockDim.x) {
     const int par = e / (int)B2, kap = e - par * (int)B2;
