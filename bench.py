@@ -388,8 +388,9 @@ def main():
         xs = [torch.from_numpy(c4_image(rank * args.c4_images + i)).to(dev)
               for i in range(args.c4_images)]
         seeds = [1 + i for i in range(args.c4_images)]
-        P.atsfft2d_batch(xs, cfg, args.est_loops, seeds, concurrency=args.concurrency,
-                         precision=args.precision, arrays=True)
+        for _ in range(3):   # every worker meets most images (workspace sizes settle)
+            P.atsfft2d_batch(xs, cfg, args.est_loops, seeds, concurrency=args.concurrency,
+                             precision=args.precision, arrays=True)
         torch.cuda.synchronize()
         samples = []
         bsampler = ClockSampler(sampler.dev)
