@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define SFFT2D_ABI_VERSION 1
+#define SFFT2D_ABI_VERSION 2
 #define SFFT2D_MAX_HISTORY 256
 
 enum sfft2d_status {
