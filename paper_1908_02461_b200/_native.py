@@ -22,6 +22,7 @@ OK, ERR_VALUE, ERR_CONFIG, ERR_CUDA, ERR_NOMEM, ERR_UNSUPPORTED, ERR_STATE = 0, 
 C64, C128 = 0, 1
 FP32, FP64 = 0, 1
 MAX_HISTORY = 256
+ABI_VERSION = 2   # include/sfft2d_b200.h SFFT2D_ABI_VERSION
 
 EXPORTS = (
     "sfft2d_abi_version", "sfft2d_ctx_create", "sfft2d_ctx_destroy", "sfft2d_ctx_last_error",
@@ -129,6 +130,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             fn = getattr(lib, name)
             fn.argtypes = args
             fn.restype = res
+        if lib.sfft2d_abi_version() != ABI_VERSION:
+            raise RuntimeError(f"{path} has ABI version {lib.sfft2d_abi_version()}, this package "
+                               f"expects {ABI_VERSION}: rebuild it (g.build())")
         _lib = lib
         return lib
 
