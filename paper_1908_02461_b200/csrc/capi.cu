@@ -859,13 +859,14 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
     const int B = 1 << lgB;
     const size_t BB = (size_t)B * B;
     C* grids = (C*)ws(c, "est_grids", (size_t)L * BB * sizeof(C));
-    fold_spectrum<T, Tin>(c, x, lgN, lgB, tb, hp, L, grids, (T*)nullptr, nullptr, st);
+    // natural-order folds (coalesced writes; k_estimate reads the permuted view)
+    fold_spectrum<T, Tin>(c, x, lgN, lgB, tb, hp, L, grids, (T*)nullptr, nullptr, st, true);
     C* vals = (C*)ws(c, "vals", (size_t)L * m * sizeof(C));
     uint8_t* usable = (uint8_t*)ws(c, "usable", (size_t)L * m);
     const T* freq = (const T*)tb.freq[P] + ((size_t)lgB << lgN);
     pre(c, st);
     kl(k_estimate<T>, grid_for((long long)m * L), 256, 0, st, grids, L, keys, m_dev, dp, lgN, lgB, freq, (const C*)tb.tw[P], gain_floor, vals, usable,
-        (long)m);
+        (long)m, true);
     post(c, "k_estimate", st, 0);
     pre(c, st);
     kl(k_median<T>, grid_for(m, 128), 128, 0, st, vals, usable, L, (long)m, m_dev, med, mags,
@@ -1879,12 +1880,12 @@ int sfft2d_estimate_loops(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_ho
       const size_t BB = (size_t)b * b;
       C* grids = (C*)ws(c, "est_grids", (size_t)nloops * BB * sizeof(C));
       fold_spectrum<T, Tin>(c, (const Tin*)xd, lgN, lgB, tb, up.first.data(), nloops, grids,
-                            (T*)nullptr, nullptr, st);
+                            (T*)nullptr, nullptr, st, true);
       const T* freq = (const T*)tb.freq[P] + ((size_t)lgB << lgN);
       pre(c, st);
       kl(k_estimate<T>, grid_for((long long)m * nloops), 256, 0, st, (const C*)grids, nloops, keys,
          (const unsigned*)m_dev, (const Perm*)up.second, lgN, lgB, freq, (const C*)tb.tw[P],
-         gain_floor, (C*)vals, usable, (long)m);
+         gain_floor, (C*)vals, usable, (long)m, true);
       post(c, "k_estimate", st, 0);
     });
     ck(cudaStreamSynchronize(st), "sync");

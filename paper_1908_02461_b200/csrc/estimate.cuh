@@ -23,7 +23,8 @@ __global__ void k_estimate(const cplx<T>* __restrict__ spec, int nloops, const i
                            const unsigned* __restrict__ m_dev, const Perm* __restrict__ perms,
                            int lgN, int lgB, const T* __restrict__ freq,
                            const cplx<T>* __restrict__ tw, double gain_floor,
-                           cplx<T>* __restrict__ vals, uint8_t* __restrict__ usable, long stride) {
+                           cplx<T>* __restrict__ vals, uint8_t* __restrict__ usable, long stride,
+                           bool natural_grid = false) {
   pdl_wait();
   using C = cplx<T>;
   const long m = *m_dev;
@@ -44,7 +45,19 @@ __global__ void k_estimate(const cplx<T>* __restrict__ spec, int nloops, const i
     const unsigned oi = (qi - (ui << lgw)) & maskN, oj = (qj - (uj << lgw)) & maskN;
     const T gain = freq[oi] * freq[oj];
     const C ph = tw[(p.t1 * i + p.t2 * j) & maskN];
-    const C z = spec[(size_t)l * B * B + (size_t)(ui & maskB) * B + (uj & maskB)];
+    C z;
+    if (natural_grid) {
+      // spec holds Y^ of the natural-order fold (coalesced fold writes): with
+      // Z[a, b] = Y[s1 a + t1, s2 b + t2] (mod B),
+      // Z^[a, b] = exp(+2 pi i (s1i t1 a + s2i t2 b) / B) Y^[s1i a, s2i b]
+      const unsigned a = ui & maskB, b = uj & maskB;
+      const unsigned ra = (p.s1i * a) & maskB, cb = (p.s2i * b) & maskB;
+      const unsigned ex = (p.s1i * p.t1 * a + p.s2i * p.t2 * b) & maskB;
+      const C w = tw[ex << lgw];
+      z = cmul(spec[(size_t)l * B * B + (size_t)ra * B + cb], mk<T>(w.x, -w.y));
+    } else {
+      z = spec[(size_t)l * B * B + (size_t)(ui & maskB) * B + (uj & maskB)];
+    }
     const bool ok = (double)fabs(gain) >= gain_floor;
     C v = cmul(z, ph);
     if (ok) { v.x = v.x / gain; v.y = v.y / gain; }
