@@ -463,7 +463,9 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
   if (g == 1 && B >= 512 && lgN - lgB <= 5 && y_direct) {
     // wide single-loop fold, grid written directly
     const double by = sup * sup * sizeof(Tin) + (double)BB * sizeof(C);
-    const int rh = B >= 1024 ? 2 : 1;   // RH=4 needs 128 registers (2 CTAs/SM)
+    // RH=2 (two bucket rows per CTA) in fp32; fp64 accumulators would need 128
+    // registers (2 CTAs/SM), so fp64 keeps RH=1
+    const int rh = (B >= 1024 && sizeof(T) == 4) ? 2 : 1;
     const dim3 grid_w(B / 512, B / rh);
     pre(c, st);
     if (rh == 2)

@@ -712,19 +712,21 @@ k_fold_wide2(const Tin* __restrict__ x, const T* __restrict__ space, const T* __
         u[ii][cq] = mk<T>(0, 0);
         u2[ii][0][cq] = u2[ii][1][cq] = mk<T>(0, 0);
       }
-    // row aliases in batches of 8: all 16 row-segment loads of a batch are
-    // issued before the first FMA (A = 4 runs one half batch)
-    for (int jb = 0; jb < A; jb += 8) {
-      C v[8][2][2];                          // [row alias in batch][ii][cq]
+    // row aliases in batches of JB = 8: all 16 row-segment loads of a batch are
+    // issued before the first FMA (fp64 too: JB = 4 halved the registers but
+    // measured 61 -> 71 us — loads in flight matter more than occupancy here)
+    constexpr int JB = 8;
+    for (int jb = 0; jb < A; jb += JB) {
+      C v[JB][2][2];                         // [row alias in batch][ii][cq]
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj)
+      for (int jj = 0; jj < JB; ++jj)
 #pragma unroll
         for (int ii = 0; ii < 2; ++ii)
           if (jj < 4 || A > 4)
             ColLoad<Tin, T, 2>::ld(x + kap + ((i0 + ii) << lgB) + ((size_t)(rho + ((jb + jj) << lgB)) << lgN),
                                    v[jj][ii]);
 #pragma unroll
-      for (int jj = 0; jj < 8; ++jj) {
+      for (int jj = 0; jj < JB; ++jj) {
         if (jj >= 4 && A <= 4) break;
         const int jp = jj & 1;
         const T w = s_w[jb + jj], w2 = s_w2[jb + jj];
