@@ -647,13 +647,17 @@ unsigned lmax_tuner(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long l
     // streaming bands: ~2 CTAs per SM, a ring of row buffers per CTA
     int nslot = (int)std::max<size_t>(4, std::min<size_t>(8, (96 * 1024 - wb) / row));
     if (nslot * row + wb > kMaxDynSmem) nslot = (int)((kMaxDynSmem - wb) / row);
-    const int band = (B + 2 * kNumSMs - 1) / (2 * kNumSMs);
+    // ~2 CTAs per SM; the fp64 register windows of k_lmax_win (86 registers x
+    // 512 threads) fit one CTA per SM, so their bands are sized for one wave
+    const bool win = live_most && !cand && B <= 4096;
+    const int cps = (win && sizeof(T) == 8 && B >= 2048) ? 1 : 2;
+    const int band = (B + cps * kNumSMs - 1) / (cps * kNumSMs);
     const int thr = 512;
     const int grid = (B + band - 1) / band;
     const size_t sm = nslot * row + wb;
     const Publish pub = make_publish(c, (unsigned)grid);
     pre(c, st);
-    if (live_most && !cand && B <= 4096) {
+    if (win) {
       // most bins pass the floor: register neighbourhood windows, one warp per
       // 128-column group (fewer threads for narrow grids)
       const int tw = std::min(512, B / 4);
