@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define SFFT2D_ABI_VERSION 2
+#define SFFT2D_ABI_VERSION 3
 #define SFFT2D_MAX_HISTORY 256
 
 enum sfft2d_status {
@@ -240,6 +240,19 @@ int sfft2d_local_maxima(sfft2d_ctx* ctx, const void* grid, int b, double mag_flo
  * index order to out_flat[nseg][num] (device).                            */
 int sfft2d_top_bins(sfft2d_ctx* ctx, const void* grids, int b, int nseg, int64_t num,
                     int precision, int32_t* out_flat, void* stream);
+
+/* ---- workload generator (no reference counterpart:
+ * the reference generates on the host, signals.py:42-65) ----
+ * out (device, n x n, SFFT2D_C64 or SFFT2D_C128) = ifft2(S) + noise_sd * (n1 + i n2)
+ * where S holds coeffs[i] (interleaved re/im doubles, host) at (rows[i],
+ * cols[i]) (host int64) and n1, n2 are standard normals from Philox4x32-10
+ * keyed by noise_seed, counter = flat element index (Box-Muller in double;
+ * paper_1908_02461_b200/csrc/generate.cuh).  The inverse DFT runs through the
+ * library's own forward FFT (fp32 for C64, fp64 for C128); needs the twiddle
+ * table of side n (sfft2d_ctx_set_tables).  Stream-ordered, no host sync.  */
+int sfft2d_generate(sfft2d_ctx* ctx, int n, int64_t k, const int64_t* rows, const int64_t* cols,
+                    const double* coeffs, double noise_sd, uint64_t noise_seed, int out_dtype,
+                    void* out, void* stream);
 
 #ifdef __cplusplus
 }

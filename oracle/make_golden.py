@@ -304,6 +304,43 @@ def case_c4():
     _ats_case("c4_k200", img.x, 8, 102, False, extra=_gen_meta(img, snr=25.0, mag="loguniform"))
 
 
+def c4_bench_image(i: int):
+    """bench.py's c4 image i (same definition as bench.c4_image): seed 100000 + i,
+    k ~ U[20, 200] from that seed, log-uniform magnitudes, 25 dB."""
+    seed = 100_000 + i
+    k = int(np.random.default_rng(seed).integers(20, 201))
+    return sparse_image(1024, k, seed, snr_db=25.0, magnitude="loguniform")
+
+
+def case_c4_batch():
+    # the first 12 images of the bench's c4 batch (rng seed 1 + i, as in the
+    # bench leg), so the batched leg carries a parity spot-check
+    for i in range(12):
+        img = c4_bench_image(i)
+        _ats_case(f"c4b_{i:02d}", img.x, 8, 1 + i, False,
+                  extra=_gen_meta(img, snr=25.0, mag="loguniform", index=i))
+
+
+def _c5_sweep(k, seed):
+    img = sparse_image(16384, k, seed, snr_db=15.0, cluster_frac=0.2, cluster_side=64)
+    x = img.x
+    meta = _gen_meta(img, snr=15.0, cluster=0.2)
+    del img
+    _ats_case(f"c5_ats_k{k}", x, 8, seed + 1, False, extra=meta)
+
+
+def case_c5_k256():
+    _c5_sweep(256, 5)
+
+
+def case_c5_k1024():
+    _c5_sweep(1024, 5)
+
+
+def case_c5_k4096():
+    _c5_sweep(4096, 5)
+
+
 def case_c5():
     # 16384^2 complex64, k=64, 20% in the wrap-around DC 64x64 block, 15 dB
     img = sparse_image(16384, 64, 5, snr_db=15.0, cluster_frac=0.2, cluster_side=64)

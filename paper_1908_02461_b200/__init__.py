@@ -19,7 +19,8 @@ from .engine import (ConfigurationError, SfftConfig, default_bins, estimate_once
 from .hashing import (BinGrid, FlatWindow, PermutationParams, WindowCache, all_pass_window,
                       binned_spectrum, build_flat_window, draw_permutation, hash_coord,
                       identity_permutation, mod_inverse, offset_coord, unhash_bin)
-from .signals import error_metric, load_signal, planted_image, save_signal, sparse_image
+from .signals import (device_sparse_image, error_metric, load_signal, planted_image, save_signal,
+                      sparse_image)
 from .tuner import (TunerConfig, TunerState, atsfft2d, atsfft2d_arrays, count_local_maxima,
                     detect_sparsity, update_bins)
 
@@ -31,5 +32,5 @@ __all__ = [
     "planted_image", "sparse_image", "TunerConfig", "TunerState", "atsfft2d", "atsfft2d_arrays",
     "count_local_maxima", "detect_sparsity", "update_bins", "atsfft2d_batch", "sfft2d_batch",
     "seek_location_once", "vote_and_select", "estimate_once", "median_combine", "save_signal",
-    "load_signal",
+    "load_signal", "device_sparse_image",
 ]

@@ -22,7 +22,7 @@ OK, ERR_VALUE, ERR_CONFIG, ERR_CUDA, ERR_NOMEM, ERR_UNSUPPORTED, ERR_STATE = 0, 
 C64, C128 = 0, 1
 FP32, FP64 = 0, 1
 MAX_HISTORY = 256
-ABI_VERSION = 2   # include/sfft2d_b200.h SFFT2D_ABI_VERSION
+ABI_VERSION = 3   # include/sfft2d_b200.h SFFT2D_ABI_VERSION
 
 EXPORTS = (
     "sfft2d_abi_version", "sfft2d_ctx_create", "sfft2d_ctx_destroy", "sfft2d_ctx_last_error",
@@ -31,7 +31,7 @@ EXPORTS = (
     "sfft2d_local_maxima", "sfft2d_top_bins", "sfft2d_ctx_set_profiling",
     "sfft2d_ctx_profile_report", "sfft2d_atsfft_bitgen", "sfft2d_detect_sparsity_bitgen",
     "sfft2d_ctx_sync_us", "sfft2d_sfft_votes", "sfft2d_sfft_from_votes",
-    "sfft2d_estimate_loops", "sfft2d_median_select",
+    "sfft2d_estimate_loops", "sfft2d_median_select", "sfft2d_generate",
 )
 
 
@@ -125,6 +125,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                        i32, i32, vp, vp, vp], i32),
             "sfft2d_median_select": ([vp, i32, vp, i64, vp, vp, i32, i64, dbl, i32, vp,
                                       P(ResultC)], i32),
+            "sfft2d_generate": ([vp, i32, i64, vp, vp, vp, dbl, ctypes.c_uint64, i32, vp, vp],
+                                i32),
         }
         for name, (args, res) in sig.items():
             fn = getattr(lib, name)

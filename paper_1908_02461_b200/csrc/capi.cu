@@ -27,6 +27,7 @@
 #include "fft.cuh"
 #include "fft_launch.cuh"
 #include "fold.cuh"
+#include "generate.cuh"
 #include "host.cuh"
 #include "select.cuh"
 #include "vote.cuh"
@@ -2098,6 +2099,51 @@ int sfft2d_top_bins(sfft2d_ctx* c, const void* grids, int b, int nseg, int64_t n
       unsigned* tots = (unsigned*)ws(c, "api_tot", (size_t)nseg * 4 + 16);
       compact(c, sb, sc, BB, nseg, out_flat, (long)num, tots, st);
     });
+  });
+}
+
+int sfft2d_generate(sfft2d_ctx* c, int n, int64_t k, const int64_t* rows, const int64_t* cols,
+                    const double* coeffs, double noise_sd, uint64_t noise_seed, int out_dtype,
+                    void* out, void* stream) {
+  return guarded(c, [&] {
+    check_side(n);
+    if (!out || k < 0 || (k > 0 && (!rows || !cols || !coeffs)) || (long long)k > (long long)n * n)
+      fail(SFFT2D_ERR_VALUE, "bad arguments");
+    if (!(noise_sd >= 0.0) || !std::isfinite(noise_sd)) fail(SFFT2D_ERR_VALUE, "noise sd must be finite and >= 0");
+    for (int64_t i = 0; i < k; ++i)
+      if (rows[i] < 0 || rows[i] >= n || cols[i] < 0 || cols[i] >= n)
+        fail(SFFT2D_ERR_VALUE, "coefficient position outside the image");
+    const DevTables& tb = find_twiddles(c, n);
+    cudaStream_t st = (cudaStream_t)stream;
+    c->ws_st = st;
+    c->launches = 0;
+    const int lgN = ilog2(n);
+    const long total = (long)n * n;
+    auto run = [&](auto t) {
+      using T = decltype(t);
+      using C = cplx<T>;
+      C* g = (C*)out;
+      ck(cudaMemsetAsync(g, 0, (size_t)total * sizeof(C), st), "memset");
+      if (k > 0) {
+        char* buf = (char*)ws(c, "gen_coef", (size_t)k * 32);
+        ck(cudaMemcpyAsync(buf, rows, (size_t)k * 8, cudaMemcpyHostToDevice, st), "H2D rows");
+        ck(cudaMemcpyAsync(buf + (size_t)k * 8, cols, (size_t)k * 8, cudaMemcpyHostToDevice, st), "H2D cols");
+        ck(cudaMemcpyAsync(buf + (size_t)k * 16, coeffs, (size_t)k * 16, cudaMemcpyHostToDevice, st),
+           "H2D coeffs");
+        pre(c, st);
+        kl(k_gen_scatter<T>, (unsigned)((k + 255) / 256), 256, 0, st, g, lgN, (const int64_t*)buf,
+           (const int64_t*)(buf + (size_t)k * 8), (const double2*)(buf + (size_t)k * 16), (int)k);
+        post(c, "k_gen_scatter", st, (double)k * 32);
+        fft2d_grids<T>(c, g, lgN, 1, (const C*)tb.tw[prec_of<T>()], tb.lgn, g, (T*)nullptr, nullptr, st);
+      }
+      pre(c, st);
+      kl(k_gen_finish<T>, grid_for(total, 256, kNumSMs * 8), 256, 0, st, g, total,
+         1.0 / ((double)n * (double)n), noise_sd, (uint32_t)noise_seed, (uint32_t)(noise_seed >> 32));
+      post(c, "k_gen_finish", st, 2.0 * total * sizeof(C));
+    };
+    if (out_dtype == SFFT2D_C64) run(float());
+    else if (out_dtype == SFFT2D_C128) run(double());
+    else fail(SFFT2D_ERR_VALUE, "unknown out_dtype");
   });
 }
 

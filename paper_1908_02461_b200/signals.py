@@ -27,7 +27,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-__all__ = ["SparseImage", "sparse_image", "planted_image", "error_metric", "image_digest",
+__all__ = ["SparseImage", "DeviceSparseImage", "sparse_image", "device_sparse_image", "planted_image", "error_metric", "image_digest",
            "save_signal", "load_signal"]
 
 
@@ -50,24 +50,9 @@ def _is_pow2(v: int) -> bool:
     return v >= 1 and (v & (v - 1)) == 0
 
 
-def sparse_image(
-    n: int,
-    k: int,
-    seed: int,
-    *,
-    snr_db: float | None = None,
-    magnitude: str = "unit",
-    mag_range: tuple[float, float] = (0.1, 10.0),
-    cluster_frac: float = 0.0,
-    cluster_side: int = 64,
-    dtype=np.complex64,
-) -> SparseImage:
-    """Seeded k-sparse-spectrum image, optionally noisy (see module docstring)."""
-    if not _is_pow2(n):
-        raise ValueError(f"side {n} is not a power of 2")
-    if k < 0 or k > n * n:
-        raise ValueError(f"sparsity {k} out of range for side {n}")
-    rng = np.random.default_rng(seed)
+def _draw_spectrum(rng, n, k, magnitude, mag_range, cluster_frac, cluster_side):
+    """Positions (clustered fraction first, then uniform distinct draws),
+    phases and magnitudes, in that stream order."""
     n_clu = int(round(cluster_frac * k)) if cluster_frac > 0 else 0
     side = min(cluster_side, n)
     if n_clu > side * side:
@@ -99,6 +84,25 @@ def sparse_image(
     else:
         raise ValueError(f"unknown magnitude law {magnitude!r}")
     coeffs = mags * np.exp(1j * phases)
+    return rows, cols, coeffs
+
+
+def sparse_image(
+    n: int,
+    k: int,
+    seed: int,
+    *,
+    snr_db: float | None = None,
+    magnitude: str = "unit",
+    mag_range: tuple[float, float] = (0.1, 10.0),
+    cluster_frac: float = 0.0,
+    cluster_side: int = 64,
+    dtype=np.complex64,
+) -> SparseImage:
+    """Seeded k-sparse-spectrum image, optionally noisy (see module docstring)."""
+    _check_side_k(n, k)
+    rng = np.random.default_rng(seed)
+    rows, cols, coeffs = _draw_spectrum(rng, n, k, magnitude, mag_range, cluster_frac, cluster_side)
     spec = np.zeros((n, n), dtype=np.complex128)
     spec[rows, cols] = coeffs
     x = np.fft.ifft2(spec)
@@ -109,6 +113,89 @@ def sparse_image(
         x += sd * rng.standard_normal((n, n))
         x += 1j * sd * rng.standard_normal((n, n))
     return SparseImage(n, k, seed, np.ascontiguousarray(x.astype(dtype)), rows, cols, coeffs)
+
+
+@dataclass(frozen=True)
+class DeviceSparseImage:
+    n: int
+    k: int
+    seed: int
+    x: object                     # torch.Tensor (n, n) complex64 / complex128 on the device
+    rows: np.ndarray
+    cols: np.ndarray
+    coeffs: np.ndarray
+    noise_sd: float
+    noise_seed: int
+
+    @property
+    def truth(self) -> dict:
+        return {(int(i), int(j)): complex(c) for i, j, c in zip(self.rows, self.cols, self.coeffs)}
+
+
+def _check_side_k(n, k):
+    if not _is_pow2(n):
+        raise ValueError(f"side {n} is not a power of 2")
+    if k < 0 or k > n * n:
+        raise ValueError(f"sparsity {k} out of range for side {n}")
+
+
+def device_sparse_image(
+    n: int,
+    k: int,
+    seed: int,
+    *,
+    snr_db: float | None = None,
+    magnitude: str = "unit",
+    mag_range: tuple[float, float] = (0.1, 10.0),
+    cluster_frac: float = 0.0,
+    cluster_side: int = 64,
+    dtype=np.complex64,
+    device=None,
+    out=None,
+) -> DeviceSparseImage:
+    """The same workload built in HBM by the library's generator
+    (``sfft2d_generate``, csrc/generate.cuh): positions, phases and magnitudes
+    are drawn on the host exactly as ``sparse_image`` draws them (same seed ->
+    same coefficients), the inverse DFT runs through the library's own FFT, and
+    the noise is Philox4x32-10 normals keyed by a 63-bit seed drawn next from
+    the same stream.  Noise power uses Parseval, ``mean|x_clean|^2 =
+    sum|c|^2 / n^4`` (the host generator's ``np.mean(np.abs(x)**2)`` up to
+    roundoff).  ``out``: optional preallocated (n, n) device tensor."""
+    from . import _native
+    torch = _native._torch()
+    _check_side_k(n, k)
+    rng = np.random.default_rng(seed)
+    rows, cols, coeffs = _draw_spectrum(rng, n, k, magnitude, mag_range, cluster_frac,
+                                        cluster_side)
+    noise_seed = int(rng.integers(2**63))
+    sd = 0.0
+    if snr_db is not None:
+        power = float(np.sum(np.abs(coeffs) ** 2)) / float(n) ** 4
+        sd = float(np.sqrt(power * 10.0 ** (-snr_db / 10.0) / 2.0))
+    if np.dtype(dtype) == np.complex64:
+        tdt, code = torch.complex64, _native.C64
+    elif np.dtype(dtype) == np.complex128:
+        tdt, code = torch.complex128, _native.C128
+    else:
+        raise ValueError(f"unsupported dtype {dtype!r}")
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else
+                       (device.index if isinstance(device, torch.device) else int(device)))
+    if out is None:
+        out = torch.empty((n, n), dtype=tdt, device=dev)
+    elif out.shape != (n, n) or out.dtype != tdt or out.device != dev or not out.is_contiguous():
+        raise ValueError("out must be a contiguous (n, n) tensor of the requested dtype on the device")
+    ctx = _native.context(dev.index)
+    from .tuner import TunerConfig
+    tc = TunerConfig()   # the transforms' default tables (any table of side n holds the twiddles)
+    ctx.ensure_tables(n, tc.window_delta_pass, tc.window_delta_stop)
+    r = np.ascontiguousarray(rows, dtype=np.int64)
+    c = np.ascontiguousarray(cols, dtype=np.int64)
+    cf = np.ascontiguousarray(coeffs, dtype=np.complex128)
+    with torch.cuda.device(dev):
+        st = torch.cuda.current_stream(dev).cuda_stream
+        ctx.check(ctx.lib.sfft2d_generate(ctx.handle, n, int(k), r.ctypes.data, c.ctypes.data,
+                                          cf.ctypes.data, sd, noise_seed, code, out.data_ptr(), st))
+    return DeviceSparseImage(n, k, seed, out, rows, cols, coeffs, sd, noise_seed)
 
 
 def planted_image(n: int, k: int, seed: int) -> SparseImage:

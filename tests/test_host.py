@@ -24,7 +24,7 @@ def test_library_exports_header_symbols():
     lib = ctypes.CDLL(_native.LIB_PATH)
     for name in declared:
         assert hasattr(lib, name), name
-    assert _native.load_library().sfft2d_abi_version() == 2
+    assert _native.load_library().sfft2d_abi_version() == 3
 
 
 def test_struct_layouts_match_header():
