@@ -26,9 +26,16 @@
  *    data-dependent decision points of the algorithm (tuner counts).
  *  - Return value: SFFT2D_OK or a negative status; nothing throws across the
  *    ABI.  sfft2d_ctx_last_error returns the message of the last failure.
- *  - A context owns a grow-only device workspace and the registered tables;
- *    it is bound to one device and must not be used concurrently from two
- *    host threads.
+ *  - Device workspace: by default a context grows named buffers stream-
+ *    ordered from its OWN memory pool (never the device's default pool, whose
+ *    attributes are left untouched).  A caller that owns all device memory
+ *    (e.g. torch's caching allocator) hands the context one arena with
+ *    sfft2d_ctx_set_workspace; the library then never allocates device memory
+ *    and reports SFFT2D_ERR_NOMEM when the arena is too small.  The size a
+ *    workload needs is sfft2d_ctx_workspace_size's `peak` after running it
+ *    once.  Small pinned host buffers (count publication, result staging)
+ *    stay library-owned.  A context is bound to one device and must not be
+ *    used concurrently from two host threads.
  */
 #ifndef SFFT2D_B200_H
 #define SFFT2D_B200_H
@@ -240,6 +247,14 @@ int sfft2d_local_maxima(sfft2d_ctx* ctx, const void* grid, int b, double mag_flo
  * index order to out_flat[nseg][num] (device).                            */
 int sfft2d_top_bins(sfft2d_ctx* ctx, const void* grids, int b, int nseg, int64_t num,
                     int precision, int32_t* out_flat, void* stream);
+
+/* Caller-owned device workspace: `base` (device, at
+ * least `bytes`) replaces the context's pool for every later call; NULL / 0
+ * returns to the pool.  Synchronises the device (buffers are dropped).      */
+int sfft2d_ctx_set_workspace(sfft2d_ctx* ctx, void* base, int64_t bytes);
+/* Workspace bytes currently held and the high-water mark since the last
+ * sfft2d_ctx_set_workspace (or context creation).                          */
+int sfft2d_ctx_workspace_size(const sfft2d_ctx* ctx, int64_t* in_use, int64_t* peak);
 
 /* ---- workload generator (no reference counterpart:
  * the reference generates on the host, signals.py:42-65) ----

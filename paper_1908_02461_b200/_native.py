@@ -32,6 +32,7 @@ EXPORTS = (
     "sfft2d_ctx_profile_report", "sfft2d_atsfft_bitgen", "sfft2d_detect_sparsity_bitgen",
     "sfft2d_ctx_sync_us", "sfft2d_sfft_votes", "sfft2d_sfft_from_votes",
     "sfft2d_estimate_loops", "sfft2d_median_select", "sfft2d_generate",
+    "sfft2d_ctx_set_workspace", "sfft2d_ctx_workspace_size",
 )
 
 
@@ -125,6 +126,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                                        i32, i32, vp, vp, vp], i32),
             "sfft2d_median_select": ([vp, i32, vp, i64, vp, vp, i32, i64, dbl, i32, vp,
                                       P(ResultC)], i32),
+            "sfft2d_ctx_set_workspace": ([vp, vp, i64], i32),
+            "sfft2d_ctx_workspace_size": ([vp, P(i64), P(i64)], i32),
             "sfft2d_generate": ([vp, i32, i64, vp, vp, vp, dbl, ctypes.c_uint64, i32, vp, vp],
                                 i32),
         }
@@ -196,6 +199,26 @@ class Context:
             name, cnt, ms, by = line.split()
             out[name] = (int(cnt), float(ms), float(by))
         return out
+
+    def workspace_size(self) -> tuple:
+        """(bytes in use, high-water mark) of this context's device workspace."""
+        a, b = ctypes.c_int64(), ctypes.c_int64()
+        self.check(self.lib.sfft2d_ctx_workspace_size(self.handle, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, b.value
+
+    def use_workspace(self, buf) -> None:
+        """Run every later call of this context inside the caller-owned device
+        buffer `buf` (a CUDA uint8 tensor, kept alive here); None returns to
+        the context's own pool."""
+        if buf is None:
+            self.check(self.lib.sfft2d_ctx_set_workspace(self.handle, None, 0))
+            self._ws_buf = None
+            return
+        if not buf.is_cuda or not buf.is_contiguous():
+            raise ValueError("workspace must be a contiguous CUDA tensor")
+        self.check(self.lib.sfft2d_ctx_set_workspace(self.handle, buf.data_ptr(),
+                                                     buf.numel() * buf.element_size()))
+        self._ws_buf = buf
 
     def ensure_tables(self, n: int, delta_pass: float, delta_stop: float):
         key = (n, float(delta_pass), float(delta_stop))

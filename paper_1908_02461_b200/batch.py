@@ -92,6 +92,20 @@ def warm_workers(fn, concurrency: int, device=None) -> None:
     list(_pool(concurrency).map(one, range(concurrency)))
 
 
+def _shared_generators(rngs) -> bool:
+    """True when one numpy Generator object is passed for several items: the
+    native controller draws straight from its bit generator, so those items
+    must run one after another in input order (as sequential calls would)."""
+    import numpy as np
+    seen = set()
+    for r in rngs:
+        if isinstance(r, np.random.Generator):
+            if id(r) in seen:
+                return True
+            seen.add(id(r))
+    return False
+
+
 def atsfft2d_batch(xs, cfg: TunerConfig, est_loops: int, rngs, *, concurrency: int = 4,
                    precision: str = "fp64", device=None, arrays: bool = False):
     """``atsfft2d`` over a batch: ``xs`` images, ``rngs`` one seed/Generator per
@@ -100,6 +114,8 @@ def atsfft2d_batch(xs, cfg: TunerConfig, est_loops: int, rngs, *, concurrency: i
     if len(xs) != len(rngs):
         raise ValueError("need one rng per image")
     fn = atsfft2d_arrays if arrays else atsfft2d
+    if _shared_generators(rngs):
+        concurrency = 1
 
     def one(i):
         return fn(xs[i], cfg, est_loops, rngs[i], precision=precision, device=device)
@@ -113,6 +129,8 @@ def sfft2d_batch(xs, cfg: SfftConfig, rngs, *, concurrency: int = 4, precision: 
     if len(xs) != len(rngs):
         raise ValueError("need one rng per image")
     fn = sfft2d_arrays if arrays else sfft2d
+    if _shared_generators(rngs):
+        concurrency = 1
 
     def one(i):
         return fn(xs[i], cfg, rngs[i], precision=precision, device=device)

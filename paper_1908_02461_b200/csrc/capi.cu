@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <string_view>
 #include <unordered_map>
 #include <mutex>
@@ -63,6 +64,14 @@ struct sfft2d_ctx {
   std::vector<DevTables> tables;
   // named workspace buffers (names are string literals: views stay valid)
   std::unordered_map<std::string_view, std::pair<void*, size_t>> bufs;
+  // workspace source: the context's own memory pool (default; a private pool
+  // so the process-wide default pool keeps its attributes), or a caller-owned
+  // device arena (sfft2d_ctx_set_workspace) sub-allocated first-fit
+  cudaMemPool_t pool = nullptr;
+  char* arena = nullptr;
+  size_t arena_bytes = 0;
+  std::map<size_t, size_t> arena_free;   // offset -> size of free blocks
+  size_t ws_in_use = 0, ws_peak = 0;
   unsigned* pinned = nullptr;  // small host scratch for counts
   Perm* perm_pinned = nullptr; // staging for permutations drawn on demand
   // last results
@@ -114,32 +123,72 @@ size_t pow2_cap(size_t bytes) {
   return cap;
 }
 
+static void arena_release(sfft2d_ctx* c, void* p, size_t bytes) {
+  size_t off = (size_t)((char*)p - c->arena);
+  auto it = c->arena_free.emplace(off, bytes).first;
+  auto nx = std::next(it);   // coalesce with the following free block
+  if (nx != c->arena_free.end() && it->first + it->second == nx->first) {
+    it->second += nx->second;
+    c->arena_free.erase(nx);
+  }
+  if (it != c->arena_free.begin()) {   // and with the preceding one
+    auto pv = std::prev(it);
+    if (pv->first + pv->second == it->first) {
+      pv->second += it->second;
+      c->arena_free.erase(it);
+    }
+  }
+}
+
+static void* arena_take(sfft2d_ctx* c, size_t bytes) {
+  for (auto it = c->arena_free.begin(); it != c->arena_free.end(); ++it) {
+    if (it->second < bytes) continue;
+    const size_t off = it->first, rest = it->second - bytes;
+    c->arena_free.erase(it);
+    if (rest) c->arena_free.emplace(off + bytes, rest);
+    return c->arena + off;
+  }
+  return nullptr;
+}
+
 void* ws(sfft2d_ctx* c, const char* name, size_t bytes) {
   auto& e = c->bufs[name];
   if (bytes == 0) bytes = 16;
   if (e.second < bytes) {
-    // Stream-ordered growth from the device's memory pool: cudaMalloc /
-    // cudaFree would synchronise the whole device and stall every other
-    // in-flight transform.  The side (vote) stream may still read the old
-    // buffer, so the free is ordered after its pending work.
+    // Stream-ordered growth: cudaMalloc / cudaFree would synchronise the
+    // whole device and stall every other in-flight transform.  The side
+    // (vote) stream may still read the old buffer, so its release is ordered
+    // after that stream's pending work (and, in arena mode, reuse of the
+    // released range happens only in work enqueued later on this stream).
     cudaStream_t s = c->ws_st;
     if (e.first) {
       ck(cudaEventRecord(c->ev_ws, c->vote_st), "cudaEventRecord");
       ck(cudaStreamWaitEvent(s, c->ev_ws, 0), "cudaStreamWaitEvent");
-      ck(cudaFreeAsync(e.first, s), "cudaFreeAsync");
+      if (c->arena) arena_release(c, e.first, e.second);
+      else ck(cudaFreeAsync(e.first, s), "cudaFreeAsync");
+      c->ws_in_use -= e.second;
     }
     e.first = nullptr;
     e.second = 0;
     const size_t cap = pow2_cap(bytes);
     if (getenv("SFFT2D_TRACE_ALLOC"))
       fprintf(stderr, "[sfft2d] ctx %p workspace '%s' -> %zu bytes\n", (void*)c, name, cap);
-    if (cudaMallocAsync(&e.first, cap, s) != cudaSuccess) {
+    if (c->arena) {
+      e.first = arena_take(c, cap);
+      if (!e.first)
+        fail(SFFT2D_ERR_NOMEM, std::string("caller workspace exhausted: '") + name + "' needs " +
+                                   std::to_string(cap) + " more bytes (" +
+                                   std::to_string(c->ws_in_use) + " in use of " +
+                                   std::to_string(c->arena_bytes) + ")");
+    } else if (cudaMallocFromPoolAsync(&e.first, cap, c->pool, s) != cudaSuccess) {
       cudaGetLastError();
       e.first = nullptr;
       fail(SFFT2D_ERR_NOMEM, std::string("cannot allocate workspace '") + name + "' of " +
                                  std::to_string(cap) + " bytes");
     }
     e.second = cap;
+    c->ws_in_use += cap;
+    c->ws_peak = std::max(c->ws_peak, c->ws_in_use);
   }
   return e.first;
 }
@@ -188,6 +237,23 @@ void allow_smem_ptr(const void* kernel) {
   ck(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem),
      "cudaFuncSetAttribute");
   done[key] = true;
+}
+
+int ctas_per_sm_ptr(const void* kernel, int threads, size_t smem) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, const void*, int, size_t>, int> cache;
+  int dev = 0;
+  ck(cudaGetDevice(&dev), "cudaGetDevice");
+  const auto key = std::make_tuple(dev, kernel, threads, smem);
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kernel, threads, smem),
+     "cudaOccupancyMaxActiveBlocksPerMultiprocessor");
+  n = std::max(n, 1);
+  cache[key] = n;
+  return n;
 }
 
 }  // namespace sfft
@@ -648,20 +714,25 @@ unsigned lmax_tuner(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long l
     // streaming bands: ~2 CTAs per SM, a ring of row buffers per CTA
     int nslot = (int)std::max<size_t>(4, std::min<size_t>(8, (96 * 1024 - wb) / row));
     if (nslot * row + wb > kMaxDynSmem) nslot = (int)((kMaxDynSmem - wb) / row);
-    // ~2 CTAs per SM; the fp64 register windows of k_lmax_win (86 registers x
-    // 512 threads) fit one CTA per SM, so their bands are sized for one wave
+    // ~2 CTAs per SM, or fewer when the kernel's registers / shared memory
+    // allow fewer (fp64 register windows of k_lmax_win: one CTA per SM at 512
+    // threads): the bands are sized for one wave of resident CTAs
     const bool win = live_most && !cand && B <= 4096;
-    const int cps = (win && sizeof(T) == 8 && B >= 2048) ? 1 : 2;
-    const int band = (B + cps * kNumSMs - 1) / (cps * kNumSMs);
     const int thr = 512;
-    const int grid = (B + band - 1) / band;
     const size_t sm = nslot * row + wb;
+    const int tw_win = std::min(512, B / 4);
+    const int resident = win ? ((B / 128 > 16) ? ctas_per_sm(k_lmax_win<T, 2>, tw_win, sm)
+                                               : ctas_per_sm(k_lmax_win<T, 1>, tw_win, sm))
+                             : ctas_per_sm(k_lmax_stream<T>, thr, sm);
+    const int cps = std::max(1, std::min(2, resident));
+    const int band = (B + cps * kNumSMs - 1) / (cps * kNumSMs);
+    const int grid = (B + band - 1) / band;
     const Publish pub = make_publish(c, (unsigned)grid);
     pre(c, st);
     if (win) {
       // most bins pass the floor: register neighbourhood windows, one warp per
       // 128-column group (fewer threads for narrow grids)
-      const int tw = std::min(512, B / 4);
+      const int tw = tw_win;
       if (B / 128 > 16)
         kl(k_lmax_win<T, 2>, grid, tw, sm, st, mags, lgB, perm ? s1 : 1u, perm ? s2 : 1u,
            perm ? s2inv : 1u, band, nslot, peak, floor_rel, list, count, pub);
@@ -1138,8 +1209,10 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
         // always follows when max_iters >= 2: fold both from one read
         const long zs = std::min<long>(n / bb, 2L * kNumSMs / bb);
         static const bool spec0_on = getenv("SFFT2D_NO_SPEC0") == nullptr;
+        // (an explicit permutation list must hold pass 1's permutation: the
+        // reference may never draw it, and the library must not overrun)
         if (spec_on && spec0_on && pi == 0 && max_iters >= 2 && (size_t)n * sizeof(Tin) >= kRingSegBytes &&
-            bb < 512 && zs > 1) {
+            bb < 512 && zs > 1 && (ps.bitgen || ps.n_arr > 1)) {
           const Perm* sq = &ps.get(1, st);
           spec_grid = (C*)ws(c, "spec_small", (size_t)zs * BB * sizeof(C));
           spec_pi = 1;
@@ -1175,7 +1248,8 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       // ring pair (128 <= B <= 256, full-support rows) or wide pair (B >= 512)
       const bool ring_pair = bb >= 128 && 2 * bb <= 512 && (size_t)n * sizeof(Tin) >= kRingSegBytes;
       const bool wide_pair = bb >= 512 && lgN - lgb <= 5 && lgN - lgb >= 2;
-      if (!pre_y && spec_on && do_estimate && 2 * bb < n && (ring_pair || wide_pair)) {
+      if (!pre_y && spec_on && do_estimate && 2 * bb < n && (ring_pair || wide_pair) &&
+          (ps.bitgen || pi + 1 < ps.n_arr)) {
         sq = &ps.get(pi + 1, st);
         const int zmax = ring_pair ? std::max(1, (int)(2L * kNumSMs / bb)) : 1;
         sy = spec_grid = (C*)ws(c, "spec_y", (size_t)zmax * 4 * BB * sizeof(C));
@@ -1600,11 +1674,16 @@ int sfft2d_ctx_create(int device, sfft2d_ctx** out) {
     ck(cudaStreamCreateWithFlags(&c->vote_st, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaEventCreateWithFlags(&c->ev_lmax, cudaEventDisableTiming), "cudaEventCreate");
     ck(cudaEventCreateWithFlags(&c->ev_ws, cudaEventDisableTiming), "cudaEventCreate");
-    // keep freed workspace in the device pool (no release at sync points)
-    cudaMemPool_t pool;
-    ck(cudaDeviceGetDefaultMemPool(&pool, device), "cudaDeviceGetDefaultMemPool");
+    // the context's own memory pool, keeping freed workspace (no release at
+    // sync points); the device's default pool is left untouched
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    ck(cudaMemPoolCreate(&c->pool, &props), "cudaMemPoolCreate");
     uint64_t keep = UINT64_MAX;
-    ck(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep), "cudaMemPoolSetAttribute");
+    ck(cudaMemPoolSetAttribute(c->pool, cudaMemPoolAttrReleaseThreshold, &keep), "cudaMemPoolSetAttribute");
     for (int i = 0; i < 2; ++i)
       ck(cudaEventCreateWithFlags(&c->ev_vote[i], cudaEventDisableTiming), "cudaEventCreate");
   });
@@ -1621,8 +1700,11 @@ void sfft2d_ctx_destroy(sfft2d_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  for (auto& kv : c->bufs)
-    if (kv.second.first) cudaFree(kv.second.first);
+  if (!c->arena)
+    for (auto& kv : c->bufs)
+      if (kv.second.first) cudaFreeAsync(kv.second.first, 0);
+  cudaDeviceSynchronize();
+  if (c->pool) cudaMemPoolDestroy(c->pool);
   for (auto& t : c->tables)
     for (int p = 0; p < 2; ++p) {
       cudaFree(t.space[p]);
@@ -2100,6 +2182,34 @@ int sfft2d_top_bins(sfft2d_ctx* c, const void* grids, int b, int nseg, int64_t n
       compact(c, sb, sc, BB, nseg, out_flat, (long)num, tots, st);
     });
   });
+}
+
+int sfft2d_ctx_set_workspace(sfft2d_ctx* c, void* base, int64_t bytes) {
+  return guarded(c, [&] {
+    if (bytes < 0 || (bytes > 0 && !base)) fail(SFFT2D_ERR_VALUE, "bad workspace");
+    ck(cudaDeviceSynchronize(), "sync");   // nothing may still use the old buffers
+    for (auto& kv : c->bufs)
+      if (kv.second.first && !c->arena) ck(cudaFreeAsync(kv.second.first, 0), "cudaFreeAsync");
+    ck(cudaDeviceSynchronize(), "sync");
+    c->bufs.clear();
+    c->arena_free.clear();
+    c->ws_in_use = 0;
+    c->ws_peak = 0;
+    c->arena = (char*)base;
+    c->arena_bytes = base ? (size_t)bytes : 0;
+    if (c->arena) {
+      // 256-byte aligned start (every named buffer is a multiple of 4 KiB)
+      const size_t skew = (256 - ((uintptr_t)c->arena & 255)) & 255;
+      if (c->arena_bytes > skew) c->arena_free.emplace(skew, c->arena_bytes - skew);
+    }
+  });
+}
+
+int sfft2d_ctx_workspace_size(const sfft2d_ctx* c, int64_t* in_use, int64_t* peak) {
+  if (!c) return SFFT2D_ERR_STATE;
+  if (in_use) *in_use = (int64_t)c->ws_in_use;
+  if (peak) *peak = (int64_t)c->ws_peak;
+  return SFFT2D_OK;
 }
 
 int sfft2d_generate(sfft2d_ctx* c, int n, int64_t k, const int64_t* rows, const int64_t* cols,

@@ -53,6 +53,16 @@ inline void allow_smem(K kernel) {
   allow_smem_ptr((const void*)kernel);
 }
 
+// resident CTAs per SM of `kernel` at (threads, dynamic smem), queried once
+// per device/kernel/shape from the occupancy calculator (so grid sizing
+// follows the compiled register count instead of a hard-coded assumption)
+int ctas_per_sm_ptr(const void* kernel, int threads, size_t smem);
+template <typename K>
+inline int ctas_per_sm(K kernel, int threads, size_t smem) {
+  if (smem > 0) allow_smem(kernel);
+  return ctas_per_sm_ptr((const void*)kernel, threads, smem);
+}
+
 // Launch with programmatic stream serialisation (PDL): the kernel may be
 // scheduled while its predecessor in the stream drains; it waits in pdl_wait()
 // before touching memory.  Launch errors throw.  Kernels launched with dynamic

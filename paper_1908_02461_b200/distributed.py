@@ -37,12 +37,74 @@ from .engine import ConfigurationError, SfftConfig, _fetch, _stream, to_dict
 from .hashing import draw_permutation
 
 __all__ = ["loop_shard", "batch_shard", "merge_votes", "sfft2d_loopsplit", "atsfft2d_sharded",
-           "vote_bytes", "merge_estimates", "atsfft2d_loopsplit"]
+           "vote_bytes", "merge_estimates", "atsfft2d_loopsplit", "gather_shards", "agree"]
 
 
 def _dist():
     import torch.distributed as dist
     return dist
+
+
+def _group_info(group):
+    dist = _dist()
+    if dist.is_available() and dist.is_initialized():
+        return dist.get_rank(group), dist.get_world_size(group)
+    return 0, 1
+
+
+def _all_reduce(t, op, group=None):
+    """all_reduce that also works for device tensors on a gloo group (staged
+    through host memory; NCCL reduces in place on the device)."""
+    dist = _dist()
+    if t.is_cuda and dist.get_backend(group) == "gloo":
+        h = t.cpu()
+        dist.all_reduce(h, op=op, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=op, group=group)
+    return t
+
+
+# error classes carried by agree(): a rank-local failure before or between
+# collectives must not leave the other ranks blocked in the next all_reduce
+_ERR_NONE, _ERR_VALUE, _ERR_CONFIG, _ERR_OTHER = 0, 1, 2, 3
+
+
+def agree(fn, group=None):
+    """Run the rank-local step fn() and agree on its outcome: if any rank
+    raised, EVERY rank raises (the same exception class where possible) after
+    one small all-reduce, instead of the healthy ranks waiting forever in the
+    next collective.  Returns fn()'s value."""
+    rank, world = _group_info(group)
+    err, out = None, None
+    try:
+        out = fn()
+    except Exception as e:  # noqa: BLE001 - re-raised below on every rank
+        err = e
+    if world == 1:
+        if err is not None:
+            raise err
+        return out
+    torch = _native._torch()
+    code = _ERR_NONE if err is None else (
+        _ERR_CONFIG if isinstance(err, ConfigurationError) else
+        _ERR_VALUE if isinstance(err, ValueError) else _ERR_OTHER)
+    dist = _dist()
+    on_dev = dist.get_backend(group) == "nccl"
+    flag = torch.tensor([code], dtype=torch.int32,
+                        device=torch.device("cuda", torch.cuda.current_device()) if on_dev else "cpu")
+    dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+    worst = int(flag.item())
+    if worst == _ERR_NONE:
+        return out
+    if err is not None:
+        raise err
+    msg = f"another rank failed during the split transform (error class {worst})"
+    if worst == _ERR_CONFIG:
+        raise ConfigurationError(msg)
+    if worst == _ERR_VALUE:
+        raise ValueError(msg)
+    raise RuntimeError(msg)
 
 
 def loop_shard(loops: int, rank: int, world: int) -> list:
@@ -66,7 +128,7 @@ def merge_votes(counts, group=None):
     Loops per coordinate <= L <= 255, so uint8 cannot overflow."""
     dist = _dist()
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
-        dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
+        _all_reduce(counts, dist.ReduceOp.SUM, group)
     return counts
 
 
@@ -75,11 +137,7 @@ def sfft2d_loopsplit(x, cfg: SfftConfig, rng, *, group=None, precision: str = "f
     """`sfft2d` with the location loops split across the ranks of `group`
     (every rank passes the same x, cfg and rng and gets the same result)."""
     torch = _native._torch()
-    dist = _dist()
-    if dist.is_available() and dist.is_initialized():
-        rank, world = dist.get_rank(group), dist.get_world_size(group)
-    else:
-        rank, world = 0, 1
+    rank, world = _group_info(group)
     img = as_device_image(x, device)
     if img.n != cfg.n:
         raise ConfigurationError(f"config built for n={cfg.n}, signal has n={img.n}")
@@ -96,11 +154,19 @@ def sfft2d_loopsplit(x, cfg: SfftConfig, rng, *, group=None, precision: str = "f
     counts = torch.zeros(vote_bytes(cfg.n), dtype=torch.uint8, device=img.tensor.device)
     with torch.cuda.device(img.device):
         st = _stream(torch, img.device)
-        if mine:
-            ctx.check(ctx.lib.sfft2d_sfft_votes(
-                ctx.handle, img.tensor.data_ptr(), img.dtype_code, 0, ctypes.byref(ccfg),
-                _native.perm_array([perms[l] for l in mine]), len(mine), prec, st,
-                counts.data_ptr()))
+
+        def location():
+            if mine:   # the native location phase checks for NaN/Inf first
+                ctx.check(ctx.lib.sfft2d_sfft_votes(
+                    ctx.handle, img.tensor.data_ptr(), img.dtype_code, 0, ctypes.byref(ccfg),
+                    _native.perm_array([perms[l] for l in mine]), len(mine), prec, st,
+                    counts.data_ptr()))
+            elif not bool(torch.isfinite(torch.view_as_real(img.tensor)).all()):
+                # a rank without location loops still validates its input
+                # (as_complex_matrix, corefft.py:49-50) so every rank agrees
+                raise ValueError("matrix contains NaN or Inf")
+
+        agree(location, group)
         merge_votes(counts, group)
         # estimation loops split too: candidates = coordinates voted by at
         # least vote_threshold loops (ascending, engine.py:148-160); rank r
@@ -114,7 +180,10 @@ def sfft2d_loopsplit(x, cfg: SfftConfig, rng, *, group=None, precision: str = "f
         cdt = torch.complex128 if prec == _native.FP64 else torch.complex64
         vals = torch.zeros((cfg.loops, m), dtype=cdt, device=counts.device)
         usable = torch.zeros((cfg.loops, m), dtype=torch.uint8, device=counts.device)
-        if mine:
+
+        def estimation():
+            if not mine:
+                return
             lv = torch.empty((len(mine), m), dtype=cdt, device=counts.device)
             lu = torch.empty((len(mine), m), dtype=torch.uint8, device=counts.device)
             ctx.check(ctx.lib.sfft2d_estimate_loops(
@@ -125,6 +194,8 @@ def sfft2d_loopsplit(x, cfg: SfftConfig, rng, *, group=None, precision: str = "f
             idx = torch.as_tensor(mine, device=counts.device)
             vals.index_copy_(0, idx, lv)
             usable.index_copy_(0, idx, lu)
+
+        agree(estimation, group)
         merge_estimates(vals, usable, group)
         res = _native.ResultC()
         ctx.check(ctx.lib.sfft2d_median_select(
@@ -137,19 +208,28 @@ def atsfft2d_sharded(xs, cfg, est_loops: int, rngs, *, group=None, concurrency: 
                      precision: str = "fp64", device=None):
     """Batch of independent ATSFFTs sharded over ranks (c4); returns the full
     list of (spectrum, TunerState) in input order on every rank."""
-    dist = _dist()
-    if dist.is_available() and dist.is_initialized():
-        rank, world = dist.get_rank(group), dist.get_world_size(group)
-    else:
-        rank, world = 0, 1
+    rank, world = _group_info(group)
+    if len(xs) != len(rngs):
+        raise ValueError("need one rng per image")
     idx = batch_shard(len(xs), rank, world)
-    local = atsfft2d_batch([xs[i] for i in idx], cfg, est_loops, [rngs[i] for i in idx],
-                           concurrency=concurrency, precision=precision, device=device)
+    local = agree(lambda: atsfft2d_batch([xs[i] for i in idx], cfg, est_loops,
+                                         [rngs[i] for i in idx], concurrency=concurrency,
+                                         precision=precision, device=device), group)
+    return gather_shards(idx, local, len(xs), group)
+
+
+def gather_shards(idx, local, n_items: int, group=None) -> list:
+    """Every rank's (item index, result) pairs gathered into the full list in
+    input order, on every rank (results are small Python objects)."""
+    rank, world = _group_info(group)
     if world == 1:
-        return local
+        out = [None] * n_items
+        for i, r in zip(idx, local):
+            out[i] = r
+        return out
     gathered = [None] * world
-    dist.all_gather_object(gathered, list(zip(idx, local)), group=group)
-    out = [None] * len(xs)
+    _dist().all_gather_object(gathered, list(zip(idx, local)), group=group)
+    out = [None] * n_items
     for part in gathered:
         for i, r in part:
             out[i] = r
@@ -164,8 +244,8 @@ def merge_estimates(vals, usable, group=None):
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         torch = _native._torch()
         re = torch.view_as_real(vals) if vals.is_complex() else vals
-        dist.all_reduce(re, op=dist.ReduceOp.SUM, group=group)
-        dist.all_reduce(usable, op=dist.ReduceOp.SUM, group=group)
+        _all_reduce(re, dist.ReduceOp.SUM, group)
+        _all_reduce(usable, dist.ReduceOp.SUM, group)
     return vals, usable
 
 
@@ -177,19 +257,15 @@ def atsfft2d_loopsplit(x, cfg, est_loops: int, rng, *, group=None, precision: st
     Generator passed as `rng` advances exactly as under the reference."""
     from .tuner import _run_ats
     torch = _native._torch()
-    dist = _dist()
-    if dist.is_available() and dist.is_initialized():
-        rank, world = dist.get_rank(group), dist.get_world_size(group)
-    else:
-        rank, world = 0, 1
+    rank, world = _group_info(group)
     gen = rng if isinstance(rng, np.random.Generator) else np.random.default_rng(rng)
     img = as_device_image(x, device)
     n = img.n
     # detection with the votes left on the device (the reference's
     # detect_sparsity, tuner.py:142-241); candidates = tally >= threshold,
     # ascending keys i*n + j (engine.py:148-160 order)
-    state, (vkeys, vtal) = _run_ats(img.tensor, cfg, 0, gen, precision, img.device, False,
-                                    on_device=True)
+    state, (vkeys, vtal) = agree(lambda: _run_ats(img.tensor, cfg, 0, gen, precision, img.device,
+                                                  False, on_device=True), group)
     if state.detected_k == 0 or vkeys.numel() == 0:
         return {}, state
     thr = (max(state.vote_passes, 1) + 1) // 2
@@ -217,7 +293,10 @@ def atsfft2d_loopsplit(x, cfg, est_loops: int, rng, *, group=None, precision: st
     ctx.ensure_tables(n, cfg.window_delta_pass, cfg.window_delta_stop)
     with torch.cuda.device(img.device):
         st = _stream(torch, img.device)
-        if mine:
+
+        def estimation():
+            if not mine:
+                return
             lv = torch.empty((len(mine), m), dtype=cdt, device=dev)
             lu = torch.empty((len(mine), m), dtype=torch.uint8, device=dev)
             ctx.check(ctx.lib.sfft2d_estimate_loops(
@@ -228,6 +307,11 @@ def atsfft2d_loopsplit(x, cfg, est_loops: int, rng, *, group=None, precision: st
             idx = torch.as_tensor(mine, device=dev)
             vals.index_copy_(0, idx, lv)
             usable.index_copy_(0, idx, lu)
+
+        if L > 1:
+            agree(estimation, group)
+        else:
+            estimation()
         if L > 1:
             merge_estimates(vals, usable, group)
         res = _native.ResultC()

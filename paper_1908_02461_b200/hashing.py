@@ -219,6 +219,22 @@ def host_tables(n: int, delta_pass: float, delta_stop: float):
     return np.ascontiguousarray(space), np.ascontiguousarray(freq), tw
 
 
+def check_window(window: FlatWindow) -> None:
+    """The device applies the registered window tables of (n, delta_pass,
+    delta_stop), i.e. exactly build_flat_window's weights (all_pass_window's
+    at B = n).  A FlatWindow with any other weights would silently get a
+    different window than the reference applies (hashing.py:330), so it is
+    rejected."""
+    want = (all_pass_window(window.n) if window.b_bins == window.n else
+            _HOST_WINDOWS.get(window.n, window.b_bins, window.delta_stop, window.delta_pass))
+    if window is want:
+        return
+    if not (np.array_equal(np.asarray(window.space_1d), want.space_1d) and
+            np.array_equal(np.asarray(window.freq_1d), want.freq_1d)):
+        raise ValueError("window weights differ from build_flat_window(n, b, delta_stop, "
+                         "delta_pass=...): only the library's flat windows are supported")
+
+
 @dataclass(frozen=True)
 class BinGrid:
     """DFT of the permuted, filtered, folded signal (hashing.py:300-305)."""
@@ -239,6 +255,7 @@ def binned_spectrum(x, p: PermutationParams | list, window: FlatWindow, b: int, 
     n = img.n
     if window.n != n or b != window.b_bins:
         raise ValueError("window does not match the requested (n, b)")
+    check_window(window)
     perms = p if isinstance(p, (list, tuple)) else [p]
     prec = _native.precision_code(precision)
     ctx = _native.context(img.device)

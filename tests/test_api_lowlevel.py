@@ -92,3 +92,33 @@ def test_composed_pipeline_recovers_planted_support():
     assert set(top) == set(sig.truth)
     for key in top:
         assert abs(med[key] - sig.truth[key]) < 1e-6
+
+
+@pytest.mark.gpu
+def test_caller_owned_workspace():
+    # the caller (torch) owns the device workspace; the
+    # library sub-allocates it, reports the size a workload needs, and fails
+    # with a status (no allocation of its own) when it is too small
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1908_02461_b200 import _native
+    img = P.sparse_image(1024, 30, 3, snr_db=25.0)
+    x = torch.from_numpy(img.x).cuda()
+    ctx = _native.context()
+    ref, rs = P.atsfft2d(x, P.TunerConfig(), 8, 5)
+    _, peak = ctx.workspace_size()
+    assert peak > 0
+    buf = torch.empty(2 * peak, dtype=torch.uint8, device="cuda")
+    try:
+        ctx.use_workspace(buf)
+        got, gs = P.atsfft2d(x, P.TunerConfig(), 8, 5)
+        assert got == ref and gs == rs
+        assert 0 < ctx.workspace_size()[1] <= buf.numel()
+        ctx.use_workspace(torch.empty(1 << 16, dtype=torch.uint8, device="cuda"))
+        with pytest.raises(_native.StatusError, match="workspace exhausted"):
+            P.atsfft2d(x, P.TunerConfig(), 8, 5)
+    finally:
+        ctx.use_workspace(None)
+    again, _ = P.atsfft2d(x, P.TunerConfig(), 8, 5)
+    assert again == ref

@@ -67,22 +67,24 @@ def test_loopsplit_vote_allreduce_matches_single_process():
 
 
 def _worker_batch(rank, world, port, out_path):
+    # the product's shard + gather (D.batch_shard, D.agree, D.gather_shards, the
+    # code atsfft2d_sharded runs around its per-rank GPU batch), with the oracle
+    # as the per-rank compute
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     n_items = 5
     idx = D.batch_shard(n_items, rank, world)
-    local = []
-    for i in idx:
-        img = sparse_image(64, 3, 10 + i, snr_db=25.0)
-        (cs, vs), st = O.atsfft(img.x, O.TunerParams(), 4, 20 + i)
-        local.append((i, (cs.tolist(), [complex(v) for v in vs], st["detected_k"])))
-    gathered = [None] * world
-    dist.all_gather_object(gathered, local)
+
+    def compute():
+        local = []
+        for i in idx:
+            img = sparse_image(64, 3, 10 + i, snr_db=25.0)
+            (cs, vs), st = O.atsfft(img.x, O.TunerParams(), 4, 20 + i)
+            local.append((cs.tolist(), [complex(v) for v in vs], st["detected_k"]))
+        return local
+
+    out = D.gather_shards(idx, D.agree(compute), n_items)
     if rank == 0:
-        out = [None] * n_items
-        for part in gathered:
-            for i, r in part:
-                out[i] = r
         torch.save(out, out_path)
     dist.barrier()
     dist.destroy_process_group()
@@ -97,6 +99,37 @@ def test_batch_shard_gather_matches_sequential():
         img = sparse_image(64, 3, 10 + i, snr_db=25.0)
         (cs, vs), st = O.atsfft(img.x, O.TunerParams(), 4, 20 + i)
         assert got[i] == (cs.tolist(), [complex(v) for v in vs], st["detected_k"])
+
+
+def _worker_agree(rank, world, port, out_path):
+    # a failure on ONE rank before a collective makes every rank raise (no
+    # rank left blocked in the next all_reduce); ValueError class preserved
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def step():
+        if rank == 1:
+            raise ValueError("matrix contains NaN or Inf")
+        return 7
+
+    try:
+        D.agree(step)
+        outcome = "returned"
+    except ValueError as e:
+        outcome = f"ValueError:{e}"
+    ok = D.agree(lambda: 3)
+    torch.save((outcome, ok), out_path + f".{rank}")
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_agree_raises_on_every_rank():
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "agree")
+        mp.spawn(_worker_agree, args=(2, _free_port(), out), nprocs=2, join=True)
+        r0, r1 = torch.load(out + ".0"), torch.load(out + ".1")
+    assert r0[0].startswith("ValueError:another rank failed") and r0[1] == 3
+    assert r1 == ("ValueError:matrix contains NaN or Inf", 3)
 
 
 def test_shards_partition():

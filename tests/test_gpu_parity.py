@@ -36,6 +36,26 @@ def _close_values(got: dict, ref: dict, tol: float):
         err = abs(got[key] - v) / max(abs(v), 1e-3 * vmax, 1e-300)
         worst = max(worst, err)
     assert worst <= tol, worst
+    _check_order(list(got), ref, tol)
+
+
+def _check_order(got_keys: list, ref: dict, tol: float):
+    """The dict's iteration order is the reference's: row-major (i, j), or
+    lexsort(-|v|, i, j) after a top-k cut (engine.py:245-253).  Row-major
+    order must match exactly; in the magnitude order two entries may only
+    trade places when their reference magnitudes are equal within the value
+    tolerance (a near-tie of the sort key: unit-magnitude noiseless spectra
+    differ only in the last ulps of |v|, which no two float64 codes share)."""
+    ref_keys = list(ref)
+    if got_keys == ref_keys:
+        return
+    assert ref_keys != sorted(ref_keys), "row-major order differs from the reference"
+    pos = {key: i for i, key in enumerate(ref_keys)}
+    mags = [abs(ref[key]) for key in got_keys]
+    for i, key in enumerate(got_keys):
+        j = pos[key]
+        if i != j:   # displaced: its magnitude ties (within tol) the one it displaced
+            assert abs(mags[i] - abs(ref[ref_keys[i]])) <= 2 * tol * max(mags[i], 1e-300), key
 
 
 def _ref_dict(g):
@@ -197,7 +217,47 @@ def _tuner(g):
 NOISELESS = {"ats_n256_k8", "ats_n64_k1_b8", "ats_dc", "ats_noconv", "c3_ats_clean"}
 
 
-def _check_state(state, g, name="", precision="fp64"):
+def _near_tie_pass(x, g, t, rel=1e-12):
+    """Whether tuner pass t of the reference trajectory (its B, its t-th
+    permutation draw) holds a magnitude near-tie that decides a count: a bin
+    at or above the floor within `rel` of its largest 8-neighbour, or a bin
+    within `rel` of the floor itself."""
+    O.FAST = True
+    try:
+        a = O.as_c128(x)
+        n = a.shape[0]
+        tc = _tuner(g)
+        gen = np.random.default_rng(int(g["seed"]))
+        perms = [O.draw_perm(n, gen) for _ in range(t + 1)]
+        b = int(g["hist"][t, 0])
+        win = O.cached_window(n, b, tc.window_delta_stop, tc.window_delta_pass)
+        m = np.abs(O.bucket_spectrum(a, perms[t], win, b))
+    finally:
+        O.FAST = False
+    top = m.max()
+    if top == 0:
+        return False
+    nb = np.max([np.roll(m, (du, dv), axis=(0, 1)) for du in (-1, 0, 1) for dv in (-1, 0, 1)
+                 if du or dv], axis=0)
+    live = m >= tc.mag_floor * top * (1 - rel)
+    tie_nb = np.any(live & (np.abs(m - nb) <= rel * m))
+    tie_floor = np.any(np.abs(m - tc.mag_floor * top) <= rel * top)
+    return bool(tie_nb or tie_floor)
+
+
+def _check_state(state, g, name="", precision="fp64", x=None):
+    if name in NOISELESS and precision == "fp64":
+        # exact trajectory unless the first differing pass holds a near-tie
+        # that the last ulp decides (proven per case from the oracle's grids)
+        got = [(b, c) for b, c, _ in state.history]
+        ref = [(int(b), int(c)) for b, c in g["hist"][:, :2]]
+        if got == ref:
+            return
+        t = next(i for i, (u, v) in enumerate(zip(got, ref)) if u != v) if any(
+            u != v for u, v in zip(got, ref)) else min(len(got), len(ref)) - 1
+        assert got[t][0] == ref[t][0], (t, got[t], ref[t])   # same B: only a count flips
+        assert x is not None and _near_tie_pass(x, g, t), (name, t, got[t], ref[t])
+        return
     if name in NOISELESS:
         return
     if precision == "fp32":
@@ -224,7 +284,7 @@ def test_atsfft_fp64_vs_reference(name):
     g = golden(name)
     x = fixture_input(g)
     out, state = P.atsfft2d(x, _tuner(g), int(g["est_loops"]), int(g["seed"]), precision="fp64")
-    _check_state(state, g, name)
+    _check_state(state, g, name, x=x)
     _close_values(out, _ref_dict(g), TOL["fp64"])
 
 
@@ -363,4 +423,41 @@ def test_c5_atsfft_vs_reference(precision):
     x = fixture_input(g)
     out, state = P.atsfft2d(x, _tuner(g), int(g["est_loops"]), int(g["seed"]), precision=precision)
     _check_state(state, g, "c5_ats_k64", precision)
+    _close_values(out, _ref_dict(g), TOL[precision])
+
+
+# ------------------------------------------------------------- c4 batch images
+C4B = [f"c4b_{i:02d}" for i in range(12)]
+
+
+@pytest.mark.parametrize("name", C4B)
+def test_c4_bench_images_fp64_vs_reference(name):
+    # the first 12 images of the bench's c4 batch (k ~ U[20, 200], log-uniform
+    # magnitudes, 25 dB): full state + votes-derived support exact
+    g = golden(name)
+    x = fixture_input(g)
+    out, state = P.atsfft2d(x, _tuner(g), int(g["est_loops"]), int(g["seed"]), precision="fp64")
+    _check_state(state, g, name)
+    _close_values(out, _ref_dict(g), TOL["fp64"])
+
+
+def test_c4_bench_images_fp32_batch_vs_reference():
+    # the same images through the batch API in fp32 (what the bench times)
+    gs = [golden(nm) for nm in C4B]
+    xs = [fixture_input(g) for g in gs]
+    res = P.atsfft2d_batch(xs, P.TunerConfig(), 8, [int(g["seed"]) for g in gs], concurrency=4,
+                           precision="fp32")
+    for (out, state), g, nm in zip(res, gs, C4B):
+        _check_state(state, g, nm, "fp32")
+        _close_values(out, _ref_dict(g), TOL["fp32"])
+
+
+# ------------------------------------------------------------- c5 sparsity sweep
+@pytest.mark.parametrize("k", [256, 1024, 4096])
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_c5_sweep_vs_reference(k, precision):
+    g = golden(f"c5_ats_k{k}")
+    x = fixture_input(g)
+    out, state = P.atsfft2d(x, _tuner(g), int(g["est_loops"]), int(g["seed"]), precision=precision)
+    _check_state(state, g, f"c5_ats_k{k}", precision)
     _close_values(out, _ref_dict(g), TOL[precision])

@@ -225,3 +225,22 @@ def test_numeric_inputs_accepted_like_reference(dtype):
     ref = O.as_c128(x)
     assert a.shape == (4, 4) and np.array_equal(a.astype(np.complex128), ref)
     assert code == (_native.C64 if dtype == np.complex64 else _native.C128)
+
+
+def test_check_window_rejects_foreign_weights():
+    import dataclasses
+    from paper_1908_02461_b200 import hashing as H
+    w = H.build_flat_window(256, 16, 1e-8, delta_pass=1e-3)
+    H.check_window(w)
+    H.check_window(H.all_pass_window(256))
+    with pytest.raises(ValueError, match="window weights differ"):
+        H.check_window(dataclasses.replace(w, space_1d=w.space_1d * (1 + 1e-9)))
+    with pytest.raises(ValueError, match="window weights differ"):
+        H.check_window(dataclasses.replace(w, freq_1d=np.roll(w.freq_1d, 1)))
+
+
+def test_batch_detects_shared_generators():
+    from paper_1908_02461_b200.batch import _shared_generators
+    g = np.random.default_rng(1)
+    assert _shared_generators([g, np.random.default_rng(1), g])
+    assert not _shared_generators([g, np.random.default_rng(1), 3, 3])
