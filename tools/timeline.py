@@ -1,6 +1,6 @@
-"""GPU timeline of c3 ATSFFT transforms from a CUPTI kernel trace
+"""GPU timeline of one workload's transforms from a CUPTI kernel trace
 (torch.profiler): busy vs idle time per transform and the largest gaps.
-python tools/timeline.py [fp32|fp64] [reps]"""
+python tools/timeline.py [fp32|fp64] [reps] [c3|c1|c2|c3sfft|c5]"""
 import json
 import os
 import sys
@@ -14,14 +14,41 @@ import paper_1908_02461_b200 as P  # noqa: E402
 
 prec = sys.argv[1] if len(sys.argv) > 1 else "fp32"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
-img = P.sparse_image(4096, 100, 7, snr_db=20.0)
-x = torch.from_numpy(img.x).cuda()
+work = sys.argv[3] if len(sys.argv) > 3 else "c3"
+if work == "c1":
+    sig = P.planted_image(256, 10, 1)
+    x = torch.from_numpy(sig.x).cuda()
+    def call():
+        return P.sfft2d_arrays(x, P.SfftConfig(n=256, k=10), 2, precision=prec)
+elif work == "c3sfft":
+    x = torch.from_numpy(P.sparse_image(4096, 100, 7, snr_db=20.0).x).cuda()
+    def call():
+        return P.sfft2d_arrays(x, P.SfftConfig(n=4096, k=100), 12, precision=prec)
+elif work == "c2":
+    x = torch.from_numpy(P.sparse_image(1024, 50, 7, snr_db=30.0).x).cuda()
+    def call():
+        return P.atsfft2d_arrays(x, P.TunerConfig(), 8, 11, precision=prec)
+elif work.startswith("c5"):
+    k5 = int(work[3:] or 64) if len(work) > 2 else 64
+    x = P.device_sparse_image(16384, k5, 5, snr_db=15.0, cluster_frac=0.2, cluster_side=64).x
+    def call():
+        return P.atsfft2d_arrays(x, P.TunerConfig(), 8, 6, precision=prec)
+else:
+    x = torch.from_numpy(P.sparse_image(4096, 100, 7, snr_db=20.0).x).cuda()
+    def call():
+        return P.atsfft2d_arrays(x, P.TunerConfig(), 8, 11, precision=prec)
 for _ in range(3):
-    P.atsfft2d_arrays(x, P.TunerConfig(), 8, 11, precision=prec)
+    call()
 torch.cuda.synchronize()
+import time  # noqa: E402
+t0w = time.perf_counter()
+for _ in range(reps):
+    call()
+torch.cuda.synchronize()
+print(f"{work} {prec}: host wall {(time.perf_counter() - t0w) / reps * 1e3:.3f} ms per transform (no profiler)")
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(reps):
-        P.atsfft2d_arrays(x, P.TunerConfig(), 8, 11, precision=prec)
+        call()
     torch.cuda.synchronize()
 path = os.path.join(tempfile.mkdtemp(), "t.json")
 prof.export_chrome_trace(path)
