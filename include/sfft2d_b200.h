@@ -139,6 +139,22 @@ int sfft2d_sfft(sfft2d_ctx* ctx, const void* x, int x_dtype, int x_on_host,
                 const sfft2d_sfft_config* cfg, const sfft2d_perm* perms, int precision,
                 void* stream, sfft2d_result* res);
 
+/* Algorithm 1's stream derivation (engine.py:266-280) done natively: from the
+ * caller's numpy Generator (`Generator.bit_generator.ctypes.bit_generator`,
+ * a bitgen_t*), 2*loops child seeds rng.integers(2**63), each child
+ * np.random.default_rng(seed) (numpy's SeedSequence + PCG64, restated in
+ * csrc/npyrng.h) and one draw_permutation per child (hashing.py:72-80):
+ * out[0..loops) location loops, out[loops..2 loops) estimation loops.
+ * Host only (no device work); the caller's Generator advances exactly as
+ * under the reference.                                                     */
+int sfft2d_sfft_draw_perms(void* numpy_bitgen, int n, int loops, sfft2d_perm* out);
+
+/* sfft2d with the permutations derived natively from the caller's Generator
+ * (sfft2d_sfft_draw_perms then sfft2d_sfft).                               */
+int sfft2d_sfft_bitgen(sfft2d_ctx* ctx, const void* x, int x_dtype, int x_on_host,
+                       const sfft2d_sfft_config* cfg, void* numpy_bitgen, int precision,
+                       void* stream, sfft2d_result* res);
+
 /* Loop split across devices: the location phase of
  * sfft2d for a SUBSET of the location loops (engine.py:130-145, per-loop
  * dedup).  counts: device uint8[n*n rounded up to a multiple of 32], set to the

@@ -32,7 +32,8 @@ EXPORTS = (
     "sfft2d_ctx_profile_report", "sfft2d_atsfft_bitgen", "sfft2d_detect_sparsity_bitgen",
     "sfft2d_ctx_sync_us", "sfft2d_sfft_votes", "sfft2d_sfft_from_votes",
     "sfft2d_estimate_loops", "sfft2d_median_select", "sfft2d_generate",
-    "sfft2d_ctx_set_workspace", "sfft2d_ctx_workspace_size",
+    "sfft2d_ctx_set_workspace", "sfft2d_ctx_workspace_size", "sfft2d_sfft_draw_perms",
+    "sfft2d_sfft_bitgen",
 )
 
 
@@ -127,6 +128,8 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
             "sfft2d_median_select": ([vp, i32, vp, i64, vp, vp, i32, i64, dbl, i32, vp,
                                       P(ResultC)], i32),
             "sfft2d_ctx_set_workspace": ([vp, vp, i64], i32),
+            "sfft2d_sfft_draw_perms": ([vp, i32, i32, P(Perm)], i32),
+            "sfft2d_sfft_bitgen": ([vp, vp, i32, i32, P(SfftCfg), vp, i32, vp, P(ResultC)], i32),
             "sfft2d_ctx_workspace_size": ([vp, P(i64), P(i64)], i32),
             "sfft2d_generate": ([vp, i32, i64, vp, vp, vp, dbl, ctypes.c_uint64, i32, vp, vp],
                                 i32),

@@ -30,6 +30,7 @@
 #include "fold.cuh"
 #include "generate.cuh"
 #include "host.cuh"
+#include "npyrng.h"
 #include "select.cuh"
 #include "vote.cuh"
 
@@ -73,7 +74,9 @@ struct sfft2d_ctx {
   std::map<size_t, size_t> arena_free;   // offset -> size of free blocks
   size_t ws_in_use = 0, ws_peak = 0;
   unsigned* pinned = nullptr;  // small host scratch for counts
-  Perm* perm_pinned = nullptr; // staging for permutations drawn on demand
+  Perm* perm_pinned = nullptr; // pinned ring staging permutation uploads
+  int perm_pos = 0;             // next free ring entry
+  cudaEvent_t ev_perm = nullptr;   // after the latest upload from the ring
   // last results
   long long res_count = 0;
   int res_prec = SFFT2D_FP64;
@@ -94,6 +97,7 @@ struct sfft2d_ctx {
   unsigned seq = 0;
   cudaStream_t vote_st = nullptr;
   cudaEvent_t ev_lmax = nullptr;
+  cudaEvent_t ev_pass[4] = {nullptr, nullptr, nullptr, nullptr};   // per tuner pass: list complete
   cudaEvent_t ev_vote[2] = {nullptr, nullptr};
   // optional per-launch profiling (CUDA events on the launching stream)
   bool profiling = false;
@@ -273,7 +277,61 @@ const DevTables& find_twiddles(sfft2d_ctx* c, int n) {
   fail(SFFT2D_ERR_STATE, "no twiddle table registered for n=" + std::to_string(n));
 }
 
-constexpr int kPermPinned = 1024;
+constexpr int kPermPinned = 4096;
+
+// `count` pinned ring entries that are free to write now: uploads are
+// stream-ordered, so the ring wraps only after the latest upload completed
+// (one event wait every ~kPermPinned / count calls, instead of a stream
+// synchronisation per upload)
+Perm* perm_stage(sfft2d_ctx* c, int count) {
+  if (count > kPermPinned) fail(SFFT2D_ERR_UNSUPPORTED, "too many permutations");
+  if (c->perm_pos + count > kPermPinned) {
+    ck(cudaEventSynchronize(c->ev_perm), "cudaEventSynchronize");
+    c->perm_pos = 0;
+  }
+  Perm* p = c->perm_pinned + c->perm_pos;
+  c->perm_pos += count;
+  return p;
+}
+
+// draw_permutation (hashing.py:72-80) on a numpy bitgen_t: the reference's
+// four Generator.integers calls in order, with numpy's bounded routine
+Perm draw_perm_bitgen(void* bitgen, int n) {
+  uint64_t v[4] = {0, 0, 0, 0};
+  if (n > 1) {
+    random_bounded_uint64_fill(bitgen, 0, (uint64_t)(n / 2 - 1), 1, false, &v[0]);
+    random_bounded_uint64_fill(bitgen, 0, (uint64_t)(n / 2 - 1), 1, false, &v[1]);
+  }
+  random_bounded_uint64_fill(bitgen, 0, (uint64_t)(n - 1), 1, false, &v[2]);
+  random_bounded_uint64_fill(bitgen, 0, (uint64_t)(n - 1), 1, false, &v[3]);
+  const uint32_t mask = (uint32_t)n - 1u;
+  Perm q;
+  q.s1 = n > 1 ? (uint32_t)(2 * v[0] + 1) : 1u;
+  q.s2 = n > 1 ? (uint32_t)(2 * v[1] + 1) : 1u;
+  q.t1 = (uint32_t)v[2];
+  q.t2 = (uint32_t)v[3];
+  uint32_t a = q.s1, b = q.s2;   // inverses mod 2^k by Newton iteration
+  for (int i = 0; i < 5; ++i) { a *= 2u - q.s1 * a; b *= 2u - q.s2 * b; }
+  q.s1i = a & mask;
+  q.s2i = b & mask;
+  return q;
+}
+
+// Algorithm 1's stream derivation (engine.py:266-280): 2L child seeds
+// rng.integers(2**63) from the caller's stream, each child
+// np.random.default_rng(seed) (npyrng.h), one draw_permutation per child
+void sfft_child_perms(void* bitgen, int n, int loops, sfft2d_perm* out) {
+  std::vector<uint64_t> seeds(2 * loops);
+  for (auto& sd : seeds) random_bounded_uint64_fill(bitgen, 0, (1ULL << 63) - 1, 1, false, &sd);
+  for (int i = 0; i < 2 * loops; ++i) {
+    npyrng::Pcg64 st;
+    npyrng::default_rng(seeds[i], &st);
+    npyrng::bitgen_t bg;
+    npyrng::bind(&bg, &st);
+    const Perm q = draw_perm_bitgen(&bg, n);
+    out[i] = sfft2d_perm{q.s1, q.s2, q.t1, q.t2, q.s1i, q.s2i};
+  }
+}
 
 Perm to_perm(const sfft2d_perm& p, int n) {
   const long long m = n;
@@ -313,20 +371,7 @@ struct PermSource {
       Perm q;
       const int k = (int)hp.size();
       if (bitgen) {
-        uint64_t v[4] = {0, 0, 0, 0};
-        if (n > 1) {
-          random_bounded_uint64_fill(bitgen, 0, (uint64_t)(n / 2 - 1), 1, false, &v[0]);
-          random_bounded_uint64_fill(bitgen, 0, (uint64_t)(n / 2 - 1), 1, false, &v[1]);
-        }
-        random_bounded_uint64_fill(bitgen, 0, (uint64_t)(n - 1), 1, false, &v[2]);
-        random_bounded_uint64_fill(bitgen, 0, (uint64_t)(n - 1), 1, false, &v[3]);
-        const uint32_t mask = (uint32_t)n - 1u;
-        q.s1 = n > 1 ? (uint32_t)(2 * v[0] + 1) : 1u;
-        q.s2 = n > 1 ? (uint32_t)(2 * v[1] + 1) : 1u;
-        q.t1 = (uint32_t)v[2];
-        q.t2 = (uint32_t)v[3];
-        q.s1i = inv_pow2(q.s1, mask);
-        q.s2i = inv_pow2(q.s2, mask);
+        q = draw_perm_bitgen(bitgen, n);
       } else {
         if (k >= n_arr) fail(SFFT2D_ERR_VALUE, "permutation list exhausted");
         q = to_perm(arr[k], n);
@@ -337,10 +382,11 @@ struct PermSource {
     return hp[i];
   }
   // device copies are only needed by the estimation loops: one copy for them
-  void upload(int from, int count, cudaStream_t st) {
+  void upload(int from, int count, cudaStream_t st, cudaEvent_t done) {
     ck(cudaMemcpyAsync(dev + from, pinned + from, (size_t)count * sizeof(Perm),
                        cudaMemcpyHostToDevice, st),
        "H2D perms");
+    ck(cudaEventRecord(done, st), "cudaEventRecord");
   }
   int used() const { return (int)hp.size(); }
 };
@@ -352,6 +398,10 @@ unsigned read_u32(sfft2d_ctx* c, const unsigned* dev, cudaStream_t st) {
   c->t_sync_end = std::chrono::steady_clock::now();
   c->sync_us += std::chrono::duration<double, std::micro>(c->t_sync_end - t0).count();
   return c->pinned[0];
+}
+
+void raise_if_nonfinite(sfft2d_ctx* c) {   // after a synchronisation of the stream
+  if (c->pinned[1]) fail(SFFT2D_ERR_VALUE, "matrix contains NaN or Inf");
 }
 
 // Mapped pinned host buffer for results (grow-only).
@@ -374,21 +424,28 @@ void* host_out(sfft2d_ctx* c, size_t bytes) {
 }
 
 // Prepare a count publication for a launch of `grid` CTAs.
+// One 16-byte mapped slot per publication sequence number (a ring of
+// kPubSlots): a pass enqueued speculatively behind the one being waited for
+// publishes into its own slot instead of overwriting the word the host spins on.
+constexpr unsigned kPubSlots = 256;
+
+volatile unsigned* pub_slot_h(sfft2d_ctx* c, unsigned seq) { return c->mapped_h + 4 * (seq % kPubSlots); }
+
 Publish make_publish(sfft2d_ctx* c, unsigned grid) {
   Publish p;
   p.done = c->done_d;
   c->done_base += grid;
   p.target = c->done_base;
-  p.slot = c->mapped_d;
   p.seq = ++c->seq;
+  p.slot = c->mapped_d + 4 * (p.seq % kPubSlots);
   return p;
 }
 
 // Spin on the mapped slot until the launch published `seq`; returns the count.
 unsigned wait_published(sfft2d_ctx* c, unsigned seq, cudaStream_t st) {
   const auto t0 = std::chrono::steady_clock::now();
-  volatile unsigned* h = c->mapped_h;
-  volatile unsigned long long* h64 = reinterpret_cast<volatile unsigned long long*>(c->mapped_h);
+  volatile unsigned* h = pub_slot_h(c, seq);
+  volatile unsigned long long* h64 = reinterpret_cast<volatile unsigned long long*>(h);
   for (unsigned long spin = 0;; ++spin) {
     const unsigned long long word = *h64;   // (count << 32) | seq, one device store
     if ((unsigned)word == seq) {
@@ -628,8 +685,8 @@ void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTable
         fft2d_grids<T>(c, y, lgB, g, tw, lgN, sp, mg, pk, st);
       } else {
         pre(c, st);
-        kl(k_fold_reduce_fft_small<T>, g, 1024, BB * sizeof(C), st, dst, gm.Z, g, lgB, pp, tw, lgN,
-                                                                    y);
+        kl(k_fold_reduce_fft_small<T>, g, 1024, small_fft_smem<T>(lgB), st, dst, gm.Z, g, lgB, pp, tw,
+           lgN, y);
         post(c, "k_fold_reduce_fft_small", st, (double)(gm.Z + 1) * g * BB * sizeof(C));
         if (sp && sp != y)
           ck(cudaMemcpyAsync(sp, y, (size_t)g * BB * sizeof(C), cudaMemcpyDeviceToDevice, st), "copy");
@@ -1000,8 +1057,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   ps.n = n;
   ps.cap = max_iters + 2 + L;
   ps.hp.reserve(ps.cap);
-  ps.pinned = c->perm_pinned;
-  if (ps.cap > kPermPinned) fail(SFFT2D_ERR_UNSUPPORTED, "too many permutations");
+  ps.pinned = perm_stage(c, ps.cap);
   ps.dev = (Perm*)ws(c, "perms", (size_t)ps.cap * sizeof(Perm));
   Perm* dp = ps.dev;
   const long nkeys = (long)n * n;
@@ -1050,6 +1106,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   int vote_passes = 0;
   bool last_valid = false;
   int last_b = 0, last_pi = 0;
+  cudaEvent_t last_ready = nullptr;
   long long last_count = 0;
 
   // sides >= 2048: the dense FFT stops after four-step pass A (x_hat is never
@@ -1093,8 +1150,8 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   c->done_base = 0;
   // per-pass count slots (zeroed once), double-buffered maxima lists: the
   // vote of pass k runs on the side stream while pass k+1 proceeds
-  unsigned* cnt_slots = (unsigned*)ws(c, "lm_counts", (size_t)SFFT2D_MAX_HISTORY * 4);
-  ck(cudaMemsetAsync(cnt_slots, 0, (size_t)SFFT2D_MAX_HISTORY * 4, st), "memset");
+  unsigned* cnt_slots = (unsigned*)ws(c, "lm_counts", (size_t)2 * SFFT2D_MAX_HISTORY * 4);
+  ck(cudaMemsetAsync(cnt_slots, 0, (size_t)2 * SFFT2D_MAX_HISTORY * 4, st), "memset");
   int32_t* maxlists[2] = {maxlist, (int32_t*)ws(c, "maxlist2", (size_t)(nkeys / 4 + 64) * 4)};
   bool vote_pending[2] = {false, false};
   int npass = 0;
@@ -1103,7 +1160,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   // the budget cast nothing): in deferred mode the pass's maxima list is
   // archived for k_vote_lazy (bitmap passes B <= 512, short list passes), else
   // one atomic per preimage coordinate into the histogram on the side stream
-  auto vote_list = [&](const Perm& pv, int lgb, int slot, long long count) {
+  auto vote_list = [&](const Perm& pv, int lgb, int slot, long long count, cudaEvent_t list_ready) {
     if (count <= 0) return;
     const int w = n >> lgb;
     const long long len = (w == 1) ? 3 : std::min<long long>(w + 2, n);
@@ -1120,7 +1177,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
         const int words = lazy_bm_words(lgb);
         P.off = bm_used;
         cudaStream_t vs = c->profiling ? st : c->vote_st;
-        ck(cudaStreamWaitEvent(vs, c->ev_lmax, 0), "cudaStreamWaitEvent");
+        ck(cudaStreamWaitEvent(vs, list_ready, 0), "cudaStreamWaitEvent");
         ck(cudaMemsetAsync(bmarch + bm_used, 0, (size_t)words * 4, vs), "memset bitmap");
         pre(c, vs);
         kl(k_vote_bitmap, grid_for(count, 256, kNumSMs), 256, 0, vs,
@@ -1132,6 +1189,8 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
         bm_used += words;
         return;
       }
+      // (stream order: a speculative pass enqueued after this list's pass
+      // writes the other list buffer)
       ck(cudaMemcpyAsync(arch + arch_used, maxlists[slot & 1], (size_t)count * 4,
                          cudaMemcpyDeviceToDevice, st), "archive maxima");
       arch_used += count;
@@ -1140,7 +1199,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     // profiling serialises the votes onto the main stream so every launch's
     // event pair times that kernel alone
     cudaStream_t vs = c->profiling ? st : c->vote_st;
-    ck(cudaStreamWaitEvent(vs, c->ev_lmax, 0), "cudaStreamWaitEvent");
+    ck(cudaStreamWaitEvent(vs, list_ready, 0), "cudaStreamWaitEvent");
     zero_hist(vs);
     hist_used = true;
     const long long total = count * len * len;
@@ -1163,13 +1222,34 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   static const bool spec_on = getenv("SFFT2D_NO_SPEC") == nullptr;
   int spec_pi = -1, spec_b = 0, spec_z = 1;
   C* spec_grid = nullptr;
-  auto run_pass = [&](int bb) -> long long {
-    const int pi = pidx++;
+  // A tuner pass is enqueued (fold / FFT / local maxima, count published to
+  // its own mapped slot) and finished later (host reads the count, casts the
+  // vote).  While the host waits for pass t, the predicted pass t + 1 is
+  // already in the stream (pass 1 repeats pass 0's B; afterwards the tuner
+  // doubles B until the counts settle): the permutation of pass t + 1 is the
+  // next draw whatever its B, so a hit is exactly the pass the reference runs
+  // and hides one host round trip; a miss is discarded (its slot, list and
+  // publication are never read) and the real pass is enqueued behind it.
+  struct Ticket {
+    int pi = -1, slot = -1, bb = 0;
+    unsigned seq = 0;
+    bool emitted = false;   // first B = N pass: above-floor candidates listed
+    Perm p;
+    cudaEvent_t ready = nullptr;   // the pass's maxima list is complete
+  };
+  static const bool pipe_on = getenv("SFFT2D_NO_PIPELINE") == nullptr;
+  int ev_next = 0;
+  auto enqueue_pass = [&](int bb, int pi) -> Ticket {
+    Ticket tk;
+    tk.pi = pi;
+    tk.bb = bb;
     const Perm p = ps.get(pi, st);
+    tk.p = p;
     const int lgb = ilog2(bb);
     const size_t BB = (size_t)bb * bb;
     const int slot = npass++;
-    if (slot >= SFFT2D_MAX_HISTORY) fail(SFFT2D_ERR_UNSUPPORTED, "too many tuner passes");
+    tk.slot = slot;
+    if (slot >= 2 * SFFT2D_MAX_HISTORY) fail(SFFT2D_ERR_UNSUPPORTED, "too many tuner passes");
     int32_t* ml = maxlists[slot & 1];
     unsigned* cnt = cnt_slots + slot;
     if (vote_pending[slot & 1])   // the vote two passes back still reads this list
@@ -1178,15 +1258,17 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     if (bb == n) {
       // B = N: |Z_p[k1, k2]| = |x_hat[s1i k1, s2i k2]| — one dense FFT serves every pass
       ensure_xhat(true);
-      if (cand_ready && cand_n <= nkeys / 32) {
-        const unsigned grid = grid_for(std::max<long long>(cand_n, 1), 256, kNumSMs * 8);
+      const bool listed = cand_ready || cand_pending;   // the device count is exact either way
+      if (listed && (!cand_ready || cand_n <= nkeys / 32)) {
+        const unsigned grid = cand_ready ? grid_for(std::max<long long>(cand_n, 1), 256, kNumSMs * 8)
+                                         : (unsigned)(kNumSMs * 8);
         const Publish pub = make_publish(c, grid);
         seq = pub.seq;
         pre(c, st);
         kl(k_lmax_cand<T>, grid, 256, 0, st, (const T*)M, lgb, p.s1i, p.s2i, p.s1, p.s2,
            (const int32_t*)cand, (const unsigned*)cand_cnt, ml, cnt, pub);
-        post(c, "k_lmax_cand", st, (double)cand_n * 9 * sizeof(T));
-      } else if (!cand_ready) {
+        post(c, "k_lmax_cand", st, (double)(cand_ready ? cand_n : nkeys / 32) * 9 * sizeof(T));
+      } else if (!listed) {
         cand = (int32_t*)ws(c, "cand", (size_t)nkeys * 4);
         cand_cnt = (unsigned*)ws(c, "cand_cnt", 16);
         ck(cudaMemsetAsync(cand_cnt, 0, 16, st), "memset");
@@ -1194,6 +1276,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
         seq = lmax_tuner<T>(c, M, lgb, peakM, cf.mag_floor, ml, cnt, st, true, p.s1i, p.s2i, p.s2,
                             cand, cand_cnt, &emitted);
         cand_pending = emitted;
+        tk.emitted = emitted;
       } else {
         seq = lmax_tuner<T>(c, M, lgb, peakM, cf.mag_floor, ml, cnt, st, true, p.s1i, p.s2i, p.s2);
       }
@@ -1236,7 +1319,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       // |Z[k1,k2]| = |Y^[s1i k1, s2i k2]| for the natural-order fold Y
       // (Z[a,b] = Y[s1 a + t1, s2 b + t2]; the tau shifts are a phase):
       // fold without the bucket scatter, FFT Y, and test the permuted view
-      // speculation: B >= 512 folds also produce the next pass's grid at 2B
+      // speculation: B >= 128 folds also produce the next pass's grid at 2B
       // (its permutation is the next draw whatever the next pass is; with
       // estimation loops to follow that draw is always made, so drawing it
       // early leaves the caller's Generator exactly where the reference does)
@@ -1263,22 +1346,38 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       seq = lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, ml, cnt, st, true, p.s1i & mb, p.s2i & mb,
                           p.s2 & mb, nullptr, nullptr, nullptr, true);
     }
-    ck(cudaEventRecord(c->ev_lmax, st), "cudaEventRecord");   // the maxima list is complete
-    const long long count = wait_published(c, seq, st);
-    if (cand_pending) {   // the candidate count rides along with the maxima count
-      cand_n = ((volatile unsigned*)c->mapped_h)[2];
+    tk.seq = seq;
+    tk.ready = c->ev_pass[ev_next];
+    ev_next = (ev_next + 1) % 4;
+    ck(cudaEventRecord(tk.ready, st), "cudaEventRecord");   // the maxima list is complete
+    return tk;
+  };
+  // a speculative pass that the tuner did not take: nothing of it is read;
+  // its fold speculation (if any) is dropped and a candidate listing it
+  // started is redone by the next B = N pass
+  auto discard_pass = [&](const Ticket& tk) {
+    spec_pi = -1;
+    if (tk.emitted) cand_pending = false;
+  };
+  auto finish_pass = [&](const Ticket& tk) -> long long {
+    const long long count = wait_published(c, tk.seq, st);
+    if (tk.emitted) {   // the candidate count rides along with the maxima count
+      cand_n = pub_slot_h(c, tk.seq)[2];
       cand_pending = false;
       cand_ready = true;
     }
+    pidx = tk.pi + 1;
     last_valid = true;
-    last_b = bb;
-    last_pi = pi;
+    last_b = tk.bb;
+    last_pi = tk.pi;
     last_count = count;
-    last_slot = slot;
-    const long long w = n / bb;
+    last_slot = tk.slot;
+    last_ready = tk.ready;
+    const int lgb = ilog2(tk.bb);
+    const long long w = n / tk.bb;
     const long long len = (w == 1) ? 3 : std::min<long long>(w + 2, n);
     if (count > 0 && count * len * len <= budget) {   // tuner.py:165,175
-      vote_list(p, lgb, slot, count);
+      vote_list(tk.p, lgb, tk.slot, count, tk.ready);
       ++vote_passes;
       have_votes = true;
     }
@@ -1301,29 +1400,48 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   bool moved = false;
   bool converged = false;
   long long prev = -1;
+  Ticket cur;
+  if (max_iters > 0) cur = enqueue_pass(b, pidx);
   for (int it = 0; it < max_iters; ++it) {
-    const long long cnt = run_pass(b);
+    // the predicted next pass goes into the stream before this pass's count
+    // is read (pass 1: same B; later: B doubled, capped at n)
+    Ticket spec;
+    bool have_spec = false;
+    if (pipe_on && it + 1 < max_iters && (ps.bitgen || cur.pi + 1 < ps.n_arr)) {
+      spec = enqueue_pass(it == 0 ? b : std::min(2 * b, n), cur.pi + 1);
+      have_spec = true;
+    }
+    const long long cnt = finish_pass(cur);
     bool has = false;
+    bool stop = false;
     double r = 0.0;
     if (prev < 0) {
       has = false;
     } else if (prev == 0 && cnt == 0) {
       push(b, cnt, 0.0, true);
       converged = true;
-      break;
+      stop = true;
     } else {
       has = true;
       r = (prev == 0) ? INFINITY : std::fabs(1.0 - (double)cnt / (double)prev);
     }
-    push(b, cnt, r, has);
-    if (has && cf.delta1 <= r && r < cf.delta2) {
-      converged = true;
-      break;
+    if (!stop) {
+      push(b, cnt, r, has);
+      if (has && cf.delta1 <= r && r < cf.delta2) {
+        converged = true;
+        stop = true;
+      }
     }
-    int& sc = seen[std::make_pair(b, cnt)];
-    ++sc;
-    if (sc >= 3 && moved) {
-      converged = true;
+    if (!stop) {
+      int& sc = seen[std::make_pair(b, cnt)];
+      ++sc;
+      if (sc >= 3 && moved) {
+        converged = true;
+        stop = true;
+      }
+    }
+    if (stop) {
+      if (have_spec) discard_pass(spec);
       break;
     }
     prev = cnt;
@@ -1331,6 +1449,13 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       const int nb = update_bins(b, r, cf, n);
       moved = moved || nb != b;
       b = nb;
+    }
+    if (it + 1 >= max_iters) break;
+    if (have_spec && spec.bb == b) {
+      cur = spec;
+    } else {
+      if (have_spec) discard_pass(spec);
+      cur = enqueue_pass(b, pidx);
     }
   }
   long long maxc = 0;
@@ -1340,13 +1465,21 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     btop = std::max(btop, S->hist_bins[i]);
   }
   if (S->passes > 0 && maxc > 0) {
+    // confirmation passes at 2 b_top and 4 b_top (tuner.py:209-226): both
+    // are certain now, so both are enqueued before either count is read
+    Ticket conf[2];
+    int nconf = 0;
     for (int mult = 2; mult <= 4; mult *= 2) {
       const long long bc = (long long)mult * btop;
       if (bc <= n) {
-        const long long cnt = run_pass((int)bc);
-        push((int)bc, cnt, NAN, false);
-        maxc = std::max(maxc, cnt);
+        conf[nconf] = enqueue_pass((int)bc, pidx + nconf);
+        ++nconf;
       }
+    }
+    for (int i = 0; i < nconf; ++i) {
+      const long long cnt = finish_pass(conf[i]);
+      push(conf[i].bb, cnt, NAN, false);
+      maxc = std::max(maxc, cnt);
     }
   }
   int bdet = b;
@@ -1375,9 +1508,9 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   if (!have_votes && last_valid && maxc > 0) {
     // every pass exceeded the vote budget: fall back to the final pass (tuner.py:228-234)
     if (last_count > 0) {
-      // its list and count slot are intact; the side stream must see the list
-      ck(cudaEventRecord(c->ev_lmax, st), "cudaEventRecord");
-      vote_list(ps.hp[last_pi], ilog2(last_b), last_slot, last_count);
+      // its list and count slot are intact (later passes were discarded
+      // speculation writing the other list buffer)
+      vote_list(ps.hp[last_pi], ilog2(last_b), last_slot, last_count, last_ready);
       have_votes = true;
     }
     vote_passes = 1;
@@ -1464,7 +1597,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
                                 std::to_string(best) + " bin budget");
   }
   for (int i = 0; i < L; ++i) ps.get(pidx + i, st);
-  ps.upload(pidx, L, st);
+  ps.upload(pidx, L, st, c->ev_perm);
   const bool dense = (best == n);
   if (dense) ensure_xhat(false);
   estimate_and_select<T, Tin>(c, x, lgN, ilog2(best), tb, ps.hp.data() + pidx, dp + pidx, L, keys, m,
@@ -1533,12 +1666,13 @@ int sfft_location(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, con
 template <typename T, typename Tin>
 void sfft_from_hist(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, const DevTables& tb,
                     const uint32_t* hist, int mode, const Perm* hp_est, const Perm* dp_est,
-                    cudaStream_t st, sfft2d_result* res) {
+                    cudaStream_t st, sfft2d_result* res, bool nan_pending = false) {
   const int n = cf.n, lgN = ilog2(n), lgb = ilog2(cf.b_bins);
   const long nkeys = (long)n * n;
   int32_t* keys = (int32_t*)ws(c, "keys", (size_t)nkeys * 4);
   unsigned* kt = (unsigned*)ws(c, "keys_tot", 16);
   const unsigned m = hist_compact(c, hist, nkeys, mode, (unsigned)cf.vote_threshold, keys, kt, st);
+  if (nan_pending) raise_if_nonfinite(c);   // the scan's flag came with that synchronisation
   res->count = 0;
   res->ordered_by_magnitude = 0;
   res->n_candidates = m;
@@ -1558,14 +1692,23 @@ void check_sfft_cfg(const sfft2d_sfft_config& cf) {
   if (num > (long long)b * b) fail(SFFT2D_ERR_CONFIG, "d_factor*k exceeds the bin budget");
 }
 
+// NaN/Inf scan of x (as_complex_matrix, corefft.py:49-50) whose flag lands in
+// pinned[1] with the next synchronisation of `st` (no sync of its own)
 template <typename Tin>
-void check_finite_now(sfft2d_ctx* c, const Tin* x, long nkeys, cudaStream_t st) {
+void check_finite_async(sfft2d_ctx* c, const Tin* x, long nkeys, cudaStream_t st) {
   unsigned* finite = (unsigned*)ws(c, "finite", 16);
   ck(cudaMemsetAsync(finite, 0, 16, st), "memset");
   pre(c, st);
   kl(k_check_finite<Tin>, grid_for(nkeys, 256, kNumSMs * 8), 256, 0, st, x, nkeys, finite);
   post(c, "k_check_finite", st, (double)nkeys * sizeof(Tin));
-  if (read_u32(c, finite, st)) fail(SFFT2D_ERR_VALUE, "matrix contains NaN or Inf");
+  ck(cudaMemcpyAsync(c->pinned + 1, finite, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H");
+}
+
+template <typename Tin>
+void check_finite_now(sfft2d_ctx* c, const Tin* x, long nkeys, cudaStream_t st) {
+  check_finite_async<Tin>(c, x, nkeys, st);
+  ck(cudaStreamSynchronize(st), "sync");
+  raise_if_nonfinite(c);
 }
 
 // Upload `count` permutations to a named device array; returns (host, device).
@@ -1575,11 +1718,11 @@ std::pair<std::vector<Perm>, Perm*> upload_perms(sfft2d_ctx* c, const char* name
   std::vector<Perm> hp(std::max(count, 1));
   for (int i = 0; i < count; ++i) hp[i] = to_perm(perms[i], n);
   Perm* dp = (Perm*)ws(c, name, hp.size() * sizeof(Perm));
-  for (int i = 0; i < count; ++i) c->perm_pinned[i] = hp[i];
-  if (count > kPermPinned) fail(SFFT2D_ERR_UNSUPPORTED, "too many permutations");
-  ck(cudaMemcpyAsync(dp, c->perm_pinned, (size_t)count * sizeof(Perm), cudaMemcpyHostToDevice, st),
+  Perm* stage = perm_stage(c, std::max(count, 1));
+  for (int i = 0; i < count; ++i) stage[i] = hp[i];
+  ck(cudaMemcpyAsync(dp, stage, (size_t)count * sizeof(Perm), cudaMemcpyHostToDevice, st),
      "H2D perms");
-  ck(cudaStreamSynchronize(st), "sync");   // perm_pinned is reused by the next upload
+  ck(cudaEventRecord(c->ev_perm, st), "cudaEventRecord");   // the ring slot is in flight
   return {hp, dp};
 }
 
@@ -1590,11 +1733,13 @@ void run_sfft(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, const s
   const int L = cf.loops;
   const DevTables& tb = find_tables(c, cf.n, cf.window_delta_pass, cf.window_delta_stop);
   auto up = upload_perms(c, "perms", perms, 2 * L, cf.n, st);
-  check_finite_now<Tin>(c, x, (long)cf.n * cf.n, st);
+  // the NaN/Inf verdict is read at the first synchronisation (the candidate
+  // count); nothing before it leaves the device
+  check_finite_async<Tin>(c, x, (long)cf.n * cf.n, st);
   uint32_t* hist = (uint32_t*)ws(c, "hist", hist_bytes((long)cf.n * cf.n, kVoteAdd8));
   const int mode = sfft_location<T, Tin>(c, x, cf, tb, up.first.data(), up.second, L, false, hist, st);
   res->perms_used = 2 * L;
-  sfft_from_hist<T, Tin>(c, x, cf, tb, hist, mode, up.first.data() + L, up.second + L, st, res);
+  sfft_from_hist<T, Tin>(c, x, cf, tb, hist, mode, up.first.data() + L, up.second + L, st, res, true);
 }
 
 template <typename F>
@@ -1666,14 +1811,18 @@ int sfft2d_ctx_create(int device, sfft2d_ctx** out) {
   int rc = guarded(c, [&] {
     ck(cudaMallocHost(&c->pinned, 4096), "cudaMallocHost");
     ck(cudaMallocHost(&c->perm_pinned, kPermPinned * sizeof(Perm)), "cudaMallocHost");
-    ck(cudaHostAlloc((void**)&c->mapped_h, 64, cudaHostAllocMapped), "cudaHostAlloc");
-    std::memset(c->mapped_h, 0, 64);
+    ck(cudaHostAlloc((void**)&c->mapped_h, 16 * kPubSlots, cudaHostAllocMapped), "cudaHostAlloc");
+    std::memset(c->mapped_h, 0, 16 * kPubSlots);
     ck(cudaHostGetDevicePointer((void**)&c->mapped_d, c->mapped_h, 0), "cudaHostGetDevicePointer");
     ck(cudaMalloc(&c->done_d, 64), "cudaMalloc");
     ck(cudaMemset(c->done_d, 0, 64), "cudaMemset");
     ck(cudaStreamCreateWithFlags(&c->vote_st, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaEventCreateWithFlags(&c->ev_lmax, cudaEventDisableTiming), "cudaEventCreate");
     ck(cudaEventCreateWithFlags(&c->ev_ws, cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventCreateWithFlags(&c->ev_perm, cudaEventDisableTiming), "cudaEventCreate");
+    for (int i = 0; i < 4; ++i)
+      ck(cudaEventCreateWithFlags(&c->ev_pass[i], cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventRecord(c->ev_perm, 0), "cudaEventRecord");
     // the context's own memory pool, keeping freed workspace (no release at
     // sync points); the device's default pool is left untouched
     cudaMemPoolProps props = {};
@@ -1719,6 +1868,9 @@ void sfft2d_ctx_destroy(sfft2d_ctx* c) {
   if (c->vote_st) cudaStreamDestroy(c->vote_st);
   if (c->ev_lmax) cudaEventDestroy(c->ev_lmax);
   if (c->ev_ws) cudaEventDestroy(c->ev_ws);
+  if (c->ev_perm) cudaEventDestroy(c->ev_perm);
+  for (int i = 0; i < 4; ++i)
+    if (c->ev_pass[i]) cudaEventDestroy(c->ev_pass[i]);
   for (int i = 0; i < 2; ++i)
     if (c->ev_vote[i]) cudaEventDestroy(c->ev_vote[i]);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -1825,6 +1977,25 @@ int sfft2d_sfft(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host,
     c->res_prec = precision;
     c->has_res = true;
   });
+}
+
+int sfft2d_sfft_draw_perms(void* numpy_bitgen, int n, int loops, sfft2d_perm* out) {
+  if (!numpy_bitgen || !out || loops < 1 || !is_pow2(n)) return SFFT2D_ERR_VALUE;
+  try {
+    sfft_child_perms(numpy_bitgen, n, loops, out);
+  } catch (...) {
+    return SFFT2D_ERR_VALUE;
+  }
+  return SFFT2D_OK;
+}
+
+int sfft2d_sfft_bitgen(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host,
+                       const sfft2d_sfft_config* cfg, void* numpy_bitgen, int precision,
+                       void* stream, sfft2d_result* res) {
+  if (!cfg || !numpy_bitgen || cfg->loops < 1 || cfg->loops > kMaxLoops) return SFFT2D_ERR_VALUE;
+  std::vector<sfft2d_perm> perms(2 * cfg->loops);
+  if (is_pow2(cfg->n)) sfft_child_perms(numpy_bitgen, cfg->n, cfg->loops, perms.data());
+  return sfft2d_sfft(c, x, x_dtype, x_on_host, cfg, perms.data(), precision, stream, res);
 }
 
 static int atsfft_impl(sfft2d_ctx* c, const void* x, int x_dtype, int x_on_host, int n,

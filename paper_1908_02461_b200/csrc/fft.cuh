@@ -77,6 +77,8 @@ __device__ void fft_stages(cplx<T>* base, int count, int lgL, int es, int ss,
 }
 
 // Whole-grid 2D FFT of `ngrids` B x B grids, one CTA per grid, in place.
+// Rows padded to B + 1 elements (bank-conflict-free column stages), length-B
+// twiddles staged in shared memory: dynamic smem = (B (B + 1) + B) elements.
 template <typename T>
 __global__ void k_fft2d_small(cplx<T>* __restrict__ grids, int lgB,
                               const cplx<T>* __restrict__ tw, int lgN) {
@@ -84,16 +86,18 @@ __global__ void k_fft2d_small(cplx<T>* __restrict__ grids, int lgB,
   using C = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   C* s = reinterpret_cast<C*>(smem_raw);
-  const int B = 1 << lgB, BB = B * B;
+  const int B = 1 << lgB, BB = B * B, RS = B + 1;
+  C* tws = s + (size_t)B * RS;
   C* g = grids + (size_t)blockIdx.x * BB;
+  for (int k = threadIdx.x; k < B; k += blockDim.x) tws[k] = tw[k << (lgN - lgB)];
   for (int e = threadIdx.x; e < BB; e += blockDim.x) {
     const int u = e >> lgB, v = e & (B - 1);
-    s[bitrev(u, lgB) * B + bitrev(v, lgB)] = g[e];
+    s[bitrev(u, lgB) * RS + bitrev(v, lgB)] = g[e];
   }
   __syncthreads();
-  fft_stages<T>(s, B, lgB, 1, B, tw, lgN);   // rows
-  fft_stages<T>(s, B, lgB, B, 1, tw, lgN);   // columns
-  for (int e = threadIdx.x; e < BB; e += blockDim.x) g[e] = s[e];
+  fft_stages<T>(s, B, lgB, 1, RS, tws, lgB);    // rows
+  fft_stages<T>(s, B, lgB, RS, 1, tws, lgB);    // columns
+  for (int e = threadIdx.x; e < BB; e += blockDim.x) g[e] = s[(e >> lgB) * RS + (e & (B - 1))];
 }
 
 // Row pass over `nrows` rows of length B (rows of all grids concatenated).

@@ -102,7 +102,7 @@ void fft2d_grids(sfft2d_ctx* c, cplx<T>* grids, int lgB, int ngrids, const cplx<
   if (BB * sizeof(C) <= (size_t)kSmall2DBytes) {
     const int threads = B * B / 4 >= 256 ? 256 : (B * B / 4 >= 32 ? B * B / 4 : 32);
     pre(c, st);
-    kl(k_fft2d_small<T>, ngrids, threads, BB * sizeof(C), st, grids, lgB, tw, lgN);
+    kl(k_fft2d_small<T>, ngrids, threads, ((size_t)B * (B + 1) + B) * sizeof(C), st, grids, lgB, tw, lgN);
     post(c, "k_fft2d_small", st, 2 * gb);
     if (wc && out != grids)
       ck(cudaMemcpyAsync(out, grids, BB * ngrids * sizeof(C), cudaMemcpyDeviceToDevice, st), "copy");

@@ -791,6 +791,15 @@ __global__ void k_fold_reduce(const cplx<T>* __restrict__ part, int Z, int nloop
 }
 
 // Small grids: reduce partials + permute + whole 2D FFT in one CTA per loop.
+// Rows padded to B + 1 elements (the column stages are then bank-conflict
+// free) and the length-B twiddles staged in shared memory; dynamic smem =
+// small_fft_smem<T>(lgB).
+template <typename T>
+__host__ __device__ inline size_t small_fft_smem(int lgB) {
+  const size_t B = (size_t)1 << lgB;
+  return (B * (B + 1) + B) * sizeof(cplx<T>);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(1024) k_fold_reduce_fft_small(const cplx<T>* __restrict__ part, int Z, int nloops,
                                         int lgB, PermPack pp, const cplx<T>* __restrict__ tw,
@@ -801,20 +810,23 @@ __global__ void __launch_bounds__(1024) k_fold_reduce_fft_small(const cplx<T>* _
   C* s = reinterpret_cast<C*>(smem_raw);
   const int B = 1 << lgB;
   const int BB = B * B;
+  const int RS = B + 1;
+  C* tws = s + (size_t)B * RS;
   const int l = blockIdx.x;
   const unsigned maskB = (unsigned)B - 1u;
+  for (int k = threadIdx.x; k < B; k += blockDim.x) tws[k] = tw[k << (lgN - lgB)];
   for (int e = threadIdx.x; e < BB; e += blockDim.x) {
     const unsigned rho = (unsigned)(e >> lgB), kap = (unsigned)(e & (B - 1));
     const C v = sum_partials(part + (size_t)l * BB + e, (size_t)nloops * BB, Z);
     const unsigned a = (pp.p[l].s1i * (rho - pp.p[l].t1)) & maskB;
     const unsigned b = (pp.p[l].s2i * (kap - pp.p[l].t2)) & maskB;
-    s[bitrev(a, lgB) * B + bitrev(b, lgB)] = v;
+    s[bitrev(a, lgB) * RS + bitrev(b, lgB)] = v;
   }
   __syncthreads();
-  fft_stages<T>(s, B, lgB, 1, B, tw, lgN);
-  fft_stages<T>(s, B, lgB, B, 1, tw, lgN);
+  fft_stages<T>(s, B, lgB, 1, RS, tws, lgB);
+  fft_stages<T>(s, B, lgB, RS, 1, tws, lgB);
   C* out = spec + (size_t)l * BB;
-  for (int e = threadIdx.x; e < BB; e += blockDim.x) out[e] = s[e];
+  for (int e = threadIdx.x; e < BB; e += blockDim.x) out[e] = s[(e >> lgB) * RS + (e & (B - 1))];
 }
 
 // Tuner pass for small grids (B*B*sizeof(C) <= kSmall2DBytes), one CTA:

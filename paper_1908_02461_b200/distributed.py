@@ -33,7 +33,7 @@ import numpy as np
 from . import _native
 from ._tensors import as_device_image
 from .batch import atsfft2d_batch
-from .engine import ConfigurationError, SfftConfig, _fetch, _stream, to_dict
+from .engine import ConfigurationError, SfftConfig, _fetch, _stream, sfft_perms, to_dict
 from .hashing import draw_permutation
 
 __all__ = ["loop_shard", "batch_shard", "merge_votes", "sfft2d_loopsplit", "atsfft2d_sharded",
@@ -142,9 +142,7 @@ def sfft2d_loopsplit(x, cfg: SfftConfig, rng, *, group=None, precision: str = "f
     if img.n != cfg.n:
         raise ConfigurationError(f"config built for n={cfg.n}, signal has n={img.n}")
     prec = _native.precision_code(precision)
-    gen = np.random.default_rng(rng)
-    loop_rngs = [np.random.default_rng(int(gen.integers(2**63))) for _ in range(2 * cfg.loops)]
-    perms = [draw_permutation(cfg.n, g) for g in loop_rngs]
+    perms = sfft_perms(rng, cfg.n, cfg.loops)   # engine.py:266-280, derived natively
     mine = loop_shard(cfg.loops, rank, world)
     ctx = _native.context(img.device)
     ctx.ensure_tables(cfg.n, cfg.window_delta_pass, cfg.window_delta_stop)

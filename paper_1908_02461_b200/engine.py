@@ -111,6 +111,19 @@ def _stream(torch, device):
     return torch.cuda.current_stream(device).cuda_stream
 
 
+def sfft_perms(rng, n: int, loops: int) -> list:
+    """The reference's per-loop permutations (engine.py:266-280) for an int
+    seed or Generator, derived natively (sfft2d_sfft_draw_perms): location
+    loops [0, loops), estimation loops [loops, 2 loops)."""
+    from .tuner import _generator
+    gen, bitgen, _ = _generator(rng)
+    out = (_native.Perm * (2 * loops))()
+    rc = _native.load_library().sfft2d_sfft_draw_perms(bitgen, n, loops, out)
+    if rc != _native.OK:
+        raise ValueError(f"cannot draw permutations for n={n}, loops={loops}")
+    return list(out)
+
+
 def sfft2d_arrays(x, cfg: SfftConfig, rng, *, cache: WindowCache | None = None,
                   precision: str = "fp64", device=None):
     """``sfft2d`` returning (coords int64[m, 2], values[m]) in the reference's
@@ -120,9 +133,11 @@ def sfft2d_arrays(x, cfg: SfftConfig, rng, *, cache: WindowCache | None = None,
     if img.n != cfg.n:
         raise ConfigurationError(f"config built for n={cfg.n}, signal has n={img.n}")
     prec = _native.precision_code(precision)
-    rng = np.random.default_rng(rng)
-    loop_rngs = [np.random.default_rng(int(rng.integers(2**63))) for _ in range(2 * cfg.loops)]
-    perms = [draw_permutation(cfg.n, g) for g in loop_rngs]
+    # the per-loop streams (engine.py:266-280: 2L child Generators seeded from
+    # rng.integers(2**63), one draw_permutation each) are derived natively from
+    # the caller's bit generator (sfft2d_sfft_bitgen, csrc/npyrng.h)
+    from .tuner import _generator
+    gen, bitgen, snapshot = _generator(rng)
     ctx = _native.context(img.device)
     ctx.ensure_tables(cfg.n, cfg.window_delta_pass, cfg.window_delta_stop)
     ccfg = _native.SfftCfg(cfg.n, cfg.k, cfg.loops, cfg.d_factor, cfg.vote_threshold, cfg.b_bins,
@@ -135,8 +150,11 @@ def sfft2d_arrays(x, cfg: SfftConfig, rng, *, cache: WindowCache | None = None,
             ptr, on_host = img.tensor.data_ptr(), 0
         else:
             ptr, on_host = img.host.ctypes.data, 1
-        ctx.check(ctx.lib.sfft2d_sfft(ctx.handle, ptr, img.dtype_code, on_host, ctypes.byref(ccfg),
-                                      _native.perm_array(perms), prec, st, ctypes.byref(res)))
+        rc = ctx.lib.sfft2d_sfft_bitgen(ctx.handle, ptr, img.dtype_code, on_host, ctypes.byref(ccfg),
+                                        bitgen, prec, st, ctypes.byref(res))
+        if rc == _native.ERR_VALUE and snapshot is not None:
+            gen.bit_generator.state = snapshot   # the reference validates x before drawing
+        ctx.check(rc)
         ctx.last_launches = int(res.gpu_launches)
         return _fetch(ctx, res, st, prec)
 

@@ -244,3 +244,22 @@ def test_batch_detects_shared_generators():
     g = np.random.default_rng(1)
     assert _shared_generators([g, np.random.default_rng(1), g])
     assert not _shared_generators([g, np.random.default_rng(1), 3, 3])
+
+
+@pytest.mark.parametrize("seed", [0, 1, 12, 2**40 + 3, 2**62 + 12345])
+@pytest.mark.parametrize("n", [16, 256, 4096, 16384])
+def test_native_sfft_streams_match_numpy(seed, n):
+    # engine.py:266-280 restated natively (numpy SeedSequence + PCG64 in
+    # csrc/npyrng.h): the 2L child permutations and the caller's Generator
+    # advance are numpy's own (host-only entry point, no GPU needed)
+    lib = _native.load_library()
+    loops = 8
+    g1, g2 = np.random.default_rng(seed), np.random.default_rng(seed)
+    out = (_native.Perm * (2 * loops))()
+    assert lib.sfft2d_sfft_draw_perms(g1.bit_generator.ctypes.bit_generator.value, n, loops,
+                                      out) == 0
+    kids = [np.random.default_rng(int(g2.integers(2**63))) for _ in range(2 * loops)]
+    want = [hashing.draw_permutation(n, k) for k in kids]
+    got = [(o.sigma1, o.sigma2, o.tau1, o.tau2, o.sigma1_inv, o.sigma2_inv) for o in out]
+    assert got == [(p.sigma1, p.sigma2, p.tau1, p.tau2, p.sigma1_inv, p.sigma2_inv) for p in want]
+    assert g1.integers(1 << 40) == g2.integers(1 << 40)
