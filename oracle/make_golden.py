@@ -146,6 +146,10 @@ def case_localmax():
     g[4, 2] = 1e-4
     grids.append(g)
     grids.append(np.zeros((8, 8), complex))
+    # non-power-of-two sides: the reference accepts any square grid >= 4x4
+    for side in (5, 12, 100):
+        grids.append(rng.normal(size=(side, side)) + 1j * rng.normal(size=(side, side)))
+    grids.append(np.abs(rng.normal(size=(6, 6))).round(1).astype(np.complex128))
     for i, gr in enumerate(grids):
         cnt, coords = count_local_maxima(gr, 1e-3)
         out[f"grid{i}"] = gr
@@ -348,6 +352,17 @@ def case_c5():
     meta = _gen_meta(img, snr=15.0, cluster=0.2)
     del img
     _ats_case("c5_ats_k64", x, 8, 6, False, extra=meta)
+
+
+def case_harness():
+    """The reference harness's own rows for a tiny grid (bench.py:142-187),
+    as its CSV: the GPU harness must reproduce the error / detection columns
+    cell by cell (same signal and algorithm seeds)."""
+    from sfft2d import bench as ref_bench
+    spec = ref_bench.ExperimentSpec(algorithms=("dense", "sfft", "atsfft"), sizes=(64, 128),
+                                    sparsities=(4,), trials=3, seed=11)
+    rows = ref_bench.run_experiment(spec)
+    ref_bench.write_rows_csv(rows, os.path.join(OUT, "ref_harness_tiny.csv"))
 
 
 CASES = {name[5:]: fn for name, fn in globals().items() if name.startswith("case_")}

@@ -2302,7 +2302,7 @@ int sfft2d_fft2d(sfft2d_ctx* c, void* grids, int b, int count, int n_table, int 
 int sfft2d_local_maxima(sfft2d_ctx* c, const void* grid, int b, double mag_floor, int precision,
                         int64_t* count, int32_t* out_flat, int64_t capacity, void* stream) {
   return guarded(c, [&] {
-    if (!is_pow2(b) || b < 4) fail(SFFT2D_ERR_VALUE, "bin grid must be at least 4x4 and a power of 2");
+    if (b < 4 || b > 65536) fail(SFFT2D_ERR_VALUE, "bin grid must be at least 4x4");
     cudaStream_t st = (cudaStream_t)stream;
     c->ws_st = st;
     dispatch_prec(precision, [&](auto t) {
@@ -2315,7 +2315,22 @@ int sfft2d_local_maxima(sfft2d_ctx* c, const void* grid, int b, double mag_floor
       kl(k_mags<T>, dim3(grid_for(BB, 256, 1024), 1), 256, 0, st, (const cplx<T>*)grid, BB, mg, pk);
       post(c, "k_mags", st, 0);
       int32_t* tmp = (int32_t*)ws(c, "api_lm", (size_t)(BB / 4 + 64) * 4);
-      const long long cnt = local_maxima_dev<T>(c, mg, ilog2(b), pk, mag_floor, tmp, st);
+      long long cnt;
+      if (is_pow2(b)) {
+        cnt = local_maxima_dev<T>(c, mg, ilog2(b), pk, mag_floor, tmp, st);
+      } else {
+        // any square grid (tuner.py:97-118 accepts every side >= 4)
+        const int nblk = blocks_for(BB);
+        uint32_t* bits = (uint32_t*)ws(c, "lm_bits", words_for(BB) * 4);
+        unsigned* cnts = (unsigned*)ws(c, "lm_cnt", (size_t)nblk * 4);
+        unsigned* tot = (unsigned*)ws(c, "lm_tot", 16);
+        pre(c, st);
+        kl(k_lmax_bits_any<T>, dim3(nblk, 1), kCmpThreads, 0, st, (const T*)mg, b, (const unsigned long long*)pk,
+           mag_floor, bits, cnts);
+        post(c, "k_lmax_bits_any", st, (double)BB * sizeof(T) + BB / 8.0);
+        compact(c, bits, cnts, BB, 1, tmp, 0, tot, st);
+        cnt = read_u32(c, tot, st);
+      }
       if (count) *count = cnt;
       const long long cp = std::min<long long>(cnt, capacity);
       if (out_flat && cp > 0)

@@ -74,6 +74,51 @@ __global__ void k_lmax_bits(const T* __restrict__ mags, int lgB, int nseg_stride
   }
 }
 
+// Local maxima of a B x B grid of ANY side B >= 4 (the public
+// count_local_maxima accepts every square grid, tuner.py:97-118; the tuner's
+// own grids are powers of two and use the kernels above/below).  Same bit /
+// block-count layout as k_lmax_bits, toroidal neighbours by modulo.
+template <typename T>
+__global__ void k_lmax_bits_any(const T* __restrict__ m, int B,
+                                const unsigned long long* __restrict__ peak, double floor_rel,
+                                uint32_t* __restrict__ bits, unsigned* __restrict__ blk_counts) {
+  pdl_wait();
+  const long BB = (long)B * B;
+  const long wps = words_for(BB);
+  const double pk = fkey_inv(peak[0]);
+  const bool live = pk > 0.0;
+  const double fl = floor_rel * pk;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long w0 = (long)blockIdx.x * kCmpWords + warp * 32;
+  unsigned cnt = 0;
+  for (int i = 0; i < 32; ++i) {
+    const long w = w0 + i;
+    const long e = w * 32 + lane;
+    bool f = false;
+    if (live && e < BB) {
+      const long r = e / B, c = e - r * B;
+      const T v = m[e];
+      if ((double)v >= fl) {
+        const long rm = (r + B - 1) % B * B, r0 = r * B, rp = (r + 1) % B * B;
+        const long cm = (c + B - 1) % B, cp = (c + 1) % B;
+        f = v > m[rm + cm] && v > m[rm + c] && v > m[rm + cp] && v > m[r0 + cm] &&
+            v > m[r0 + cp] && v > m[rp + cm] && v > m[rp + c] && v > m[rp + cp];
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, f);
+    if (lane == 0 && w < wps) bits[w] = bal;
+    cnt += __popc(bal);
+  }
+  __shared__ unsigned s_cnt[kCmpThreads / 32];
+  if (lane == 0) s_cnt[warp] = cnt;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int i = 0; i < kCmpThreads / 32; ++i) t += s_cnt[i];
+    blk_counts[blockIdx.x] = t;
+  }
+}
+
 // Tiled local maxima: CTA = `rb` output rows of the B x B magnitude grid
 //   G[r][c] = M[(s1*r) mod B][(s2*c) mod B]      (s1 = s2 = 1 for a plain grid)
 // The rb + 2 SOURCE rows it needs (one halo row each side, toroidal) are

@@ -154,8 +154,6 @@ def count_local_maxima(bins, mag_floor: float, *, precision: str = "fp64", devic
     b = int((t if t is not None else a).shape[0])
     if b < 4:
         raise ValueError("bin grid must be at least 4x4")
-    if not is_power_of_two(b):
-        raise ValueError(f"bin grid side {b} must be a power of 2 on the GPU path")
     prec = _native.precision_code(precision)
     cdt = torch.complex128 if prec == _native.FP64 else torch.complex64
     if t is None:
