@@ -55,6 +55,11 @@ struct DevTables {
   void* freq[2] = {nullptr, nullptr};
   void* tw[2] = {nullptr, nullptr};
   std::vector<int> support;  // samples per axis with nonzero window weight, per log2(B)
+  std::vector<std::vector<int>> nz;   // those samples' indices, per log2(B)
+  // per log2(B): R when the window is untruncated (support N) and its DC-
+  // normalised response F vanishes (|F| <= 1e-14) beyond |d| = R <= 4, else 0
+  // (k_estimate_conv)
+  std::vector<int> conv_r;
 };
 
 }  // namespace
@@ -514,12 +519,26 @@ PermPack identity_pack(int g) {
   return pp;
 }
 
+// ATSFFT estimation at B < N with an untruncated window from the dense
+// spectrum (k_estimate_conv; SFFT2D_NO_CONV=1: folds + FFTs, for A/B runs)
+bool conv_on() {
+  static const bool on = getenv("SFFT2D_NO_CONV") == nullptr;
+  return on;
+}
+
+// multi-loop folds for B < 512 go through k_fold_ml (SFFT2D_OLD_MLFOLD=1:
+// k_fold, for A/B runs)
+bool ml_fold_on() {
+  static const bool on = getenv("SFFT2D_OLD_MLFOLD") == nullptr;
+  return on;
+}
+
 template <typename T, typename Tin>
 FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTables& tb,
                     const Perm* hp, int g, void* y_direct, cudaStream_t st,
                     unsigned long long* zero_peak = nullptr, bool natural = false,
                     const Perm* spec_q = nullptr, void* spec_y = nullptr, int* spec_z = nullptr,
-                    bool spec_same = false) {
+                    bool spec_same = false, unsigned* nonfinite = nullptr) {
   using C = cplx<T>;
   const int B = 1 << lgB;
   const size_t BB = (size_t)B * B;
@@ -625,6 +644,34 @@ FoldOut fold_launch(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTabl
     post(c, "k_fold_ring", st, sup * sup * sizeof(Tin) + (double)gr.Z * BB * sizeof(C));
     return FoldOut{dstr, gr.Z};
   }
+  if (g > 1 && B < 512 && ml_fold_on()) {
+    // multi-loop fold: column tiles x bucket rows x row chunks, UNR 16-byte
+    // loads in flight per thread
+    const int N = 1 << lgN;
+    const int twc = std::min(N, 512);
+    const int tiles = N / twc;
+    const int aliases = N >> lgB;
+    int zr = (aliases + kFoldMaxRows - 1) / kFoldMaxRows;
+    const long ctas = (long)tiles * B;
+    if (ctas < 2L * kNumSMs) zr = std::max<long>(zr, std::min<long>(aliases, (2L * kNumSMs + ctas - 1) / ctas));
+    const int rpc = (aliases + zr - 1) / zr;
+    zr = (aliases + rpc - 1) / rpc;
+    // the column tiles of one bucket row are summed inside a thread-block
+    // cluster (DSMEM), so c3 (8 tiles) writes its grid directly
+    const int csz = std::min(tiles, 8);
+    const int zp = (tiles / csz) * zr;
+    C* dstm = (zp == 1) ? (C*)y_direct : (C*)ws(c, "fold_part", (size_t)zp * g * BB * sizeof(C));
+    const size_t dynm = (size_t)kMaxFoldLoops * (twc + B) * sizeof(C);
+    pre(c, st);
+    if constexpr (sizeof(T) == 4)
+      klc(k_fold_ml<Tin, T, kMaxFoldLoops, 8>, dim3(tiles, B, zr), 256, dynm, st, csz, x, space, pp, g,
+          lgN, lgB, twc, rpc, natural, zp, dstm, nonfinite);
+    else
+      klc(k_fold_ml<Tin, T, kMaxFoldLoops, 4>, dim3(tiles, B, zr), 256, dynm, st, csz, x, space, pp, g,
+          lgN, lgB, twc, rpc, natural, zp, dstm, nonfinite);
+    post(c, "k_fold_ml", st, sup * sup * sizeof(Tin) + (double)zp * g * BB * sizeof(C));
+    return FoldOut{dstm, zp};
+  }
   C* dst = (gm.Z == 1) ? (C*)y_direct : (C*)ws(c, "fold_part", (size_t)gm.Z * g * BB * sizeof(C));
   const double fold_bytes = sup * sup * sizeof(Tin) + (double)gm.Z * g * BB * sizeof(C);
   pre(c, st);
@@ -646,7 +693,7 @@ void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTable
                    const Perm* hp, int nloops, cplx<T>* spec, T* mags, unsigned long long* peaks,
                    cudaStream_t st, bool natural = false, cplx<T>* prefolded = nullptr,
                    const Perm* spec_q = nullptr, cplx<T>* spec_y = nullptr, int pre_z = 1,
-                   int* spec_z = nullptr) {
+                   int* spec_z = nullptr, unsigned* nonfinite = nullptr) {
   using C = cplx<T>;
   const int B = 1 << lgB;
   const int P = prec_of<T>();
@@ -676,7 +723,7 @@ void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTable
       if (pk) ck(cudaMemsetAsync(pk, 0, sizeof(unsigned long long), st), "memset");
     } else {
       fo = fold_launch<T, Tin>(c, x, lgN, lgB, tb, hp + g0, g, y, st, (nloops == 1) ? pk : nullptr,
-                               natural, spec_q, spec_y, spec_z);
+                               natural, spec_q, spec_y, spec_z, false, nonfinite);
     }
     C* dst = (C*)fo.data;
     struct { int Z; } gm{fo.Z};
@@ -962,7 +1009,8 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
                          const Perm* hp, const Perm* dp, int L, const int32_t* keys, unsigned m,
                          const unsigned* m_dev, long long k, double gain_floor, double prune_rel,
                          bool dense, const cplx<T>* xhat, cudaStream_t st, sfft2d_result* res,
-                         const cplx<T>* dscratch = nullptr) {
+                         const cplx<T>* dscratch = nullptr, const cplx<T>* xconv = nullptr,
+                         int conv_r = 0) {
   using C = cplx<T>;
   const int P = prec_of<T>();
   C* med = (C*)ws(c, "med", (size_t)m * sizeof(C));
@@ -993,16 +1041,36 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
     if (L > kMaxLoops) fail(SFFT2D_ERR_UNSUPPORTED, "more than 64 estimation loops");
     const int B = 1 << lgB;
     const size_t BB = (size_t)B * B;
-    C* grids = (C*)ws(c, "est_grids", (size_t)L * BB * sizeof(C));
-    // natural-order folds (coalesced writes; k_estimate reads the permuted view)
-    fold_spectrum<T, Tin>(c, x, lgN, lgB, tb, hp, L, grids, (T*)nullptr, nullptr, st, true);
     C* vals = (C*)ws(c, "vals", (size_t)L * m * sizeof(C));
     uint8_t* usable = (uint8_t*)ws(c, "usable", (size_t)L * m);
     const T* freq = (const T*)tb.freq[P] + ((size_t)lgB << lgN);
-    pre(c, st);
-    kl(k_estimate<T>, grid_for((long long)m * L), 256, 0, st, grids, L, keys, m_dev, dp, lgN, lgB, freq, (const C*)tb.tw[P], gain_floor, vals, usable,
-        (long)m, true);
-    post(c, "k_estimate", st, 0);
+    if (xconv) {
+      // untruncated window: (2R+1)^2 gathers of the dense spectrum per
+      // (candidate, loop) replace the L folds and B x B FFTs
+      pre(c, st);
+      auto go = [&](auto RC) {
+        constexpr int R = decltype(RC)::value;
+        kl(k_estimate_conv<T, R>, grid_for((long long)m * L), 256, 0, st, xconv, L, keys, m_dev, dp, lgN,
+           lgB, freq, (const C*)tb.tw[P], gain_floor, vals, usable, (long)m);
+      };
+      switch (conv_r) {
+        case 1: go(std::integral_constant<int, 1>{}); break;
+        case 2: go(std::integral_constant<int, 2>{}); break;
+        case 3: go(std::integral_constant<int, 3>{}); break;
+        case 4: go(std::integral_constant<int, 4>{}); break;
+        default: fail(SFFT2D_ERR_STATE, "convolution estimate outside its tap range");
+      }
+      const double taps = (double)(2 * conv_r + 1) * (2 * conv_r + 1);
+      post(c, "k_estimate_conv", st, (double)m * L * taps * sizeof(C));
+    } else {
+      C* grids = (C*)ws(c, "est_grids", (size_t)L * BB * sizeof(C));
+      // natural-order folds (coalesced writes; k_estimate reads the permuted view)
+      fold_spectrum<T, Tin>(c, x, lgN, lgB, tb, hp, L, grids, (T*)nullptr, nullptr, st, true);
+      pre(c, st);
+      kl(k_estimate<T>, grid_for((long long)m * L), 256, 0, st, grids, L, keys, m_dev, dp, lgN, lgB, freq, (const C*)tb.tw[P], gain_floor, vals, usable,
+          (long)m, true);
+      post(c, "k_estimate", st, 0);
+    }
     pre(c, st);
     kl(k_median<T>, grid_for(m, 128), 128, 0, st, vals, usable, L, (long)m, m_dev, med, mags,
                                                    alive, alive_cnt, peak);
@@ -1144,6 +1212,23 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       ck(cudaMemsetAsync(peakM, 0, 16, st), "memset");
       mags_of<T>(c, xhat, nkeys, 1, M, peakM, st);
     }
+  };
+
+  // the complex dense spectrum in natural order (k_estimate_conv): stored by
+  // the unfactored dense FFT; the factored one runs pass B once more with a
+  // complex output
+  C* xfull = nullptr;
+  auto dense_xhat_complex = [&]() -> const C* {
+    if (!factored) {
+      ensure_xhat(false);
+      return xhat;
+    }
+    if (!xfull) {
+      ensure_xhat(false);
+      xfull = (C*)ws(c, "xhat_full", (size_t)nkeys * sizeof(C));
+      dense_fft_xhat<T>(c, xfull, lgN, (const C*)tb.tw[prec_of<T>()], st);
+    }
+    return xfull;
   };
 
   ck(cudaMemsetAsync(c->done_d, 0, sizeof(unsigned), st), "memset");
@@ -1600,9 +1685,19 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   ps.upload(pidx, L, st, c->ev_perm);
   const bool dense = (best == n);
   if (dense) ensure_xhat(false);
-  estimate_and_select<T, Tin>(c, x, lgN, ilog2(best), tb, ps.hp.data() + pidx, dp + pidx, L, keys, m,
+  // B < N with an untruncated window: estimate from the dense spectrum when
+  // it is already (partly) computed, or when B >= N/4 (a dense FFT is then
+  // cheaper than L folds + L B x B FFTs)
+  const int lgbest = ilog2(best);
+  const cplx<T>* xconv = nullptr;
+  const int conv_r = tb.conv_r[lgbest];
+  if (!dense && conv_r > 0 && conv_on() &&
+      (xhat_ready || dscratch || (long long)best * 4 >= (long long)n)) {
+    xconv = dense_xhat_complex();
+  }
+  estimate_and_select<T, Tin>(c, x, lgN, lgbest, tb, ps.hp.data() + pidx, dp + pidx, L, keys, m,
                               kt, k, cf.gain_floor, cf.prune_rel, dense, xhat, st, res,
-                              dense ? dscratch : nullptr);
+                              dense ? dscratch : nullptr, xconv, conv_r);
   pidx += L;
   S->perms_used = pidx;
   S->perms_drawn = (int32_t)ps.used();
@@ -1617,13 +1712,14 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
 template <typename T, typename Tin>
 int sfft_location(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, const DevTables& tb,
                   const Perm* hp, const Perm* dp, int nloc, bool want_counts, uint32_t* out,
-                  cudaStream_t st) {
+                  cudaStream_t st, unsigned* nonfinite = nullptr) {
   const int n = cf.n, lgN = ilog2(n), b = cf.b_bins, lgb = ilog2(b);
   const long BB = (long)b * b;
   const long nkeys = (long)n * n;
   const long long num = std::max(1LL, (long long)cf.d_factor * cf.k);
   T* mags = (T*)ws(c, "loc_mags", (size_t)nloc * BB * sizeof(T));
-  fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, hp, nloc, (cplx<T>*)nullptr, mags, nullptr, st);
+  fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, hp, nloc, (cplx<T>*)nullptr, mags, nullptr, st, false,
+                        nullptr, nullptr, nullptr, 1, nullptr, nonfinite);
   int32_t* bins = (int32_t*)ws(c, "loc_bins", (size_t)nloc * num * 4);
   if (num >= BB) {
     pre(c, st);
@@ -1704,6 +1800,24 @@ void check_finite_async(sfft2d_ctx* c, const Tin* x, long nkeys, cudaStream_t st
   ck(cudaMemcpyAsync(c->pinned + 1, finite, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H");
 }
 
+// True when the location fold of these loops goes through k_fold_ml (which
+// then checks every sample it reads) and the loops' row windows together
+// cover all n rows, so that fold reads every sample of x.  The converted
+// value is checked, so a c128 input folded in fp32 keeps the separate scan
+// (a finite double can overflow float).
+template <typename T, typename Tin>
+bool fold_reads_all(const DevTables& tb, int lgb, const Perm* hp, int loops, int n) {
+  if (loops < 2 || (1 << lgb) >= 512 || !ml_fold_on()) return false;
+  if (sizeof(Tin) == 16 && sizeof(T) == 4) return false;
+  std::vector<unsigned char> cov((size_t)n, 0);
+  const unsigned maskN = (unsigned)n - 1u;
+  for (int l = 0; l < loops; ++l)
+    for (int u : tb.nz[lgb]) cov[(hp[l].s1 * (unsigned)u + hp[l].t1) & maskN] = 1;
+  for (int r = 0; r < n; ++r)
+    if (!cov[r]) return false;
+  return true;
+}
+
 template <typename Tin>
 void check_finite_now(sfft2d_ctx* c, const Tin* x, long nkeys, cudaStream_t st) {
   check_finite_async<Tin>(c, x, nkeys, st);
@@ -1734,10 +1848,21 @@ void run_sfft(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, const s
   const DevTables& tb = find_tables(c, cf.n, cf.window_delta_pass, cf.window_delta_stop);
   auto up = upload_perms(c, "perms", perms, 2 * L, cf.n, st);
   // the NaN/Inf verdict is read at the first synchronisation (the candidate
-  // count); nothing before it leaves the device
-  check_finite_async<Tin>(c, x, (long)cf.n * cf.n, st);
+  // count); nothing before it leaves the device.  When the location loops'
+  // windows together cover every row, the multi-loop fold reads every sample
+  // and checks them as it goes; otherwise one k_check_finite pass.
+  unsigned* fin = nullptr;
+  if (fold_reads_all<T, Tin>(tb, ilog2(cf.b_bins), up.first.data(), L, cf.n)) {
+    fin = (unsigned*)ws(c, "finite", 16);
+    ck(cudaMemsetAsync(fin, 0, 16, st), "memset");
+  } else {
+    check_finite_async<Tin>(c, x, (long)cf.n * cf.n, st);
+  }
   uint32_t* hist = (uint32_t*)ws(c, "hist", hist_bytes((long)cf.n * cf.n, kVoteAdd8));
-  const int mode = sfft_location<T, Tin>(c, x, cf, tb, up.first.data(), up.second, L, false, hist, st);
+  const int mode = sfft_location<T, Tin>(c, x, cf, tb, up.first.data(), up.second, L, false, hist, st,
+                                         fin);
+  if (fin)
+    ck(cudaMemcpyAsync(c->pinned + 1, fin, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H");
   res->perms_used = 2 * L;
   sfft_from_hist<T, Tin>(c, x, cf, tb, hist, mode, up.first.data() + L, up.second + L, st, res, true);
 }
@@ -1904,10 +2029,20 @@ int sfft2d_ctx_set_tables(sfft2d_ctx* c, int n, double dpass, double dstop, cons
     up(freq, rows, &t.freq[SFFT2D_FP64], &t.freq[SFFT2D_FP32]);
     up(twiddle, (size_t)2 * n, &t.tw[SFFT2D_FP64], &t.tw[SFFT2D_FP32]);
     t.support.assign(t.lgn + 1, n);
+    t.nz.assign(t.lgn + 1, {});
     for (int lb = 0; lb <= t.lgn; ++lb) {
-      int nz = 0;
-      for (int i = 0; i < n; ++i) nz += space[(size_t)lb * n + i] != 0.0;
-      t.support[lb] = nz;
+      for (int i = 0; i < n; ++i)
+        if (space[(size_t)lb * n + i] != 0.0) t.nz[lb].push_back(i);
+      t.support[lb] = (int)t.nz[lb].size();
+    }
+    t.conv_r.assign(t.lgn + 1, 0);
+    for (int lb = 1; lb < t.lgn; ++lb) {
+      if (t.support[lb] != n) continue;
+      const double* f = freq + (size_t)lb * n;
+      int r = 0;
+      for (int d = 1; d <= n / 2; ++d)
+        if (std::fabs(f[d]) > 1e-14 * std::fabs(f[0]) || std::fabs(f[n - d]) > 1e-14 * std::fabs(f[0])) r = d;
+      t.conv_r[lb] = (r >= 1 && r <= 4) ? r : 0;
     }
     c->tables.push_back(t);
   });

@@ -148,6 +148,79 @@ __global__ void k_estimate_dense_fs(const cplx<T>* __restrict__ A, int lgN, int 
   if (lane == 0 && best) atomicMax(peak, best);
 }
 
+// Estimation from the dense spectrum (B < N with an untruncated window,
+// S(B) = N): the hashed spectrum is the spectrum of g . y (y = permuted x,
+// g = space window), i.e. the circular convolution of y^ with g^ = N F
+// (F = freq row, DC-normalised; g sums to N), sampled at k w:
+//   Z^[k1, k2] = sum_{d1, d2} F[d1] F[d2] y^[k1 w - d1, k2 w - d2],
+//   y^[f1, f2] = e^{+2 pi i (f1 s1i t1 + f2 s2i t2) / N} x^[s1i f1, s2i f2].
+// With q = s i = w u + o (the bucket u and offset o of _estimate_arrays,
+// engine.py:163-177) and e = o + d, the reference's value
+// Z^[u_i, u_j] e^{-2 pi i (t1 i + t2 j)/N} / (F[o_i] F[o_j]) is exactly
+//   sum_{d1, d2} F[d1] F[d2] tw[t1 s1i e1 + t2 s2i e2] x^[i - s1i e1, j - s2i e2] / gain.
+// F[d] vanishes (below 1e-14, roundoff of the host table) for |d| > R, R = 2
+// at w = 2: 25 gathers of x^ per (candidate, loop) instead of a fold of x and
+// a B x B FFT per loop.  Same usable/gain rule as k_estimate.
+template <typename T, int R>
+__global__ void k_estimate_conv(const cplx<T>* __restrict__ xhat, int nloops,
+                                const int32_t* __restrict__ keys, const unsigned* __restrict__ m_dev,
+                                const Perm* __restrict__ perms, int lgN, int lgB,
+                                const T* __restrict__ freq, const cplx<T>* __restrict__ tw,
+                                double gain_floor, cplx<T>* __restrict__ vals,
+                                uint8_t* __restrict__ usable, long stride) {
+  pdl_wait();
+  using C = cplx<T>;
+  constexpr int K = 2 * R + 1;
+  const long m = *m_dev;
+  const unsigned maskN = (1u << lgN) - 1u;
+  const int lgw = lgN - lgB;
+  const unsigned hw = (unsigned)((1 << lgw) / 2);
+  const long total = m * nloops;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total;
+       e += (long)gridDim.x * blockDim.x) {
+    const int l = (int)(e / m);
+    const long idx = e - (long)l * m;
+    const Perm p = perms[l];
+    const unsigned key = (unsigned)keys[idx];
+    const unsigned i = key >> lgN, j = key & maskN;
+    const unsigned qi = (p.s1 * i) & maskN, qj = (p.s2 * j) & maskN;
+    const unsigned ui = (qi + hw) >> lgw, uj = (qj + hw) >> lgw;
+    const unsigned oi = (qi - (ui << lgw)) & maskN, oj = (qj - (uj << lgw)) & maskN;
+    const T gain = freq[oi] * freq[oj];
+    const bool ok = (double)fabs(gain) >= gain_floor;
+    C v = mk<T>(0, 0);
+    if (ok) {
+      unsigned rowo[K];
+      C c2[K];
+      unsigned colv[K];
+#pragma unroll
+      for (int d = 0; d < K; ++d) {
+        const unsigned e1 = (oi + (unsigned)(d - R)) & maskN;
+        rowo[d] = ((i - p.s1i * e1) & maskN) << lgN;
+        const unsigned e2 = (oj + (unsigned)(d - R)) & maskN;
+        colv[d] = (j - p.s2i * e2) & maskN;
+        const T f2 = freq[(unsigned)(d - R) & maskN];
+        const C t2 = tw[(p.t2 * p.s2i * e2) & maskN];
+        c2[d] = mk<T>(f2 * t2.x, f2 * t2.y);
+      }
+      C acc = mk<T>(0, 0);
+#pragma unroll
+      for (int d1 = 0; d1 < K; ++d1) {
+        C inner = mk<T>(0, 0);
+#pragma unroll
+        for (int d2 = 0; d2 < K; ++d2) inner = cadd(inner, cmul(c2[d2], xhat[(size_t)rowo[d1] + colv[d2]]));
+        const unsigned e1 = (oi + (unsigned)(d1 - R)) & maskN;
+        const T f1 = freq[(unsigned)(d1 - R) & maskN];
+        const C t1 = tw[(p.t1 * p.s1i * e1) & maskN];
+        acc = cadd(acc, cmul(mk<T>(f1 * t1.x, f1 * t1.y), inner));
+      }
+      v = mk<T>(acc.x / gain, acc.y / gain);
+    }
+    vals[(size_t)l * stride + idx] = v;
+    usable[(size_t)l * stride + idx] = ok ? 1 : 0;
+  }
+}
+
 template <typename T>
 __device__ __forceinline__ void isort(T* a, int n) {
   for (int i = 1; i < n; ++i) {

@@ -10,6 +10,7 @@ template void dense_fft<double, double2>(sfft2d_ctx*, const double2*, cplx<doubl
                                  const cplx<double>*, cudaStream_t, unsigned*);
 template cplx<double>* dense_fft_front<double, double2>(sfft2d_ctx*, const double2*, int, const cplx<double>*,
                                                  cudaStream_t, unsigned*);
+template void dense_fft_xhat<double>(sfft2d_ctx*, cplx<double>*, int, const cplx<double>*, cudaStream_t);
 template void dense_fft_mags<double>(sfft2d_ctx*, double*, unsigned long long*, int, const cplx<double>*,
                                   cudaStream_t);
 }  // namespace sfft

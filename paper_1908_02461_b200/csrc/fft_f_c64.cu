@@ -10,6 +10,7 @@ template void dense_fft<float, float2>(sfft2d_ctx*, const float2*, cplx<float>*,
                                  const cplx<float>*, cudaStream_t, unsigned*);
 template cplx<float>* dense_fft_front<float, float2>(sfft2d_ctx*, const float2*, int, const cplx<float>*,
                                                  cudaStream_t, unsigned*);
+template void dense_fft_xhat<float>(sfft2d_ctx*, cplx<float>*, int, const cplx<float>*, cudaStream_t);
 template void dense_fft_mags<float>(sfft2d_ctx*, float*, unsigned long long*, int, const cplx<float>*,
                                   cudaStream_t);
 // fp64 only: on c3 (4096^2) skipping the 268 MB complex128 x_hat write saves

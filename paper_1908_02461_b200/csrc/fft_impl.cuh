@@ -168,6 +168,23 @@ cplx<T>* dense_fft_front(sfft2d_ctx* c, const Tin* x, int lgN, const cplx<T>* tw
 }
 
 template <typename T>
+void dense_fft_xhat(sfft2d_ctx* c, cplx<T>* out, int lgN, const cplx<T>* tw, cudaStream_t st) {
+  using C = cplx<T>;
+  const int N = 1 << lgN;
+  const FftPlan2D pl = plan_fft2d<T>(lgN);
+  const double nn = (double)N * N;
+  C* scratch = (C*)ws(c, "fft_scratch", (size_t)N * N * sizeof(C));
+  pre(c, st);
+  with_lg<5, 7>(pl.lgL2, [&](auto LGc) {
+    constexpr int LG2 = decltype(LGc)::value;
+    kl(k_fftcB<T, true, false, LG2>, dim3(N >> pl.lgccB, 1 << pl.lgL1, 1), pl.thrB, pl.smem_B, st,
+       (const C*)scratch, out, (T*)nullptr, (unsigned long long*)nullptr, pl.lgL1, pl.lgL2, pl.lgccB,
+       tw, lgN);
+  });
+  post(c, "k_fftcB", st, 2 * nn * sizeof(C));
+}
+
+template <typename T>
 void dense_fft_mags(sfft2d_ctx* c, T* mags, unsigned long long* peak, int lgN, const cplx<T>* tw,
                     cudaStream_t st) {
   using C = cplx<T>;

@@ -38,6 +38,8 @@ template <typename T, typename Tin>
 cplx<T>* dense_fft_front(sfft2d_ctx* c, const Tin* x, int lgN, const cplx<T>* tw, cudaStream_t st,
                          unsigned* nonfinite);
 template <typename T>
+void dense_fft_xhat(sfft2d_ctx* c, cplx<T>* out, int lgN, const cplx<T>* tw, cudaStream_t st);
+template <typename T>
 void dense_fft_mags(sfft2d_ctx* c, T* mags, unsigned long long* peak, int lgN, const cplx<T>* tw,
                     cudaStream_t st);
 

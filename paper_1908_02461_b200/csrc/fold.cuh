@@ -24,6 +24,7 @@
 #pragma once
 #include "common.cuh"
 #include "fft.cuh"
+#include <cooperative_groups.h>
 
 namespace sfft {
 
@@ -253,6 +254,155 @@ k_fold(const Tin* __restrict__ x, const T* __restrict__ space, PermPack pp, int 
       }
     }
   }
+}
+
+// Multi-loop fold for B < 512 (the SFFT's L location / estimation loops, all
+// from one read of x): CTA = (column tile of TWC <= 512 columns, bucket row
+// rho, row chunk z).  Each thread owns 2 adjacent columns for the whole CTA,
+// so the row sums u_l(c) = sum_r wr_l[r] x[r, c] stay in registers and are
+// scaled by wc_l(c) once at the end; rows are unrolled by UNR with all UNR
+// 16-byte loads issued before the first FMA (UNR loads in flight per thread —
+// k_fold's per-column-block loop kept 2, which held the 8-loop c3 fold at
+// 0.23 of HBM).  The TWC / B aliases of each kappa inside the tile are summed
+// in shared memory in a fixed order; the tile's row of the bucket grid goes
+// to partial (tile, z) [Zp][NL][B][B] (natural order), or straight to the
+// grid when Zp == 1.
+template <typename Tin, typename T, int NL, int UNR>
+__global__ void __launch_bounds__(256)
+k_fold_ml(const Tin* __restrict__ x, const T* __restrict__ space, PermPack pp, int nloops,
+          int lgN, int lgB, int TWC, int rpc, bool natural, int zp, cplx<T>* __restrict__ dst,
+          unsigned* __restrict__ nonfinite = nullptr) {
+  pdl_wait();
+  using C = cplx<T>;
+  __shared__ T s_w[NL * kFoldMaxRows];
+  __shared__ int s_rows[kFoldMaxRows];
+  __shared__ int s_nnz;
+  extern __shared__ __align__(16) unsigned char smem_raw[];   // [NL][TWC] alias reduction
+  const int N = 1 << lgN, B = 1 << lgB;
+  const unsigned maskN = (unsigned)N - 1u, maskB = (unsigned)B - 1u;
+  const int tile = blockIdx.x, rho = blockIdx.y, z = blockIdx.z;
+  const int aliases = N >> lgB;
+  const int j0 = z * rpc;
+  const int cnt = min(rpc, aliases - j0);
+  const int tid = threadIdx.x;
+  for (int jj = tid; jj < cnt; jj += blockDim.x) {
+    const unsigned r = (unsigned)(rho + (j0 + jj) * B);
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {
+      T w = (T)0;
+      if (l < nloops) w = __ldg(space + ((pp.p[l].s1i * (r - pp.p[l].t1)) & maskN));
+      s_w[l * kFoldMaxRows + jj] = w;
+    }
+  }
+  __syncthreads();
+  if (tid < 32) {
+    int base = 0;
+    for (int c0 = 0; c0 < cnt; c0 += 32) {
+      const int jj = c0 + tid;
+      bool nz = false;
+      if (jj < cnt) {
+#pragma unroll
+        for (int l = 0; l < NL; ++l) nz |= (s_w[l * kFoldMaxRows + jj] != (T)0);
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, nz);
+      if (nz) s_rows[base + __popc(bal & ((1u << tid) - 1u))] = jj;
+      base += __popc(bal);
+    }
+    if (tid == 0) s_nnz = base;
+  }
+  __syncthreads();
+  const int nnz = s_nnz;
+  const int cc = tid * 2;                       // column inside the tile
+  const bool act = cc < TWC;
+  const int c0 = tile * TWC + cc;
+  C u[NL][2];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) { u[l][0] = mk<T>(0, 0); u[l][1] = mk<T>(0, 0); }
+  bool bad = false;   // NaN/Inf among the samples read (as_complex_matrix, corefft.py:49-50)
+  if (act) {
+    const Tin* col = x + c0;
+    for (int i = 0; i < nnz; i += UNR) {
+      C v[UNR][2];
+      int jr[UNR];
+#pragma unroll
+      for (int k = 0; k < UNR; ++k) {
+        jr[k] = (i + k < nnz) ? s_rows[i + k] : -1;
+        if (jr[k] >= 0) {
+          const size_t r = (size_t)(rho + (j0 + jr[k]) * B);
+          ColLoad<Tin, T, 2>::ld(col + (r << lgN), v[k]);
+        } else {
+          v[k][0] = mk<T>(0, 0);
+          v[k][1] = mk<T>(0, 0);
+        }
+      }
+      if (nonfinite) {
+#pragma unroll
+        for (int k = 0; k < UNR; ++k)
+          bad |= !isfinite(v[k][0].x) || !isfinite(v[k][0].y) || !isfinite(v[k][1].x) ||
+                 !isfinite(v[k][1].y);
+      }
+#pragma unroll
+      for (int k = 0; k < UNR; ++k) {
+        if (jr[k] < 0) break;
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+          const T wr = s_w[l * kFoldMaxRows + jr[k]];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            u[l][q].x = fma(wr, v[k][q].x, u[l][q].x);
+            u[l][q].y = fma(wr, v[k][q].y, u[l][q].y);
+          }
+        }
+      }
+    }
+  }
+  if (nonfinite && __any_sync(0xffffffffu, bad) && (tid & 31) == 0) atomicOr(nonfinite, 1u);
+  C* red = reinterpret_cast<C*>(smem_raw);
+  if (act) {
+#pragma unroll
+    for (int l = 0; l < NL; ++l)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        T w = (T)0;
+        if (l < nloops) w = __ldg(space + ((pp.p[l].s2i * ((unsigned)(c0 + q) - pp.p[l].t2)) & maskN));
+        red[l * TWC + cc + q] = mk<T>(w * u[l][q].x, w * u[l][q].y);
+      }
+  }
+  __syncthreads();
+  const size_t BB = (size_t)B * B;
+  const int reps = TWC >> lgB;
+  C* resv = red + (size_t)NL * TWC;             // [nloops][B] row of this tile
+  for (int e = tid; e < nloops * B; e += blockDim.x) {
+    const int l = e >> lgB;
+    const int kap = e & (B - 1);
+    C s = mk<T>(0, 0);
+    for (int a = 0; a < reps; ++a) s = cadd(s, red[l * TWC + kap + (a << lgB)]);
+    resv[e] = s;
+  }
+  // the cluster's tiles (consecutive along x) are summed through distributed
+  // shared memory in rank order; each CTA of the cluster emits a slice
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int csz = (int)cl.num_blocks();
+  const int rank = (int)cl.block_rank();
+  cl.sync();
+  const int tot = nloops * B;
+  const int per = (tot + csz - 1) / csz;
+  for (int e = rank * per + tid; e < min(tot, (rank + 1) * per); e += blockDim.x) {
+    C s = mk<T>(0, 0);
+    for (int q = 0; q < csz; ++q) s = cadd(s, cl.map_shared_rank(resv, q)[e]);
+    const int l = e >> lgB;
+    const int kap = e & (B - 1);
+    if (zp == 1) {
+      const unsigned ra = natural ? (unsigned)rho : (pp.p[l].s1i * ((unsigned)rho - pp.p[l].t1)) & maskB;
+      const unsigned cb = natural ? (unsigned)kap : (pp.p[l].s2i * ((unsigned)kap - pp.p[l].t2)) & maskB;
+      dst[l * BB + (size_t)ra * B + cb] = s;
+    } else {
+      const size_t part = (size_t)(tile / csz) * gridDim.z + z;
+      dst[(part * nloops + l) * BB + (size_t)rho * B + kap] = s;
+    }
+  }
+  cl.sync();   // peers have finished reading this CTA's shared memory
 }
 
 // Ring-buffered single-loop fold for B < TW (= 512 columns per tile, 256
