@@ -33,6 +33,7 @@
 #include "npyrng.h"
 #include "select.cuh"
 #include "vote.cuh"
+#include "passconv.cuh"
 
 using namespace sfft;
 
@@ -1323,6 +1324,11 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     cudaEvent_t ready = nullptr;   // the pass's maxima list is complete
   };
   static const bool pipe_on = getenv("SFFT2D_NO_PIPELINE") == nullptr;
+  // the B = N/2 pass from the dense spectrum: x_hat stored (not factored),
+  // untruncated 5-tap window, 512 <= B <= 2048 (SFFT2D_NO_PASSCONV=1: fold + FFT)
+  static const bool passconv_on = getenv("SFFT2D_NO_PASSCONV") == nullptr;
+  const bool passconv_ok = passconv_on && !factored && n >= 1024 && n <= 4096 &&
+                           tb.conv_r[lgN - 1] == 2 && (size_t)3 * n * sizeof(C) <= 200 * 1024;
   int ev_next = 0;
   auto enqueue_pass = [&](int bb, int pi) -> Ticket {
     Ticket tk;
@@ -1365,6 +1371,28 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       } else {
         seq = lmax_tuner<T>(c, M, lgb, peakM, cf.mag_floor, ml, cnt, st, true, p.s1i, p.s2i, p.s2);
       }
+    } else if (2 * bb == n && passconv_ok) {
+      // B = N/2 from the dense spectrum (k_pass_conv): the dense FFT is
+      // computed here, one pass early, and serves the B = N passes after it
+      ensure_xhat(true);
+      T* mg = (T*)ws(c, "grid_mag", BB * sizeof(T));
+      unsigned long long* pk = (unsigned long long*)ws(c, "gpeak", 16);
+      ck(cudaMemsetAsync(pk, 0, 16, st), "memset");
+      const T* freq = (const T*)tb.freq[prec_of<T>()] + ((size_t)lgb << lgN);
+      const C* tw = (const C*)tb.tw[prec_of<T>()];
+      constexpr int RB = sizeof(T) == 4 ? 4 : 2;
+      const size_t sm = (size_t)3 * n * sizeof(C);
+      pre(c, st);
+      if (bb == 2048)
+        kl(k_pass_conv<T, 8, RB, 3>, bb / RB, 256, sm, st, (const C*)xhat, lgN, p, freq, tw, mg, pk);
+      else if (bb == 1024)
+        kl(k_pass_conv<T, 4, RB, 3>, bb / RB, 256, sm, st, (const C*)xhat, lgN, p, freq, tw, mg, pk);
+      else
+        kl(k_pass_conv<T, 2, RB, 3>, bb / RB, 256, sm, st, (const C*)xhat, lgN, p, freq, tw, mg, pk);
+      post(c, "k_pass_conv", st,
+           (double)(bb / RB) * (2 * RB + 3) * n * sizeof(C) + (double)BB * sizeof(T));
+      seq = lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, ml, cnt, st, true, 1u, 1u, 1u, nullptr, nullptr,
+                          nullptr, true);
     } else if (BB * sizeof(C) <= (size_t)kSmall2DBytes) {
       C* y = (C*)ws(c, "fold_y", BB * sizeof(C));
       FoldOut fo{y, 1};
