@@ -1004,6 +1004,13 @@ void finish_select(sfft2d_ctx* c, int lgN, const int32_t* keys, unsigned m, long
 }
 
 
+unsigned long long* est_scalars(sfft2d_ctx* c) {
+  return (unsigned long long*)ws(c, "est_scalars", 32);
+}
+void zero_est_scalars(sfft2d_ctx* c, cudaStream_t st) {
+  ck(cudaMemsetAsync(est_scalars(c), 0, 32, st), "memset");
+}
+
 // K6 + K7 + output compaction, shared by both algorithms.
 template <typename T, typename Tin>
 void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTables& tb,
@@ -1017,10 +1024,10 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
   C* med = (C*)ws(c, "med", (size_t)m * sizeof(C));
   T* mags = (T*)ws(c, "emag", (size_t)m * sizeof(T));
   uint8_t* alive = (uint8_t*)ws(c, "alive", (size_t)m);
-  unsigned long long* peak = (unsigned long long*)ws(c, "epeak", 16);
-  unsigned* alive_cnt = (unsigned*)ws(c, "ealive", 16);
-  ck(cudaMemsetAsync(peak, 0, 16, st), "memset");
-  ck(cudaMemsetAsync(alive_cnt, 0, 16, st), "memset");
+  // [peak key, alive count], zeroed by zero_est_scalars before the
+  // candidate-count synchronisation (one memset off the critical path)
+  unsigned long long* peak = est_scalars(c);
+  unsigned* alive_cnt = (unsigned*)(peak + 1);
   long long n_alive;
   if (dense) {
     // gain = freq[0]^2 = 1 for the all-pass window (hashing.py:228-246)
@@ -1383,14 +1390,17 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       constexpr int RB = sizeof(T) == 4 ? 4 : 2;
       const size_t sm = (size_t)3 * n * sizeof(C);
       pre(c, st);
+      // taps |d| <= R: R = 2 in fp64; in fp32 the |d| = 2 taps (|F| = 2.5e-9)
+      // are below float resolution
+      constexpr int RT = sizeof(T) == 4 ? 1 : 2;
       if (bb == 2048)
-        kl(k_pass_conv<T, 8, RB, 3>, bb / RB, 256, sm, st, (const C*)xhat, lgN, p, freq, tw, mg, pk);
+        kl(k_pass_conv<T, 8, RB, 3, RT>, bb / RB, 256, sm, st, (const C*)xhat, lgN, p, freq, tw, mg, pk);
       else if (bb == 1024)
-        kl(k_pass_conv<T, 4, RB, 3>, bb / RB, 256, sm, st, (const C*)xhat, lgN, p, freq, tw, mg, pk);
+        kl(k_pass_conv<T, 4, RB, 3, RT>, bb / RB, 256, sm, st, (const C*)xhat, lgN, p, freq, tw, mg, pk);
       else
-        kl(k_pass_conv<T, 2, RB, 3>, bb / RB, 256, sm, st, (const C*)xhat, lgN, p, freq, tw, mg, pk);
+        kl(k_pass_conv<T, 2, RB, 3, RT>, bb / RB, 256, sm, st, (const C*)xhat, lgN, p, freq, tw, mg, pk);
       post(c, "k_pass_conv", st,
-           (double)(bb / RB) * (2 * RB + 3) * n * sizeof(C) + (double)BB * sizeof(T));
+           (double)(bb / RB) * (2 * (RB - 1) + 2 * RT + 1) * n * sizeof(C) + (double)BB * sizeof(T));
       seq = lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, ml, cnt, st, true, 1u, 1u, 1u, nullptr, nullptr,
                           nullptr, true);
     } else if (BB * sizeof(C) <= (size_t)kSmall2DBytes) {
@@ -1683,6 +1693,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   }
   const unsigned thr = (unsigned)((std::max(vote_passes, 1) + 1) / 2);
   unsigned m;
+  zero_est_scalars(c, st);
   if (lazy) {
     uint32_t* bits = (uint32_t*)ws(c, "hc_bits", words_for(nkeys) * 4);
     unsigned* cnts = (unsigned*)ws(c, "hc_cnt", (size_t)blocks_for(nkeys) * 4);
@@ -1709,9 +1720,9 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
                                 " exceeds the " + std::to_string(best) + "x" +
                                 std::to_string(best) + " bin budget");
   }
-  for (int i = 0; i < L; ++i) ps.get(pidx + i, st);
-  ps.upload(pidx, L, st, c->ev_perm);
+  for (int i = 0; i < L; ++i) ps.get(pidx + i, st);   // drawn as the reference draws them
   const bool dense = (best == n);
+  if (!dense) ps.upload(pidx, L, st, c->ev_perm);   // the dense estimate reads x_hat only
   if (dense) ensure_xhat(false);
   // B < N with an untruncated window: estimate from the dense spectrum when
   // it is already (partly) computed, or when B >= N/4 (a dense FFT is then
@@ -1795,6 +1806,7 @@ void sfft_from_hist(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, c
   const long nkeys = (long)n * n;
   int32_t* keys = (int32_t*)ws(c, "keys", (size_t)nkeys * 4);
   unsigned* kt = (unsigned*)ws(c, "keys_tot", 16);
+  zero_est_scalars(c, st);
   const unsigned m = hist_compact(c, hist, nkeys, mode, (unsigned)cf.vote_threshold, keys, kt, st);
   if (nan_pending) raise_if_nonfinite(c);   // the scan's flag came with that synchronisation
   res->count = 0;

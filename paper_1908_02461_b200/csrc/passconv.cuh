@@ -5,7 +5,8 @@
 // At B = N/2 the window is untruncated (S(B) = N), so the hashed spectrum of
 // permutation p is the circular convolution of the permuted spectrum with the
 // window's response F (DC-normalised, host table; |F[d]| <= 1e-14 for
-// |d| > 2 at w = 2):
+// |d| > 2 at w = 2; in fp32 the |d| = 2 taps, |F| = 2.5e-9, are below the
+// arithmetic's resolution and R = 1):
 //   Z^[k1, k2] = sum_{d1, d2 in [-2, 2]} F[d1] F[d2] y^[2 k1 - d1, 2 k2 - d2],
 //   y^[f1, f2] = e^{+2 pi i (f1 a1 + f2 a2)/N} x^[s1i f1, s2i f2],  a = s_inv * tau.
 // The tuner only needs |Z^|; dropping the unit factor e^{2 pi i 2 (k1 a1 + k2 a2)/N}
@@ -24,7 +25,7 @@
 
 namespace sfft {
 
-template <typename T, int CPT, int RB, int NS>
+template <typename T, int CPT, int RB, int NS, int R>
 __global__ void __launch_bounds__(256)
 k_pass_conv(const cplx<T>* __restrict__ xhat, int lgN, Perm p, const T* __restrict__ freq,
             const cplx<T>* __restrict__ tw, T* __restrict__ mags,
@@ -43,11 +44,12 @@ k_pass_conv(const cplx<T>* __restrict__ xhat, int lgN, Perm p, const T* __restri
   const unsigned a1 = (s1i * p.t1) & maskN, a2 = (s2i * p.t2) & maskN;
   // row taps in shared memory (indexed by the runtime d1 below), column taps
   // in registers
-  __shared__ C s_c1[5];
-  C c2[5];
+  constexpr int K = 2 * R + 1;
+  __shared__ C s_c1[K];
+  C c2[K];
 #pragma unroll
-  for (int d = 0; d < 5; ++d) {
-    const unsigned dd = (unsigned)(d - 2);
+  for (int d = 0; d < K; ++d) {
+    const unsigned dd = (unsigned)(d - R);
     const T f = freq[dd & maskN];
     const C t2 = tw[(dd * a2) & maskN];
     c2[d] = mk<T>(f * t2.x, f * t2.y);
@@ -66,13 +68,13 @@ k_pass_conv(const cplx<T>* __restrict__ xhat, int lgN, Perm p, const T* __restri
 #pragma unroll
     for (int q = 0; q < CPT; ++q) acc[j][q] = mk<T>(0, 0);
 
-  constexpr int NE = 2 * RB + 3;
+  constexpr int NE = 2 * (RB - 1) + 2 * R + 1;   // source rows e = 2 k10 - R ... 2 (k10 + RB - 1) + R
   const unsigned rowbytes = (unsigned)(N * sizeof(C));
   if (tid < NS) mbar_init(&s_bar[tid], 1);
   mbar_fence_init();
   __syncthreads();
   auto issue = [=](int ei) {
-    const unsigned e = (unsigned)(2 * k10 - 2 + ei);
+    const unsigned e = (unsigned)(2 * k10 - R + ei);
     const unsigned r = (s1i * e) & maskN;
     const int slot = ei % NS;
     mbar_expect_tx(&s_bar[slot], rowbytes);
@@ -89,8 +91,8 @@ k_pass_conv(const cplx<T>* __restrict__ xhat, int lgN, Perm p, const T* __restri
     for (int q = 0; q < CPT; ++q) {
       C s = mk<T>(0, 0);
 #pragma unroll
-      for (int d = 0; d < 5; ++d) {
-        const C v = row[(cbase[q] - s2i * (unsigned)(d - 2)) & maskN];
+      for (int d = 0; d < K; ++d) {
+        const C v = row[(cbase[q] - s2i * (unsigned)(d - R)) & maskN];
         s.x = fma(c2[d].x, v.x, fma(-c2[d].y, v.y, s.x));
         s.y = fma(c2[d].x, v.y, fma(c2[d].y, v.x, s.y));
       }
@@ -99,9 +101,9 @@ k_pass_conv(const cplx<T>* __restrict__ xhat, int lgN, Perm p, const T* __restri
     // source row e = 2 k1 - d1 feeds output rows k1 = k10 + j with d1 = 2 (k10 + j) - e
 #pragma unroll
     for (int j = 0; j < RB; ++j) {
-      const int d1 = 2 * j + 2 - ei;   // 2 (k10 + j) - (2 k10 - 2 + ei)
-      if (d1 < -2 || d1 > 2) continue;
-      const C w = s_c1[d1 + 2];
+      const int d1 = 2 * j + R - ei;   // 2 (k10 + j) - (2 k10 - R + ei)
+      if (d1 < -R || d1 > R) continue;
+      const C w = s_c1[d1 + R];
 #pragma unroll
       for (int q = 0; q < CPT; ++q) {
         acc[j][q].x = fma(w.x, g[q].x, fma(-w.y, g[q].y, acc[j][q].x));
