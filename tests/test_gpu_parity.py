@@ -27,16 +27,34 @@ def _need_gpu():
 
 
 def _close_values(got: dict, ref: dict, tol: float):
-    assert set(got) == set(ref), (len(set(got) - set(ref)), len(set(ref) - set(got)))
+    """Same support and values within tol.  fp32 only: a coefficient may be
+    on one side alone when its magnitude sits within the value tolerance of a
+    selection boundary of the reference's float64 median (the prune level
+    prune_rel * max|v|, engine.py:249, or the smallest kept magnitude of a
+    top-k cut): the fp32 median is within tol of the float64 one, so the
+    comparison against that boundary can go either way — in noise-dominated
+    outputs with tens of thousands of coefficients (c5 k=1024) a few do."""
+    only_got, only_ref = set(got) - set(ref), set(ref) - set(got)
+    if tol < 1e-6 or not ref:
+        assert not only_got and not only_ref, (len(only_got), len(only_ref))
     if not ref:
         return
     vmax = max(abs(v) for v in ref.values())
+    if only_got or only_ref:
+        bounds = [1e-3 * vmax, min(abs(v) for v in ref.values())]
+        for key in only_got | only_ref:
+            m = abs(got[key]) if key in got else abs(ref[key])
+            assert any(abs(m - b) <= 2 * tol * b for b in bounds), (key, m, bounds)
+        assert len(only_got) + len(only_ref) <= max(2, len(ref) // 10000), (len(only_got), len(only_ref))
     worst = 0.0
     for key, v in ref.items():
+        if key not in got:
+            continue
         err = abs(got[key] - v) / max(abs(v), 1e-3 * vmax, 1e-300)
         worst = max(worst, err)
     assert worst <= tol, worst
-    _check_order(list(got), ref, tol)
+    common = [key for key in got if key in ref]
+    _check_order(common, {key: ref[key] for key in ref if key in got}, tol)
 
 
 def _check_order(got_keys: list, ref: dict, tol: float):
