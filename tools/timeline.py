@@ -79,5 +79,16 @@ for nm, (cnt, dur) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
 gaps.sort(reverse=True)
 big = [g for g in gaps if g[0] > 2.0]
 print(f"gaps > 2 us: {len(big) / reps:.1f}/transform totalling {sum(g for g, _ in big) / reps:.1f} us")
-for g, nm in gaps[:12]:
+for g, nm in gaps[:6]:
     print(f"  {g:7.1f} us before {nm}")
+# gaps by the position of the following kernel inside a transform (the last
+# transform's sequence; memsets/memcpys in between count as idle)
+per = len(ks) // reps
+seq = ks[-per:]
+print("idle before each kernel of the last transform (> 1 us):")
+prev_end = None
+for i, e in enumerate(seq):
+    nm = e["name"].split("(")[0].split("<")[0].replace("void ", "").replace("sfft::", "")
+    if prev_end is not None and e["ts"] - prev_end > 1.0:
+        print(f"  [{i:2d}] {e['ts'] - prev_end:6.1f} us before {nm}")
+    prev_end = max(prev_end or 0, e["ts"] + e["dur"])
