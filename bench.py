@@ -63,7 +63,7 @@ ALL_LEGS = ("c3_fp64", "c1", "c2", "c4", "c5", "c3_sfft")
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--precision", choices=["fp32", "fp64"], default="fp32")
@@ -79,7 +79,6 @@ def parse():
     ap.add_argument("--c4-images", type=int, default=2048)
     ap.add_argument("--c5-ks", default="64,256,1024,4096")
     ap.add_argument("--concurrency", type=int, default=6)
-    ap.add_argument("--ref-steps", type=int, default=3)
     return ap.parse_args()
 
 
@@ -385,44 +384,8 @@ class Bench:
                    "d2h_bytes_per_step": d2h[0] // max(args.steps, 1)}
         gc.enable()
 
-        # kernel-level + transform-level roofline (instrumented pass, same workload)
-        ctx.set_profiling(True)
-        nprof = max(1, min(args.profile_steps, args.steps))
-        pe0 = torch.cuda.Event(enable_timing=True)
-        pe1 = torch.cuda.Event(enable_timing=True)
-        pe0.record(self.stream)
-        for _ in range(nprof):
-            step(x_dev)
-        pe1.record(self.stream)
-        torch.cuda.synchronize()
-        rep = ctx.profile_report()
-        ctx.set_profiling(False)
-        prof_ms = pe0.elapsed_time(pe1)
-        peak, peak_kind = peaks()
-        roofline = None
-        if rep:
-            name, (cnt, tms, tbytes) = max(rep.items(), key=lambda kv: kv[1][1])
-            achieved = (tbytes / cnt) / (tms / cnt / 1e3) / 1e9
-            traffic = kernel_traffic(f"c3/{args.precision}").get(name)
-            bytes_tr = sum(v[2] for v in rep.values()) / nprof
-            roofline = {
-                "bound": "hbm", "kernel": name, "achieved": achieved, "peak": peak,
-                "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                "traffic_source": (f"profiles/kernel_traffic.json c3/{args.precision} (ncu --set full)"
-                                   if traffic is not None else None),
-                "alg_bytes_per_launch": tbytes / cnt, "launches_per_step": cnt / nprof,
-                "avg_launch_us": tms / cnt * 1e3, "share_of_step": tms / prof_ms,
-                "transform": {
-                    "alg_bytes_per_transform": bytes_tr,
-                    "achieved_in_flight": bytes_tr * value / self.world / 1e9,
-                    "frac_in_flight": bytes_tr * value / self.world / 1e9 / peak,
-                    "achieved_single": bytes_tr / (latency["ms_per_transform"] / 1e3) / 1e9,
-                    "frac_single": bytes_tr / (latency["ms_per_transform"] / 1e3) / 1e9 / peak,
-                    "note": "sum of every kernel's algorithmic bytes (DESIGN.md §3) per transform"},
-            }
-        kernels = {k: {"launches_per_step": v[0] / nprof, "ms_per_step": v[1] / nprof,
-                       "GBps": (v[2] / v[1] / 1e6) if v[1] > 0 else None}
-                   for k, v in sorted(rep.items(), key=lambda kv: -kv[1][1])[:10]}
+        roofline, kernels = self.roofline(step, x_dev, f"c3/{args.precision}", value,
+                                          latency["ms_per_transform"])
 
         # dense cuFFT of the same image, for context only
         xc = x_dev.to(torch.complex64)
@@ -440,6 +403,61 @@ class Bench:
         return dict(value=value, ms_max=ms_max, launches=launches, clocks=clocks, latency=latency,
                     e2e=e2e, roofline=roofline, kernels=kernels, parity=parity,
                     cufft_ms=c0.elapsed_time(c1) / 10, state=state, conc=conc)
+
+    def roofline(self, step, x, traffic_key, value, single_ms):
+        """Kernel-level + transform-level roofline from an instrumented pass of
+        the same workload (library per-launch CUDA events on the launching
+        stream, algorithmic bytes per DESIGN.md §3)."""
+        from paper_1908_02461_b200 import _native
+        torch, args = self.torch, self.args
+        ctx = _native.context(self.local)
+        ctx.set_profiling(True)
+        nprof = max(1, min(args.profile_steps, args.steps))
+        pe0 = torch.cuda.Event(enable_timing=True)
+        pe1 = torch.cuda.Event(enable_timing=True)
+        pe0.record(self.stream)
+        for _ in range(nprof):
+            step(x)
+        pe1.record(self.stream)
+        torch.cuda.synchronize()
+        rep = ctx.profile_report()
+        ctx.set_profiling(False)
+        prof_ms = pe0.elapsed_time(pe1)
+        peak, peak_kind = peaks()
+        if not rep:
+            return None, {}
+        # dominant kernel of the HBM roofline: the one moving the most
+        # algorithmic bytes per step (the per-launch event brackets add a few
+        # microseconds to every launch, which would rank the latency-bound
+        # small kernels first by time; the longest kernel is reported beside it)
+        name, (cnt, tms, tbytes) = max(rep.items(), key=lambda kv: kv[1][2])
+        tname, (tcnt, ttms, ttbytes) = max(rep.items(), key=lambda kv: kv[1][1])
+        achieved = (tbytes / cnt) / (tms / cnt / 1e3) / 1e9
+        traffic = kernel_traffic(traffic_key).get(name)
+        bytes_tr = sum(v[2] for v in rep.values()) / nprof
+        roof = {
+            "bound": "hbm", "kernel": name, "selection": "most algorithmic bytes per step",
+            "longest_kernel": {"kernel": tname, "share_of_step": ttms / prof_ms,
+                               "avg_launch_us": ttms / tcnt * 1e3,
+                               "achieved_GBps": (ttbytes / tcnt) / (ttms / tcnt / 1e3) / 1e9},
+            "achieved": achieved, "peak": peak,
+            "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "traffic_source": (f"profiles/kernel_traffic.json {traffic_key} (ncu --set full)"
+                               if traffic is not None else None),
+            "alg_bytes_per_launch": tbytes / cnt, "launches_per_step": cnt / nprof,
+            "avg_launch_us": tms / cnt * 1e3, "share_of_step": tms / prof_ms,
+            "transform": {
+                "alg_bytes_per_transform": bytes_tr,
+                "achieved_in_flight": bytes_tr * value / self.world / 1e9,
+                "frac_in_flight": bytes_tr * value / self.world / 1e9 / peak,
+                "achieved_single": bytes_tr / (single_ms / 1e3) / 1e9,
+                "frac_single": bytes_tr / (single_ms / 1e3) / 1e9 / peak,
+                "note": "sum of every kernel's algorithmic bytes (DESIGN.md §3) per transform"},
+        }
+        kernels = {k: {"launches_per_step": v[0] / nprof, "ms_per_step": v[1] / nprof,
+                       "GBps": (v[2] / v[1] / 1e6) if v[1] > 0 else None}
+                   for k, v in sorted(rep.items(), key=lambda kv: -kv[1][1])[:10]}
+        return roof, kernels
 
     # ------------------------------------------------------------ other legs
     def leg_c3_fp64(self):
@@ -461,10 +479,12 @@ class Bench:
                                                           and args.k == 100 and args.snr == 20.0) else None
         ms, _ = self.timed(lambda: self.run_steps([xs[i % conc] for i in range(steps)], step, conc))
         lat, _ = self.timed(lambda: self.run_steps([xs[0]] * steps, step, 1))
+        value = self.world * steps / (ms / 1e3)
+        roof, kernels = self.roofline(step, xs[0], "c3/fp64", value, lat / steps)
         return {"workload": "c3 in fp64 (verification mode, the reference's float64 arithmetic)",
-                "value": self.world * steps / (ms / 1e3), "unit": UNIT, "in_flight": conc,
+                "value": value, "unit": UNIT, "in_flight": conc,
                 "steps": steps, "ms_per_transform_single": lat / steps, "parity": parity,
-                "scaling": "weak"}
+                "roofline": roof, "kernels": kernels, "scaling": "weak"}
 
     def _small_leg(self, x, fn, steps, gold, precision, conc, ats):
         torch = self.torch
@@ -603,6 +623,9 @@ class Bench:
                 "detected_k": state.detected_k, "b_estimate": state.b_estimate,
                 "passes": len(state.history), "recovered": len(res),
                 "planted_recovered": sum(1 for key in truth if key in res) / max(len(truth), 1)}
+        out["parity"] = ("device-generated images are timed here; the host-generated c5 images "
+                         "(k = 64, 256, 1024, 4096) are pinned to the reference goldens by "
+                         "tests/test_gpu_parity.py::test_c5_atsfft_vs_reference / test_c5_sweep_vs_reference")
         del buf
         return out
 
@@ -637,6 +660,13 @@ class Bench:
                 "parallelism": (f"location + estimation loops split over {self.world} rank(s)"
                                 if self.world > 1 else "1 rank"), "scaling": "strong",
                 "parity": parity}
+
+
+def c3_config(args) -> dict:
+    """The workload both arms report (BASELINE.json configs[2])."""
+    return {"workload": f"c3: ATSFFT {args.n}x{args.n} complex64, k={args.k}, {args.snr:g} dB SNR, "
+                        f"TunerConfig() defaults, est_loops={args.est_loops}, one transform per step",
+            "l2": "inputs larger than L2 (134 MB image)"}
 
 
 def cpu_baseline(x, args):
@@ -679,14 +709,13 @@ def main_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": c3["ms_max"] / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32" if args.precision == "fp32" else "f64", "data": "synthetic",
-            "config": {"workload": f"c3: ATSFFT {args.n}x{args.n} complex64, k={args.k}, "
-                                   f"{args.snr:g} dB SNR, TunerConfig() defaults, est_loops="
-                                   f"{args.est_loops}, one transform per rank per step, "
-                                   f"{c3['conc']} distinct images, {c3['conc']} transforms in flight "
-                                   f"(one CUDA stream each)",
-                       "precision": args.precision, "l2": "inputs larger than L2 (134 MB image)",
-                       "parallelism": (f"replicas: independent c3 transforms on each of {b.world} "
-                                       "rank(s) (the tuner passes are sequential)")},
+            "config": c3_config(args),
+            "execution": {"precision": args.precision,
+                          "in_flight": f"{c3['conc']} distinct images, {c3['conc']} transforms in "
+                                       "flight (one CUDA stream + native context each)",
+                          "parallelism": (f"replicas: independent c3 transforms on each of {b.world} "
+                                          "rank(s) (the ATSFFT tuner passes are sequential and c3's "
+                                          "b_estimate = N leaves nothing to split; DESIGN.md §6)")},
             "e2e": c3["e2e"], "latency": c3["latency"], "roofline": c3["roofline"],
             "cpu_baseline": cpu, "clocks": c3["clocks"], "gpu_launches": c3["launches"],
             "kernels": c3["kernels"], "parity": c3["parity"], "legs": legs,
@@ -734,45 +763,54 @@ def _refpkg_worker(job):
 
 
 def run_reference(args):
+    """The reference arm: K steps, a step = one full c3 transform by the
+    numpy oracle port, spread over the host's cores (one process each), plus
+    the UNMODIFIED reference package (baseline/_ref) on c1, c2 and c3 in the
+    same pool.  Same metric, unit and config as our arm."""
     world, rank, _ = dist_env()
     if rank != 0:
         return 0
     import multiprocessing as mp
     img = workload(args, 0)
     cores = os.cpu_count() or 1
-    procs = max(1, min(cores, 16))
-    steps = max(3, min(args.steps, args.ref_steps))
+    procs = max(1, min(cores, 16, args.steps))
+    steps = args.steps
     ctx = mp.get_context("fork")
     refpkg = None
     have_pkg = os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "sfft2d"))
     t_all = time.perf_counter()
     with ctx.Pool(procs) as pool:
+        pend = None
         if have_pkg:
-            # the unmodified reference, one process per config, in parallel
-            # (c3 alone is ~2 min on one core, so it runs once)
-            jobs = [("c1", 3), ("c2", 3), ("c3", 1)]
-            got = dict(pool.map(_refpkg_worker, jobs, chunksize=1))
+            # the unmodified reference, one process per config, alongside the
+            # port's steps (c3 alone is ~2 min on one core, so it runs once)
+            pend = pool.map_async(_refpkg_worker, [("c3", 1), ("c1", 3), ("c2", 3)], chunksize=1)
+        # warm-up: one untimed transform per worker process (W > 0)
+        if args.warmup > 0:
+            pool.map(_port_worker, [(img.x, args.est_loops, 11)] * procs, chunksize=1)
+        t0 = time.perf_counter()
+        times = pool.map(_port_worker, [(img.x, args.est_loops, 11)] * steps, chunksize=1)
+        dt = time.perf_counter() - t0
+        if pend is not None:
+            got = dict(pend.get())
             refpkg = {"source": "baseline/_ref (pip --no-deps install of /root/reference/pkg, "
                                 "unmodified), 1 process per config, 1 thread each",
                       "per_config": {k: {"seconds_per_transform": float(np.median(v)),
                                          "transforms_per_s": 1.0 / float(np.median(v)),
                                          "reps": len(v)} for k, v in got.items()}}
-        t0 = time.perf_counter()
-        for _ in range(steps):
-            pool.map(_port_worker, [(img.x, args.est_loops, 11)] * procs)
-        dt = time.perf_counter() - t0
-    value = steps * procs / dt
+    value = steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": steps, "requested_steps": args.steps, "warmup": 0,
+        "steps": steps, "warmup": args.warmup,
         "ms_per_step": dt / steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"c3: ATSFFT {args.n}x{args.n} c64, k={args.k}, {args.snr:g} dB, "
-                               f"est_loops={args.est_loops}", "parallelism": f"{procs} host processes"},
+        "config": c3_config(args),
+        "execution": f"{steps} transforms over {procs} host processes (1 thread each)",
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port",
                          "cpu_model": cpu_model(), "host_cpus": cores,
-                         "sample": f"{steps} step(s) x {procs} concurrent full c3 transforms of the "
-                                   "numpy oracle port (pocketfft FFTs), one per process"},
+                         "seconds_per_transform_median": float(np.median(times)),
+                         "sample": f"{steps} full c3 transforms of the numpy oracle port "
+                                   f"(pocketfft FFTs) on {procs} processes"},
         "reference_package": refpkg,
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": time.perf_counter() - t_all,

@@ -1399,8 +1399,9 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
         kl(k_pass_conv<T, 4, RB, 3, RT>, bb / RB, 256, sm, st, (const C*)xhat, lgN, p, freq, tw, mg, pk);
       else
         kl(k_pass_conv<T, 2, RB, 3, RT>, bb / RB, 256, sm, st, (const C*)xhat, lgN, p, freq, tw, mg, pk);
-      post(c, "k_pass_conv", st,
-           (double)(bb / RB) * (2 * (RB - 1) + 2 * RT + 1) * n * sizeof(C) + (double)BB * sizeof(T));
+      // algorithmic bytes: x_hat once + |Z| (the band halo rows re-read,
+      // (2 RB + 2 RT - 1) / (2 RB) of x_hat, are the kernel's own overhead)
+      post(c, "k_pass_conv", st, (double)n * n * sizeof(C) + (double)BB * sizeof(T));
       seq = lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, ml, cnt, st, true, 1u, 1u, 1u, nullptr, nullptr,
                           nullptr, true);
     } else if (BB * sizeof(C) <= (size_t)kSmall2DBytes) {
