@@ -591,12 +591,13 @@ class Bench:
 
     def leg_c5(self):
         """configs[4]: 16384^2 c64 (2 GiB), 20% of the k coefficients in the
-        64x64 wrap-around DC block, unit magnitude, 15 dB, ATSFFT with the
-        estimation loops split over the ranks (atsfft2d_loopsplit: one
-        zero-padded sum all-reduce of the [L, m] estimates).  Images from the
+        64x64 wrap-around DC block, unit magnitude, 15 dB, ATSFFT.  The tuner
+        passes are sequential and the estimation now reads the dense spectrum
+        (k_estimate_conv at b_estimate = 8192, x_hat itself at N): nothing of
+        one transform is left to split, so at N > 1 every rank runs its own
+        transform (replicas, weak scaling).  Images from the
         device generator (the reference-pinned c5 cases are GPU tests)."""
         import paper_1908_02461_b200 as P
-        from paper_1908_02461_b200 import distributed as D
         from paper_1908_02461_b200.signals import device_sparse_image
         torch = self.torch
         ks = [int(v) for v in self.args.c5_ks.split(",") if v.strip()]
@@ -604,22 +605,20 @@ class Bench:
         buf = torch.empty((16384, 16384), dtype=torch.complex64, device=self.dev)
         out = {"workload": "c5: ATSFFT 16384x16384 complex64, 20% of k in the 64x64 DC block, 15 dB, "
                            "est_loops=8, fp32, device-generated",
-               "parallelism": (f"estimation loops split over {self.world} rank(s)" if self.world > 1
-                               else "1 rank"), "scaling": "strong", "per_k": {}}
+               "parallelism": f"replicas: one transform per rank, {self.world} rank(s)",
+               "scaling": "weak", "per_k": {}}
         for k in ks:
-            img = device_sparse_image(16384, k, 5, snr_db=15.0, cluster_frac=0.2, cluster_side=64,
-                                      device=self.dev, out=buf)
+            img = device_sparse_image(16384, k, 5 + 1000 * self.rank, snr_db=15.0, cluster_frac=0.2,
+                                      cluster_side=64, device=self.dev, out=buf)
 
             def one():
-                if self.world > 1:
-                    return D.atsfft2d_loopsplit(img.x, cfg, 8, 6, precision="fp32")
                 return P.atsfft2d(img.x, cfg, 8, 6, precision="fp32")
             res, state = one()
             reps = 3
             ms, _ = self.timed(lambda: [one() for _ in range(reps)])
             truth = img.truth
             out["per_k"][str(k)] = {
-                "ms_per_transform": ms / reps, "transforms_per_s": reps / (ms / 1e3),
+                "ms_per_transform": ms / reps, "transforms_per_s": self.world * reps / (ms / 1e3),
                 "detected_k": state.detected_k, "b_estimate": state.b_estimate,
                 "passes": len(state.history), "recovered": len(res),
                 "planted_recovered": sum(1 for key in truth if key in res) / max(len(truth), 1)}
