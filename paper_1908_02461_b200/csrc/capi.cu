@@ -70,7 +70,11 @@ struct sfft2d_ctx {
   std::string err;
   std::vector<DevTables> tables;
   // named workspace buffers (names are string literals: views stay valid)
-  std::unordered_map<std::string_view, std::pair<void*, size_t>> bufs;
+  // (three sets: a tuner pass's private buffers live in set slot % 3, so the
+  // post-fold work of pass t on the side stream never shares a buffer with
+  // the folds of passes t + 1 and t + 2 on the main stream)
+  std::unordered_map<std::string_view, std::pair<void*, size_t>> bufs[3];
+  int ws_set = 0;
   // workspace source: the context's own memory pool (default; a private pool
   // so the process-wide default pool keeps its attributes), or a caller-owned
   // device arena (sfft2d_ctx_set_workspace) sub-allocated first-fit
@@ -99,11 +103,11 @@ struct sfft2d_ctx {
   void* out_v_h = nullptr;
   unsigned* mapped_d = nullptr;
   unsigned* done_d = nullptr;
-  unsigned done_base = 0;
   unsigned seq = 0;
   cudaStream_t vote_st = nullptr;
   cudaEvent_t ev_lmax = nullptr;
   cudaEvent_t ev_pass[4] = {nullptr, nullptr, nullptr, nullptr};   // per tuner pass: list complete
+  cudaEvent_t ev_fold[4] = {nullptr, nullptr, nullptr, nullptr};   // per tuner pass: fold complete
   cudaEvent_t ev_vote[2] = {nullptr, nullptr};
   // optional per-launch profiling (CUDA events on the launching stream)
   bool profiling = false;
@@ -162,7 +166,7 @@ static void* arena_take(sfft2d_ctx* c, size_t bytes) {
 }
 
 void* ws(sfft2d_ctx* c, const char* name, size_t bytes) {
-  auto& e = c->bufs[name];
+  auto& e = c->bufs[c->ws_set][name];
   if (bytes == 0) bytes = 16;
   if (e.second < bytes) {
     // Stream-ordered growth: cudaMalloc / cudaFree would synchronise the
@@ -437,12 +441,13 @@ constexpr unsigned kPubSlots = 256;
 
 volatile unsigned* pub_slot_h(sfft2d_ctx* c, unsigned seq) { return c->mapped_h + 4 * (seq % kPubSlots); }
 
+// Each publication has its own CTA ticket counter (one per seq slot, reset by
+// the last CTA), so publishing kernels on different streams may overlap.
 Publish make_publish(sfft2d_ctx* c, unsigned grid) {
   Publish p;
-  p.done = c->done_d;
-  c->done_base += grid;
-  p.target = c->done_base;
   p.seq = ++c->seq;
+  p.done = c->done_d + (p.seq % kPubSlots);
+  p.target = grid;
   p.slot = c->mapped_d + 4 * (p.seq % kPubSlots);
   return p;
 }
@@ -694,7 +699,8 @@ void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTable
                    const Perm* hp, int nloops, cplx<T>* spec, T* mags, unsigned long long* peaks,
                    cudaStream_t st, bool natural = false, cplx<T>* prefolded = nullptr,
                    const Perm* spec_q = nullptr, cplx<T>* spec_y = nullptr, int pre_z = 1,
-                   int* spec_z = nullptr, unsigned* nonfinite = nullptr) {
+                   int* spec_z = nullptr, unsigned* nonfinite = nullptr,
+                   cudaStream_t post_st = nullptr, cudaEvent_t handoff = nullptr) {
   using C = cplx<T>;
   const int B = 1 << lgB;
   const int P = prec_of<T>();
@@ -728,6 +734,16 @@ void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTable
     }
     C* dst = (C*)fo.data;
     struct { int Z; } gm{fo.Z};
+    // post-fold work (partial sums, FFT, |Z|) on post_st once the fold is done
+    // (tuner passes: the next pass's fold proceeds on st meanwhile)
+    const cudaStream_t main_st = st;
+    const cudaStream_t ws_saved = c->ws_st;
+    if (post_st) {
+      ck(cudaEventRecord(handoff, main_st), "cudaEventRecord");
+      ck(cudaStreamWaitEvent(post_st, handoff, 0), "cudaStreamWaitEvent");
+      st = post_st;
+      c->ws_st = post_st;
+    }
     if (small) {
       if (gm.Z == 1) {
         fft2d_grids<T>(c, y, lgB, g, tw, lgN, sp, mg, pk, st);
@@ -748,6 +764,8 @@ void fold_spectrum(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const DevTable
       }
       fft2d_grids<T>(c, y, lgB, g, tw, lgN, sp, mg, pk, st);
     }
+    st = main_st;
+    c->ws_st = ws_saved;
   }
 }
 
@@ -1169,6 +1187,16 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   unsigned* finite = (unsigned*)ws(c, "finite", 16);
   ck(cudaMemsetAsync(finite, 0, 16, st), "memset");
   bool finite_scanned = false;
+  // whatever path leaves run_ats, later work on st is ordered after the side
+  // stream's (post-fold work of speculative passes, votes)
+  struct JoinSide {
+    sfft2d_ctx* c;
+    cudaStream_t st;
+    ~JoinSide() {
+      cudaEventRecord(c->ev_lmax, c->vote_st);
+      cudaStreamWaitEvent(st, c->ev_lmax, 0);
+    }
+  } join_side{c, st};
 
   std::memset(S, 0, sizeof(*S));
   int b = std::max(4, std::min(cf.b0, n));
@@ -1239,8 +1267,6 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     return xfull;
   };
 
-  ck(cudaMemsetAsync(c->done_d, 0, sizeof(unsigned), st), "memset");
-  c->done_base = 0;
   // per-pass count slots (zeroed once), double-buffered maxima lists: the
   // vote of pass k runs on the side stream while pass k+1 proceeds
   unsigned* cnt_slots = (unsigned*)ws(c, "lm_counts", (size_t)2 * SFFT2D_MAX_HISTORY * 4);
@@ -1284,6 +1310,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       }
       // (stream order: a speculative pass enqueued after this list's pass
       // writes the other list buffer)
+      ck(cudaStreamWaitEvent(st, list_ready, 0), "cudaStreamWaitEvent");
       ck(cudaMemcpyAsync(arch + arch_used, maxlists[slot & 1], (size_t)count * 4,
                          cudaMemcpyDeviceToDevice, st), "archive maxima");
       arch_used += count;
@@ -1329,8 +1356,10 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     bool emitted = false;   // first B = N pass: above-floor candidates listed
     Perm p;
     cudaEvent_t ready = nullptr;   // the pass's maxima list is complete
+    cudaStream_t lst = nullptr;     // the stream that publishes the count
   };
   static const bool pipe_on = getenv("SFFT2D_NO_PIPELINE") == nullptr;
+  static const bool pass_pipe_on = getenv("SFFT2D_NO_PASS_PIPE") == nullptr;
   // the B = N/2 pass from the dense spectrum: x_hat stored (not factored),
   // untruncated 5-tap window, 512 <= B <= 2048 (SFFT2D_NO_PASSCONV=1: fold + FFT)
   static const bool passconv_on = getenv("SFFT2D_NO_PASSCONV") == nullptr;
@@ -1350,10 +1379,20 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     if (slot >= 2 * SFFT2D_MAX_HISTORY) fail(SFFT2D_ERR_UNSUPPORTED, "too many tuner passes");
     int32_t* ml = maxlists[slot & 1];
     unsigned* cnt = cnt_slots + slot;
-    if (vote_pending[slot & 1])   // the vote two passes back still reads this list
-      ck(cudaStreamWaitEvent(st, c->ev_vote[slot & 1], 0), "cudaStreamWaitEvent");
+    // the vote two passes back still reads this list: a list written on the
+    // main stream waits for it; the side stream runs votes and lists in order
+    auto wait_list_free = [&]() {
+      if (vote_pending[slot & 1])
+        ck(cudaStreamWaitEvent(st, c->ev_vote[slot & 1], 0), "cudaStreamWaitEvent");
+    };
+    // post-fold work of passes at B < N (reduce, FFT, |Z|, local maxima) goes
+    // to the side stream, so the next (speculated) pass's fold runs beside it;
+    // the pass's private workspace is set slot % 3 (SFFT2D_NO_PASS_PIPE=1: one stream)
+    const bool side = pass_pipe_on && !c->profiling;
+    cudaStream_t lst = st;   // the stream that writes this pass's maxima list
     unsigned seq;
     if (bb == n) {
+      wait_list_free();
       // B = N: |Z_p[k1, k2]| = |x_hat[s1i k1, s2i k2]| — one dense FFT serves every pass
       ensure_xhat(true);
       const bool listed = cand_ready || cand_pending;   // the device count is exact either way
@@ -1381,6 +1420,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     } else if (2 * bb == n && passconv_ok) {
       // B = N/2 from the dense spectrum (k_pass_conv): the dense FFT is
       // computed here, one pass early, and serves the B = N passes after it
+      wait_list_free();
       ensure_xhat(true);
       T* mg = (T*)ws(c, "grid_mag", BB * sizeof(T));
       unsigned long long* pk = (unsigned long long*)ws(c, "gpeak", 16);
@@ -1405,6 +1445,8 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       seq = lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, ml, cnt, st, true, 1u, 1u, 1u, nullptr, nullptr,
                           nullptr, true);
     } else if (BB * sizeof(C) <= (size_t)kSmall2DBytes) {
+      if (!side) wait_list_free();
+      c->ws_set = side ? slot % 3 : 0;
       C* y = (C*)ws(c, "fold_y", BB * sizeof(C));
       FoldOut fo{y, 1};
       if (spec_pi == pi && spec_b == bb) {
@@ -1432,12 +1474,20 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       }
       const Publish pub = make_publish(c, 1);
       seq = pub.seq;
-      pre(c, st);
+      if (side) {
+        ck(cudaEventRecord(c->ev_fold[ev_next], st), "cudaEventRecord");
+        ck(cudaStreamWaitEvent(c->vote_st, c->ev_fold[ev_next], 0), "cudaStreamWaitEvent");
+        lst = c->vote_st;
+      }
+      pre(c, lst);
       if (BB > 4 * 1024) fail(SFFT2D_ERR_UNSUPPORTED, "small pass holds at most 4 bins per thread");
-      kl(k_small_pass<T>, 1, 1024, (size_t)bb * (bb + 1) * sizeof(C) + BB * sizeof(T) + bb * sizeof(C), st, (const C*)fo.data, fo.Z, fo.Z == 1, lgb, p, (const C*)tb.tw[prec_of<T>()], lgN,
+      kl(k_small_pass<T>, 1, 1024, (size_t)bb * (bb + 1) * sizeof(C) + BB * sizeof(T) + bb * sizeof(C), lst, (const C*)fo.data, fo.Z, fo.Z == 1, lgb, p, (const C*)tb.tw[prec_of<T>()], lgN,
           cf.mag_floor, ml, cnt, pub);
-      post(c, "k_small_pass", st, (double)(fo.Z + 1) * BB * sizeof(C));
+      post(c, "k_small_pass", lst, (double)(fo.Z + 1) * BB * sizeof(C));
+      c->ws_set = 0;
     } else {
+      if (!side) wait_list_free();
+      c->ws_set = side ? slot % 3 : 0;
       T* mg = (T*)ws(c, "grid_mag", BB * sizeof(T));
       unsigned long long* pk = (unsigned long long*)ws(c, "gpeak", 16);
       // |Z[k1,k2]| = |Y^[s1i k1, s2i k2]| for the natural-order fold Y
@@ -1463,17 +1513,23 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
         spec_pi = pi + 1;
         spec_b = 2 * bb;
       }
+      if (side) lst = c->vote_st;
       fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, &p, 1, (C*)nullptr, mg, pk, st, true, pre_y, sq, sy,
-                            pre_z, &spec_z);
+                            pre_z, &spec_z, nullptr, side ? lst : nullptr, c->ev_fold[ev_next]);
       const unsigned mb = (unsigned)bb - 1u;
       // B < N: the fold aliases the noise floor into most buckets
-      seq = lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, ml, cnt, st, true, p.s1i & mb, p.s2i & mb,
+      const cudaStream_t ws_saved = c->ws_st;
+      c->ws_st = lst;
+      seq = lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, ml, cnt, lst, true, p.s1i & mb, p.s2i & mb,
                           p.s2 & mb, nullptr, nullptr, nullptr, true);
+      c->ws_st = ws_saved;
+      c->ws_set = 0;
     }
     tk.seq = seq;
     tk.ready = c->ev_pass[ev_next];
     ev_next = (ev_next + 1) % 4;
-    ck(cudaEventRecord(tk.ready, st), "cudaEventRecord");   // the maxima list is complete
+    ck(cudaEventRecord(tk.ready, lst), "cudaEventRecord");   // the maxima list is complete
+    tk.lst = lst;
     return tk;
   };
   // a speculative pass that the tuner did not take: nothing of it is read;
@@ -1484,7 +1540,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     if (tk.emitted) cand_pending = false;
   };
   auto finish_pass = [&](const Ticket& tk) -> long long {
-    const long long count = wait_published(c, tk.seq, st);
+    const long long count = wait_published(c, tk.seq, tk.lst ? tk.lst : st);
     if (tk.emitted) {   // the candidate count rides along with the maxima count
       cand_n = pub_slot_h(c, tk.seq)[2];
       cand_pending = false;
@@ -1980,14 +2036,16 @@ int sfft2d_ctx_create(int device, sfft2d_ctx** out) {
     ck(cudaHostAlloc((void**)&c->mapped_h, 16 * kPubSlots, cudaHostAllocMapped), "cudaHostAlloc");
     std::memset(c->mapped_h, 0, 16 * kPubSlots);
     ck(cudaHostGetDevicePointer((void**)&c->mapped_d, c->mapped_h, 0), "cudaHostGetDevicePointer");
-    ck(cudaMalloc(&c->done_d, 64), "cudaMalloc");
-    ck(cudaMemset(c->done_d, 0, 64), "cudaMemset");
+    ck(cudaMalloc(&c->done_d, 4 * kPubSlots), "cudaMalloc");
+    ck(cudaMemset(c->done_d, 0, 4 * kPubSlots), "cudaMemset");
     ck(cudaStreamCreateWithFlags(&c->vote_st, cudaStreamNonBlocking), "cudaStreamCreate");
     ck(cudaEventCreateWithFlags(&c->ev_lmax, cudaEventDisableTiming), "cudaEventCreate");
     ck(cudaEventCreateWithFlags(&c->ev_ws, cudaEventDisableTiming), "cudaEventCreate");
     ck(cudaEventCreateWithFlags(&c->ev_perm, cudaEventDisableTiming), "cudaEventCreate");
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 4; ++i) {
       ck(cudaEventCreateWithFlags(&c->ev_pass[i], cudaEventDisableTiming), "cudaEventCreate");
+      ck(cudaEventCreateWithFlags(&c->ev_fold[i], cudaEventDisableTiming), "cudaEventCreate");
+    }
     ck(cudaEventRecord(c->ev_perm, 0), "cudaEventRecord");
     // the context's own memory pool, keeping freed workspace (no release at
     // sync points); the device's default pool is left untouched
@@ -2016,8 +2074,9 @@ void sfft2d_ctx_destroy(sfft2d_ctx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   if (!c->arena)
-    for (auto& kv : c->bufs)
-      if (kv.second.first) cudaFreeAsync(kv.second.first, 0);
+    for (auto& set : c->bufs)
+      for (auto& kv : set)
+        if (kv.second.first) cudaFreeAsync(kv.second.first, 0);
   cudaDeviceSynchronize();
   if (c->pool) cudaMemPoolDestroy(c->pool);
   for (auto& t : c->tables)
@@ -2035,8 +2094,10 @@ void sfft2d_ctx_destroy(sfft2d_ctx* c) {
   if (c->ev_lmax) cudaEventDestroy(c->ev_lmax);
   if (c->ev_ws) cudaEventDestroy(c->ev_ws);
   if (c->ev_perm) cudaEventDestroy(c->ev_perm);
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 4; ++i) {
     if (c->ev_pass[i]) cudaEventDestroy(c->ev_pass[i]);
+    if (c->ev_fold[i]) cudaEventDestroy(c->ev_fold[i]);
+  }
   for (int i = 0; i < 2; ++i)
     if (c->ev_vote[i]) cudaEventDestroy(c->ev_vote[i]);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
@@ -2550,10 +2611,11 @@ int sfft2d_ctx_set_workspace(sfft2d_ctx* c, void* base, int64_t bytes) {
   return guarded(c, [&] {
     if (bytes < 0 || (bytes > 0 && !base)) fail(SFFT2D_ERR_VALUE, "bad workspace");
     ck(cudaDeviceSynchronize(), "sync");   // nothing may still use the old buffers
-    for (auto& kv : c->bufs)
-      if (kv.second.first && !c->arena) ck(cudaFreeAsync(kv.second.first, 0), "cudaFreeAsync");
+    for (auto& set : c->bufs)
+      for (auto& kv : set)
+        if (kv.second.first && !c->arena) ck(cudaFreeAsync(kv.second.first, 0), "cudaFreeAsync");
     ck(cudaDeviceSynchronize(), "sync");
-    c->bufs.clear();
+    for (auto& set : c->bufs) set.clear();
     c->arena_free.clear();
     c->ws_in_use = 0;
     c->ws_peak = 0;

@@ -141,6 +141,9 @@ __device__ __forceinline__ void publish_count(unsigned* count, unsigned* done, u
     // so no system-scope fence (a ~2 us PCIe round trip each) is needed
     *reinterpret_cast<volatile unsigned long long*>(slot) =
         ((unsigned long long)v << 32) | (unsigned long long)seq;
+    // the ticket counter is this publication's own (one per seq slot): reset
+    // it for the slot's next use (every CTA of this launch has taken its ticket)
+    atomicExch(done, 0u);
   }
 }
 
