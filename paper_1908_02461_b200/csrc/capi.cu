@@ -1481,8 +1481,13 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       }
       pre(c, lst);
       if (BB > 4 * 1024) fail(SFFT2D_ERR_UNSUPPORTED, "small pass holds at most 4 bins per thread");
-      kl(k_small_pass<T>, 1, 1024, (size_t)bb * (bb + 1) * sizeof(C) + BB * sizeof(T) + bb * sizeof(C), lst, (const C*)fo.data, fo.Z, fo.Z == 1, lgb, p, (const C*)tb.tw[prec_of<T>()], lgN,
-          cf.mag_floor, ml, cnt, pub);
+      const size_t sps = (size_t)bb * (bb + 1) * sizeof(C) + BB * sizeof(T) + bb * sizeof(C);
+      if (BB <= 1024)   // one (bin, partial-slice) slot per thread
+        kl(k_small_pass<T, 1>, 1, 1024, sps, lst, (const C*)fo.data, fo.Z, fo.Z == 1, lgb, p,
+           (const C*)tb.tw[prec_of<T>()], lgN, cf.mag_floor, ml, cnt, pub);
+      else
+        kl(k_small_pass<T, 4>, 1, 1024, sps, lst, (const C*)fo.data, fo.Z, fo.Z == 1, lgb, p,
+           (const C*)tb.tw[prec_of<T>()], lgN, cf.mag_floor, ml, cnt, pub);
       post(c, "k_small_pass", lst, (double)(fo.Z + 1) * BB * sizeof(C));
       c->ws_set = 0;
     } else {

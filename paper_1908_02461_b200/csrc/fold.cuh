@@ -983,7 +983,7 @@ __global__ void __launch_bounds__(1024) k_fold_reduce_fft_small(const cplx<T>* _
 // reduce the fold partials (or take the already permuted grid), 2D FFT in
 // shared memory, |Z| and its peak, strict 8-neighbour toroidal maxima above
 // floor_rel * peak, appended (unordered) to `list` with the count in `count`.
-template <typename T>
+template <typename T, int kSlots = 4>
 __global__ void __launch_bounds__(1024)
 k_small_pass(const cplx<T>* __restrict__ part, int Z, bool permuted, int lgB, Perm p,
              const cplx<T>* __restrict__ tw, int lgN, double floor_rel,
@@ -1007,9 +1007,9 @@ k_small_pass(const cplx<T>* __restrict__ part, int Z, bool permuted, int lgB, Pe
   const int tpe_lg = BB >= (int)blockDim.x ? 0 : min(5, __ffs(blockDim.x / BB) - 1);
   const int tpe = 1 << tpe_lg;
   const int zs = (Z + tpe - 1) >> tpe_lg;
-  // up to 4 slots per thread, their partial sums loaded together (all loads
-  // in flight before the first use)
-  constexpr int kSlots = 4;
+  // up to kSlots slots per thread (1 when the grid's bins x slices fit the
+  // block: B <= 32), their partial sums loaded together (all loads in
+  // flight before the first use)
   C vv[kSlots];
   const int total = BB << tpe_lg;
   const C* src[kSlots];
