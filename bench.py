@@ -272,10 +272,20 @@ class Bench:
         self.args = args
         self.torch, self.dist = torch, dist
         self.world, self.rank, self.local = dist_env()
+        # SFFT2D_BENCH_SAME_DEVICE=1: every rank on cuda:0 with gloo — a
+        # plumbing check of the N > 1 path on a one-GPU box (the ranks' kernels
+        # never wait on one another; the numbers are not a scaling measurement)
+        self.same = os.environ.get("SFFT2D_BENCH_SAME_DEVICE") == "1"
+        if self.same:
+            self.local = 0
         torch.cuda.set_device(self.local)
         if self.world > 1:
-            dist.init_process_group("nccl", init_method="env://", world_size=self.world,
-                                    rank=self.rank, device_id=torch.device("cuda", self.local))
+            if self.same:
+                dist.init_process_group("gloo", init_method="env://", world_size=self.world,
+                                        rank=self.rank)
+            else:
+                dist.init_process_group("nccl", init_method="env://", world_size=self.world,
+                                        rank=self.rank, device_id=torch.device("cuda", self.local))
         self.dev = torch.device("cuda", self.local)
         self.stream = torch.cuda.current_stream(self.dev)
         vis = [v for v in os.environ.get("CUDA_VISIBLE_DEVICES", "").split(",") if v.strip()]
@@ -284,12 +294,16 @@ class Bench:
 
     def barrier(self):
         if self.world > 1:
-            self.dist.barrier(device_ids=[self.local])
+            if self.same:
+                self.dist.barrier()
+            else:
+                self.dist.barrier(device_ids=[self.local])
 
     def max_over_ranks(self, v: float) -> float:
         if self.world == 1:
             return v
-        t = self.torch.tensor([v], dtype=self.torch.float64, device=self.dev)
+        t = self.torch.tensor([v], dtype=self.torch.float64,
+                              device="cpu" if self.same else self.dev)
         self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
         return float(t.item())
 
