@@ -875,6 +875,19 @@ unsigned lmax_tuner(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long l
   int rb = std::max(1, std::min(B / 128, smem_rows - 2));
   while (B % rb) --rb;
   const size_t sm = (size_t)(rb + 2) * B * sizeof(T) + (size_t)rb * B / 32 * sizeof(unsigned);
+  static const bool tri_on = getenv("SFFT2D_NO_LMAX_TRI") == nullptr;
+  if (perm && !live_most && B >= 8192 && 3 * row <= kMaxDynSmem && tri_on) {
+    // a B = N view too wide for the ring but three rows fit shared memory:
+    // each row tested against its two neighbour rows staged by TMA
+    const unsigned grid = (unsigned)std::min(B, kNumSMs);
+    const Publish pub = make_publish(c, grid);
+    pre(c, st);
+    kl(k_lmax_tri<T>, grid, 512, 3 * row, st, mags, lgB, s1, s2, inv_pow2(s1, (uint32_t)B - 1u), s2inv,
+       peak, floor_rel, list, count, pub, cand, cand_count);
+    if (emitted) *emitted = cand != nullptr;
+    post(c, "k_lmax_tri", st, by);
+    return pub.seq;
+  }
   if (sm > kMaxDynSmem || (perm && !live_most && B >= 8192)) {
     // rows too long to stage (fp64 at B = 16384), or a B = N view too wide for
     // the ring (fp32 16384: one 3-row tile per SM): test straight from global

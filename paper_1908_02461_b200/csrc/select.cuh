@@ -644,6 +644,107 @@ __global__ void k_lmax_direct(const T* __restrict__ M, int lgB, unsigned s1, uns
 // through the permutation (SURVEY.md §7 hard part 2: tuner passes at B = N are
 // permuted views of |x_hat|).  CTA per output row; the source row is staged in
 // shared memory so both the read and the write are coalesced.
+// B = N view whose rows are too long for the ring of k_lmax_stream (fp32
+// B = 16384, fp64 B = 8192: 64 KB rows) but of which THREE rows fit shared
+// memory: the view neighbours of natural bin (R, C) are the natural bins
+// (R -+ s1, C -+ s2) (as in k_lmax_direct), so a CTA stages the natural rows
+// R - s1, R, R + s1 with TMA bulk copies (one mbarrier) and tests row R with
+// every neighbour from shared memory — 3 coalesced row reads per row instead
+// of 8 scattered 4-byte reads per above-floor bin (c5 k = 4096: most bins
+// are above the floor).  Persistent over rows; same outputs as k_lmax_direct
+// (unordered list of view keys, count, optional above-floor candidate list).
+template <typename T>
+__global__ void __launch_bounds__(512)
+k_lmax_tri(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, unsigned s1inv,
+           unsigned s2inv, const unsigned long long* __restrict__ peak, double floor_rel,
+           int32_t* __restrict__ list, unsigned* __restrict__ count, Publish pub,
+           int32_t* __restrict__ cand, unsigned* __restrict__ cand_count) {
+  pdl_wait();
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) unsigned long long s_bar;
+  __shared__ unsigned s_wf[16], s_wc[16], s_base[2];
+  const int B = 1 << lgB;
+  const unsigned mask = (unsigned)B - 1u;
+  T* up = reinterpret_cast<T*>(smem_raw);
+  T* md = up + B;
+  T* dn = md + B;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int per = B / blockDim.x;   // columns per thread (<= 32: one bit each)
+  const double pk = fkey_inv(*peak);
+  const double fl = floor_rel * pk;
+  T flT = sizeof(T) == 4 ? (T)__double2float_ru(fl) : (T)fl;
+  if (!(pk > 0.0))
+    flT = sizeof(T) == 4 ? (T)__int_as_float(0x7f800000) : (T)__longlong_as_double(0x7ff0000000000000ll);
+  const unsigned row_bytes = (unsigned)(sizeof(T) << lgB);
+  if (threadIdx.x == 0) mbar_init(&s_bar, 1);
+  mbar_fence_init();
+  __syncthreads();
+  unsigned phase = 0;
+  for (unsigned R = blockIdx.x; R < (unsigned)B; R += gridDim.x) {
+    if (threadIdx.x == 0) {
+      mbar_expect_tx(&s_bar, 3u * row_bytes);
+      bulk_g2s(up, M + ((size_t)((R - s1) & mask) << lgB), row_bytes, &s_bar);
+      bulk_g2s(md, M + ((size_t)R << lgB), row_bytes, &s_bar);
+      bulk_g2s(dn, M + ((size_t)((R + s1) & mask) << lgB), row_bytes, &s_bar);
+    }
+    mbar_wait(&s_bar, phase);
+    phase ^= 1u;
+    // test the row: bit q of fm / cm = column q * blockDim + tid is a maximum /
+    // above the floor
+    unsigned fm = 0u, cm = 0u;
+    for (int q = 0; q < per; ++q) {
+      const unsigned C = (unsigned)(q * blockDim.x + threadIdx.x);
+      const T v = md[C];
+      if (v >= flT) {
+        cm |= 1u << q;
+        const unsigned Cl = (C - s2) & mask, Cr = (C + s2) & mask;
+        const T nb = fmax(fmax(fmax(up[Cl], up[C]), fmax(up[Cr], md[Cl])),
+                          fmax(fmax(md[Cr], dn[Cl]), fmax(dn[C], dn[Cr])));
+        if (v > nb) fm |= 1u << q;
+      }
+    }
+    if (!cand) cm = 0u;
+    // one global atomic per row and list (a single hot counter took one
+    // atomic per warp per 32 bins before: c5's dense B = N views were bound
+    // by it); positions inside the row from a block scan
+    const unsigned nf = (unsigned)__popc(fm), nc = (unsigned)__popc(cm);
+    const unsigned xf = warp_incl_scan(nf), xc = warp_incl_scan(nc);
+    if (lane == 31) { s_wf[warp] = xf; s_wc[warp] = xc; }
+    __syncthreads();   // (also: every thread is done with the three rows)
+    if (threadIdx.x == 0) {
+      unsigned tf = 0, tc = 0;
+      for (int w = 0; w < nwarps; ++w) {
+        const unsigned a = s_wf[w], b = s_wc[w];
+        s_wf[w] = tf;
+        s_wc[w] = tc;
+        tf += a;
+        tc += b;
+      }
+      s_base[0] = tf ? atomicAdd(count, tf) : 0u;
+      s_base[1] = tc ? atomicAdd(cand_count, tc) : 0u;
+    }
+    __syncthreads();
+    unsigned pf = s_base[0] + s_wf[warp] + xf - nf;
+    unsigned pc = s_base[1] + s_wc[warp] + xc - nc;
+    const unsigned keyrow = ((s1inv * R) & mask) << lgB;
+    while (fm) {
+      const int q = __ffs(fm) - 1;
+      fm &= fm - 1u;
+      const unsigned C = (unsigned)(q * blockDim.x + threadIdx.x);
+      list[pf++] = (int32_t)(keyrow | ((s2inv * C) & mask));
+    }
+    while (cm) {
+      const int q = __ffs(cm) - 1;
+      cm &= cm - 1u;
+      cand[pc++] = (int32_t)(((size_t)R << lgB) | (unsigned)(q * blockDim.x + threadIdx.x));
+    }
+  }
+  if (pub.slot) {
+    __syncthreads();
+    if (threadIdx.x == 0) publish_count(count, pub.done, pub.target, pub.slot, pub.seq, cand_count);
+  }
+}
+
 template <typename T>
 __global__ void k_permute_grid(const T* __restrict__ M, int lgN, unsigned s1i, unsigned s2i,
                                T* __restrict__ G) {

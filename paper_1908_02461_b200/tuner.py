@@ -94,6 +94,7 @@ def _state(sc: _native.TunerStateC) -> TunerState:
                     b_detect=int(sc.b_detect), b_estimate=int(sc.b_estimate),
                     vote_passes=int(sc.vote_passes))
     st.pass_us = sc.hist_us[:n]   # diagnostic, not compared
+    st.n_candidates = int(sc.n_candidates)   # diagnostic: coordinates estimated
     return st
 
 

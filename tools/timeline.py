@@ -29,7 +29,7 @@ elif work == "c2":
     def call():
         return P.atsfft2d_arrays(x, P.TunerConfig(), 8, 11, precision=prec)
 elif work.startswith("c5"):
-    k5 = int(work[3:] or 64) if len(work) > 2 else 64
+    k5 = int(work[2:] or 64) if len(work) > 2 else 64
     x = P.device_sparse_image(16384, k5, 5, snr_db=15.0, cluster_frac=0.2, cluster_side=64).x
     def call():
         return P.atsfft2d_arrays(x, P.TunerConfig(), 8, 6, precision=prec)
@@ -45,6 +45,12 @@ t0w = time.perf_counter()
 for _ in range(reps):
     call()
 torch.cuda.synchronize()
+_out = call()
+try:
+    print(f"state: passes {len(_out[1].history)}, detected_k {_out[1].detected_k}, b_estimate "
+          f"{_out[1].b_estimate}, candidates {getattr(_out[1], 'n_candidates', None)}")
+except Exception:  # noqa: BLE001 - SFFT calls return no state
+    pass
 print(f"{work} {prec}: host wall {(time.perf_counter() - t0w) / reps * 1e3:.3f} ms per transform (no profiler)")
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(reps):
