@@ -541,6 +541,29 @@ k_lmax_win(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, unsigned 
 // pass): view (r, c) = (s1i^-1 R, s2i^-1 C) has its view neighbours at the
 // natural bins (R +- s1, C +- s2) (s1, s2 = the view multipliers).  Bins below
 // the floor can never be counted, so the count equals k_lmax_stream's.
+// Append the flagged keys of the whole block to `list` with ONE global atomic
+// per call (block scan for the positions): every thread of the block calls it
+// (block-uniform loops).  `s_tmp` holds 33 unsigneds of shared memory.
+__device__ __forceinline__ void block_emit(bool f, int32_t key, int32_t* __restrict__ list,
+                                           unsigned* __restrict__ count, unsigned* s_tmp) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const unsigned bal = __ballot_sync(0xffffffffu, f);
+  if (lane == 0) s_tmp[warp] = (unsigned)__popc(bal);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int w = 0; w < nwarps; ++w) {
+      const unsigned a = s_tmp[w];
+      s_tmp[w] = t;
+      t += a;
+    }
+    s_tmp[32] = t ? atomicAdd(count, t) : 0u;
+  }
+  __syncthreads();
+  if (f) list[s_tmp[32] + s_tmp[warp] + __popc(bal & ((1u << lane) - 1u))] = key;
+  __syncthreads();   // s_tmp is reused by the next call
+}
+
 template <typename T>
 __global__ void k_lmax_cand(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2,
                             unsigned s1inv, unsigned s2inv, const int32_t* __restrict__ cand,
@@ -549,7 +572,7 @@ __global__ void k_lmax_cand(const T* __restrict__ M, int lgB, unsigned s1, unsig
   pdl_wait();
   const unsigned mask = (1u << lgB) - 1u;
   const unsigned n = *cand_count;
-  const int lane = threadIdx.x & 31;
+  __shared__ unsigned s_tmp[33];
   for (unsigned e0 = blockIdx.x * blockDim.x; e0 < n; e0 += gridDim.x * blockDim.x) {
     const unsigned e = e0 + threadIdx.x;
     bool f = false;
@@ -567,13 +590,7 @@ __global__ void k_lmax_cand(const T* __restrict__ M, int lgB, unsigned s1, unsig
           (v > dn[Cl]) & (v > dn[C]) & (v > dn[Cr]);
       key = (((s1inv * R) & mask) << lgB) | ((s2inv * C) & mask);
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, f);
-    if (bal) {
-      unsigned base = 0;
-      if (lane == 0) base = atomicAdd(count, (unsigned)__popc(bal));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (f) list[base + __popc(bal & ((1u << lane) - 1u))] = (int32_t)key;
-    }
+    block_emit(f, (int32_t)key, list, count, s_tmp);
   }
   if (pub.slot) {
     __syncthreads();
@@ -595,24 +612,19 @@ __global__ void k_lmax_direct(const T* __restrict__ M, int lgB, unsigned s1, uns
   pdl_wait();
   const unsigned mask = (1u << lgB) - 1u;
   const size_t n = (size_t)1 << (2 * lgB);
-  const int lane = threadIdx.x & 31;
   const double pk = fkey_inv(*peak);
   const double fl = floor_rel * pk;
   T flT = sizeof(T) == 4 ? (T)__double2float_ru(fl) : (T)fl;
   if (!(pk > 0.0))
     flT = sizeof(T) == 4 ? (T)__int_as_float(0x7f800000) : (T)__longlong_as_double(0x7ff0000000000000ll);
+  __shared__ unsigned s_tmp[33];
   for (size_t e0 = (size_t)blockIdx.x * blockDim.x; e0 < n; e0 += (size_t)gridDim.x * blockDim.x) {
     const size_t e = e0 + threadIdx.x;
     const T v = e < n ? M[e] : (T)0;
     const bool live = e < n && v >= flT;
-    if (!__any_sync(0xffffffffu, live)) continue;
-    if (cand) {
-      const unsigned cb = __ballot_sync(0xffffffffu, live);
-      unsigned b0 = 0;
-      if (lane == 0) b0 = atomicAdd(cand_count, (unsigned)__popc(cb));
-      b0 = __shfl_sync(0xffffffffu, b0, 0);
-      if (live) cand[b0 + __popc(cb & ((1u << lane) - 1u))] = (int32_t)e;
-    }
+    // (block-uniform: one global atomic per block and list per iteration)
+    if (!__syncthreads_or(live)) continue;
+    if (cand) block_emit(live, (int32_t)e, cand, cand_count, s_tmp);
     bool f = false;
     unsigned key = 0;
     if (live) {
@@ -626,13 +638,7 @@ __global__ void k_lmax_direct(const T* __restrict__ M, int lgB, unsigned s1, uns
           (v > dn[Cl]) & (v > dn[C]) & (v > dn[Cr]);
       key = (((s1inv * R) & mask) << lgB) | ((s2inv * C) & mask);
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, f);
-    if (bal) {
-      unsigned b0 = 0;
-      if (lane == 0) b0 = atomicAdd(count, (unsigned)__popc(bal));
-      b0 = __shfl_sync(0xffffffffu, b0, 0);
-      if (f) list[b0 + __popc(bal & ((1u << lane) - 1u))] = (int32_t)key;
-    }
+    block_emit(f, (int32_t)key, list, count, s_tmp);
   }
   if (pub.slot) {
     __syncthreads();

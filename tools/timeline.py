@@ -45,13 +45,14 @@ t0w = time.perf_counter()
 for _ in range(reps):
     call()
 torch.cuda.synchronize()
+_wall = (time.perf_counter() - t0w) / reps
+print(f"{work} {prec}: host wall {_wall * 1e3:.3f} ms per transform (no profiler)")
 _out = call()
 try:
     print(f"state: passes {len(_out[1].history)}, detected_k {_out[1].detected_k}, b_estimate "
           f"{_out[1].b_estimate}, candidates {getattr(_out[1], 'n_candidates', None)}")
 except Exception:  # noqa: BLE001 - SFFT calls return no state
     pass
-print(f"{work} {prec}: host wall {(time.perf_counter() - t0w) / reps * 1e3:.3f} ms per transform (no profiler)")
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(reps):
         call()
