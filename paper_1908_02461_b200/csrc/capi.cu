@@ -1114,7 +1114,10 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
     kl(k_median<T>, grid_for(m, 128), 128, 0, st, vals, usable, L, (long)m, m_dev, med, mags,
                                                    alive, alive_cnt, peak);
     post(c, "k_median", st, 0);
-    n_alive = read_u32(c, alive_cnt, st);
+    // the alive count decides whether a top-k cut is needed (alive > k); with
+    // m <= k candidates no cut is possible, so the count is not read (one
+    // host synchronisation less; an all-dead result still compacts to 0)
+    n_alive = ((long long)m <= k) ? (long long)m : (long long)read_u32(c, alive_cnt, st);
   }
   finish_select<T>(c, lgN, keys, m, k, prune_rel, med, mags, alive, peak, n_alive, st, res);
 }
