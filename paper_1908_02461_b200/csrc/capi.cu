@@ -1728,11 +1728,21 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   auto lazy_votes = [&](unsigned thr_, uint32_t* bits, unsigned* cnts, uint32_t* hist_out) {
     int lgG = 13;
     while (lgG < 15 && ((long long)1 << (lgG + 1)) * (2 * kNumSMs) <= nkeys) ++lgG;
-    const size_t smem = vote_lazy_smem(lgN, lgG, lp.lgBmax);
+    // every bitmap pass staged at once when they fit beside the tallies
+    // (k_vote_lazy2, no per-pass barriers); else one at a time
+    static const bool v2_on = getenv("SFFT2D_OLD_VOTE_LAZY") == nullptr;
+    const size_t smem2 = ((size_t)1 << lgG) + (size_t)bm_used * 4;
     pre(c, st);
-    kl(k_vote_lazy, (unsigned)(nkeys >> lgG), 256, smem, st, (const int32_t*)arch,
-       (const uint32_t*)bmarch, lp, lgN, lgG,
-       (const uint32_t*)(hist_used ? hist : nullptr), hist_out, thr_, bits, cnts);
+    if (v2_on && smem2 <= kMaxDynSmem) {
+      kl(k_vote_lazy2, (unsigned)(nkeys >> lgG), 256, smem2, st, (const int32_t*)arch,
+         (const uint32_t*)bmarch, (int)bm_used, lp, lgN, lgG,
+         (const uint32_t*)(hist_used ? hist : nullptr), hist_out, thr_, bits, cnts);
+    } else {
+      const size_t smem = vote_lazy_smem(lgN, lgG, lp.lgBmax);
+      kl(k_vote_lazy, (unsigned)(nkeys >> lgG), 256, smem, st, (const int32_t*)arch,
+         (const uint32_t*)bmarch, lp, lgN, lgG,
+         (const uint32_t*)(hist_used ? hist : nullptr), hist_out, thr_, bits, cnts);
+    }
     post(c, "k_vote_lazy", st, (double)nkeys / 8.0 + (hist_used ? (double)nkeys : 0.0) +
                                    (hist_out ? (double)nkeys : 0.0));
   };

@@ -296,6 +296,153 @@ __global__ void __launch_bounds__(256) k_vote_lazy(const int32_t* __restrict__ a
 }
 
 // dynamic shared memory of k_vote_lazy
+// Barrier-free variant of k_vote_lazy (the same tallies): EVERY bitmap pass
+// (bm_words words at the head of the bitmap archive) is staged in shared
+// memory once, then each warp takes (tile row, bitmap pass) items on its
+// own — the lanes scan the row's candidate bin rows chunk by chunk, and every
+// maximum's w + 2 column preimages are spread over the lanes — so the block
+// synchronises only before and after the tallies.  (k_vote_lazy, one pass at
+// a time with three block barriers per pass, spent its time at those
+// barriers: ncu stall "barrier" 6.2 per issued instruction, shared atomics at
+// 7% of the pipe's peak, c3.)  List passes as in k_vote_lazy, strided over
+// all warps.
+__global__ void __launch_bounds__(256) k_vote_lazy2(const int32_t* __restrict__ arch,
+                                                     const uint32_t* __restrict__ bmarch,
+                                                     int bm_words, LazyPasses lp, int lgN, int lgG,
+                                                     const uint32_t* __restrict__ hist_init,
+                                                     uint32_t* __restrict__ hist_out, unsigned thr,
+                                                     uint32_t* __restrict__ bits,
+                                                     unsigned* __restrict__ blk_counts) {
+  pdl_wait();
+  extern __shared__ __align__(16) uint32_t sm_vote[];
+  __shared__ unsigned s_warp[32];
+  const int N = 1 << lgN, G = 1 << lgG, R = G >> lgN;
+  const unsigned maskN = (unsigned)N - 1u;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int lane = tid & 31, warp = tid >> 5, nwarps = nt >> 5;
+  const size_t k0 = (size_t)blockIdx.x << lgG;
+  const unsigned i0 = (unsigned)(k0 >> lgN);
+  uint32_t* s_tal = sm_vote;            // G bytes
+  uint32_t* s_bm = s_tal + G / 4;       // every bitmap pass, archive layout
+  uint4* t4 = reinterpret_cast<uint4*>(s_tal);
+  for (int e = tid * 4; e < bm_words; e += nt * 4) cp_async16(s_bm + e, bmarch + e);
+  cp_async_commit();
+  if (hist_init) {
+    const uint4* h4 = reinterpret_cast<const uint4*>(hist_init + k0 / 4);
+    for (int e = tid; e < G / 16; e += nt) t4[e] = h4[e];
+  } else {
+    for (int e = tid; e < G / 16; e += nt) t4[e] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  // bitmap passes, in archive order
+  int nbm = 0;
+  for (int ps = 0; ps < lp.n; ++ps) nbm += lp.v[ps].lgB <= lp.lgBmax;
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  const int items = R * nbm;
+  for (int item = warp; item < items; item += nwarps) {
+    const int r = item % R;
+    int k = item / R, ps = 0;
+    for (;; ++ps)   // the k-th bitmap pass
+      if (lp.v[ps].lgB <= lp.lgBmax && k-- == 0) break;
+    const LazyPass& P = lp.v[ps];
+    const int lgB = P.lgB, B = 1 << lgB;
+    const unsigned maskB = (unsigned)B - 1u;
+    const int lgw = lgN - lgB, w = 1 << lgw;
+    const int len = (w == 1) ? 3 : w + 2;
+    const int shiftlo = w / 2 + 1;   // floor(w/2) + expand
+    const uint32_t* s_bits = s_bm + P.off;
+    const uint32_t* s_flag = s_bits + (((B * B + 31) / 32 + 3) & ~3);
+    const unsigned t = (P.p.s1 * (i0 + (unsigned)r)) & maskN;
+    const int hi = (int)((t + (unsigned)N + (unsigned)shiftlo) >> lgw);
+    const int lo = (int)((t + (unsigned)N + (unsigned)shiftlo - (unsigned)len + (unsigned)w) >> lgw);
+    const int chunks = (B + 31) / 32;
+    const unsigned cmask = B >= 32 ? 0xffffffffu : ((1u << B) - 1u);
+    const unsigned rowkey = (unsigned)r << lgN;
+    for (int q0 = 0; q0 < chunks; q0 += 32) {
+      const int q = q0 + lane;
+      unsigned rb[3] = {0u, 0u, 0u};
+      int na = 0;
+      unsigned any = 0u;
+      if (q < chunks) {
+        for (int a = lo; a <= hi; ++a) {
+          const unsigned am = (unsigned)a & maskB;
+          if (!((s_flag[am >> 5] >> (am & 31u)) & 1u)) continue;
+          const unsigned bit0 = am * (unsigned)B + (unsigned)q * 32u;
+          rb[na] = B >= 32 ? s_bits[bit0 >> 5] : (s_bits[bit0 >> 5] >> (bit0 & 31u)) & cmask;
+          any |= rb[na++];
+        }
+      }
+      // every lane's maxima in turn; the warp spreads each one's len column
+      // preimages over its lanes
+      unsigned ballot = __ballot_sync(0xffffffffu, any != 0u);
+      while (ballot) {
+        const int src = __ffs(ballot) - 1;
+        unsigned bitsrc = __shfl_sync(0xffffffffu, any, src);
+        const unsigned r0 = __shfl_sync(0xffffffffu, rb[0], src);
+        const unsigned r1 = __shfl_sync(0xffffffffu, rb[1], src);
+        const unsigned r2 = __shfl_sync(0xffffffffu, rb[2], src);
+        const int qs = __shfl_sync(0xffffffffu, q, src);
+        while (bitsrc) {
+          const int kk = __ffs(bitsrc) - 1;
+          bitsrc &= bitsrc - 1u;
+          const unsigned m = ((r0 >> kk) & 1u) + ((r1 >> kk) & 1u) + ((r2 >> kk) & 1u);
+          const unsigned b = (unsigned)(qs * 32 + kk);
+          for (int rr = lane; rr < len; rr += 32) {
+            const unsigned v = (b * (unsigned)w - (unsigned)shiftlo + (unsigned)rr) & maskN;
+            lazy_add(s_tal, rowkey | ((P.p.s2i * v) & maskN), m);
+          }
+        }
+        ballot &= ballot - 1u;
+      }
+    }
+  }
+  // list passes: every maximum's len x len preimage tested against the tile
+  for (int ps = 0; ps < lp.n; ++ps) {
+    const LazyPass& P = lp.v[ps];
+    if (P.lgB <= lp.lgBmax) continue;
+    const int lgB = P.lgB;
+    const unsigned maskB = (1u << lgB) - 1u;
+    const int lgw = lgN - lgB, w = 1 << lgw;
+    const int len = (w == 1) ? 3 : w + 2;
+    const int shiftlo = w / 2 + 1;
+    const int32_t* L = arch + P.off;
+    for (int e = tid; e < P.count; e += nt) {
+      const unsigned bin = (unsigned)L[e];
+      const unsigned a = bin >> lgB, b = bin & maskB;
+      for (int u = 0; u < len; ++u) {
+        const unsigned tt = (a * (unsigned)w - (unsigned)shiftlo + (unsigned)u) & maskN;
+        const unsigned r = ((P.p.s1i * tt) & maskN) - i0;
+        if (r >= (unsigned)R) continue;
+        for (int v = 0; v < len; ++v) {
+          const unsigned tv = (b * (unsigned)w - (unsigned)shiftlo + (unsigned)v) & maskN;
+          lazy_add(s_tal, (r << lgN) | ((P.p.s2i * tv) & maskN), 1u);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (hist_out) {
+    uint4* h4 = reinterpret_cast<uint4*>(hist_out + k0 / 4);
+    for (int e = tid; e < G / 16; e += nt) h4[e] = t4[e];
+  }
+  if (bits) {
+    for (int blk = 0; blk < G / kCmpElems; ++blk) {
+      const int wl = blk * kCmpWords + tid;
+      uint32_t word = 0;
+      const unsigned thr4 = thr * 0x01010101u;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint32_t m = __vcmpgeu4(s_tal[wl * 8 + u], thr4) & 0x01010101u;
+        word |= ((m | (m >> 7) | (m >> 14) | (m >> 21)) & 15u) << (u * 4);
+      }
+      bits[(k0 >> 5) + wl] = word;
+      const unsigned pre = block_excl_scan256(__popc(word), s_warp);
+      if (tid == kCmpThreads - 1) blk_counts[(k0 >> lgG) * (G / kCmpElems) + blk] = pre + __popc(word);
+      __syncthreads();
+    }
+  }
+}
+
 inline size_t vote_lazy_smem(int lgN, int lgG, int lgBmax) {
   const long G = 1L << lgG, Bm = 1L << lgBmax, R = G >> lgN;
   return (size_t)(G / 4 + 2L * lazy_bm_words(lgBmax) + R * Bm) * 4;
