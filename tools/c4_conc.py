@@ -1,4 +1,5 @@
-"""c4 batched throughput vs in-flight concurrency: python tools/c4_conc.py [images]"""
+"""c4 batched throughput vs in-flight concurrency: python tools/c4_conc.py [images]
+(device-generated c4 images, bench.c4_params seeds)."""
 import os
 import sys
 import time
@@ -8,11 +9,15 @@ import torch  # noqa: E402
 
 import bench  # noqa: E402
 import paper_1908_02461_b200 as P  # noqa: E402
+from paper_1908_02461_b200.signals import device_sparse_image  # noqa: E402
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 96
-xs = [torch.from_numpy(bench.c4_image(i)).cuda() for i in range(n)]
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
+xs = []
+for i in range(n):
+    seed, k = bench.c4_params(i)
+    xs.append(device_sparse_image(1024, k, seed, snr_db=25.0, magnitude="loguniform").x)
 seeds = [1 + i for i in range(n)]
-for conc in (4, 6, 8, 12, 16):
+for conc in (4, 6, 8, 12, 16, 24):
     P.atsfft2d_batch(xs, P.TunerConfig(), 8, seeds, concurrency=conc, precision="fp32", arrays=True)
     torch.cuda.synchronize()
     best = 0.0
