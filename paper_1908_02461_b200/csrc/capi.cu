@@ -108,6 +108,7 @@ struct sfft2d_ctx {
   cudaEvent_t ev_lmax = nullptr;
   cudaEvent_t ev_pass[4] = {nullptr, nullptr, nullptr, nullptr};   // per tuner pass: list complete
   cudaEvent_t ev_fold[4] = {nullptr, nullptr, nullptr, nullptr};   // per tuner pass: fold complete
+  cudaEvent_t ev_fork_votes = nullptr;
   cudaEvent_t ev_vote[2] = {nullptr, nullptr};
   // optional per-launch profiling (CUDA events on the launching stream)
   bool profiling = false;
@@ -1347,6 +1348,53 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     vote_pending[slot & 1] = true;
   };
 
+  // deferred-vote tallies of the archived passes in `lp` (tile by tile in
+  // shared memory), seeded from the histogram when it holds votes already;
+  // thresholded into the compaction bitmask (bits) or written to hist_out
+  auto launch_lazy = [&](cudaStream_t s2, unsigned thr_, uint32_t* bits, unsigned* cnts,
+                         uint32_t* hist_out) {
+    int lgG = 13;
+    while (lgG < 15 && ((long long)1 << (lgG + 1)) * (2 * kNumSMs) <= nkeys) ++lgG;
+    // every bitmap pass staged at once when they fit beside the tallies
+    // (k_vote_lazy2, no per-pass barriers); else one at a time
+    static const bool v2_on = getenv("SFFT2D_OLD_VOTE_LAZY") == nullptr;
+    const size_t smem2 = ((size_t)1 << lgG) + (size_t)bm_used * 4;
+    pre(c, s2);
+    if (v2_on && smem2 <= kMaxDynSmem) {
+      kl(k_vote_lazy2, (unsigned)(nkeys >> lgG), 256, smem2, s2, (const int32_t*)arch,
+         (const uint32_t*)bmarch, (int)bm_used, lp, lgN, lgG,
+         (const uint32_t*)(hist_used ? hist : nullptr), hist_out, thr_, bits, cnts);
+    } else {
+      const size_t smem = vote_lazy_smem(lgN, lgG, lp.lgBmax);
+      kl(k_vote_lazy, (unsigned)(nkeys >> lgG), 256, smem, s2, (const int32_t*)arch,
+         (const uint32_t*)bmarch, lp, lgN, lgG,
+         (const uint32_t*)(hist_used ? hist : nullptr), hist_out, thr_, bits, cnts);
+    }
+    post(c, "k_vote_lazy", s2, (double)nkeys / 8.0 + (hist_used ? (double)nkeys : 0.0) +
+                                   (hist_out ? (double)nkeys : 0.0));
+  };
+  // Once the trajectory reaches B = N only short passes follow: the passes
+  // archived so far are tallied into the histogram on the side stream while
+  // they run, and the final tally adds only the later passes
+  // (SFFT2D_NO_EARLY_VOTES=1: one tally at the end)
+  static const bool early_votes_on = getenv("SFFT2D_NO_EARLY_VOTES") == nullptr;
+  bool early_voted = false;
+  auto early_votes = [&]() {
+    if (!lazy || early_voted || lp.n == 0 || c->profiling || !early_votes_on) return;
+    early_voted = true;
+    cudaStream_t vs = c->vote_st;
+    // list-pass archives are copied on the main stream
+    ck(cudaEventRecord(c->ev_fork_votes, st), "cudaEventRecord");
+    ck(cudaStreamWaitEvent(vs, c->ev_fork_votes, 0), "cudaStreamWaitEvent");
+    const cudaStream_t ws_saved = c->ws_st;
+    c->ws_st = vs;
+    launch_lazy(vs, 0u, nullptr, nullptr, hist);
+    c->ws_st = ws_saved;
+    hist_used = true;      // the histogram now seeds every later tally
+    hist_zeroed = true;    // (and must not be cleared by a later atomic vote)
+    lp.n = 0;              // tallied; later passes are archived from scratch
+  };
+
   // B = N views after the first one test only the above-floor bins of |x_hat|
   // that the first B = N pass listed (while they are few)
   int32_t* cand = nullptr;
@@ -1613,6 +1661,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       have_spec = true;
     }
     const long long cnt = finish_pass(cur);
+    if (cur.bb == n) early_votes();
     bool has = false;
     bool stop = false;
     double r = 0.0;
@@ -1726,26 +1775,9 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   // memory; either thresholded into the compaction bitmask (bits != nullptr)
   // or written out as the histogram (the detect_sparsity API's tallies)
   auto lazy_votes = [&](unsigned thr_, uint32_t* bits, unsigned* cnts, uint32_t* hist_out) {
-    int lgG = 13;
-    while (lgG < 15 && ((long long)1 << (lgG + 1)) * (2 * kNumSMs) <= nkeys) ++lgG;
-    // every bitmap pass staged at once when they fit beside the tallies
-    // (k_vote_lazy2, no per-pass barriers); else one at a time
-    static const bool v2_on = getenv("SFFT2D_OLD_VOTE_LAZY") == nullptr;
-    const size_t smem2 = ((size_t)1 << lgG) + (size_t)bm_used * 4;
-    pre(c, st);
-    if (v2_on && smem2 <= kMaxDynSmem) {
-      kl(k_vote_lazy2, (unsigned)(nkeys >> lgG), 256, smem2, st, (const int32_t*)arch,
-         (const uint32_t*)bmarch, (int)bm_used, lp, lgN, lgG,
-         (const uint32_t*)(hist_used ? hist : nullptr), hist_out, thr_, bits, cnts);
-    } else {
-      const size_t smem = vote_lazy_smem(lgN, lgG, lp.lgBmax);
-      kl(k_vote_lazy, (unsigned)(nkeys >> lgG), 256, smem, st, (const int32_t*)arch,
-         (const uint32_t*)bmarch, lp, lgN, lgG,
-         (const uint32_t*)(hist_used ? hist : nullptr), hist_out, thr_, bits, cnts);
-    }
-    post(c, "k_vote_lazy", st, (double)nkeys / 8.0 + (hist_used ? (double)nkeys : 0.0) +
-                                   (hist_out ? (double)nkeys : 0.0));
+    launch_lazy(st, thr_, bits, cnts, hist_out);
   };
+
 
   if (!do_estimate) {
     unsigned nv = 0;
@@ -2073,6 +2105,7 @@ int sfft2d_ctx_create(int device, sfft2d_ctx** out) {
     ck(cudaEventCreateWithFlags(&c->ev_lmax, cudaEventDisableTiming), "cudaEventCreate");
     ck(cudaEventCreateWithFlags(&c->ev_ws, cudaEventDisableTiming), "cudaEventCreate");
     ck(cudaEventCreateWithFlags(&c->ev_perm, cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventCreateWithFlags(&c->ev_fork_votes, cudaEventDisableTiming), "cudaEventCreate");
     for (int i = 0; i < 4; ++i) {
       ck(cudaEventCreateWithFlags(&c->ev_pass[i], cudaEventDisableTiming), "cudaEventCreate");
       ck(cudaEventCreateWithFlags(&c->ev_fold[i], cudaEventDisableTiming), "cudaEventCreate");
@@ -2125,6 +2158,7 @@ void sfft2d_ctx_destroy(sfft2d_ctx* c) {
   if (c->ev_lmax) cudaEventDestroy(c->ev_lmax);
   if (c->ev_ws) cudaEventDestroy(c->ev_ws);
   if (c->ev_perm) cudaEventDestroy(c->ev_perm);
+  if (c->ev_fork_votes) cudaEventDestroy(c->ev_fork_votes);
   for (int i = 0; i < 4; ++i) {
     if (c->ev_pass[i]) cudaEventDestroy(c->ev_pass[i]);
     if (c->ev_fold[i]) cudaEventDestroy(c->ev_fold[i]);

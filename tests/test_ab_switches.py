@@ -22,6 +22,7 @@ SWITCHES = {
     "SFFT2D_NO_PASS_PIPE": ["c2_ats"],            # post-fold work on the main stream
     "SFFT2D_OLD_VOTE_LAZY": ["c2_ats"],           # one-pass-at-a-time lazy votes
     "SFFT2D_NO_SPEC": ["c2_ats"],                 # no speculative next-pass folds
+    "SFFT2D_NO_EARLY_VOTES": ["c2_ats"],          # one vote tally at the end
 }
 
 SCRIPT = r"""
