@@ -1195,9 +1195,14 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   }
   int32_t* arch = lazy ? (int32_t*)ws(c, "vote_arch", (size_t)arch_cap * kLazyMax * 4) : nullptr;
   long long arch_used = 0;
-  uint32_t* bmarch = lazy ? (uint32_t*)ws(c, "vote_bm", (size_t)lazy_bm_words(std::min(9, lgN)) * kLazyMax * 4)
+  // bitmap archive: the passes' bitmaps built by k_vote_bitmap, then one
+  // staging bitmap per tuner slot that k_small_pass writes itself (B <= 64)
+  const long long small_base = (long long)lazy_bm_words(std::min(9, lgN)) * kLazyMax;
+  const int small_words = lazy_bm_words(6);
+  uint32_t* bmarch = lazy ? (uint32_t*)ws(c, "vote_bm", (size_t)(small_base + 2LL * SFFT2D_MAX_HISTORY * small_words) * 4)
                           : nullptr;
   long long bm_used = 0;
+  int bm_smem_used = 0;   // words of k_vote_lazy2's shared copy of the bitmap passes
   bool hist_used = false;
   // NaN/Inf check (as_complex_matrix, corefft.py:49-50): fused into the dense
   // FFT's row pass when the trajectory reaches B = N, else one pass at the end
@@ -1229,6 +1234,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   int last_b = 0, last_pi = 0;
   cudaEvent_t last_ready = nullptr;
   long long last_count = 0;
+  long long last_bm_off = -1;
 
   // sides >= 2048: the dense FFT stops after four-step pass A (x_hat is never
   // stored), pass B writes |x_hat| only when a B = N tuner pass needs it
@@ -1296,7 +1302,8 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   // the budget cast nothing): in deferred mode the pass's maxima list is
   // archived for k_vote_lazy (bitmap passes B <= 512, short list passes), else
   // one atomic per preimage coordinate into the histogram on the side stream
-  auto vote_list = [&](const Perm& pv, int lgb, int slot, long long count, cudaEvent_t list_ready) {
+  auto vote_list = [&](const Perm& pv, int lgb, int slot, long long count, cudaEvent_t list_ready,
+                       long long prebuilt_off) {
     if (count <= 0) return;
     const int w = n >> lgb;
     const long long len = (w == 1) ? 3 : std::min<long long>(w + 2, n);
@@ -1311,6 +1318,12 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
         // stream (off the tuner's critical path; joined before k_vote_lazy)
         lp.lgBmax = std::max(lp.lgBmax, lgb);
         const int words = lazy_bm_words(lgb);
+        P.soff = bm_smem_used;
+        bm_smem_used += words;
+        if (prebuilt_off >= 0) {   // written by the pass's own k_small_pass
+          P.off = prebuilt_off;
+          return;
+        }
         P.off = bm_used;
         cudaStream_t vs = c->profiling ? st : c->vote_st;
         ck(cudaStreamWaitEvent(vs, list_ready, 0), "cudaStreamWaitEvent");
@@ -1358,7 +1371,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     // every bitmap pass staged at once when they fit beside the tallies
     // (k_vote_lazy2, no per-pass barriers); else one at a time
     static const bool v2_on = getenv("SFFT2D_OLD_VOTE_LAZY") == nullptr;
-    const size_t smem2 = ((size_t)1 << lgG) + (size_t)bm_used * 4;
+    const size_t smem2 = ((size_t)1 << lgG) + (size_t)bm_smem_used * 4;
     pre(c, s2);
     if (v2_on && smem2 <= kMaxDynSmem) {
       kl(k_vote_lazy2, (unsigned)(nkeys >> lgG), 256, smem2, s2, (const int32_t*)arch,
@@ -1393,6 +1406,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     hist_used = true;      // the histogram now seeds every later tally
     hist_zeroed = true;    // (and must not be cleared by a later atomic vote)
     lp.n = 0;              // tallied; later passes are archived from scratch
+    bm_smem_used = 0;
   };
 
   // B = N views after the first one test only the above-floor bins of |x_hat|
@@ -1421,9 +1435,11 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     Perm p;
     cudaEvent_t ready = nullptr;   // the pass's maxima list is complete
     cudaStream_t lst = nullptr;     // the stream that publishes the count
+    long long bm_off = -1;          // vote bitmap written by the pass itself (k_small_pass)
   };
   static const bool pipe_on = getenv("SFFT2D_NO_PIPELINE") == nullptr;
   static const bool pass_pipe_on = getenv("SFFT2D_NO_PASS_PIPE") == nullptr;
+  static const bool small_bm_on = getenv("SFFT2D_NO_SMALL_BITMAP") == nullptr;
   // the B = N/2 pass from the dense spectrum: x_hat stored (not factored),
   // untruncated 5-tap window, 512 <= B <= 2048 (SFFT2D_NO_PASSCONV=1: fold + FFT)
   static const bool passconv_on = getenv("SFFT2D_NO_PASSCONV") == nullptr;
@@ -1546,12 +1562,19 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       pre(c, lst);
       if (BB > 4 * 1024) fail(SFFT2D_ERR_UNSUPPORTED, "small pass holds at most 4 bins per thread");
       const size_t sps = (size_t)bb * (bb + 1) * sizeof(C) + BB * sizeof(T) + bb * sizeof(C);
+      // the pass writes its own vote bitmap (used if it votes): no bitmap
+      // kernel / memset later
+      uint32_t* sbm = nullptr;
+      if (lazy && lgb <= 6 && small_bm_on) {
+        tk.bm_off = small_base + (long long)slot * small_words;
+        sbm = bmarch + tk.bm_off;
+      }
       if (BB <= 1024)   // one (bin, partial-slice) slot per thread
         kl(k_small_pass<T, 1>, 1, 1024, sps, lst, (const C*)fo.data, fo.Z, fo.Z == 1, lgb, p,
-           (const C*)tb.tw[prec_of<T>()], lgN, cf.mag_floor, ml, cnt, pub);
+           (const C*)tb.tw[prec_of<T>()], lgN, cf.mag_floor, ml, cnt, pub, sbm);
       else
         kl(k_small_pass<T, 4>, 1, 1024, sps, lst, (const C*)fo.data, fo.Z, fo.Z == 1, lgb, p,
-           (const C*)tb.tw[prec_of<T>()], lgN, cf.mag_floor, ml, cnt, pub);
+           (const C*)tb.tw[prec_of<T>()], lgN, cf.mag_floor, ml, cnt, pub, sbm);
       post(c, "k_small_pass", lst, (double)(fo.Z + 1) * BB * sizeof(C));
       c->ws_set = 0;
     } else {
@@ -1622,11 +1645,12 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     last_count = count;
     last_slot = tk.slot;
     last_ready = tk.ready;
+    last_bm_off = tk.bm_off;
     const int lgb = ilog2(tk.bb);
     const long long w = n / tk.bb;
     const long long len = (w == 1) ? 3 : std::min<long long>(w + 2, n);
     if (count > 0 && count * len * len <= budget) {   // tuner.py:165,175
-      vote_list(tk.p, lgb, tk.slot, count, tk.ready);
+      vote_list(tk.p, lgb, tk.slot, count, tk.ready, tk.bm_off);
       ++vote_passes;
       have_votes = true;
     }
@@ -1760,7 +1784,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     if (last_count > 0) {
       // its list and count slot are intact (later passes were discarded
       // speculation writing the other list buffer)
-      vote_list(ps.hp[last_pi], ilog2(last_b), last_slot, last_count, last_ready);
+      vote_list(ps.hp[last_pi], ilog2(last_b), last_slot, last_count, last_ready, last_bm_off);
       have_votes = true;
     }
     vote_passes = 1;

@@ -988,7 +988,7 @@ __global__ void __launch_bounds__(1024)
 k_small_pass(const cplx<T>* __restrict__ part, int Z, bool permuted, int lgB, Perm p,
              const cplx<T>* __restrict__ tw, int lgN, double floor_rel,
              int32_t* __restrict__ list, unsigned* __restrict__ count,
-             Publish pub = Publish{nullptr, 0, nullptr, 0}) {
+             Publish pub = Publish{nullptr, 0, nullptr, 0}, uint32_t* __restrict__ bm = nullptr) {
   pdl_wait();
   using C = cplx<T>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1000,7 +1000,8 @@ k_small_pass(const cplx<T>* __restrict__ part, int Z, bool permuted, int lgB, Pe
   T* m = reinterpret_cast<T*>(s + (size_t)B * RS);
   __shared__ unsigned long long s_peak;
   __shared__ unsigned s_n;
-  if (threadIdx.x == 0) { s_peak = 0; s_n = 0; }
+  __shared__ unsigned s_rowflag[2];   // B <= 64: bin rows holding a maximum
+  if (threadIdx.x == 0) { s_peak = 0; s_n = 0; s_rowflag[0] = 0u; s_rowflag[1] = 0u; }
   const unsigned maskB = (unsigned)B - 1u;
   // tpe threads per bin split the Z partials (fixed combination order:
   // deterministic); a shuffle tree joins the slices
@@ -1091,15 +1092,27 @@ k_small_pass(const cplx<T>* __restrict__ part, int Z, bool permuted, int lgB, Pe
       }
     }
     const unsigned bal = __ballot_sync(0xffffffffu, f);
+    // the vote bitmap of the pass (k_vote_bitmap's layout: bin bits, then
+    // row flags), written whole: every word of the grid once
+    if (bm && (threadIdx.x & 31) == 0 && (e - (int)(threadIdx.x & 31)) < BB)
+      bm[(e - (int)(threadIdx.x & 31)) >> 5] = bal;
     if (bal) {
       unsigned base = 0;
       if ((threadIdx.x & 31) == 0) base = atomicAdd(&s_n, (unsigned)__popc(bal));
       base = __shfl_sync(0xffffffffu, base, 0);
-      if (f) list[base + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = e;
+      if (f) {
+        list[base + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u))] = e;
+        if (bm) atomicOr(&s_rowflag[(e >> lgB) >> 5], 1u << ((e >> lgB) & 31));
+      }
     }
   }
   __syncthreads();
   if (threadIdx.x == 0) {
+    if (bm) {
+      uint32_t* flags = bm + (((BB + 31) / 32 + 3) & ~3);
+      flags[0] = s_rowflag[0];
+      if (B > 32) flags[1] = s_rowflag[1];
+    }
     *count = s_n;
     if (pub.slot) publish_count(count, pub.done, pub.target, pub.slot, pub.seq);
   }

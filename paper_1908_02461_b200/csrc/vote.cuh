@@ -99,6 +99,7 @@ struct LazyPass {
   int count;
   long long off;                    // list passes: first entry in the list archive;
                                     // bitmap passes: first word of the bitmap archive
+  int soff;                         // bitmap passes: first word in k_vote_lazy2's shared copy
 };
 
 // words of one archived bitmap pass: B^2 bits, then B row-flag bits, each
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(256) k_vote_lazy(const int32_t* __restrict__ a
 // all warps.
 __global__ void __launch_bounds__(256) k_vote_lazy2(const int32_t* __restrict__ arch,
                                                      const uint32_t* __restrict__ bmarch,
-                                                     int bm_words, LazyPasses lp, int lgN, int lgG,
+                                                     int /*smem bitmap words*/, LazyPasses lp, int lgN, int lgG,
                                                      const uint32_t* __restrict__ hist_init,
                                                      uint32_t* __restrict__ hist_out, unsigned thr,
                                                      uint32_t* __restrict__ bits,
@@ -323,9 +324,15 @@ __global__ void __launch_bounds__(256) k_vote_lazy2(const int32_t* __restrict__ 
   const size_t k0 = (size_t)blockIdx.x << lgG;
   const unsigned i0 = (unsigned)(k0 >> lgN);
   uint32_t* s_tal = sm_vote;            // G bytes
-  uint32_t* s_bm = s_tal + G / 4;       // every bitmap pass, archive layout
+  uint32_t* s_bm = s_tal + G / 4;       // every bitmap pass, at its soff
   uint4* t4 = reinterpret_cast<uint4*>(s_tal);
-  for (int e = tid * 4; e < bm_words; e += nt * 4) cp_async16(s_bm + e, bmarch + e);
+  for (int ps = 0; ps < lp.n; ++ps) {
+    if (lp.v[ps].lgB > lp.lgBmax) continue;
+    const int words = lazy_bm_words(lp.v[ps].lgB);
+    const uint32_t* src = bmarch + lp.v[ps].off;
+    uint32_t* dst = s_bm + lp.v[ps].soff;
+    for (int e = tid * 4; e < words; e += nt * 4) cp_async16(dst + e, src + e);
+  }
   cp_async_commit();
   if (hist_init) {
     const uint4* h4 = reinterpret_cast<const uint4*>(hist_init + k0 / 4);
@@ -350,7 +357,7 @@ __global__ void __launch_bounds__(256) k_vote_lazy2(const int32_t* __restrict__ 
     const int lgw = lgN - lgB, w = 1 << lgw;
     const int len = (w == 1) ? 3 : w + 2;
     const int shiftlo = w / 2 + 1;   // floor(w/2) + expand
-    const uint32_t* s_bits = s_bm + P.off;
+    const uint32_t* s_bits = s_bm + P.soff;
     const uint32_t* s_flag = s_bits + (((B * B + 31) / 32 + 3) & ~3);
     const unsigned t = (P.p.s1 * (i0 + (unsigned)r)) & maskN;
     const int hi = (int)((t + (unsigned)N + (unsigned)shiftlo) >> lgw);

@@ -23,6 +23,7 @@ SWITCHES = {
     "SFFT2D_OLD_VOTE_LAZY": ["c2_ats"],           # one-pass-at-a-time lazy votes
     "SFFT2D_NO_SPEC": ["c2_ats"],                 # no speculative next-pass folds
     "SFFT2D_NO_EARLY_VOTES": ["c2_ats"],          # one vote tally at the end
+    "SFFT2D_NO_SMALL_BITMAP": ["c2_ats"],         # small-pass vote bitmaps by k_vote_bitmap
 }
 
 SCRIPT = r"""
