@@ -976,7 +976,7 @@ unsigned hist_compact(sfft2d_ctx* c, const uint32_t* hist, long nkeys, int mode,
 template <typename T, typename Tin>
 void dense_xhat(sfft2d_ctx* c, const Tin* x, int lgN, const DevTables& tb, cplx<T>* xhat, T* mags,
                 unsigned long long* peak, cudaStream_t st, unsigned* nonfinite = nullptr) {
-  if (peak) ck(cudaMemsetAsync(peak, 0, sizeof(unsigned long long), st), "memset");
+  // (peak: zeroed by the caller — run_ats's per-call scratch)
   dense_fft<T, Tin>(c, x, xhat, mags, peak, lgN, (const cplx<T>*)tb.tw[prec_of<T>()], st,
                     nonfinite);
 }
@@ -1036,8 +1036,22 @@ void finish_select(sfft2d_ctx* c, int lgN, const int32_t* keys, unsigned m, long
 }
 
 
+// Per-call scratch of small counters, zeroed by ONE memset at the start of a
+// tuner run (each cudaMemsetAsync is a stream op of its own): the NaN flag,
+// the estimation scalars, the candidate count, the dense peak, one peak per
+// tuner slot and one count per tuner slot.
+constexpr size_t kScrFinite = 0, kScrEst = 16, kScrCand = 48, kScrXpeak = 64, kScrPeaks = 80;
+constexpr size_t kScrCounts = kScrPeaks + 8 * 2 * SFFT2D_MAX_HISTORY;
+constexpr size_t kScrBytes = kScrCounts + 4 * 2 * SFFT2D_MAX_HISTORY;
+unsigned char* call_scratch(sfft2d_ctx* c) {
+  const int saved = c->ws_set;
+  c->ws_set = 0;
+  unsigned char* p = (unsigned char*)ws(c, "call_scratch", kScrBytes);
+  c->ws_set = saved;
+  return p;
+}
 unsigned long long* est_scalars(sfft2d_ctx* c) {
-  return (unsigned long long*)ws(c, "est_scalars", 32);
+  return (unsigned long long*)(call_scratch(c) + kScrEst);
 }
 void zero_est_scalars(sfft2d_ctx* c, cudaStream_t st) {
   ck(cudaMemsetAsync(est_scalars(c), 0, 32, st), "memset");
@@ -1206,8 +1220,9 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
   bool hist_used = false;
   // NaN/Inf check (as_complex_matrix, corefft.py:49-50): fused into the dense
   // FFT's row pass when the trajectory reaches B = N, else one pass at the end
-  unsigned* finite = (unsigned*)ws(c, "finite", 16);
-  ck(cudaMemsetAsync(finite, 0, 16, st), "memset");
+  unsigned char* scr = call_scratch(c);
+  ck(cudaMemsetAsync(scr, 0, kScrBytes, st), "memset scratch");
+  unsigned* finite = (unsigned*)(scr + kScrFinite);
   bool finite_scanned = false;
   // whatever path leaves run_ats, later work on st is ordered after the side
   // stream's (post-fold work of speculative passes, votes)
@@ -1249,8 +1264,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       }
       if (need_mags && !M) {
         M = (T*)ws(c, "xmag", (size_t)nkeys * sizeof(T));
-        peakM = (unsigned long long*)ws(c, "xpeak", 16);
-        ck(cudaMemsetAsync(peakM, 0, 16, st), "memset");
+        peakM = (unsigned long long*)(scr + kScrXpeak);   // zeroed with the scratch
         dense_fft_mags<T>(c, M, peakM, lgN, tw, st);
       }
       return;
@@ -1259,7 +1273,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       xhat = (C*)ws(c, "xhat", (size_t)nkeys * sizeof(C));
       if (need_mags) {
         M = (T*)ws(c, "xmag", (size_t)nkeys * sizeof(T));
-        peakM = (unsigned long long*)ws(c, "xpeak", 16);
+        peakM = (unsigned long long*)(scr + kScrXpeak);
       }
       dense_xhat<T, Tin>(c, x, lgN, tb, xhat, M, peakM, st, finite);   // |x_hat|, peak, NaN check
       finite_scanned = true;
@@ -1267,8 +1281,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     }
     if (need_mags && !M) {
       M = (T*)ws(c, "xmag", (size_t)nkeys * sizeof(T));
-      peakM = (unsigned long long*)ws(c, "xpeak", 16);
-      ck(cudaMemsetAsync(peakM, 0, 16, st), "memset");
+      peakM = (unsigned long long*)(scr + kScrXpeak);
       mags_of<T>(c, xhat, nkeys, 1, M, peakM, st);
     }
   };
@@ -1292,8 +1305,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
 
   // per-pass count slots (zeroed once), double-buffered maxima lists: the
   // vote of pass k runs on the side stream while pass k+1 proceeds
-  unsigned* cnt_slots = (unsigned*)ws(c, "lm_counts", (size_t)2 * SFFT2D_MAX_HISTORY * 4);
-  ck(cudaMemsetAsync(cnt_slots, 0, (size_t)2 * SFFT2D_MAX_HISTORY * 4, st), "memset");
+  unsigned* cnt_slots = (unsigned*)(scr + kScrCounts);   // zeroed with the scratch
   int32_t* maxlists[2] = {maxlist, (int32_t*)ws(c, "maxlist2", (size_t)(nkeys / 4 + 64) * 4)};
   bool vote_pending[2] = {false, false};
   int npass = 0;
@@ -1487,8 +1499,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
         post(c, "k_lmax_cand", st, (double)(cand_ready ? cand_n : nkeys / 32) * 9 * sizeof(T));
       } else if (!listed) {
         cand = (int32_t*)ws(c, "cand", (size_t)nkeys * 4);
-        cand_cnt = (unsigned*)ws(c, "cand_cnt", 16);
-        ck(cudaMemsetAsync(cand_cnt, 0, 16, st), "memset");
+        cand_cnt = (unsigned*)(scr + kScrCand);   // zeroed with the scratch
         bool emitted = false;
         seq = lmax_tuner<T>(c, M, lgb, peakM, cf.mag_floor, ml, cnt, st, true, p.s1i, p.s2i, p.s2,
                             cand, cand_cnt, &emitted);
@@ -1503,8 +1514,8 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       wait_list_free();
       ensure_xhat(true);
       T* mg = (T*)ws(c, "grid_mag", BB * sizeof(T));
-      unsigned long long* pk = (unsigned long long*)ws(c, "gpeak", 16);
-      ck(cudaMemsetAsync(pk, 0, 16, st), "memset");
+      // this slot's peak, zeroed with the scratch
+      unsigned long long* pk = (unsigned long long*)(scr + kScrPeaks) + slot;
       const T* freq = (const T*)tb.freq[prec_of<T>()] + ((size_t)lgb << lgN);
       const C* tw = (const C*)tb.tw[prec_of<T>()];
       constexpr int RB = sizeof(T) == 4 ? 4 : 2;
@@ -1836,8 +1847,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     return;
   }
   const unsigned thr = (unsigned)((std::max(vote_passes, 1) + 1) / 2);
-  unsigned m;
-  zero_est_scalars(c, st);
+  unsigned m;   // (the estimation scalars were zeroed with the scratch)
   if (lazy) {
     uint32_t* bits = (uint32_t*)ws(c, "hc_bits", words_for(nkeys) * 4);
     unsigned* cnts = (unsigned*)ws(c, "hc_cnt", (size_t)blocks_for(nkeys) * 4);

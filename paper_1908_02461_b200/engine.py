@@ -110,6 +110,11 @@ def to_dict(ij: np.ndarray, vals: np.ndarray) -> dict:
 
 
 def _stream(torch, device):
+    """The raw handle of `device`'s current stream (torch's C getter when it
+    exists: ~1 us less than building a torch.cuda.Stream object per call)."""
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return raw(device if isinstance(device, int) else torch.device(device).index)
     return torch.cuda.current_stream(device).cuda_stream
 
 
