@@ -332,4 +332,93 @@ __global__ void k_gather_out(const int32_t* __restrict__ pos, const unsigned* __
   }
 }
 
+// Fused K6 + K7 tail for a dense (B == N) estimate of a small candidate set
+// with no top-k cut (engine.py:163-253 with b_estimate = N): ONE CTA reads
+// x_hat at the m candidates (every loop's estimate is x_hat[i, j], see
+// k_estimate_dense), takes the peak |v|, prunes against prune_rel * peak,
+// compacts the survivors in key order and writes (i, j), values and the count
+// straight into mapped host memory.  m is read from device memory, so the
+// launch does not wait for the host to learn the candidate count: when
+// m > limit (the host sized the launch for at most `limit` candidates, and
+// limit <= k guarantees that no cut is needed) the kernel only reports m and
+// the host takes the general path.  Publication: slot[2] = m, slot[3] = the
+// NaN/Inf flag of the input scan, then (count, seq) as one 8-byte word after
+// a system fence — the host spins on seq (no stream synchronisation).  Same
+// predicate and order as k_estimate_dense + k_final_bits + compaction +
+// k_gather_out.
+constexpr unsigned kFinishSmallMax = 16384;
+constexpr unsigned kFinishFallback = 0xffffffffu;
+
+template <typename T>
+__global__ void __launch_bounds__(1024)
+k_finish_dense_small(const cplx<T>* __restrict__ xhat, const int32_t* __restrict__ keys,
+                     const unsigned* __restrict__ m_dev, unsigned limit, bool usable_all,
+                     double prune_rel, const unsigned* __restrict__ nonfinite, int lgN,
+                     int64_t* __restrict__ out_ij, cplx<T>* __restrict__ out_v,
+                     volatile unsigned* slot, unsigned seq) {
+  pdl_wait();
+  __shared__ unsigned long long s_best[32];
+  __shared__ unsigned s_warp[32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned m = *m_dev;
+  const unsigned bad = nonfinite ? *nonfinite : 0u;
+  auto publish = [&](unsigned count) {   // thread 0, after the block's output writes
+    slot[2] = m;
+    slot[3] = bad;
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned long long*>(slot) =
+        ((unsigned long long)count << 32) | (unsigned long long)seq;
+  };
+  if (m > limit || m == 0u || bad || !usable_all) {   // block-uniform
+    if (tid == 0) publish(m > limit ? kFinishFallback : 0u);
+    return;
+  }
+  const unsigned per = (m + 1023u) >> 10;            // <= kFinishSmallMax / 1024
+  const unsigned i0 = min(m, (unsigned)tid * per), i1 = min(m, i0 + per);
+  unsigned long long best = 0ull;
+#pragma unroll 4
+  for (unsigned i = i0; i < i1; ++i) {
+    const unsigned long long k = fkey(cabs_(xhat[(uint32_t)keys[i]]));
+    best = k > best ? k : best;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+    best = t > best ? t : best;
+  }
+  if (lane == 0) s_best[warp] = best;
+  __syncthreads();
+  best = s_best[lane];
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
+    best = t > best ? t : best;
+  }
+  const double floor_v = prune_rel > 0 ? prune_rel * fkey_inv(best) : -1.0;
+  unsigned keep = 0;                                  // bit j: candidate i0 + j survives
+  for (unsigned i = i0; i < i1; ++i) {
+    const T a = cabs_(xhat[(uint32_t)keys[i]]);
+    if (prune_rel <= 0 || (double)a >= floor_v) keep |= 1u << (i - i0);
+  }
+  const unsigned cnt = (unsigned)__popc(keep);
+  const unsigned inc = warp_incl_scan(cnt);
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  if (warp == 0) s_warp[lane] = warp_incl_scan(s_warp[lane]);
+  __syncthreads();
+  unsigned pos = inc - cnt + (warp ? s_warp[warp - 1] : 0u);
+  const unsigned total = s_warp[31];
+  const unsigned maskN = (1u << lgN) - 1u;
+  while (keep) {
+    const unsigned j = (unsigned)__ffs(keep) - 1u;
+    keep &= keep - 1u;
+    const unsigned key = (unsigned)keys[i0 + j];
+    out_ij[2 * (size_t)pos] = key >> lgN;
+    out_ij[2 * (size_t)pos + 1] = key & maskN;
+    out_v[pos] = xhat[key];
+    ++pos;
+  }
+  if (cnt) __threadfence_system();   // the results land before the count
+  __syncthreads();
+  if (tid == 0) publish(total);
+}
+
 }  // namespace sfft
