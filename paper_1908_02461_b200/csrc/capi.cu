@@ -828,7 +828,7 @@ unsigned lmax_tuner(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long l
                     double floor_rel, int32_t* list, unsigned* count, cudaStream_t st, bool perm,
                     unsigned s1, unsigned s2, unsigned s2inv, int32_t* cand = nullptr,
                     unsigned* cand_count = nullptr, bool* emitted = nullptr,
-                    bool live_most = false) {
+                    bool live_most = false, bool count64 = false) {
   if (emitted) *emitted = false;
   const int B = 1 << lgB;
   const double by = (double)B * B * sizeof(T);
@@ -844,6 +844,34 @@ unsigned lmax_tuner(sfft2d_ctx* c, const T* mags, int lgB, const unsigned long l
     const bool win = live_most && !cand && B <= 4096;
     const int thr = 512;
     const size_t sm = nslot * row + wb;
+    // count64: `count` is the low word of an 8-byte slot whose high word is
+    // free for the CTA tickets (k_lmax_win2; SFFT2D_OLD_LMAX_WIN=1: k_lmax_win)
+    static const bool win2_on = getenv("SFFT2D_OLD_LMAX_WIN") == nullptr;
+    if (win && count64 && win2_on) {
+      const int groups = B / 32;
+      const int gpw = std::max(1, groups / 16);
+      const int tw2 = 32 * (groups / gpw);
+      auto go = [&](auto G) {
+        constexpr int GPW = decltype(G)::value;
+        const int resident = ctas_per_sm(k_lmax_win2<T, GPW>, tw2, sm);
+        const int cps = std::max(1, std::min(2, resident));
+        const int band = (B + cps * kNumSMs - 1) / (cps * kNumSMs);
+        const int grid = (B + band - 1) / band;
+        const Publish pub = make_publish(c, (unsigned)grid);
+        pre(c, st);
+        kl(k_lmax_win2<T, GPW>, grid, tw2, sm, st, mags, lgB, perm ? s1 : 1u, perm ? s2 : 1u, band,
+           nslot, peak, floor_rel, list, reinterpret_cast<unsigned long long*>(count),
+           (unsigned)grid, pub.slot, pub.seq);
+        post(c, "k_lmax_win", st, by);
+        return pub.seq;
+      };
+      switch (gpw) {
+        case 1: return go(std::integral_constant<int, 1>{});
+        case 2: return go(std::integral_constant<int, 2>{});
+        case 4: return go(std::integral_constant<int, 4>{});
+        default: return go(std::integral_constant<int, 8>{});
+      }
+    }
     const int tw_win = std::min(512, B / 4);
     const int resident = win ? ((B / 128 > 16) ? ctas_per_sm(k_lmax_win<T, 2>, tw_win, sm)
                                                : ctas_per_sm(k_lmax_win<T, 1>, tw_win, sm))
@@ -1042,7 +1070,7 @@ void finish_select(sfft2d_ctx* c, int lgN, const int32_t* keys, unsigned m, long
 // tuner slot and one count per tuner slot.
 constexpr size_t kScrFinite = 0, kScrEst = 16, kScrCand = 48, kScrXpeak = 64, kScrPeaks = 80;
 constexpr size_t kScrCounts = kScrPeaks + 8 * 2 * SFFT2D_MAX_HISTORY;
-constexpr size_t kScrBytes = kScrCounts + 4 * 2 * SFFT2D_MAX_HISTORY;
+constexpr size_t kScrBytes = kScrCounts + 8 * 2 * SFFT2D_MAX_HISTORY;
 unsigned char* call_scratch(sfft2d_ctx* c) {
   const int saved = c->ws_set;
   c->ws_set = 0;
@@ -1342,7 +1370,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
         ck(cudaMemsetAsync(bmarch + bm_used, 0, (size_t)words * 4, vs), "memset bitmap");
         pre(c, vs);
         kl(k_vote_bitmap, grid_for(count, 256, kNumSMs), 256, 0, vs,
-           (const int32_t*)maxlists[slot & 1], (const unsigned*)(cnt_slots + slot), lgb,
+           (const int32_t*)maxlists[slot & 1], (const unsigned*)(cnt_slots + 2 * slot), lgb,
            bmarch + bm_used);
         post(c, "k_vote_bitmap", vs, (double)count * 4.0);
         ck(cudaEventRecord(c->ev_vote[slot & 1], vs), "cudaEventRecord");
@@ -1367,7 +1395,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     const long long total = count * len * len;
     pre(c, vs);
     kl(k_vote, grid_for(total, 256, kNumSMs * 2), 256, 0, vs, maxlists[slot & 1], 0,
-       cnt_slots + slot, 0, nullptr, lgN, lgb, 1, mode, 0, hist, 0LL, pv);
+       cnt_slots + 2 * slot, 0, nullptr, lgN, lgb, 1, mode, 0, hist, 0LL, pv);
     post(c, "k_vote", vs, (double)total * 4.0);
     ck(cudaEventRecord(c->ev_vote[slot & 1], vs), "cudaEventRecord");
     vote_pending[slot & 1] = true;
@@ -1470,7 +1498,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     tk.slot = slot;
     if (slot >= 2 * SFFT2D_MAX_HISTORY) fail(SFFT2D_ERR_UNSUPPORTED, "too many tuner passes");
     int32_t* ml = maxlists[slot & 1];
-    unsigned* cnt = cnt_slots + slot;
+    unsigned* cnt = cnt_slots + 2 * slot;   // 8-byte slots: count, CTA tickets (k_lmax_win2)
     // the vote two passes back still reads this list: a list written on the
     // main stream waits for it; the side stream runs votes and lists in order
     auto wait_list_free = [&]() {
@@ -1490,7 +1518,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       const bool listed = cand_ready || cand_pending;   // the device count is exact either way
       if (listed && (!cand_ready || cand_n <= nkeys / 32)) {
         const unsigned grid = cand_ready ? grid_for(std::max<long long>(cand_n, 1), 256, kNumSMs * 8)
-                                         : (unsigned)(kNumSMs * 8);
+                                         : (unsigned)(kNumSMs * 2);
         const Publish pub = make_publish(c, grid);
         seq = pub.seq;
         pre(c, st);
@@ -1534,7 +1562,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       // (2 RB + 2 RT - 1) / (2 RB) of x_hat, are the kernel's own overhead)
       post(c, "k_pass_conv", st, (double)n * n * sizeof(C) + (double)BB * sizeof(T));
       seq = lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, ml, cnt, st, true, 1u, 1u, 1u, nullptr, nullptr,
-                          nullptr, true);
+                          nullptr, true, true);
     } else if (BB * sizeof(C) <= (size_t)kSmall2DBytes) {
       if (!side) wait_list_free();
       c->ws_set = side ? slot % 3 : 0;
@@ -1624,7 +1652,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       const cudaStream_t ws_saved = c->ws_st;
       c->ws_st = lst;
       seq = lmax_tuner<T>(c, mg, lgb, pk, cf.mag_floor, ml, cnt, lst, true, p.s1i & mb, p.s2i & mb,
-                          p.s2 & mb, nullptr, nullptr, nullptr, true);
+                          p.s2 & mb, nullptr, nullptr, nullptr, true, true);
       c->ws_st = ws_saved;
       c->ws_set = 0;
     }

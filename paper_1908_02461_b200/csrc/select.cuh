@@ -536,6 +536,146 @@ k_lmax_win(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, unsigned 
   }
 }
 
+// k_lmax_win with the lanes of a warp on 32 CONSECUTIVE VIEW COLUMNS
+// c = 32 g + lane (natural column s2 * c: an odd stride, so every shared load
+// is conflict-free).  Each lane keeps the last two view rows of its own
+// column in registers and loads ONE value per bin and row; the vertical
+// 3-maxima of the left / right neighbour columns come from the neighbour
+// lanes by shuffle (lanes 0 and 31 keep the column just outside the group in
+// a second register window, loaded by one more instruction per group and
+// row), so a bin costs 2 shared loads, 4 max and 2 shuffles instead of 3 loads
+// and 7 max, and a group's maxima are one ballot: keys rowbase | c, no scan.
+// The CTA's maxima are appended with ONE 64-bit atomic on `cd`, which holds
+// the count in its low word (read by later kernels as the list length) and
+// the CTA tickets in its high word: the CTA taking the last ticket knows the
+// final count from the same atomic and publishes (count, seq) to the mapped
+// slot — one L2 round trip per CTA instead of count atomics per warp + fence
+// + ticket + count read-back.  Same predicate, list (as a set) and
+// publication as k_lmax_win.  GPW = 32-column groups per warp
+// (blockDim.x = 32 * (B / 32 / GPW)).
+template <typename T, int GPW>
+__global__ void __launch_bounds__(512)
+k_lmax_win2(const T* __restrict__ M, int lgB, unsigned s1, unsigned s2, int band, int nslot,
+            const unsigned long long* __restrict__ peak, double floor_rel,
+            int32_t* __restrict__ list, unsigned long long* __restrict__ cd, unsigned target,
+            volatile unsigned* slot, unsigned seq) {
+  pdl_wait();
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) unsigned long long s_bar[8];
+  __shared__ unsigned s_n[17];
+  T* ring = reinterpret_cast<T*>(smem_raw);
+  const int B = 1 << lgB;
+  const unsigned mask = (unsigned)B - 1u;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  int32_t* wbuf = reinterpret_cast<int32_t*>(ring + ((size_t)nslot << lgB)) + warp * kWarpBuf;
+  const int r0 = blockIdx.x * band;
+  const int nrow = min(band, B - r0);
+  const int nload = nrow + 2;
+  const unsigned row_bytes = (unsigned)(sizeof(T) << lgB);
+  auto issue = [&](int t) {
+    const int sl = t % nslot;
+    const unsigned r = (unsigned)(r0 - 1 + t) & mask;
+    mbar_expect_tx(&s_bar[sl], row_bytes);
+    bulk_g2s(ring + ((size_t)sl << lgB), M + ((size_t)((s1 * r) & mask) << lgB), row_bytes,
+             &s_bar[sl]);
+  };
+  if (threadIdx.x < nslot) mbar_init(&s_bar[threadIdx.x], 1);
+  mbar_fence_init();
+  __syncthreads();
+  if (threadIdx.x == 0)
+    for (int t = 0; t < min(nslot, nload); ++t) issue(t);
+  const double pk = fkey_inv(*peak);
+  const double fl = floor_rel * pk;
+  T flT = sizeof(T) == 4 ? (T)__double2float_ru(fl) : (T)fl;
+  if (!(pk > 0.0))
+    flT = sizeof(T) == 4 ? (T)__int_as_float(0x7f800000) : (T)__longlong_as_double(0x7ff0000000000000ll);
+  int nbuf = 0;
+  auto flush = [&]() {   // a warp buffer that filled up before the end of the band
+    __syncwarp();
+    unsigned base = 0;
+    if (lane == 0 && nbuf) base = (unsigned)atomicAdd(cd, (unsigned long long)nbuf);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (int e = lane; e < nbuf; e += 32) list[base + e] = wbuf[e];
+    __syncwarp();
+    nbuf = 0;
+  };
+  unsigned phase = 0;
+  auto wait_slot = [&](int sl) {
+    mbar_wait(&s_bar[sl], (phase >> sl) & 1u);
+    phase ^= 1u << sl;
+  };
+  auto next = [&](int sl) { return sl + 1 == nslot ? 0 : sl + 1; };
+  unsigned oc[GPW], oe[GPW];          // natural columns of the lane's own / edge view column
+  T up[GPW], md[GPW], eu[GPW], em[GPW];
+  int su = 0, sm = next(0), sd = next(sm);
+  wait_slot(su);
+  wait_slot(sm);
+  {
+    const T* ru = ring + ((size_t)su << lgB);
+    const T* rm = ring + ((size_t)sm << lgB);
+#pragma unroll
+    for (int q = 0; q < GPW; ++q) {
+      const unsigned c = ((unsigned)(warp + q * nwarps) << 5) + (unsigned)lane;
+      oc[q] = (s2 * c) & mask;
+      oe[q] = (s2 * (lane < 16 ? c - 1u : c + 1u)) & mask;
+      up[q] = ru[oc[q]]; md[q] = rm[oc[q]];
+      eu[q] = ru[oe[q]]; em[q] = rm[oe[q]];
+    }
+  }
+  const unsigned lt = (1u << lane) - 1u;
+  for (int s = 0; s < nrow; ++s) {
+    wait_slot(sd);
+    const T* rd = ring + ((size_t)sd << lgB);
+    const unsigned rowbase = (unsigned)(r0 + s) << lgB;
+#pragma unroll
+    for (int q = 0; q < GPW; ++q) {
+      const T dn = rd[oc[q]], ed = rd[oe[q]];
+      const T vm = fmax(fmax(up[q], md[q]), dn);      // vertical 3-max of the own column
+      const T ve = fmax(fmax(eu[q], em[q]), ed);      // ... of the column outside the group
+      T vl = __shfl_up_sync(0xffffffffu, vm, 1);
+      T vr = __shfl_down_sync(0xffffffffu, vm, 1);
+      if (lane == 0) vl = ve;
+      if (lane == 31) vr = ve;
+      const T nb = fmax(fmax(vl, vr), fmax(up[q], dn));
+      const T v = md[q];
+      const bool f = (v >= flT) & (v > nb);
+      up[q] = v; md[q] = dn; eu[q] = em[q]; em[q] = ed;
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (bal) {
+        const int n = __popc(bal);
+        if (nbuf + n > kWarpBuf) flush();
+        if (f) wbuf[nbuf + __popc(bal & lt)] =
+            (int32_t)(rowbase | (((unsigned)(warp + q * nwarps) << 5) + (unsigned)lane));
+        nbuf += n;
+      }
+    }
+    __syncthreads();                           // every thread is done with load s
+    if (threadIdx.x == 0 && s + nslot < nload) issue(s + nslot);
+    su = sm;
+    sm = sd;
+    sd = next(sd);
+  }
+  // the CTA's buffered maxima: one atomic for the positions and the ticket
+  if (lane == 0) s_n[warp] = (unsigned)nbuf;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned t = 0;
+    for (int w = 0; w < nwarps; ++w) {
+      const unsigned a = s_n[w];
+      s_n[w] = t;
+      t += a;
+    }
+    const unsigned long long old = atomicAdd(cd, (1ull << 32) | (unsigned long long)t);
+    s_n[16] = (unsigned)old;
+    if ((unsigned)(old >> 32) + 1u == target && slot)
+      *reinterpret_cast<volatile unsigned long long*>(slot) =
+          ((unsigned long long)((unsigned)old + t) << 32) | (unsigned long long)seq;
+  }
+  __syncthreads();
+  const unsigned base = s_n[16] + s_n[warp];
+  for (int e = lane; e < nbuf; e += 32) list[base + e] = wbuf[e];
+}
+
 // Local maxima of a permuted view of |x_hat| at B = N tested only at the
 // above-floor bins `cand` (natural indices R*N + C, from the first B = N
 // pass): view (r, c) = (s1i^-1 R, s2i^-1 C) has its view neighbours at the
@@ -573,6 +713,11 @@ __global__ void k_lmax_cand(const T* __restrict__ M, int lgB, unsigned s1, unsig
   const unsigned mask = (1u << lgB) - 1u;
   const unsigned n = *cand_count;
   __shared__ unsigned s_tmp[33];
+  // a single CTA needs no atomics: positions from a running total, the count
+  // stored and published directly (three L2 round trips less on the tuner's
+  // critical path: count atomic, ticket, count read-back)
+  const bool solo = gridDim.x == 1;
+  unsigned run = 0;
   for (unsigned e0 = blockIdx.x * blockDim.x; e0 < n; e0 += gridDim.x * blockDim.x) {
     const unsigned e = e0 + threadIdx.x;
     bool f = false;
@@ -590,7 +735,32 @@ __global__ void k_lmax_cand(const T* __restrict__ M, int lgB, unsigned s1, unsig
           (v > dn[Cl]) & (v > dn[C]) & (v > dn[Cr]);
       key = (((s1inv * R) & mask) << lgB) | ((s2inv * C) & mask);
     }
-    block_emit(f, (int32_t)key, list, count, s_tmp);
+    if (solo) {
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+      const unsigned bal = __ballot_sync(0xffffffffu, f);
+      if (lane == 0) s_tmp[warp] = (unsigned)__popc(bal);
+      __syncthreads();
+      unsigned before = 0, total = 0;
+      for (int w = 0; w < nwarps; ++w) {
+        const unsigned a = s_tmp[w];
+        before += w < warp ? a : 0u;
+        total += a;
+      }
+      if (f) list[run + before + __popc(bal & ((1u << lane) - 1u))] = (int32_t)key;
+      run += total;
+      __syncthreads();   // s_tmp is reused by the next iteration
+    } else {
+      block_emit(f, (int32_t)key, list, count, s_tmp);
+    }
+  }
+  if (solo) {
+    if (threadIdx.x == 0) {
+      *count = run;
+      if (pub.slot)
+        *reinterpret_cast<volatile unsigned long long*>(pub.slot) =
+            ((unsigned long long)run << 32) | (unsigned long long)pub.seq;
+    }
+    return;
   }
   if (pub.slot) {
     __syncthreads();
