@@ -1018,7 +1018,7 @@ template <typename T>
 void finish_select(sfft2d_ctx* c, int lgN, const int32_t* keys, unsigned m, long long k,
                    double prune_rel, cplx<T>* med, T* mags, uint8_t* alive,
                    unsigned long long* peak, long long n_alive, cudaStream_t st,
-                   sfft2d_result* res) {
+                   sfft2d_result* res, const unsigned* alive_cnt_dev = nullptr) {
   using C = cplx<T>;
   res->n_candidates = m;
   if (n_alive == 0) {
@@ -1027,7 +1027,14 @@ void finish_select(sfft2d_ctx* c, int lgN, const int32_t* keys, unsigned m, long
     c->res_count = 0;
     return;
   }
-  const bool cut = n_alive > k;
+  // n_alive < 0: the alive count is still on the device (alive_cnt_dev) and
+  // m > k.  The exact top-k selection runs regardless: dead coordinates carry
+  // magnitude -1, so with alive <= k every alive coordinate is selected and
+  // k_final_bits drops the dead ones — the kept set is the one the reference
+  // keeps without a cut.  Only the order flag needs the count, and it is read
+  // with the final synchronisation (one host round trip less).
+  const bool deferred = n_alive < 0;
+  const bool cut = deferred ? (long long)m > k : n_alive > k;
   const int nblk = blocks_for(m);
   uint32_t* sel = nullptr;
   if (cut) {
@@ -1055,11 +1062,16 @@ void finish_select(sfft2d_ctx* c, int lgN, const int32_t* keys, unsigned m, long
   pre(c, st);
   kl(k_gather_out<T>, grid_for(m), 256, 0, st, pos, tot, keys, med, lgN, oij_d, ov_d);
   post(c, "k_gather_out", st, 0);
+  bool ordered = cut;
+  if (deferred) {
+    ck(cudaMemcpyAsync(c->pinned + 2, alive_cnt_dev, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H");
+  }
   const unsigned count = read_u32(c, tot, st);
+  if (deferred) ordered = (long long)c->pinned[2] > k;
   c->out_ij_h = oij_h;
   c->out_v_h = ov_h;
   res->count = count;
-  res->ordered_by_magnitude = cut ? 1 : 0;
+  res->ordered_by_magnitude = ordered ? 1 : 0;
   c->res_count = count;
 }
 
@@ -1092,7 +1104,8 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
                          const unsigned* m_dev, long long k, double gain_floor, double prune_rel,
                          bool dense, const cplx<T>* xhat, cudaStream_t st, sfft2d_result* res,
                          const cplx<T>* dscratch = nullptr, const cplx<T>* xconv = nullptr,
-                         int conv_r = 0) {
+                         int conv_r = 0, cplx<T>* pre_grids = nullptr,
+                         cudaEvent_t pre_ready = nullptr) {
   using C = cplx<T>;
   const int P = prec_of<T>();
   C* med = (C*)ws(c, "med", (size_t)m * sizeof(C));
@@ -1145,9 +1158,15 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
       const double taps = (double)(2 * conv_r + 1) * (2 * conv_r + 1);
       post(c, "k_estimate_conv", st, (double)m * L * taps * sizeof(C));
     } else {
-      C* grids = (C*)ws(c, "est_grids", (size_t)L * BB * sizeof(C));
-      // natural-order folds (coalesced writes; k_estimate reads the permuted view)
-      fold_spectrum<T, Tin>(c, x, lgN, lgB, tb, hp, L, grids, (T*)nullptr, nullptr, st, true);
+      C* grids = pre_grids;
+      if (pre_grids) {
+        // folded + transformed on the side stream beside the location phase
+        ck(cudaStreamWaitEvent(st, pre_ready, 0), "cudaStreamWaitEvent");
+      } else {
+        grids = (C*)ws(c, "est_grids", (size_t)L * BB * sizeof(C));
+        // natural-order folds (coalesced writes; k_estimate reads the permuted view)
+        fold_spectrum<T, Tin>(c, x, lgN, lgB, tb, hp, L, grids, (T*)nullptr, nullptr, st, true);
+      }
       pre(c, st);
       kl(k_estimate<T>, grid_for((long long)m * L), 256, 0, st, grids, L, keys, m_dev, dp, lgN, lgB, freq, (const C*)tb.tw[P], gain_floor, vals, usable,
           (long)m, true);
@@ -1160,9 +1179,14 @@ void estimate_and_select(sfft2d_ctx* c, const Tin* x, int lgN, int lgB, const De
     // the alive count decides whether a top-k cut is needed (alive > k); with
     // m <= k candidates no cut is possible, so the count is not read (one
     // host synchronisation less; an all-dead result still compacts to 0)
-    n_alive = ((long long)m <= k) ? (long long)m : (long long)read_u32(c, alive_cnt, st);
+    // (m > k: the count only decides the output order flag; finish_select
+    // reads it with its final synchronisation; SFFT2D_SYNC_ALIVE=1: read it now)
+    static const bool sync_alive = getenv("SFFT2D_SYNC_ALIVE") != nullptr;
+    n_alive = ((long long)m <= k) ? (long long)m
+                                  : (sync_alive ? (long long)read_u32(c, alive_cnt, st) : -1LL);
   }
-  finish_select<T>(c, lgN, keys, m, k, prune_rel, med, mags, alive, peak, n_alive, st, res);
+  finish_select<T>(c, lgN, keys, m, k, prune_rel, med, mags, alive, peak, n_alive, st, res,
+                   alive_cnt);
 }
 
 // ------------------------------------------------------------------ ATSFFT
@@ -1889,7 +1913,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     // m > limit (limit <= k: no top-k cut can be needed below it); the
     // general path then runs with that m.  SFFT2D_NO_FUSED_TAIL=1: general path.
     static const bool fused_tail_on = getenv("SFFT2D_NO_FUSED_TAIL") == nullptr;
-    const long long lim = std::min<long long>(maxc, (long long)kFinishSmallMax);
+    const long long lim = std::min<long long>(maxc, (long long)finish_small_max<T>());
     const int best0 = S->b_estimate;
     bool m_known = false;
     if (fused_tail_on && best0 == n && !factored && lim >= 1 &&
@@ -1905,7 +1929,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       C* ov_d = (C*)((char*)oij_d + cap * 16);
       const Publish pub = make_publish(c, 1);
       pre(c, st);
-      kl(k_finish_dense_small<T>, 1, 1024, 0, st, (const C*)xhat, (const int32_t*)keys,
+      kl(k_finish_dense_small<T>, 1, 1024, (size_t)lim * sizeof(C), st, (const C*)xhat, (const int32_t*)keys,
          (const unsigned*)kt, (unsigned)lim, 1.0 >= cf.gain_floor, cf.prune_rel,
          (const unsigned*)finite, lgN, oij_d, ov_d, pub.slot, pub.seq);
       post(c, "k_finish_dense_small", st, 0);
@@ -1989,7 +2013,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
 template <typename T, typename Tin>
 int sfft_location(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, const DevTables& tb,
                   const Perm* hp, const Perm* dp, int nloc, bool want_counts, uint32_t* out,
-                  cudaStream_t st, unsigned* nonfinite = nullptr) {
+                  cudaStream_t st, unsigned* nonfinite = nullptr, cudaEvent_t after_fold = nullptr) {
   const int n = cf.n, lgN = ilog2(n), b = cf.b_bins, lgb = ilog2(b);
   const long BB = (long)b * b;
   const long nkeys = (long)n * n;
@@ -1997,6 +2021,7 @@ int sfft_location(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, con
   T* mags = (T*)ws(c, "loc_mags", (size_t)nloc * BB * sizeof(T));
   fold_spectrum<T, Tin>(c, x, lgN, lgb, tb, hp, nloc, (cplx<T>*)nullptr, mags, nullptr, st, false,
                         nullptr, nullptr, nullptr, 1, nullptr, nonfinite);
+  if (after_fold) ck(cudaEventRecord(after_fold, st), "cudaEventRecord");
   int32_t* bins = (int32_t*)ws(c, "loc_bins", (size_t)nloc * num * 4);
   if (num >= BB) {
     pre(c, st);
@@ -2039,7 +2064,8 @@ int sfft_location(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, con
 template <typename T, typename Tin>
 void sfft_from_hist(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, const DevTables& tb,
                     const uint32_t* hist, int mode, const Perm* hp_est, const Perm* dp_est,
-                    cudaStream_t st, sfft2d_result* res, bool nan_pending = false) {
+                    cudaStream_t st, sfft2d_result* res, bool nan_pending = false,
+                    cplx<T>* pre_grids = nullptr, cudaEvent_t pre_ready = nullptr) {
   const int n = cf.n, lgN = ilog2(n), lgb = ilog2(cf.b_bins);
   const long nkeys = (long)n * n;
   int32_t* keys = (int32_t*)ws(c, "keys", (size_t)nkeys * 4);
@@ -2053,7 +2079,8 @@ void sfft_from_hist(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, c
   c->res_count = 0;
   if (m == 0) return;
   estimate_and_select<T, Tin>(c, x, lgN, lgb, tb, hp_est, dp_est, cf.loops, keys, m, kt, cf.k,
-                              cf.gain_floor, cf.prune_rel, false, (const cplx<T>*)nullptr, st, res);
+                              cf.gain_floor, cf.prune_rel, false, (const cplx<T>*)nullptr, st, res,
+                              nullptr, nullptr, 0, pre_grids, pre_ready);
 }
 
 void check_sfft_cfg(const sfft2d_sfft_config& cf) {
@@ -2137,12 +2164,48 @@ void run_sfft(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, const s
     check_finite_async<Tin>(c, x, (long)cf.n * cf.n, st);
   }
   uint32_t* hist = (uint32_t*)ws(c, "hist", hist_bytes((long)cf.n * cf.n, kVoteAdd8));
+  // The estimation loops' permutations are known up front (engine.py:267), so
+  // their folds + bucket FFTs do not wait for the candidates: they run on the
+  // side stream right after the location fold (both folds are HBM-bound reads
+  // of x; back to back they do not share the bandwidth), beside the location
+  // phase's latency-bound selection / vote kernels and the candidate-count
+  // round trip.  Same grids as the reference's lazy order; they are wasted
+  // only when no candidate survives the vote.  SFFT2D_NO_EARLY_EST=1: folded
+  // after the candidate count, on the main stream.
+  static const bool early_est_on = getenv("SFFT2D_NO_EARLY_EST") == nullptr;
+  const bool early_est = early_est_on && !c->profiling;
+  struct JoinSide {   // later work on st is ordered after the side stream's, whatever the exit
+    sfft2d_ctx* c;
+    cudaStream_t st;
+    bool on;
+    ~JoinSide() {
+      if (!on) return;
+      cudaEventRecord(c->ev_lmax, c->vote_st);
+      cudaStreamWaitEvent(st, c->ev_lmax, 0);
+    }
+  } join_side{c, st, early_est};
   const int mode = sfft_location<T, Tin>(c, x, cf, tb, up.first.data(), up.second, L, false, hist, st,
-                                         fin);
+                                         fin, early_est ? c->ev_fold[0] : nullptr);
+  cplx<T>* pre_grids = nullptr;
+  if (early_est) {
+    const cudaStream_t side = c->vote_st;
+    const size_t BB = (size_t)cf.b_bins * cf.b_bins;
+    ck(cudaStreamWaitEvent(side, c->ev_fold[0], 0), "cudaStreamWaitEvent");
+    const cudaStream_t ws_saved = c->ws_st;
+    c->ws_st = side;
+    c->ws_set = 1;   // private workspace: the location phase's buffers stay in set 0
+    pre_grids = (cplx<T>*)ws(c, "est_grids", (size_t)L * BB * sizeof(cplx<T>));
+    fold_spectrum<T, Tin>(c, x, ilog2(cf.n), ilog2(cf.b_bins), tb, up.first.data() + L, L, pre_grids,
+                          (T*)nullptr, nullptr, side, true);
+    c->ws_set = 0;
+    c->ws_st = ws_saved;
+    ck(cudaEventRecord(c->ev_fold[1], side), "cudaEventRecord");
+  }
   if (fin)
     ck(cudaMemcpyAsync(c->pinned + 1, fin, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H");
   res->perms_used = 2 * L;
-  sfft_from_hist<T, Tin>(c, x, cf, tb, hist, mode, up.first.data() + L, up.second + L, st, res, true);
+  sfft_from_hist<T, Tin>(c, x, cf, tb, hist, mode, up.first.data() + L, up.second + L, st, res, true,
+                         pre_grids, c->ev_fold[1]);
 }
 
 template <typename F>

@@ -346,8 +346,10 @@ __global__ void k_gather_out(const int32_t* __restrict__ pos, const unsigned* __
 // a system fence — the host spins on seq (no stream synchronisation).  Same
 // predicate and order as k_estimate_dense + k_final_bits + compaction +
 // k_gather_out.
-constexpr unsigned kFinishSmallMax = 16384;
+constexpr unsigned kFinishSmallBytes = 128 * 1024;   // shared copy of the candidates' values
 constexpr unsigned kFinishFallback = 0xffffffffu;
+template <typename T>
+constexpr unsigned finish_small_max() { return kFinishSmallBytes / (unsigned)sizeof(cplx<T>); }
 
 template <typename T>
 __global__ void __launch_bounds__(1024)
@@ -357,6 +359,8 @@ k_finish_dense_small(const cplx<T>* __restrict__ xhat, const int32_t* __restrict
                      int64_t* __restrict__ out_ij, cplx<T>* __restrict__ out_v,
                      volatile unsigned* slot, unsigned seq) {
   pdl_wait();
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx<T>* s_v = reinterpret_cast<cplx<T>*>(smem_raw);   // [limit] x_hat at the candidates
   __shared__ unsigned long long s_best[32];
   __shared__ unsigned s_warp[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -373,29 +377,44 @@ k_finish_dense_small(const cplx<T>* __restrict__ xhat, const int32_t* __restrict
     if (tid == 0) publish(m > limit ? kFinishFallback : 0u);
     return;
   }
-  const unsigned per = (m + 1023u) >> 10;            // <= kFinishSmallMax / 1024
-  const unsigned i0 = min(m, (unsigned)tid * per), i1 = min(m, i0 + per);
+  // gather: candidates interleaved over the threads (coalesced key reads), 8
+  // independent x_hat reads in flight per thread
   unsigned long long best = 0ull;
-#pragma unroll 4
-  for (unsigned i = i0; i < i1; ++i) {
-    const unsigned long long k = fkey(cabs_(xhat[(uint32_t)keys[i]]));
-    best = k > best ? k : best;
+  for (unsigned base = 0; base < m; base += 8u * 1024u) {
+    cplx<T> v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const unsigned i = base + (unsigned)j * 1024u + (unsigned)tid;
+      if (i < m) v[j] = xhat[(uint32_t)keys[i]];
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const unsigned i = base + (unsigned)j * 1024u + (unsigned)tid;
+      if (i < m) {
+        s_v[i] = v[j];
+        const unsigned long long k = fkey(cabs_(v[j]));
+        best = k > best ? k : best;
+      }
+    }
   }
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
     best = t > best ? t : best;
   }
   if (lane == 0) s_best[warp] = best;
-  __syncthreads();
+  __syncthreads();                                    // s_v and s_best complete
   best = s_best[lane];
   for (int o = 16; o > 0; o >>= 1) {
     const unsigned long long t = __shfl_xor_sync(0xffffffffu, best, o);
     best = t > best ? t : best;
   }
   const double floor_v = prune_rel > 0 ? prune_rel * fkey_inv(best) : -1.0;
+  // ordered compaction: a contiguous run of candidates per thread
+  const unsigned per = (m + 1023u) >> 10;            // <= 16 (fp32) / 8 (fp64)
+  const unsigned i0 = min(m, (unsigned)tid * per), i1 = min(m, i0 + per);
   unsigned keep = 0;                                  // bit j: candidate i0 + j survives
   for (unsigned i = i0; i < i1; ++i) {
-    const T a = cabs_(xhat[(uint32_t)keys[i]]);
+    const T a = cabs_(s_v[i]);
     if (prune_rel <= 0 || (double)a >= floor_v) keep |= 1u << (i - i0);
   }
   const unsigned cnt = (unsigned)__popc(keep);
@@ -413,7 +432,7 @@ k_finish_dense_small(const cplx<T>* __restrict__ xhat, const int32_t* __restrict
     const unsigned key = (unsigned)keys[i0 + j];
     out_ij[2 * (size_t)pos] = key >> lgN;
     out_ij[2 * (size_t)pos + 1] = key & maskN;
-    out_v[pos] = xhat[key];
+    out_v[pos] = s_v[i0 + j];
     ++pos;
   }
   if (cnt) __threadfence_system();   // the results land before the count

@@ -25,6 +25,8 @@ SWITCHES = {
     "SFFT2D_NO_EARLY_VOTES": ["c2_ats"],          # one vote tally at the end
     "SFFT2D_NO_SMALL_BITMAP": ["c2_ats"],         # small-pass vote bitmaps by k_vote_bitmap
     "SFFT2D_OLD_LMAX_WIN": ["c2_ats"],            # k_lmax_win (natural-column lanes, per-warp atomics)
+    "SFFT2D_NO_EARLY_EST": ["c3_sfft", "c1_sfft"],  # estimation folds after the candidate count
+    "SFFT2D_SYNC_ALIVE": ["c3_sfft", "c1_sfft"],    # alive count read before the top-k cut
     "SFFT2D_NO_FUSED_TAIL": ["c2_ats"],           # dense estimate + selection by the general kernels
 }
 
