@@ -1034,6 +1034,33 @@ void finish_select(sfft2d_ctx* c, int lgN, const int32_t* keys, unsigned m, long
   // keeps without a cut.  Only the order flag needs the count, and it is read
   // with the final synchronisation (one host round trip less).
   const bool deferred = n_alive < 0;
+  // up to kTopkCtaMax candidates: the whole tail in one CTA (k_finish_cut_small),
+  // count and alive count through the publication slot (SFFT2D_NO_FUSED_CUT=1:
+  // the general kernels below)
+  static const bool fused_cut_on = getenv("SFFT2D_NO_FUSED_CUT") == nullptr;
+  if (fused_cut_on && m <= (unsigned)kTopkCtaMax) {
+    const size_t cap = (size_t)m;
+    char* outh = (char*)host_out(c, cap * (16 + sizeof(C)) + 64);
+    int64_t* oij_h = (int64_t*)outh;
+    C* ov_h = (C*)(outh + cap * 16);
+    int64_t* oij_d;
+    ck(cudaHostGetDevicePointer((void**)&oij_d, oij_h, 0), "cudaHostGetDevicePointer");
+    C* ov_d = (C*)((char*)oij_d + cap * 16);
+    const Publish pub = make_publish(c, 1);
+    pre(c, st);
+    kl(k_finish_cut_small<T>, 1, 1024, 0, st, (const C*)med, (const T*)mags, (const uint8_t*)alive,
+       (int)m, k, prune_rel, (const unsigned long long*)peak, deferred ? -1LL : n_alive,
+       alive_cnt_dev, keys, lgN, oij_d, ov_d, pub.slot, pub.seq);
+    post(c, "k_finish_cut_small", st, 0);
+    const unsigned count = wait_published(c, pub.seq, st);
+    const long long na = deferred ? (long long)pub_slot_h(c, pub.seq)[2] : n_alive;
+    c->out_ij_h = oij_h;
+    c->out_v_h = ov_h;
+    res->count = count;
+    res->ordered_by_magnitude = na > k ? 1 : 0;
+    c->res_count = count;
+    return;
+  }
   const bool cut = deferred ? (long long)m > k : n_alive > k;
   const int nblk = blocks_for(m);
   uint32_t* sel = nullptr;
@@ -2028,12 +2055,20 @@ int sfft_location(sfft2d_ctx* c, const Tin* x, const sfft2d_sfft_config& cf, con
     kl(k_iota_segments, grid_for(BB * nloc), 256, 0, st, bins, BB, nloc);
     post(c, "k_iota_segments", st, 0);
   } else {
+    static const bool topk_list_on = getenv("SFFT2D_NO_TOPK_LIST") == nullptr;
+    if (topk_list_on && BB <= (long)kTopkCtaMax) {
+      // one CTA per loop: radix threshold, tie ranks and the ascending bin list
+      pre(c, st);
+      kl(k_topk_list_seg<T>, nloc, 1024, 0, st, (const T*)mags, (int)BB, num, bins, (long)num);
+      post(c, "k_topk_list_seg", st, (double)BB * nloc * sizeof(T));
+    } else {
     const int nblk = blocks_for(BB);
     uint32_t* sb = (uint32_t*)ws(c, "loc_selbits", (size_t)nloc * words_for(BB) * 4);
     unsigned* sc = (unsigned*)ws(c, "loc_selcnt", (size_t)nloc * nblk * 4);
     topk_bits<T>(c, mags, BB, nloc, num, sb, sc, st);
     unsigned* tots = (unsigned*)ws(c, "loc_tot", (size_t)nloc * 4 + 16);
     compact(c, sb, sc, BB, nloc, bins, (long)num, tots, st);
+    }
   }
   const size_t hb = hist_bytes(nkeys, kVoteAdd8);
   const int w = n / b;

@@ -440,4 +440,67 @@ k_finish_dense_small(const cplx<T>* __restrict__ xhat, const int32_t* __restrict
   if (tid == 0) publish(total);
 }
 
+
+// Fused K7 tail (engine.py:228-253) for up to kTopkCtaMax candidates, ONE CTA:
+// the exact top-k cut when more than k coordinates are alive (dead ones carry
+// magnitude -1; block_topk_mask), the prune against prune_rel * peak, the
+// ordered compaction and the gather of (i, j) / values into mapped host
+// memory, then (count, seq) published to the slot the host spins on with the
+// alive count in slot[2] (it decides the output order flag).  Replaces
+// k_sel_init, k_radix_select_seg, k_tie_counts, k_select_bits, k_final_bits,
+// two scans, the compaction, k_gather_out and the final stream
+// synchronisation.  n_alive_host < 0: the alive count is read from
+// alive_cnt (written by k_median).
+template <typename T>
+__global__ void __launch_bounds__(1024)
+k_finish_cut_small(const cplx<T>* __restrict__ med, const T* __restrict__ mags,
+                   const uint8_t* __restrict__ alive, int m, long long k, double prune_rel,
+                   const unsigned long long* __restrict__ peak, long long n_alive_host,
+                   const unsigned* __restrict__ alive_cnt, const int32_t* __restrict__ keys, int lgN,
+                   int64_t* __restrict__ out_ij, cplx<T>* __restrict__ out_v,
+                   volatile unsigned* slot, unsigned seq) {
+  pdl_wait();
+  __shared__ TopkScratch sc;
+  const int tid = threadIdx.x;
+  const long long n_alive = n_alive_host >= 0 ? n_alive_host : (long long)*alive_cnt;
+  const int per = (m + 1023) >> 10;
+  const int e0 = min(m, tid * per);
+  const int cnt = min(m, e0 + per) - e0;
+  T v[kTopkPer];
+#pragma unroll
+  for (int j = 0; j < kTopkPer; ++j) v[j] = j < cnt ? mags[e0 + j] : (T)-1;
+  unsigned sel = cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u);
+  unsigned dummy = 0;
+  if (n_alive > k) sel = block_topk_mask<T>(v, cnt, m, k, sc, &dummy, nullptr);   // block-uniform
+  const double floor_v = prune_rel > 0 ? prune_rel * fkey_inv(*peak) : -1.0;
+  unsigned keep = 0;
+#pragma unroll
+  for (int j = 0; j < kTopkPer; ++j) {
+    if (j < cnt && ((sel >> j) & 1u) && alive[e0 + j] &&
+        (prune_rel <= 0 || (double)v[j] >= floor_v))
+      keep |= 1u << j;
+  }
+  unsigned total = 0;
+  unsigned pos = block_excl_scan1024((unsigned)__popc(keep), sc.warp, &total);
+  const unsigned maskN = (1u << lgN) - 1u;
+  const bool any = keep != 0u;
+  while (keep) {
+    const int j = __ffs(keep) - 1;
+    keep &= keep - 1u;
+    const unsigned key = (unsigned)keys[e0 + j];
+    out_ij[2 * (size_t)pos] = key >> lgN;
+    out_ij[2 * (size_t)pos + 1] = key & maskN;
+    out_v[pos] = med[e0 + j];
+    ++pos;
+  }
+  if (any) __threadfence_system();   // the results land before the count
+  __syncthreads();
+  if (tid == 0) {
+    slot[2] = (unsigned)n_alive;
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned long long*>(slot) =
+        ((unsigned long long)total << 32) | (unsigned long long)seq;
+  }
+}
+
 }  // namespace sfft

@@ -1182,4 +1182,138 @@ __global__ void k_select_bits(const T* __restrict__ vals, long seglen,
     blk_counts[(size_t)seg * gridDim.x + blockIdx.x] = tot + __popc(word);
 }
 
+
+// ---------------------------------------------------------------- one-CTA top-k
+// Exact top-`num` selection (ties to the lowest index, engine.py:122-127) of a
+// segment of n <= kTopkCtaMax values by ONE CTA of 1024 threads, each holding
+// a contiguous run of `per` = ceil(n / 1024) <= 16 values in registers: the
+// eight radix passes of k_radix_select_seg (same digit walk, same SelState
+// result) histogram the register keys, then two block scans — tie ranks among
+// the keys equal to the threshold, output positions — give every thread the
+// selection mask of its run and the rank of its first selected value, so the
+// caller emits the selected indices in ascending order without any of the
+// k_tie_counts / k_select_bits / scan / compaction launches.
+constexpr int kTopkCtaMax = 16384;
+constexpr int kTopkPer = 16;
+
+struct TopkScratch {
+  unsigned hist[256];
+  unsigned warp[32];
+  unsigned long long prefix, mask;
+  long long need;
+};
+
+__device__ __forceinline__ unsigned block_excl_scan1024(unsigned v, unsigned* s_warp,
+                                                        unsigned* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned inc = warp_incl_scan(v);
+  if (lane == 31) s_warp[warp] = inc;
+  __syncthreads();
+  if (warp == 0) s_warp[lane] = warp_incl_scan(s_warp[lane]);
+  __syncthreads();
+  const unsigned r = inc - v + (warp ? s_warp[warp - 1] : 0u);
+  if (total) *total = s_warp[31];
+  __syncthreads();   // s_warp is reused by the next scan
+  return r;
+}
+
+// v[j] = value e0 + j of the thread's run (j < cnt); returns the selection mask
+// of the run (bit j) and, in *pos, the number of selected values before it.
+template <typename T>
+__device__ __forceinline__ unsigned block_topk_mask(const T (&v)[kTopkPer], int cnt, int n,
+                                                    long long num, TopkScratch& sc, unsigned* pos,
+                                                    unsigned* total) {
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (num >= (long long)n) {   // block-uniform: keep the whole segment
+    const unsigned mask = cnt >= 32 ? 0xffffffffu : ((1u << cnt) - 1u);
+    *pos = block_excl_scan1024((unsigned)cnt, sc.warp, total);
+    return mask;
+  }
+  if (tid == 0) { sc.prefix = 0ull; sc.mask = 0ull; sc.need = num; }
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = tid; i < 256; i += blockDim.x) sc.hist[i] = 0;
+    __syncthreads();
+    const unsigned long long prefix = sc.prefix, mask = sc.mask;
+#pragma unroll
+    for (int j = 0; j < kTopkPer; ++j) {
+      if (j < cnt) {
+        const unsigned long long k = fkey(v[j]);
+        if ((k & mask) == prefix) atomicAdd(&sc.hist[(k >> shift) & 255u], 1u);
+      }
+    }
+    __syncthreads();
+    if (tid < 32) {
+      unsigned c[8], lsum = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) { c[i] = sc.hist[255 - 8 * lane - i]; lsum += c[i]; }
+      const unsigned incl = warp_incl_scan(lsum);
+      const long long need = sc.need;
+      const unsigned hit = __ballot_sync(0xffffffffu, (long long)incl >= need);
+      const int L0 = __ffs(hit) - 1;
+      if (lane == L0) {
+        long long cum = (long long)(incl - lsum);
+        for (int i = 0; i < 8; ++i) {
+          if (cum + c[i] >= need) {
+            const unsigned d = 255u - 8u * (unsigned)lane - (unsigned)i;
+            sc.prefix |= (unsigned long long)d << shift;
+            sc.mask |= 255ull << shift;
+            sc.need = need - cum;
+            break;
+          }
+          cum += c[i];
+        }
+      }
+    }
+    __syncthreads();
+  }
+  const unsigned long long thr = sc.prefix;
+  const long long need = sc.need;
+  unsigned gt = 0, eq = 0;
+#pragma unroll
+  for (int j = 0; j < kTopkPer; ++j) {
+    if (j < cnt) {
+      const unsigned long long k = fkey(v[j]);
+      if (k > thr) gt |= 1u << j;
+      else if (k == thr) eq |= 1u << j;
+    }
+  }
+  long long rank = (long long)block_excl_scan1024((unsigned)__popc(eq), sc.warp, nullptr);
+  unsigned sel = gt;
+  while (eq) {
+    const int b = __ffs(eq) - 1;
+    eq &= eq - 1u;
+    if (rank < need) sel |= 1u << b;
+    ++rank;
+  }
+  *pos = block_excl_scan1024((unsigned)__popc(sel), sc.warp, total);
+  return sel;
+}
+
+// Top-`num` bins of each segment as an ascending index list
+// out[seg * out_stride + rank] (the location loops' top-d*k buckets,
+// engine.py:122-127): one CTA per segment, seglen <= kTopkCtaMax.
+template <typename T>
+__global__ void __launch_bounds__(1024)
+k_topk_list_seg(const T* __restrict__ vals, int seglen, long long num, int32_t* __restrict__ out,
+                long out_stride) {
+  pdl_wait();
+  __shared__ TopkScratch sc;
+  const int seg = blockIdx.x;
+  const T* v0 = vals + (size_t)seg * seglen;
+  const int per = (seglen + 1023) >> 10;
+  const int e0 = min(seglen, (int)threadIdx.x * per);
+  const int cnt = min(seglen, e0 + per) - e0;
+  T v[kTopkPer];
+#pragma unroll
+  for (int j = 0; j < kTopkPer; ++j) v[j] = j < cnt ? v0[e0 + j] : (T)0;
+  unsigned pos = 0;
+  unsigned sel = block_topk_mask<T>(v, cnt, seglen, num, sc, &pos, nullptr);
+  int32_t* o = out + (size_t)seg * out_stride;
+  while (sel) {
+    const int b = __ffs(sel) - 1;
+    sel &= sel - 1u;
+    o[pos++] = (int32_t)(e0 + b);
+  }
+}
+
 }  // namespace sfft

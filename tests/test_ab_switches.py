@@ -27,6 +27,8 @@ SWITCHES = {
     "SFFT2D_OLD_LMAX_WIN": ["c2_ats"],            # k_lmax_win (natural-column lanes, per-warp atomics)
     "SFFT2D_NO_EARLY_EST": ["c3_sfft", "c1_sfft"],  # estimation folds after the candidate count
     "SFFT2D_SYNC_ALIVE": ["c3_sfft", "c1_sfft"],    # alive count read before the top-k cut
+    "SFFT2D_NO_FUSED_CUT": ["c3_sfft", "c1_sfft", "c4b_00"],  # K7 tail by the general kernels
+    "SFFT2D_NO_TOPK_LIST": ["c3_sfft", "c1_sfft"],  # location top-k by the bitmask kernels
     "SFFT2D_NO_FUSED_TAIL": ["c2_ats"],           # dense estimate + selection by the general kernels
 }
 
