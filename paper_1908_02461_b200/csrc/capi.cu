@@ -1856,9 +1856,16 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     kl(k_check_finite<Tin>, grid_for(nkeys, 256, kNumSMs * 8), 256, 0, st, x, nkeys, finite);
     post(c, "k_check_finite", st, (double)nkeys * sizeof(Tin));
   }
-  // the NaN/Inf flag rides along with the next synchronisation
-  ck(cudaMemcpyAsync(c->pinned + 1, finite, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H");
+  // the NaN/Inf flag rides along with the next synchronisation (the fused
+  // tail publishes it itself and never enqueues this copy)
+  bool finite_fetched = false;
+  auto fetch_finite = [&]() {
+    if (finite_fetched) return;
+    finite_fetched = true;
+    ck(cudaMemcpyAsync(c->pinned + 1, finite, sizeof(unsigned), cudaMemcpyDeviceToHost, st), "D2H");
+  };
   auto nan_check = [&](bool need_sync) {
+    if (need_sync) fetch_finite();
     if (need_sync) ck(cudaStreamSynchronize(st), "sync");
     if (c->pinned[1]) {
       std::memset(S, 0, sizeof(*S));
@@ -1897,6 +1904,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     unsigned nv = 0;
     if (have_votes) {
       if (lazy) lazy_votes(0u, nullptr, nullptr, hist);
+      fetch_finite();
       nv = hist_compact(c, hist, nkeys, mode, 1u, keys, kt, st);
       nan_check(false);
       int32_t* tal = (int32_t*)ws(c, "tallies", (size_t)std::max(nv, 1u) * 4);
@@ -1931,7 +1939,6 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     uint32_t* bits = (uint32_t*)ws(c, "hc_bits", words_for(nkeys) * 4);
     unsigned* cnts = (unsigned*)ws(c, "hc_cnt", (size_t)blocks_for(nkeys) * 4);
     lazy_votes(thr, bits, cnts, nullptr);
-    compact(c, bits, cnts, nkeys, 1, keys, 0, kt, st);
     // Dense estimate (b_estimate = N, x_hat stored) of what is almost always a
     // small candidate set: the fused tail kernel is launched before the host
     // knows m (it reads m on the device) and publishes m, the NaN flag, the
@@ -1946,6 +1953,12 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
     if (fused_tail_on && best0 == n && !factored && lim >= 1 &&
         std::max(1LL, 2 * maxc) <= (long long)best0 * best0 &&
         (ps.bitgen || pidx + L <= ps.n_arr)) {
+      // compaction without the scan launch; the tail kernel sums the block
+      // counts itself (and stores m for the general path)
+      pre(c, st);
+      kl(k_compact_bits_self, blocks_for(nkeys), kCmpThreads, 0, st, (const uint32_t*)bits, nkeys,
+         (const unsigned*)cnts, keys);
+      post(c, "k_compact_bits", st, 0);
       ensure_xhat(false);
       const size_t cap = (size_t)lim;
       char* outh = (char*)host_out(c, cap * (16 + sizeof(C)) + 64);
@@ -1957,7 +1970,7 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       const Publish pub = make_publish(c, 1);
       pre(c, st);
       kl(k_finish_dense_small<T>, 1, 1024, (size_t)lim * sizeof(C), st, (const C*)xhat, (const int32_t*)keys,
-         (const unsigned*)kt, (unsigned)lim, 1.0 >= cf.gain_floor, cf.prune_rel,
+         (const unsigned*)cnts, blocks_for(nkeys), kt, (unsigned)lim, 1.0 >= cf.gain_floor, cf.prune_rel,
          (const unsigned*)finite, lgN, oij_d, ov_d, pub.slot, pub.seq);
       post(c, "k_finish_dense_small", st, 0);
       const unsigned count = wait_published(c, pub.seq, st);
@@ -1986,10 +1999,13 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       }
     }
     if (!m_known) {
+      compact(c, bits, cnts, nkeys, 1, keys, 0, kt, st);
+      fetch_finite();
       m = read_u32(c, kt, st);
       nan_check(false);
     }
   } else {
+    fetch_finite();
     m = hist_compact(c, hist, nkeys, mode, thr, keys, kt, st);
     nan_check(false);
   }

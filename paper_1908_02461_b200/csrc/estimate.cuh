@@ -354,7 +354,8 @@ constexpr unsigned finish_small_max() { return kFinishSmallBytes / (unsigned)siz
 template <typename T>
 __global__ void __launch_bounds__(1024)
 k_finish_dense_small(const cplx<T>* __restrict__ xhat, const int32_t* __restrict__ keys,
-                     const unsigned* __restrict__ m_dev, unsigned limit, bool usable_all,
+                     const unsigned* __restrict__ blk_counts, int nblk, unsigned* __restrict__ m_out,
+                     unsigned limit, bool usable_all,
                      double prune_rel, const unsigned* __restrict__ nonfinite, int lgN,
                      int64_t* __restrict__ out_ij, cplx<T>* __restrict__ out_v,
                      volatile unsigned* slot, unsigned seq) {
@@ -364,7 +365,18 @@ k_finish_dense_small(const cplx<T>* __restrict__ xhat, const int32_t* __restrict
   __shared__ unsigned long long s_best[32];
   __shared__ unsigned s_warp[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned m = *m_dev;
+  // m = the sum of the compaction's block counts (no scan launch before this
+  // kernel), also stored for the general path's kernels
+  unsigned msum = 0;
+  for (int b = tid; b < nblk; b += blockDim.x) msum += blk_counts[b];
+  for (int o = 16; o > 0; o >>= 1) msum += __shfl_xor_sync(0xffffffffu, msum, o);
+  if (lane == 0) s_warp[warp] = msum;
+  __syncthreads();
+  msum = s_warp[lane];
+  for (int o = 16; o > 0; o >>= 1) msum += __shfl_xor_sync(0xffffffffu, msum, o);
+  __syncthreads();                                    // s_warp is reused below
+  const unsigned m = msum;
+  if (tid == 0) *m_out = m;
   const unsigned bad = nonfinite ? *nonfinite : 0u;
   auto publish = [&](unsigned count) {   // thread 0, after the block's output writes
     slot[2] = m;

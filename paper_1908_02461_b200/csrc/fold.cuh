@@ -1114,7 +1114,11 @@ k_small_pass(const cplx<T>* __restrict__ part, int Z, bool permuted, int lgB, Pe
       if (B > 32) flags[1] = s_rowflag[1];
     }
     *count = s_n;
-    if (pub.slot) publish_count(count, pub.done, pub.target, pub.slot, pub.seq);
+    // a single CTA: the count goes to the host's slot directly (no ticket,
+    // fences or count read-back: three L2 round trips off every small pass)
+    if (pub.slot)
+      *reinterpret_cast<volatile unsigned long long*>(pub.slot) =
+          ((unsigned long long)s_n << 32) | (unsigned long long)pub.seq;
   }
 }
 

@@ -1009,6 +1009,33 @@ __global__ void k_compact_bits(const uint32_t* __restrict__ bits, long seglen,
   }
 }
 
+// k_compact_bits of one segment without the scan launch: every CTA sums the
+// block counts before its own (nblk <= a few thousand words, coalesced) —
+// one launch less on the tuner's tail.
+__global__ void k_compact_bits_self(const uint32_t* __restrict__ bits, long seglen,
+                                    const unsigned* __restrict__ blk_counts,
+                                    int32_t* __restrict__ out) {
+  pdl_wait();
+  __shared__ unsigned s_warp[32];
+  __shared__ unsigned s_before;
+  unsigned before = 0;
+  for (int b = threadIdx.x; b < (int)blockIdx.x; b += blockDim.x) before += blk_counts[b];
+  for (int o = 16; o > 0; o >>= 1) before += __shfl_xor_sync(0xffffffffu, before, o);
+  if (threadIdx.x == 0) s_before = 0u;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0 && before) atomicAdd(&s_before, before);
+  const long wps = words_for(seglen);
+  const long w = (long)blockIdx.x * kCmpWords + threadIdx.x;
+  uint32_t word = (w < wps) ? bits[w] : 0u;
+  const unsigned pre = block_excl_scan256(__popc(word), s_warp);   // (barriers: s_before complete)
+  unsigned pos = s_before + pre;
+  while (word) {
+    const int b = __ffs(word) - 1;
+    word &= word - 1u;
+    out[pos++] = (int32_t)(w * 32 + b);
+  }
+}
+
 // ---------------------------------------------------------------- radix select
 struct SelState {
   unsigned long long prefix;   // key bits fixed so far
@@ -1196,6 +1223,16 @@ __global__ void k_select_bits(const T* __restrict__ vals, long seglen,
 constexpr int kTopkCtaMax = 16384;
 constexpr int kTopkPer = 16;
 
+// selection key of the one-CTA top-k: any order-preserving injective key gives
+// the same selection as fkey's 64-bit one, so float values use their own 32
+// bits (4 radix passes instead of 8)
+__device__ __forceinline__ unsigned long long tkey(double v) { return fkey(v); }
+__device__ __forceinline__ unsigned long long tkey(float v) {
+  const unsigned u = __float_as_uint(v);
+  return (unsigned long long)((u & 0x80000000u) ? ~u : (u | 0x80000000u));
+}
+
+
 struct TopkScratch {
   unsigned hist[256];
   unsigned warp[32];
@@ -1230,14 +1267,14 @@ __device__ __forceinline__ unsigned block_topk_mask(const T (&v)[kTopkPer], int 
     return mask;
   }
   if (tid == 0) { sc.prefix = 0ull; sc.mask = 0ull; sc.need = num; }
-  for (int shift = 56; shift >= 0; shift -= 8) {
+  for (int shift = (sizeof(T) == 4 ? 24 : 56); shift >= 0; shift -= 8) {
     for (int i = tid; i < 256; i += blockDim.x) sc.hist[i] = 0;
     __syncthreads();
     const unsigned long long prefix = sc.prefix, mask = sc.mask;
 #pragma unroll
     for (int j = 0; j < kTopkPer; ++j) {
       if (j < cnt) {
-        const unsigned long long k = fkey(v[j]);
+        const unsigned long long k = tkey(v[j]);
         if ((k & mask) == prefix) atomicAdd(&sc.hist[(k >> shift) & 255u], 1u);
       }
     }
@@ -1272,7 +1309,7 @@ __device__ __forceinline__ unsigned block_topk_mask(const T (&v)[kTopkPer], int 
 #pragma unroll
   for (int j = 0; j < kTopkPer; ++j) {
     if (j < cnt) {
-      const unsigned long long k = fkey(v[j]);
+      const unsigned long long k = tkey(v[j]);
       if (k > thr) gt |= 1u << j;
       else if (k == thr) eq |= 1u << j;
     }
