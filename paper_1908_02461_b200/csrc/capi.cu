@@ -1603,7 +1603,21 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       // taps |d| <= R: R = 2 in fp64; in fp32 the |d| = 2 taps (|F| = 2.5e-9)
       // are below float resolution
       constexpr int RT = sizeof(T) == 4 ? 1 : 2;
-      if (bb == 2048)
+      static const bool band_on = getenv("SFFT2D_OLD_PASSCONV") == nullptr;
+      if (band_on) {
+        // bands of output rows sized for one wave of resident CTAs (at least
+        // the RB rows of the fixed-tile kernel, to bound the halo re-reads)
+        auto go = [&](auto CP) {
+          constexpr int CPT = decltype(CP)::value;
+          const int cps = std::max(1, ctas_per_sm(k_pass_conv_band<T, CPT, 3, RT>, 256, sm));
+          const int nb = std::max(RB, (bb + cps * kNumSMs - 1) / (cps * kNumSMs));
+          kl(k_pass_conv_band<T, CPT, 3, RT>, (bb + nb - 1) / nb, 256, sm, st, (const C*)xhat, lgN, p,
+             freq, tw, nb, mg, pk);
+        };
+        if (bb == 2048) go(std::integral_constant<int, 8>{});
+        else if (bb == 1024) go(std::integral_constant<int, 4>{});
+        else go(std::integral_constant<int, 2>{});
+      } else if (bb == 2048)
         kl(k_pass_conv<T, 8, RB, 3, RT>, bb / RB, 256, sm, st, (const C*)xhat, lgN, p, freq, tw, mg, pk);
       else if (bb == 1024)
         kl(k_pass_conv<T, 4, RB, 3, RT>, bb / RB, 256, sm, st, (const C*)xhat, lgN, p, freq, tw, mg, pk);
