@@ -378,30 +378,37 @@ k_finish_dense_small(const cplx<T>* __restrict__ xhat, const int32_t* __restrict
   const unsigned m = msum;
   if (tid == 0) *m_out = m;
   const unsigned bad = nonfinite ? *nonfinite : 0u;
-  auto publish = [&](unsigned count) {   // thread 0, after the block's output writes
+  // m and the NaN flag go to the slot first; the system fence that orders
+  // them (and the results) before the (count, seq) word is the one at the end
+  if (tid == 0) {
     slot[2] = m;
     slot[3] = bad;
-    __threadfence_system();
+  }
+  auto publish = [&](unsigned count) {   // thread 0, after a system fence behind every output write
     *reinterpret_cast<volatile unsigned long long*>(slot) =
         ((unsigned long long)count << 32) | (unsigned long long)seq;
   };
   if (m > limit || m == 0u || bad || !usable_all) {   // block-uniform
-    if (tid == 0) publish(m > limit ? kFinishFallback : 0u);
+    if (tid == 0) {
+      __threadfence_system();
+      publish(m > limit ? kFinishFallback : 0u);
+    }
     return;
   }
-  // gather: candidates interleaved over the threads (coalesced key reads), 8
-  // independent x_hat reads in flight per thread
+  // gather: candidates interleaved over the threads (coalesced key reads),
+  // every x_hat read of a thread in flight at once (one latency round)
+  constexpr int kPerMax = (int)(kFinishSmallBytes / sizeof(cplx<T>) / 1024u);
   unsigned long long best = 0ull;
-  for (unsigned base = 0; base < m; base += 8u * 1024u) {
-    cplx<T> v[8];
+  {
+    cplx<T> v[kPerMax];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const unsigned i = base + (unsigned)j * 1024u + (unsigned)tid;
+    for (int j = 0; j < kPerMax; ++j) {
+      const unsigned i = (unsigned)j * 1024u + (unsigned)tid;
       if (i < m) v[j] = xhat[(uint32_t)keys[i]];
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const unsigned i = base + (unsigned)j * 1024u + (unsigned)tid;
+    for (int j = 0; j < kPerMax; ++j) {
+      const unsigned i = (unsigned)j * 1024u + (unsigned)tid;
       if (i < m) {
         s_v[i] = v[j];
         const unsigned long long k = fkey(cabs_(v[j]));
@@ -447,7 +454,7 @@ k_finish_dense_small(const cplx<T>* __restrict__ xhat, const int32_t* __restrict
     out_v[pos] = s_v[i0 + j];
     ++pos;
   }
-  if (cnt) __threadfence_system();   // the results land before the count
+  if (cnt || tid == 0) __threadfence_system();   // results, m and the flag land before the count
   __syncthreads();
   if (tid == 0) publish(total);
 }
@@ -496,6 +503,7 @@ k_finish_cut_small(const cplx<T>* __restrict__ med, const T* __restrict__ mags,
   unsigned pos = block_excl_scan1024((unsigned)__popc(keep), sc.warp, &total);
   const unsigned maskN = (1u << lgN) - 1u;
   const bool any = keep != 0u;
+  if (tid == 0) slot[2] = (unsigned)n_alive;   // ordered before the count by the fence below
   while (keep) {
     const int j = __ffs(keep) - 1;
     keep &= keep - 1u;
@@ -505,11 +513,9 @@ k_finish_cut_small(const cplx<T>* __restrict__ med, const T* __restrict__ mags,
     out_v[pos] = med[e0 + j];
     ++pos;
   }
-  if (any) __threadfence_system();   // the results land before the count
+  if (any || tid == 0) __threadfence_system();   // results and alive count land before the count
   __syncthreads();
   if (tid == 0) {
-    slot[2] = (unsigned)n_alive;
-    __threadfence_system();
     *reinterpret_cast<volatile unsigned long long*>(slot) =
         ((unsigned long long)total << 32) | (unsigned long long)seq;
   }
