@@ -1332,7 +1332,14 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
 
   // sides >= 2048: the dense FFT stops after four-step pass A (x_hat is never
   // stored), pass B writes |x_hat| only when a B = N tuner pass needs it
-  const bool factored = dense_factored(lgN, prec_of<T>());
+  // ... unless the B = N/2 passes can come from the stored spectrum (k_pass_conv,
+  // N <= 4096): two passes of fold + three FFT passes cost more than the
+  // complex128 x_hat write the factored form saves (SFFT2D_FP64_FACTORED=1: as before)
+  static const bool fp64_factored_always = getenv("SFFT2D_FP64_FACTORED") != nullptr;
+  static const bool passconv_env_on = getenv("SFFT2D_NO_PASSCONV") == nullptr;
+  const bool conv_possible = passconv_env_on && !fp64_factored_always && n >= 1024 && n <= 4096 &&
+                             tb.conv_r[lgN - 1] == 2 && (size_t)3 * n * sizeof(C) <= 200 * 1024;
+  const bool factored = dense_factored(lgN, prec_of<T>()) && !conv_possible;
   C* dscratch = nullptr;
   auto ensure_xhat = [&](bool need_mags) {
     if (factored) {

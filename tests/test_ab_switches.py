@@ -30,6 +30,7 @@ SWITCHES = {
     "SFFT2D_NO_FUSED_CUT": ["c3_sfft", "c1_sfft", "c4b_00"],  # K7 tail by the general kernels
     "SFFT2D_NO_TOPK_LIST": ["c3_sfft", "c1_sfft"],  # location top-k by the bitmask kernels
     "SFFT2D_OLD_PASSCONV": ["c2_ats"],            # fixed 4-row (2 in fp64) tiles for the B = N/2 pass
+    "SFFT2D_FP64_FACTORED": ["c3_ats"],           # fp64 dense FFT without a stored x_hat (no k_pass_conv)
     "SFFT2D_NO_FUSED_TAIL": ["c2_ats"],           # dense estimate + selection by the general kernels
 }
 
