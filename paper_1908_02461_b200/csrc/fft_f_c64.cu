@@ -13,9 +13,12 @@ template cplx<float>* dense_fft_front<float, float2>(sfft2d_ctx*, const float2*,
 template void dense_fft_xhat<float>(sfft2d_ctx*, cplx<float>*, int, const cplx<float>*, cudaStream_t);
 template void dense_fft_mags<float>(sfft2d_ctx*, float*, unsigned long long*, int, const cplx<float>*,
                                   cudaStream_t);
-// fp64 only: on c3 (4096^2) skipping the 268 MB complex128 x_hat write saves
-// ~70 us per transform; in fp32 pass B gains only ~6 us while the per-candidate
-// strided DFT reads cost ~13 us more (8.4K candidates x 64 scattered sectors).
+// fp64 only: skipping the complex128 x_hat write saves ~70 us per 4096^2
+// transform; in fp32 pass B gains only ~6 us while the per-candidate strided
+// DFT reads cost ~13 us more (8.4K candidates x 64 scattered sectors).  The
+// tuner overrides this for N <= 4096, where a stored x_hat lets the B = N/2
+// passes run through k_pass_conv_band (run_ats: conv_possible), so the factored
+// form is what fp64 uses at N = 8192 and 16384.
 bool dense_factored(int lgN, int precision) {
   if (precision != SFFT2D_FP64) return false;
   const FftPlan2D pl = plan_fft2d<double>(lgN);
