@@ -236,7 +236,13 @@ __device__ __forceinline__ T median_sorted(const T* a, int n) {
   return (n & 1) ? a[n / 2] : (a[n / 2 - 1] + a[n / 2]) / (T)2;
 }
 
-// componentwise median over usable loops; dead coordinates get mag = -1
+// componentwise median; dead coordinates get mag = -1.  The reference masks
+// unusable loops with np.where(usable, vals, np.nan) on a COMPLEX array
+// (engine.py:241-242): the fill value is nan + 0j, so np.nanmedian skips those
+// loops for the real part but sees 0.0 for the imaginary part.  Restated as it
+// is: real median over the usable loops, imaginary median over all loops with
+// 0 where a loop is unusable (identical when every loop is usable, which is
+// the case whenever gain_floor is below the window's passband gain).
 template <typename T>
 __global__ void k_median(const cplx<T>* __restrict__ vals, const uint8_t* __restrict__ usable,
                          int nloops, long stride, const unsigned* __restrict__ m_dev,
@@ -255,8 +261,10 @@ __global__ void k_median(const cplx<T>* __restrict__ vals, const uint8_t* __rest
       if (usable[(size_t)l * stride + i]) {
         const cplx<T> v = vals[(size_t)l * stride + i];
         re[c] = v.x;
-        im[c] = v.y;
+        im[l] = v.y;
         ++c;
+      } else {
+        im[l] = (T)0;
       }
     }
     if (c == 0) {
@@ -266,8 +274,8 @@ __global__ void k_median(const cplx<T>* __restrict__ vals, const uint8_t* __rest
       continue;
     }
     isort(re, c);
-    isort(im, c);
-    const cplx<T> v = mk<T>(median_sorted(re, c), median_sorted(im, c));
+    isort(im, nloops);
+    const cplx<T> v = mk<T>(median_sorted(re, c), median_sorted(im, nloops));
     med[i] = v;
     alive[i] = 1;
     const T a = cabs_(v);

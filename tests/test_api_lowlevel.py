@@ -122,3 +122,55 @@ def test_caller_owned_workspace():
         ctx.use_workspace(None)
     again, _ = P.atsfft2d(x, P.TunerConfig(), 8, 5)
     assert again == ref
+
+
+def _median_select_gpu(n, keys, vals, usable, k, prune_rel, precision="fp64"):
+    """sfft2d_median_select (K7: median, top-k cut with ties to the lowest index,
+    prune, ordered output) through the C ABI."""
+    import ctypes
+    from paper_1908_02461_b200 import _native
+    from paper_1908_02461_b200.engine import _fetch, _stream, to_dict
+    prec = _native.precision_code(precision)
+    cdt = torch.complex128 if precision == "fp64" else torch.complex64
+    ctx = _native.context(0)
+    kd = torch.from_numpy(keys.astype(np.int32)).cuda()
+    vd = torch.from_numpy(vals).to(cdt).cuda().contiguous()
+    ud = torch.from_numpy(usable.astype(np.uint8)).cuda().contiguous()
+    res = _native.ResultC()
+    st = _stream(torch, 0)
+    ctx.check(ctx.lib.sfft2d_median_select(ctx.handle, n, kd.data_ptr(), int(keys.size), vd.data_ptr(),
+                                           ud.data_ptr(), int(vals.shape[0]), int(k), float(prune_rel),
+                                           prec, st, ctypes.byref(res)))
+    return to_dict(*_fetch(ctx, res, st, prec))
+
+
+@gpu
+@pytest.mark.parametrize("m,k,prune", [(500, 100, 0.0), (500, 100, 0.4), (3000, 7, 0.0),
+                                       (16384, 4000, 0.3), (40000, 9000, 0.0), (300, 1000, 0.5)])
+def test_median_select_ties_match_oracle(m, k, prune):
+    """Magnitudes drawn from a handful of exact values, so the top-k cut is
+    decided by ties almost everywhere (engine.py:245-253: lexsort(-|v|, i, j):
+    ties to the lowest coordinate), some loops unusable, some coordinates dead
+    in every loop; m <= 16384 runs the one-CTA tail (k_finish_cut_small),
+    larger m the multi-launch selection.  Support, values and dict order must
+    equal the oracle's."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    n, L = 256, 5
+    rng = np.random.default_rng(m + k)
+    keys = np.sort(rng.choice(n * n, size=m, replace=False))
+    coords = np.stack([keys // n, keys % n], axis=1).astype(np.int64)
+    mags = rng.choice([1.0, 2.0, 2.0, 3.0, 0.5], size=m)
+    phase = rng.choice([1, -1, 1j, -1j], size=m)
+    base = mags * phase
+    # every loop reports the same value where usable, so the median is exactly
+    # `base` and equal magnitudes are equal to the last bit
+    vals = np.tile(base, (L, 1)).astype(np.complex128)
+    usable = rng.random((L, m)) < 0.7
+    usable[:, rng.random(m) < 0.1] = False           # dead coordinates
+    vals[~usable] = 0.0
+    got = _median_select_gpu(n, keys, vals, usable, k, prune)
+    cs, med = O.median_pick(coords, [v for v in vals], [u for u in usable], k, prune)
+    want = O.as_dict((cs, med))
+    assert list(got) == list(want)
+    assert all(got[key] == v for key, v in want.items())
