@@ -477,3 +477,38 @@ def test_c5_sweep_vs_reference(k, precision):
     out, state = P.atsfft2d(x, _tuner(g), int(g["est_loops"]), int(g["seed"]), precision=precision)
     _check_state(state, g, f"c5_ats_k{k}", precision)
     _close_values(out, _ref_dict(g), TOL[precision])
+
+
+def test_count_local_maxima_plateaus_and_floor_ties():
+    """Small integer magnitudes: plateaus (the strict '>' must reject equal
+    neighbours, tuner.py:112-116), bins exactly at the floor (the '>=' of
+    tuner.py:111 must keep them), an all-equal grid and an all-zero grid."""
+    rng = np.random.default_rng(5)
+    for b in (4, 6, 16, 32, 48, 64, 128, 200, 512):
+        for floor in (0.25, 0.5, 1.0):
+            grid = rng.integers(0, 5, size=(b, b)).astype(np.complex128)   # |.| in {0..4}, peak 4
+            cnt, coords = P.count_local_maxima(grid, floor)
+            ocnt, ocoords = O.local_maxima(grid, floor)
+            assert cnt == ocnt, (b, floor)
+            np.testing.assert_array_equal(coords, ocoords)
+        for grid in (np.full((b, b), 3.0 + 0j), np.zeros((b, b), np.complex128)):
+            cnt, coords = P.count_local_maxima(grid, 1e-3)
+            assert cnt == 0 and coords.shape == (0, 2)
+
+
+@pytest.mark.parametrize("gain_floor", [0.9999, 1.0 - 1e-10, 1.0, 1.0 + 2e-4])
+def test_sfft_partially_unusable_loops_match_oracle(gain_floor):
+    """gain_floor inside the window's passband (gain 0.999875 at bucket offset
+    +-4, 1 - 8e-10 at +-3, exactly 1 inside, for n = 256, B = 32): a loop's
+    estimate of a coordinate is usable or not depending on its offset in the
+    bucket, so the medians run over loop subsets (and through the reference's
+    complex nan mask, engine.py:241-242); above 1 every coordinate is dead and
+    the result is empty."""
+    n, k = 256, 8
+    img = P.sparse_image(n, k, 21, snr_db=30.0, dtype=np.complex128)
+    cfg = P.SfftConfig(n=n, k=k, gain_floor=gain_floor)
+    got = P.sfft2d(img.x, cfg, 9, precision="fp64")
+    want = O.as_dict(O.sfft(img.x, O.sfft_params(n, k, gain_floor=gain_floor), 9))
+    assert list(got) == list(want)
+    for key, v in want.items():
+        assert abs(got[key] - v) <= 1e-10 * max(1.0, abs(v)), (key, got[key], v)
