@@ -512,3 +512,23 @@ def test_sfft_partially_unusable_loops_match_oracle(gain_floor):
     assert list(got) == list(want)
     for key, v in want.items():
         assert abs(got[key] - v) <= 1e-10 * max(1.0, abs(v)), (key, got[key], v)
+
+
+@pytest.mark.parametrize("gain_floor", [0.9999, 1.0 - 1e-10, 1.0 + 2e-4])
+def test_atsfft_partially_unusable_loops_match_oracle(gain_floor):
+    """Algorithm 2 with mag_floor = 0.2 on a 30 dB image (the noise maxima
+    stay below the floor, so detected_k = k and b_estimate = 32 < N: the
+    estimation loops go through the window gain; the noise breaks the exact
+    ties of a noiseless image, so the trajectory is the reference's) and a
+    gain_floor inside the passband: the estimation loops of a coordinate are
+    partly unusable and the medians take the reference's complex nan mask."""
+    img = P.sparse_image(256, 6, 3, snr_db=30.0, dtype=np.complex128)
+    cfg = P.TunerConfig(mag_floor=0.2, gain_floor=gain_floor)
+    got, state = P.atsfft2d(img.x, cfg, 8, 4, precision="fp64")
+    (cs, vs), ostate = O.atsfft(img.x, O.TunerParams(mag_floor=0.2, gain_floor=gain_floor), 8, 4)
+    want = O.as_dict((cs, vs))
+    assert [(b, c) for b, c, _ in state.history] == [(b, c) for b, c, _ in ostate["history"]]
+    assert state.b_estimate == ostate["b_estimate"] < 256
+    assert list(got) == list(want)
+    for key, v in want.items():
+        assert abs(got[key] - v) <= 1e-10 * max(1.0, abs(v)), (key, got[key], v)
