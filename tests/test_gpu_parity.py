@@ -532,3 +532,112 @@ def test_atsfft_partially_unusable_loops_match_oracle(gain_floor):
     assert list(got) == list(want)
     for key, v in want.items():
         assert abs(got[key] - v) <= 1e-10 * max(1.0, abs(v)), (key, got[key], v)
+
+
+def _fuzz_compare(got: dict, want: dict):
+    """fp64 fuzz comparison: same support, dict order and values (1e-10).  One
+    loop estimates every coordinate aliased into a bucket from the same bucket
+    value, so such coordinates have magnitudes equal up to the last ulps of
+    the phase twist; a top-k cut through a group of them is decided by those
+    ulps (numpy's own answer depends on the summation order of its FFT).  A
+    coordinate may therefore be on one side alone only when its magnitude
+    equals the smallest kept magnitude to 1e-12, and entries may trade places
+    in the magnitude order only under the same condition."""
+    only = set(got) ^ set(want)
+    if only:
+        assert len(got) == len(want)
+        bound = min(abs(v) for v in want.values())
+        for key in only:
+            m = abs(got[key]) if key in got else abs(want[key])
+            assert abs(m - bound) <= 1e-12 * bound, (key, m, bound)
+    common = {key: want[key] for key in want if key in got}
+    _check_order([key for key in got if key in common], common, 1e-10)
+    vmax = max([abs(v) for v in want.values()] or [1.0])
+    for key, v in common.items():
+        assert abs(got[key] - v) <= 1e-10 * max(abs(v), 1e-3 * vmax), (key, got[key], v)
+
+
+def _fuzz_cases():
+    rng = np.random.default_rng(2024)
+    cases = []
+    for i in range(40):
+        n = int(rng.choice([128, 256, 512]))
+        k = int(rng.choice([3, 10, 40]))
+        snr = float(rng.choice([10.0, 20.0, 30.0]))
+        b0 = int(rng.choice([4, 8, 16, 32, 64]))
+        eps1 = float(rng.uniform(0.05, 0.9))
+        eps2 = float(rng.uniform(0.2, 2.0))
+        d1 = float(rng.uniform(0.005, 0.1))
+        d2 = float(d1 + rng.uniform(0.01, 0.3))
+        iters = [None, 1, 3, 6, 12, 25][int(rng.integers(0, 6))]
+        mag_floor = float(rng.choice([1e-3, 0.05, 0.2, 0.6]))
+        prune = float(rng.choice([0.0, 1e-3, 0.3]))
+        loops = int(rng.choice([1, 2, 3, 8]))
+        cases.append((i, n, k, snr, b0, eps1, eps2, d1, d2, iters, mag_floor, prune, loops))
+    return cases
+
+
+@pytest.mark.parametrize("case", _fuzz_cases(), ids=lambda c: f"fuzz{c[0]}")
+def test_atsfft_config_fuzz_vs_oracle(case):
+    """Random tuner configurations (start bins, ratio thresholds, convergence
+    band, iteration caps including 1, magnitude floors, prune levels, loop
+    counts) on noisy images: every branch of update_bins, the cycle guard, the
+    iteration cap and the vote-budget fallback (tuner.py:121-241) against the
+    oracle — trajectory, state, support in dict order, values 1e-10."""
+    i, n, k, snr, b0, eps1, eps2, d1, d2, iters, mag_floor, prune, loops = case
+    img = P.sparse_image(n, k, 100 + i, snr_db=snr, dtype=np.complex128)
+    cfg = P.TunerConfig(b0=b0, eps1=eps1, eps2=eps2, delta1=d1, delta2=d2, max_tuning_iters=iters,
+                        mag_floor=mag_floor, prune_rel=prune)
+    oc = O.TunerParams(b0=b0, eps1=eps1, eps2=eps2, delta1=d1, delta2=d2, max_iters=iters,
+                       mag_floor=mag_floor, prune_rel=prune)
+    try:
+        (cs, vs), ostate = O.atsfft(img.x, oc, loops, 50 + i)
+        oerr = None
+    except O.OracleConfigError as e:
+        oerr = e
+    if oerr is not None:
+        with pytest.raises(P.ConfigurationError):
+            P.atsfft2d(img.x, cfg, loops, 50 + i, precision="fp64")
+        return
+    got, state = P.atsfft2d(img.x, cfg, loops, 50 + i, precision="fp64")
+    assert [(b, c) for b, c, _ in state.history] == [(b, c) for b, c, _ in ostate["history"]]
+    assert (state.converged, state.detected_k, state.b_estimate, state.vote_passes) == \
+        (ostate["converged"], ostate["detected_k"], ostate["b_estimate"], ostate["vote_passes"])
+    _fuzz_compare(got, O.as_dict((cs, vs)))
+
+
+def _sfft_fuzz_cases():
+    rng = np.random.default_rng(77)
+    cases = []
+    for i in range(40):
+        n = int(rng.choice([64, 128, 256, 512]))
+        k = int(rng.choice([1, 3, 10, 30]))
+        snr = [None, 10.0, 30.0][int(rng.integers(0, 3))]
+        loops = int(rng.choice([1, 2, 3, 5, 8, 11]))
+        d_factor = int(rng.choice([1, 2, 4]))
+        thr = int(rng.integers(1, loops + 1))
+        b = int(rng.choice([b for b in (4, 8, 16, 32, 64, 128) if b <= n]))
+        prune = float(rng.choice([0.0, 1e-3, 0.5]))
+        cases.append((i, n, k, snr, loops, d_factor, thr, b, prune))
+    return cases
+
+
+@pytest.mark.parametrize("case", _sfft_fuzz_cases(), ids=lambda c: f"sfuzz{c[0]}")
+def test_sfft_config_fuzz_vs_oracle(case):
+    """Random Algorithm 1 configurations (loop counts above and below 8, every
+    vote threshold, kept-bin factors, bin counts from 4 to 128, prune levels;
+    noiseless and noisy images) against the oracle: support in dict order and
+    values 1e-10; configurations the reference rejects must be rejected."""
+    i, n, k, snr, loops, d_factor, thr, b, prune = case
+    img = (P.planted_image(n, k, 300 + i) if snr is None
+           else P.sparse_image(n, k, 300 + i, snr_db=snr, dtype=np.complex128))
+    kw = dict(loops=loops, d_factor=d_factor, vote_threshold=thr, b_bins=b, prune_rel=prune)
+    try:
+        oc = O.sfft_params(n, k, **kw)
+    except O.OracleConfigError:
+        with pytest.raises(P.ConfigurationError):
+            P.sfft2d(img.x, P.SfftConfig(n=n, k=k, **kw), 70 + i, precision="fp64")
+        return
+    want = O.as_dict(O.sfft(img.x, oc, 70 + i))
+    got = P.sfft2d(img.x, P.SfftConfig(n=n, k=k, **kw), 70 + i, precision="fp64")
+    _fuzz_compare(got, want)
