@@ -641,3 +641,35 @@ def test_sfft_config_fuzz_vs_oracle(case):
     want = O.as_dict(O.sfft(img.x, oc, 70 + i))
     got = P.sfft2d(img.x, P.SfftConfig(n=n, k=k, **kw), 70 + i, precision="fp64")
     _fuzz_compare(got, want)
+
+
+def _fold_fuzz_cases():
+    rng = np.random.default_rng(909)
+    cases = []
+    for i in range(36):
+        n = int(rng.choice([64, 128, 256, 512, 1024, 2048, 4096], p=[.1, .15, .2, .2, .15, .12, .08]))
+        b = int(rng.choice([v for v in (4, 8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096) if v <= n]))
+        loops = int(rng.choice([1, 1, 2, 3, 8]))
+        dt = [np.complex64, np.complex128][int(rng.integers(0, 2))]
+        cases.append((i, n, b, loops, dt))
+    return cases
+
+
+@pytest.mark.parametrize("case", _fold_fuzz_cases(), ids=lambda c: f"fold{c[0]}-n{c[1]}-b{c[2]}-l{c[3]}")
+def test_binned_spectrum_geometry_fuzz_vs_oracle(case):
+    """Every fold geometry (k_fold / k_fold_ml / TMA ring / wide, partial-sum
+    slices, single and multi-loop launches, whole-grid and four-step FFTs)
+    over random (N, B, loops, input dtype) against the oracle's bucket
+    spectrum (hashing.py:308-337), 1e-12."""
+    i, n, b, loops, dt = case
+    rng = np.random.default_rng(1000 + i)
+    x = (rng.normal(size=(n, n)) + 1j * rng.normal(size=(n, n))).astype(dt)
+    win = P.build_flat_window(n, b, 1e-8, delta_pass=1e-3)
+    perms = [P.draw_permutation(n, rng) for _ in range(loops)]
+    got = P.binned_spectrum(x, perms if loops > 1 else perms[0], win, b).spectrum
+    got = got if loops > 1 else got[None]
+    ow = O.window(n, b, 1e-8, 1e-3)
+    a = O.as_c128(x)
+    for l, p in enumerate(perms):
+        ref = O.bucket_spectrum(a, O.make_perm(n, p.sigma1, p.sigma2, p.tau1, p.tau2), ow, b)
+        assert np.abs(got[l] - ref).max() <= 1e-12 * np.abs(ref).max(), (n, b, l)
