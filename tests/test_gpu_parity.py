@@ -673,3 +673,51 @@ def test_binned_spectrum_geometry_fuzz_vs_oracle(case):
     for l, p in enumerate(perms):
         ref = O.bucket_spectrum(a, O.make_perm(n, p.sigma1, p.sigma2, p.tau1, p.tau2), ow, b)
         assert np.abs(got[l] - ref).max() <= 1e-12 * np.abs(ref).max(), (n, b, l)
+
+
+@pytest.mark.parametrize("case", _fuzz_cases()[:24], ids=lambda c: f"dfuzz{c[0]}")
+def test_detect_sparsity_fuzz_votes_vs_oracle(case):
+    """The tuner's vote accumulation (tuner.py:165-179, 228-240) under the same
+    random configurations: every voted coordinate and its tally (deferred
+    shared-memory tallies, bitmap and list passes, the early tally, the
+    over-budget fallback) must equal the oracle's, with the trajectory."""
+    i, n, k, snr, b0, eps1, eps2, d1, d2, iters, mag_floor, prune, loops = case
+    img = P.sparse_image(n, k, 100 + i, snr_db=snr, dtype=np.complex128)
+    cfg = P.TunerConfig(b0=b0, eps1=eps1, eps2=eps2, delta1=d1, delta2=d2, max_tuning_iters=iters,
+                        mag_floor=mag_floor)
+    oc = O.TunerParams(b0=b0, eps1=eps1, eps2=eps2, delta1=d1, delta2=d2, max_iters=iters,
+                       mag_floor=mag_floor)
+    ostate, (ocoords, otal), _ = O.detect(O.as_c128(img.x), oc, np.random.default_rng(50 + i))
+    state, (coords, tallies) = P.detect_sparsity(img.x, cfg, 50 + i)
+    assert [(b, c) for b, c, _ in state.history] == [(b, c) for b, c, _ in ostate["history"]]
+    assert state.vote_passes == ostate["vote_passes"]
+    np.testing.assert_array_equal(coords, ocoords)
+    np.testing.assert_array_equal(tallies, otal)
+
+
+@pytest.mark.parametrize("case", _fuzz_cases()[:24], ids=lambda c: f"f32fuzz{c[0]}")
+def test_atsfft_config_fuzz_fp32_vs_oracle(case):
+    """The fp32 path under the same random configurations: support equal to
+    the oracle's (a coefficient within 1e-4 of a selection boundary may fall
+    on either side), values within 1e-4.  A count near-tie among noise bins
+    can flip in fp32 and change the bin trajectory; such a case is compared
+    only up to the first pass whose count differs, which must differ by less
+    than 1e-4 relative (at least 1 bin)."""
+    i, n, k, snr, b0, eps1, eps2, d1, d2, iters, mag_floor, prune, loops = case
+    img = P.sparse_image(n, k, 100 + i, snr_db=snr, dtype=np.complex128)
+    cfg = P.TunerConfig(b0=b0, eps1=eps1, eps2=eps2, delta1=d1, delta2=d2, max_tuning_iters=iters,
+                        mag_floor=mag_floor, prune_rel=prune)
+    oc = O.TunerParams(b0=b0, eps1=eps1, eps2=eps2, delta1=d1, delta2=d2, max_iters=iters,
+                       mag_floor=mag_floor, prune_rel=prune)
+    (cs, vs), ostate = O.atsfft(img.x, oc, loops, 50 + i)
+    got, state = P.atsfft2d(img.x, cfg, loops, 50 + i, precision="fp32")
+    gh = [(b, c) for b, c, _ in state.history]
+    oh = [(b, c) for b, c, _ in ostate["history"]]
+    if gh != oh:
+        # first differing pass: same bin count, local-maximum counts within 1e-4
+        t = next((j for j, (a, b) in enumerate(zip(gh, oh)) if a != b), min(len(gh), len(oh)))
+        assert t < min(len(gh), len(oh)), (gh, oh)
+        assert gh[t][0] == oh[t][0]
+        assert abs(gh[t][1] - oh[t][1]) <= max(1.0, 1e-4 * oh[t][1]), (t, gh[t], oh[t])
+        pytest.skip("an fp32 count near-tie changed the trajectory")
+    _close_values(got, O.as_dict((cs, vs)), 1e-4)
