@@ -574,6 +574,12 @@ def _fuzz_cases():
         prune = float(rng.choice([0.0, 1e-3, 0.3]))
         loops = int(rng.choice([1, 2, 3, 8]))
         cases.append((i, n, k, snr, b0, eps1, eps2, d1, d2, iters, mag_floor, prune, loops))
+    # edges: start bins below the minimum grid and above the image side, no
+    # tuning iterations at all, a single loop, an image of pure noise
+    for j, (n, k, snr, b0, iters, loops) in enumerate([
+            (128, 5, 20.0, 1, None, 3), (128, 5, 20.0, 2, 4, 8), (128, 5, 20.0, 1024, None, 2),
+            (256, 5, 20.0, 16, 0, 8), (256, 0, 20.0, 16, None, 8), (64, 2, 40.0, 64, None, 1)]):
+        cases.append((len(cases), n, k, snr, b0, 0.5, 1.0, 0.02, 0.05, iters, 1e-3, 1e-3, loops))
     return cases
 
 
@@ -619,6 +625,12 @@ def _sfft_fuzz_cases():
         b = int(rng.choice([b for b in (4, 8, 16, 32, 64, 128) if b <= n]))
         prune = float(rng.choice([0.0, 1e-3, 0.5]))
         cases.append((i, n, k, snr, loops, d_factor, thr, b, prune))
+    # edges: every bin kept (d_factor * k = B^2), w = 1 (B = N), the smallest
+    # grid, k = 0 (one kept bin, engine.py:116-118)
+    for n, k, snr, loops, d_factor, thr, b in [
+            (64, 8, 20.0, 3, 2, 2, 4), (128, 16, None, 5, 1, 3, 4), (64, 3, 20.0, 4, 2, 2, 64),
+            (64, 1, None, 1, 1, 1, 4), (128, 0, 20.0, 3, 2, 2, 16)]:
+        cases.append((len(cases), n, k, snr, loops, d_factor, thr, b, 1e-3))
     return cases
 
 
