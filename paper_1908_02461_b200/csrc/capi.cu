@@ -1599,7 +1599,12 @@ void run_ats(sfft2d_ctx* c, const Tin* x, int n, const sfft2d_tuner_config& cf, 
       // computed here, one pass early, and serves the B = N passes after it
       wait_list_free();
       ensure_xhat(true);
-      T* mg = (T*)ws(c, "grid_mag", BB * sizeof(T));
+      // a buffer of its own: this pass runs on the main stream in the default
+      // workspace set (0), and "grid_mag" of set 0 also belongs to the
+      // side-stream passes with slot % 3 == 0 — a speculated B = N/2 pass
+      // enqueued behind such a pass would overwrite the |Z| grid its local
+      // maxima are still being counted from (found by the large-N fuzz)
+      T* mg = (T*)ws(c, "grid_mag_conv", BB * sizeof(T));
       // this slot's peak, zeroed with the scratch
       unsigned long long* pk = (unsigned long long*)(scr + kScrPeaks) + slot;
       const T* freq = (const T*)tb.freq[prec_of<T>()] + ((size_t)lgb << lgN);

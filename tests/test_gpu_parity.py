@@ -733,3 +733,41 @@ def test_atsfft_config_fuzz_fp32_vs_oracle(case):
         assert abs(gh[t][1] - oh[t][1]) <= max(1.0, 1e-4 * oh[t][1]), (t, gh[t], oh[t])
         pytest.skip("an fp32 count near-tie changed the trajectory")
     _close_values(got, O.as_dict((cs, vs)), 1e-4)
+
+
+def _large_fuzz_cases():
+    rng = np.random.default_rng(4242)
+    cases = []
+    for i, n in enumerate([1024, 1024, 1024, 1024, 2048, 2048]):
+        k = int(rng.choice([20, 100]))
+        snr = float(rng.choice([15.0, 25.0]))
+        b0 = int(rng.choice([8, 16, 64, 128]))
+        eps1 = float(rng.uniform(0.2, 0.8))
+        eps2 = float(rng.uniform(0.6, 1.5))
+        d1 = float(rng.uniform(0.005, 0.04))
+        d2 = float(d1 + rng.uniform(0.02, 0.1))
+        mag_floor = float(rng.choice([1e-3, 0.02]))
+        loops = int(rng.choice([3, 8]))
+        cases.append((i, n, k, snr, b0, eps1, eps2, d1, d2, None, mag_floor, 1e-3, loops))
+    return cases
+
+
+@pytest.mark.parametrize("case", _large_fuzz_cases(), ids=lambda c: f"lfuzz{c[0]}-n{c[1]}")
+def test_atsfft_large_config_fuzz_vs_oracle(case):
+    """Random tuner configurations at N = 1024 and 2048: the speculative paired
+    folds, the B = N/2 pass from the dense spectrum (k_pass_conv_band), the
+    register-window local maxima at B >= 128, bitmap and list vote passes, the
+    early tally and the fused tail — trajectory, state, support, order and
+    values against the oracle."""
+    i, n, k, snr, b0, eps1, eps2, d1, d2, iters, mag_floor, prune, loops = case
+    img = P.sparse_image(n, k, 700 + i, snr_db=snr, dtype=np.complex64)
+    cfg = P.TunerConfig(b0=b0, eps1=eps1, eps2=eps2, delta1=d1, delta2=d2, mag_floor=mag_floor,
+                        prune_rel=prune)
+    oc = O.TunerParams(b0=b0, eps1=eps1, eps2=eps2, delta1=d1, delta2=d2, mag_floor=mag_floor,
+                       prune_rel=prune)
+    (cs, vs), ostate = O.atsfft(img.x, oc, loops, 800 + i)
+    got, state = P.atsfft2d(img.x, cfg, loops, 800 + i, precision="fp64")
+    assert [(b, c) for b, c, _ in state.history] == [(b, c) for b, c, _ in ostate["history"]]
+    assert (state.converged, state.detected_k, state.b_estimate, state.vote_passes) == \
+        (ostate["converged"], ostate["detected_k"], ostate["b_estimate"], ostate["vote_passes"])
+    _fuzz_compare(got, O.as_dict((cs, vs)))
